@@ -1,0 +1,229 @@
+/*
+ * lrb.h — C-ABI of the B200-native batched FP64 GEMM hot path (liblrb.so).
+ *
+ * The reference (lrbatch, header-only C++20) computes every BASELINE shape with
+ * its oracle primitive
+ *     void lrbatch::gemm_naive_raw(const double* a, const double* b, double* c,
+ *                                  size_t m, size_t k, size_t n, bool accumulate,
+ *                                  uint64_t* flops = nullptr);
+ * (reference: proj/include/lrbatch/dense.hpp:43-56), called item by item over
+ * batches packed with the LowRankBatch convention "item i of a role starts at
+ * base + i*rows*cols, row-major per item" (low_rank.hpp:147-158), e.g. at the
+ * BLR diagonal step (blr.hpp:149-153) and the tile expansion (blr.hpp:75-78).
+ * This header is the drop-in boundary for that path: plain pointers and sizes,
+ * status codes instead of exceptions, no CUDA or torch types.
+ *
+ * Conventions
+ *  - Results equal the reference FMA chain: every C entry is accumulated in
+ *    ascending k from 0 (beta = 0) or from the old C (beta = 1), one fused
+ *    multiply-add per k. The kernels use FP64 DMMA/DFMA, which round exactly
+ *    like that chain, so results are bitwise equal to gemm_naive_raw compiled
+ *    with FMA contraction (what the reference's -O3 -march=native build does).
+ *  - order 'C' = column-major (BASELINE), 'R' = row-major (the reference).
+ *  - beta must be 0 or 1: it is the reference's `accumulate` flag. With beta
+ *    = 0, C is never read.
+ *  - Device-pointer calls are asynchronous on `stream` (a cudaStream_t passed
+ *    as void*; NULL = legacy default stream). Host-buffer calls (`_host`,
+ *    lrb_gemm_naive_raw) are synchronous like the reference.
+ *  - Errors: every call returns lrb_status; lrb_last_error(ctx) holds the
+ *    message. LRB_ERR_SHAPE mirrors the reference ShapeError (common.hpp:19-22)
+ *    and names the offending pair the way dense_gemm_naive does
+ *    (dense.hpp:58-69), LRB_ERR_CAPACITY mirrors CapacityError (common.hpp:24-27).
+ *  - There is no CPU fallback: without a usable sm_100 device, lrb_create
+ *    fails with LRB_ERR_NO_DEVICE.
+ */
+#ifndef LRB_H
+#define LRB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* the library is built with -fvisibility=hidden; these are its only exports */
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define LRB_VERSION_STRING "lrb-b200 0.1.0"
+
+typedef enum lrb_status {
+  LRB_OK = 0,
+  LRB_ERR_SHAPE = 1,       /* dimension / leading-dimension / stride invariant violated */
+  LRB_ERR_CAPACITY = 2,    /* workspace or device memory exhausted */
+  LRB_ERR_ARG = 3,         /* bad enum value, null pointer, bad handle */
+  LRB_ERR_CUDA = 4,        /* CUDA runtime error (message carries cudaGetErrorString) */
+  LRB_ERR_UNSUPPORTED = 5, /* valid request outside what this build implements */
+  LRB_ERR_NO_DEVICE = 6    /* no CUDA device / not sm_100 */
+} lrb_status;
+
+typedef struct lrb_ctx lrb_ctx;           /* one per (host thread, device) */
+typedef struct lrb_ptr_plan lrb_ptr_plan; /* descriptor of a pointer-array batch */
+
+/* ---------------------------------------------------------------- context */
+lrb_status lrb_create(int device, lrb_ctx** out);
+lrb_status lrb_destroy(lrb_ctx* ctx);
+const char* lrb_last_error(const lrb_ctx* ctx); /* ctx may be NULL: thread-local last error */
+const char* lrb_version(void);
+int lrb_device_count(void); /* 0 when no driver / no device; never fails */
+int lrb_ctx_device(const lrb_ctx* ctx);
+int lrb_ctx_sm_count(const lrb_ctx* ctx);
+/* number of kernels this context has launched so far (GEMM + fill + flush) */
+uint64_t lrb_launch_count(const lrb_ctx* ctx);
+
+/* ------------------------------------------------ memory / stream helpers */
+lrb_status lrb_malloc(lrb_ctx* ctx, size_t bytes, void** dptr);
+lrb_status lrb_free(lrb_ctx* ctx, void* dptr);
+lrb_status lrb_host_alloc(lrb_ctx* ctx, size_t bytes, void** hptr); /* pinned */
+lrb_status lrb_host_free(lrb_ctx* ctx, void* hptr);
+lrb_status lrb_memcpy_h2d(lrb_ctx* ctx, void* dst, const void* src, size_t bytes);
+lrb_status lrb_memcpy_d2h(lrb_ctx* ctx, void* dst, const void* src, size_t bytes);
+lrb_status lrb_memset(lrb_ctx* ctx, void* dptr, int value, size_t bytes);
+lrb_status lrb_stream_create(lrb_ctx* ctx, void** stream);
+lrb_status lrb_stream_destroy(lrb_ctx* ctx, void* stream);
+lrb_status lrb_stream_sync(lrb_ctx* ctx, void* stream);
+lrb_status lrb_device_sync(lrb_ctx* ctx);
+/* free / total device memory in bytes */
+lrb_status lrb_mem_info(lrb_ctx* ctx, size_t* free_bytes, size_t* total_bytes);
+
+/* CUDA events for device-side timing on the launching stream */
+lrb_status lrb_event_create(lrb_ctx* ctx, void** ev);
+lrb_status lrb_event_destroy(lrb_ctx* ctx, void* ev);
+lrb_status lrb_event_record(lrb_ctx* ctx, void* ev, void* stream);
+lrb_status lrb_event_elapsed_ms(lrb_ctx* ctx, void* ev_start, void* ev_end, float* ms);
+/* write a buffer larger than L2 on `stream` (timing hygiene between reps) */
+lrb_status lrb_l2_flush(lrb_ctx* ctx, void* stream);
+
+/* ------------------------------------------------------------- hot path */
+/*
+ * Strided batch: item i uses A + i*strideA, B + i*strideB, C + i*strideC
+ * (elements). C_i = op(A_i) * op(B_i) + beta * C_i with op(A) m x k,
+ * op(B) k x n, C m x n, all in `order`. The reference's LowRankBatch packing
+ * is strideX = rows*cols, ldX = cols (order 'R'); BASELINE's is
+ * strideX = rows*cols, ldX = rows (order 'C').
+ * Replaces: lrbatch::gemm_naive_raw called per item (dense.hpp:43-56), e.g. the
+ * BLR diagonal loop (blr.hpp:149-153) and naive_multiply_batch's per-item
+ * fan-out (bench.hpp:55-77).
+ */
+lrb_status lrb_dgemm_strided_batched(lrb_ctx* ctx, char order, char opA, char opB,
+                                     int64_t m, int64_t n, int64_t k, double beta,
+                                     const double* A, int64_t lda, int64_t strideA,
+                                     const double* B, int64_t ldb, int64_t strideB,
+                                     double* C, int64_t ldc, int64_t strideC,
+                                     int64_t batch, void* stream);
+
+/*
+ * Pointer-array / variable-size batch. Dimension and leading-dimension arrays
+ * are HOST arrays of length `batch`; A/B/C are HOST arrays of DEVICE pointers.
+ * The plan buckets items by kernel variant, builds per-variant tile lists
+ * (largest k first) and uploads them once; execute is then one launch per
+ * non-empty variant. Replaces: per-item gemm_naive_raw over independently
+ * allocated blocks (blr.hpp:141-175's diagonal and scatter steps).
+ */
+lrb_status lrb_ptr_plan_create(lrb_ctx* ctx, char order, char opA, char opB, int64_t batch,
+                               const int64_t* m, const int64_t* n, const int64_t* k,
+                               const double* const* A, const int64_t* lda,
+                               const double* const* B, const int64_t* ldb,
+                               double* const* C, const int64_t* ldc, double beta,
+                               lrb_ptr_plan** out);
+lrb_status lrb_ptr_plan_execute(lrb_ctx* ctx, const lrb_ptr_plan* plan, void* stream);
+lrb_status lrb_ptr_plan_destroy(lrb_ctx* ctx, lrb_ptr_plan* plan);
+/* number of kernel launches one execute performs */
+int lrb_ptr_plan_launches(const lrb_ptr_plan* plan);
+/* one-shot create + execute + (stream-synchronised) destroy */
+lrb_status lrb_dgemm_ptr_batched(lrb_ctx* ctx, char order, char opA, char opB, int64_t batch,
+                                 const int64_t* m, const int64_t* n, const int64_t* k,
+                                 const double* const* A, const int64_t* lda,
+                                 const double* const* B, const int64_t* ldb,
+                                 double* const* C, const int64_t* ldc, double beta,
+                                 void* stream);
+
+/* ------------------------------------------------ host-buffer entry points */
+/*
+ * Drop-in for lrbatch::gemm_naive_raw (dense.hpp:43-45): row-major HOST
+ * buffers a (m x k), b (k x n), c (m x n); accumulate = reference flag;
+ * `flops` (nullable) is incremented by 2*m*n*k exactly like the reference's
+ * in-loop counter. Synchronous.
+ */
+lrb_status lrb_gemm_naive_raw(lrb_ctx* ctx, const double* a, const double* b, double* c,
+                              size_t m, size_t k, size_t n, int accumulate, uint64_t* flops);
+/*
+ * Same contract as lrb_dgemm_strided_batched but on HOST buffers: the batch
+ * is cut into chunks whose H2D copy, kernel and D2H copy are pipelined over
+ * three streams. Pinned host memory (lrb_host_alloc) gets full PCIe rate.
+ * Synchronous.
+ */
+lrb_status lrb_dgemm_strided_batched_host(lrb_ctx* ctx, char order, char opA, char opB,
+                                          int64_t m, int64_t n, int64_t k, double beta,
+                                          const double* A, int64_t lda, int64_t strideA,
+                                          const double* B, int64_t ldb, int64_t strideB,
+                                          double* C, int64_t ldc, int64_t strideC,
+                                          int64_t batch);
+
+/* ---------------------------------------------------- selector / planner */
+typedef struct lrb_selection {
+  int variant;        /* index into the variant table */
+  int tile_m, tile_n; /* C tile per CTA (column-major view) */
+  int tile_k;         /* k chunk per pipeline stage */
+  int stages;         /* shared-memory pipeline depth */
+  int threads;        /* threads per CTA (consumer warps + 1 TMA producer warp) */
+  int ctas_per_sm;    /* design occupancy */
+  int64_t tiles;      /* CTA tiles in the launch */
+  int64_t grid;       /* persistent grid size */
+  double intensity;   /* algorithmic flop / byte of the whole batch */
+  int fp64_bound;     /* 1 if intensity >= measured FP64 ridge, else HBM-bound */
+  char name[24];
+} lrb_selection;
+
+/*
+ * Per-shape kernel selector (B200 analogue of make_packing_plan,
+ * plan.hpp:66-100). ctx may be NULL (host-only: assumes 148 SMs). The choice
+ * can be forced with lrb_set_variant_override or the LRB_VARIANT environment
+ * variable (variant name), mirroring the reference's plan-override file
+ * (plan.hpp:106-158).
+ */
+lrb_status lrb_select(const lrb_ctx* ctx, char order, char opA, char opB, int64_t m, int64_t n,
+                      int64_t k, int64_t batch, lrb_selection* out);
+int lrb_variant_count(void);
+const char* lrb_variant_name(int variant);
+int lrb_variant_from_name(const char* name); /* -1 if unknown */
+lrb_status lrb_set_variant_override(lrb_ctx* ctx, int variant); /* -1 = automatic */
+
+/*
+ * Shard planner: split `batch` independent items into `nparts` contiguous
+ * ranges, begin[0..nparts] (begin[0] = 0, begin[nparts] = batch). With
+ * item_cost == NULL the split is the reference's contiguous fan-out
+ * (per = ceil(batch / nparts); bench.hpp:69-75, kernels.hpp:274-276); with
+ * costs, cuts are placed at equal cumulative cost. Host-only.
+ */
+lrb_status lrb_shard_plan(int64_t batch, const double* item_cost, int nparts, int64_t* begin);
+
+/* algorithmic accounting of one item (beta = 0: 8(mk+kn+mn) bytes; beta = 1 adds mn) */
+double lrb_item_flops(int64_t m, int64_t n, int64_t k);
+double lrb_item_bytes(int64_t m, int64_t n, int64_t k, double beta);
+
+/* ------------------------------------------------------- synthetic inputs */
+/*
+ * Fill `batch` column-major rows x cols matrices (leading dimension ld, item
+ * stride `stride` elements) with lrb_uniform(seed, role, item_offset + i, elem)
+ * from lrb_rng.h — bit-identical to the host generator.
+ */
+lrb_status lrb_fill_uniform(lrb_ctx* ctx, double* dst, int64_t rows, int64_t cols, int64_t ld,
+                            int64_t stride, int64_t batch, uint64_t seed, uint32_t role,
+                            int64_t item_offset, void* stream);
+/* pointer-array form: host arrays of device pointers and per-item dims */
+lrb_status lrb_fill_uniform_ptr(lrb_ctx* ctx, double* const* dst, const int64_t* rows,
+                                const int64_t* cols, const int64_t* ld, int64_t batch,
+                                uint64_t seed, uint32_t role, int64_t item_offset, void* stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* LRB_H */

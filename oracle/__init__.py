@@ -1,0 +1,189 @@
+"""CPU oracle for the batched FP64 GEMM hot path — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` legs may import this package. It is the checker, never the
+product: paper_2311_07602_b200 does not import it and has no CPU fallback.
+
+Two libraries:
+  * ``liblrb_oracle.so`` — the C restatement (oracle/lrb_oracle.c) of the
+    reference's gemm_naive_raw (proj/include/lrbatch/dense.hpp:43-56);
+  * ``_ref/liblrb_ref.so`` — the reference itself compiled from
+    /root/reference by the Makefile's ``ref`` target (travels prebuilt to the
+    GPU box; the reference tree does not).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liblrb_oracle.so")
+REF_SO = os.path.join(HERE, "_ref", "liblrb_ref.so")
+
+FMA_CHAIN = 0      # one fma() per k step (the device kernels' rounding)
+REF_COMPILED = 1   # the reference binary's rounding
+
+i64, dbl, vp = C.c_int64, C.c_double, C.c_void_p
+P = C.POINTER
+
+_oracle = None
+_ref = None
+
+
+def oracle_lib() -> C.CDLL:
+    global _oracle
+    if _oracle is None:
+        if not os.path.exists(ORACLE_SO):
+            raise ImportError(f"{ORACLE_SO} missing: run `make oracle`")
+        L = C.CDLL(ORACLE_SO)
+        L.oracle_gemm_naive_raw.argtypes = [vp, vp, vp, C.c_size_t, C.c_size_t, C.c_size_t,
+                                            C.c_int, P(C.c_uint64)]
+        L.oracle_gemm_naive_raw.restype = None
+        L.oracle_dgemm_strided.argtypes = [C.c_int, C.c_char, C.c_char, C.c_char, i64, i64, i64,
+                                           dbl, vp, i64, i64, vp, i64, i64, vp, i64, i64, i64,
+                                           C.c_int]
+        L.oracle_dgemm_strided.restype = C.c_int
+        L.oracle_dgemm_ptr.argtypes = [C.c_int, C.c_char, C.c_char, C.c_char, i64, P(i64), P(i64),
+                                       P(i64), P(vp), P(i64), P(vp), P(i64), P(vp), P(i64), dbl,
+                                       C.c_int]
+        L.oracle_dgemm_ptr.restype = C.c_int
+        L.oracle_fill_uniform.argtypes = [vp, i64, i64, i64, i64, i64, C.c_uint64, C.c_uint32, i64]
+        L.oracle_fill_uniform.restype = None
+        L.oracle_check_bound.argtypes = [C.c_char, C.c_char, C.c_char, i64, i64, i64, dbl, vp, i64,
+                                         vp, i64, vp, vp, vp, i64, P(dbl)]
+        L.oracle_check_bound.restype = i64
+        _oracle = L
+    return _oracle
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def ref_lib() -> C.CDLL:
+    global _ref
+    if _ref is None:
+        if not os.path.exists(REF_SO):
+            raise ImportError(f"{REF_SO} missing: run `make ref` where /root/reference exists")
+        L = C.CDLL(REF_SO)
+        L.ref_gemm_naive_raw.argtypes = [vp, vp, vp, C.c_size_t, C.c_size_t, C.c_size_t, C.c_int,
+                                         P(C.c_uint64)]
+        L.ref_gemm_naive_raw.restype = None
+        L.ref_gemm_rowmajor_batched.argtypes = [vp, vp, vp, C.c_size_t, C.c_size_t, C.c_size_t,
+                                                C.c_int, i64, C.c_int]
+        L.ref_gemm_rowmajor_batched.restype = None
+        L.ref_dgemm_colmajor_strided.argtypes = [C.c_char, C.c_char, i64, i64, i64, C.c_int, vp,
+                                                 i64, i64, vp, i64, i64, vp, i64, i64, i64,
+                                                 C.c_int]
+        L.ref_dgemm_colmajor_strided.restype = C.c_int
+        L.ref_dgemm_colmajor_ptr.argtypes = [C.c_char, C.c_char, i64, P(i64), P(i64), P(i64),
+                                             P(vp), P(i64), P(vp), P(i64), P(vp), P(i64), C.c_int,
+                                             C.c_int]
+        L.ref_dgemm_colmajor_ptr.restype = C.c_int
+        L.ref_dense_gemm_naive_error.argtypes = [C.c_size_t] * 6 + [C.c_char_p, C.c_size_t]
+        L.ref_dense_gemm_naive_error.restype = C.c_int
+        _ref = L
+    return _ref
+
+
+def _p(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+# ------------------------------------------------------------------ oracle
+def gemm_naive_raw(a, b, c, m, k, n, accumulate, flops: Optional[np.ndarray] = None):
+    fl = C.c_uint64(int(flops[0]) if flops is not None else 0)
+    oracle_lib().oracle_gemm_naive_raw(_p(a), _p(b), _p(c), m, k, n, int(bool(accumulate)),
+                                       C.byref(fl) if flops is not None else None)
+    if flops is not None:
+        flops[0] = fl.value
+
+
+def dgemm_strided(order, opA, opB, m, n, k, beta, A, lda, sA, B, ldb, sB, Cm, ldc, sC, batch,
+                  threads=1, mode=FMA_CHAIN):
+    rc = oracle_lib().oracle_dgemm_strided(mode, order.encode(), opA.encode(), opB.encode(), m, n,
+                                           k, float(beta), _p(A), lda, sA, _p(B), ldb, sB, _p(Cm),
+                                           ldc, sC, batch, threads)
+    if rc != 0:
+        raise ValueError("oracle_dgemm_strided: bad arguments")
+
+
+def _arr64(xs):
+    a = np.ascontiguousarray(np.asarray(xs, dtype=np.int64))
+    return a, a.ctypes.data_as(P(i64))
+
+
+def dgemm_ptr(order, opA, opB, m, n, k, A, lda, B, ldb, Cs, ldc, beta, threads=1, mode=FMA_CHAIN):
+    batch = len(m)
+    keep = [_arr64(x) for x in (m, n, k, lda, ldb, ldc)]
+    pa = (vp * batch)(*[_p(x) for x in A])
+    pb = (vp * batch)(*[_p(x) for x in B])
+    pc = (vp * batch)(*[_p(x) for x in Cs])
+    rc = oracle_lib().oracle_dgemm_ptr(mode, order.encode(), opA.encode(), opB.encode(), batch,
+                                       keep[0][1], keep[1][1], keep[2][1], pa, keep[3][1], pb,
+                                       keep[4][1], pc, keep[5][1], float(beta), threads)
+    if rc != 0:
+        raise ValueError("oracle_dgemm_ptr: bad arguments")
+
+
+def fill_uniform(rows, cols, ld, stride, batch, seed, role, item_offset=0) -> np.ndarray:
+    n = stride * (batch - 1) + ld * (cols - 1) + rows if batch and rows and cols else 0
+    out = np.zeros(max(n, 0), dtype=np.float64)
+    if n:
+        oracle_lib().oracle_fill_uniform(_p(out), rows, cols, ld, stride, batch, seed, role,
+                                         item_offset)
+    return out
+
+
+def check_bound(order, opA, opB, m, n, k, beta, A, lda, B, ldb, C0, Cm, Cref, ldc):
+    """(violations, max err/bound) of BASELINE's componentwise bound for one item."""
+    ratio = C.c_double(0.0)
+    bad = oracle_lib().oracle_check_bound(order.encode(), opA.encode(), opB.encode(), m, n, k,
+                                          float(beta), _p(A), lda, _p(B), ldb,
+                                          _p(C0) if C0 is not None else None, _p(Cm), _p(Cref),
+                                          ldc, C.byref(ratio))
+    return int(bad), float(ratio.value)
+
+
+# --------------------------------------------------------------- reference
+def ref_gemm_naive_raw(a, b, c, m, k, n, accumulate, flops: Optional[np.ndarray] = None):
+    fl = C.c_uint64(int(flops[0]) if flops is not None else 0)
+    ref_lib().ref_gemm_naive_raw(_p(a), _p(b), _p(c), m, k, n, int(bool(accumulate)),
+                                 C.byref(fl) if flops is not None else None)
+    if flops is not None:
+        flops[0] = fl.value
+
+
+def ref_dgemm_colmajor(opA, opB, m, n, k, accumulate, A, lda, sA, B, ldb, sB, Cm, ldc, sC, batch,
+                       threads=1):
+    rc = ref_lib().ref_dgemm_colmajor_strided(opA.encode(), opB.encode(), m, n, k,
+                                              int(bool(accumulate)), _p(A), lda, sA, _p(B), ldb,
+                                              sB, _p(Cm), ldc, sC, batch, threads)
+    if rc != 0:
+        raise ValueError("ref_dgemm_colmajor_strided: bad arguments")
+
+
+def ref_dgemm_colmajor_ptr(opA, opB, m, n, k, A, lda, B, ldb, Cs, ldc, accumulate, threads=1):
+    batch = len(m)
+    keep = [_arr64(x) for x in (m, n, k, lda, ldb, ldc)]
+    pa = (vp * batch)(*[_p(x) for x in A])
+    pb = (vp * batch)(*[_p(x) for x in B])
+    pc = (vp * batch)(*[_p(x) for x in Cs])
+    ref_lib().ref_dgemm_colmajor_ptr(opA.encode(), opB.encode(), batch, keep[0][1], keep[1][1],
+                                     keep[2][1], pa, keep[3][1], pb, keep[4][1], pc, keep[5][1],
+                                     int(bool(accumulate)), threads)
+
+
+def ref_rowmajor_batched(a, b, c, m, k, n, accumulate, batch, threads=1):
+    ref_lib().ref_gemm_rowmajor_batched(_p(a), _p(b), _p(c), m, k, n, int(bool(accumulate)),
+                                        batch, threads)
+
+
+def ref_dense_gemm_naive_error(ar, ac, br, bc, orow, ocol) -> Optional[str]:
+    buf = C.create_string_buffer(256)
+    if ref_lib().ref_dense_gemm_naive_error(ar, ac, br, bc, orow, ocol, buf, 256):
+        return buf.value.decode()
+    return None

@@ -1,0 +1,148 @@
+// ref_shim.cpp — builds the UNMODIFIED reference oracle into oracle/_ref/.
+//
+// TEST INFRASTRUCTURE ONLY: the reference itself, compiled from its own header
+// (/root/reference/proj/include/lrbatch/dense.hpp) by the top-level Makefile's
+// `ref` target, to pin the C restatement (oracle/lrb_oracle.c), to generate
+// the golden vectors under tests/golden/, and as the CPU baseline
+// (`cpu_baseline.kind = "reference"`, `bench.py --impl reference`). No
+// reference source is copied into this repository; this file only includes it.
+#include <lrbatch/dense.hpp>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+namespace {
+
+bool is_t(char o) { return o == 'T' || o == 't'; }
+
+// One column-major item through the reference primitive: the
+// column-major product C = op(A) op(B) has the bytes of the row-major
+// C^T = op(B)^T op(A)^T, so the reference is called as
+// gemm_naive_raw(op(B)^T, op(A)^T, C^T, n, k, m, accumulate) with operand
+// copies only where the stored layout is not already that row-major one
+// (transposes, padded leading dimensions). Per-entry order is unchanged.
+void colmajor_item(char opA, char opB, int64_t m, int64_t n, int64_t k, bool acc, const double* A,
+                   int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                   std::vector<double>& sa, std::vector<double>& sb, std::vector<double>& sc) {
+  // a' = op(B)^T as row-major n x k: a'[j*k + p] = op(B)(p, j)
+  const double* ap;
+  if (!is_t(opB) && ldb == k) {
+    ap = B;  // column-major k x n with ld k == row-major n x k
+  } else {
+    sa.resize(size_t(n * k));
+    for (int64_t j = 0; j < n; ++j)
+      for (int64_t p = 0; p < k; ++p)
+        sa[size_t(j * k + p)] = is_t(opB) ? B[j + p * ldb] : B[p + j * ldb];
+    ap = sa.data();
+  }
+  // b' = op(A)^T as row-major k x m: b'[p*m + i] = op(A)(i, p)
+  const double* bp;
+  if (!is_t(opA) && lda == m) {
+    bp = A;
+  } else {
+    sb.resize(size_t(k * m));
+    for (int64_t p = 0; p < k; ++p)
+      for (int64_t i = 0; i < m; ++i)
+        sb[size_t(p * m + i)] = is_t(opA) ? A[p + i * lda] : A[i + p * lda];
+    bp = sb.data();
+  }
+  if (ldc == m) {
+    lrbatch::gemm_naive_raw(ap, bp, C, size_t(n), size_t(k), size_t(m), acc);
+  } else {
+    sc.assign(size_t(n * m), 0.0);
+    if (acc)
+      for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i < m; ++i) sc[size_t(j * m + i)] = C[i + j * ldc];
+    lrbatch::gemm_naive_raw(ap, bp, sc.data(), size_t(n), size_t(k), size_t(m), acc);
+    for (int64_t j = 0; j < n; ++j)
+      for (int64_t i = 0; i < m; ++i) C[i + j * ldc] = sc[size_t(j * m + i)];
+  }
+}
+
+template <class Body>
+void fan_out(int64_t batch, int threads, Body body) {
+  // contiguous split, as naive_multiply_batch (reference bench.hpp:59-76)
+  int64_t workers = std::max<int64_t>(1, std::min<int64_t>(threads, batch));
+  if (workers == 1) {
+    body(int64_t(0), batch);
+    return;
+  }
+  const int64_t per = (batch + workers - 1) / workers;
+  std::vector<std::thread> pool;
+  for (int64_t w = 1; w < workers; ++w) {
+    const int64_t b = std::min(w * per, batch), e = std::min(b + per, batch);
+    pool.emplace_back(body, b, e);
+  }
+  body(int64_t(0), std::min(per, batch));
+  for (auto& t : pool) t.join();
+}
+
+}  // namespace
+
+extern "C" {
+
+// the reference primitive itself
+void ref_gemm_naive_raw(const double* a, const double* b, double* c, size_t m, size_t k, size_t n,
+                        int accumulate, uint64_t* flops) {
+  lrbatch::gemm_naive_raw(a, b, c, m, k, n, accumulate != 0, flops);
+}
+
+// row-major strided batch exactly as the reference packs LowRankBatch roles
+// (low_rank.hpp:147-158): one gemm_naive_raw per item
+void ref_gemm_rowmajor_batched(const double* a, const double* b, double* c, size_t m, size_t k,
+                               size_t n, int accumulate, int64_t batch, int threads) {
+  fan_out(batch, threads, [&](int64_t b0, int64_t e0) {
+    for (int64_t it = b0; it < e0; ++it)
+      lrbatch::gemm_naive_raw(a + it * m * k, b + it * k * n, c + it * m * n, m, k, n,
+                              accumulate != 0);
+  });
+}
+
+// column-major strided batch through the reference primitive (operand swap)
+int ref_dgemm_colmajor_strided(char opA, char opB, int64_t m, int64_t n, int64_t k, int accumulate,
+                               const double* A, int64_t lda, int64_t sA, const double* B,
+                               int64_t ldb, int64_t sB, double* C, int64_t ldc, int64_t sC,
+                               int64_t batch, int threads) {
+  if (m < 0 || n < 0 || k < 0 || batch < 0) return -1;
+  fan_out(batch, threads, [&](int64_t b0, int64_t e0) {
+    std::vector<double> sa, sb, sc;
+    for (int64_t it = b0; it < e0; ++it)
+      colmajor_item(opA, opB, m, n, k, accumulate != 0, A + it * sA, lda, B + it * sB, ldb,
+                    C + it * sC, ldc, sa, sb, sc);
+  });
+  return 0;
+}
+
+// column-major pointer-array batch through the reference primitive
+int ref_dgemm_colmajor_ptr(char opA, char opB, int64_t batch, const int64_t* m, const int64_t* n,
+                           const int64_t* k, const double* const* A, const int64_t* lda,
+                           const double* const* B, const int64_t* ldb, double* const* C,
+                           const int64_t* ldc, int accumulate, int threads) {
+  fan_out(batch, threads, [&](int64_t b0, int64_t e0) {
+    std::vector<double> sa, sb, sc;
+    for (int64_t it = b0; it < e0; ++it)
+      colmajor_item(opA, opB, m[it], n[it], k[it], accumulate != 0, A[it], lda[it], B[it], ldb[it],
+                    C[it], ldc[it], sa, sb, sc);
+  });
+  return 0;
+}
+
+// dense_gemm_naive's ShapeError text for shapes (ar x ac) * (br x bc) with an
+// (or x oc) output; returns 1 and fills buf when it throws, else 0
+int ref_dense_gemm_naive_error(size_t ar, size_t ac, size_t br, size_t bc, size_t orow, size_t ocol,
+                               char* buf, size_t buflen) {
+  try {
+    lrbatch::DenseBlock a(ar, ac), b(br, bc), out(orow, ocol);
+    lrbatch::dense_gemm_naive(a, b, out, false);
+  } catch (const lrbatch::ShapeError& e) {
+    std::strncpy(buf, e.what(), buflen - 1);
+    buf[buflen - 1] = 0;
+    return 1;
+  }
+  return 0;
+}
+
+}  // extern "C"

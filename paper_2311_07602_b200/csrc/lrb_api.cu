@@ -1,0 +1,801 @@
+// lrb_api.cu — the extern "C" boundary (include/lrb.h): context, validation,
+// column-major normalisation, selector, strided and pointer-array launches,
+// the pipelined host-buffer path and the shard planner.
+//
+// Reference interfaces replaced (see include/lrb.h for the per-call list):
+//   gemm_naive_raw        proj/include/lrbatch/dense.hpp:43-56
+//   dense_gemm_naive      proj/include/lrbatch/dense.hpp:58-77 (ShapeError text)
+//   make_packing_plan     proj/include/lrbatch/plan.hpp:66-100 (selector role)
+//   naive_multiply_batch  proj/include/lrbatch/bench.hpp:55-77 (contiguous split)
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <new>
+
+#include "lrb_dispatch.cuh"
+#include "lrb_internal.h"
+
+// ===================================================================== errors
+namespace {
+thread_local std::string t_last_error;
+}
+
+namespace lrb {
+
+void set_error(lrb_ctx* ctx, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  t_last_error = buf;
+  if (ctx) ctx->err = buf;
+}
+
+lrb_status fail(lrb_ctx* ctx, lrb_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  t_last_error = buf;
+  if (ctx) ctx->err = buf;
+  return st;
+}
+
+lrb_status cuda_fail(lrb_ctx* ctx, cudaError_t e, const char* where) {
+  cudaGetLastError();  // clear sticky-free errors
+  lrb_status st = (e == cudaErrorMemoryAllocation) ? LRB_ERR_CAPACITY : LRB_ERR_CUDA;
+  return fail(ctx, st, "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+lrb_status bind(lrb_ctx* ctx) {
+  if (!ctx) return fail(nullptr, LRB_ERR_ARG, "null lrb_ctx");
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  return LRB_OK;
+}
+
+// ============================================================ variant table
+struct VariantMeta {
+  const char* name;
+  int mb, nb, kb, stages, threads, minb;
+  size_t smem;
+};
+
+#define LRB_X(id, nm, ...)                                                                  \
+  {VariantTraits<id>::name, VariantTraits<id>::Cfg<false, false>::MB,                       \
+   VariantTraits<id>::Cfg<false, false>::NB, VariantTraits<id>::Cfg<false, false>::KB,      \
+   VariantTraits<id>::Cfg<false, false>::STAGES, VariantTraits<id>::Cfg<false, false>::THREADS, \
+   VariantTraits<id>::Cfg<false, false>::MINB, VariantTraits<id>::Cfg<false, false>::SMEM_BYTES},
+static const VariantMeta kVariants[LRB_NUM_VARIANTS] = {LRB_VARIANT_LIST(LRB_X)};
+#undef LRB_X
+
+#define LRB_X(id, ...) &launch_variant<id>,
+static const LaunchFn kLaunch[LRB_NUM_VARIANTS] = {LRB_VARIANT_LIST(LRB_X)};
+#undef LRB_X
+
+// Measured on this pool's B200 (tools/microbench/fp64_peaks.cu, profiles/):
+// DFMA and DMMA both 36.9 TFLOP/s; HBM copy 6553.6 GB/s (MEASURED_PEAKS.json).
+constexpr double kFp64PeakFlops = 36.9e12;
+constexpr double kHbmBytesPerS = 6553.6e9;
+
+// Automatic choice on the column-major view (m x n output, inner k).
+int auto_variant(int64_t m, int64_t n) {
+  if (n <= 64 && n <= m) {
+    if (n <= 8) return LRB_V_N8;
+    if (n <= 16) return LRB_V_N16;
+    if (n <= 32) return LRB_V_N32;
+    return LRB_V_N64;
+  }
+  if (m <= 64 && m < n) {
+    if (m <= 8) return LRB_V_M8;
+    if (m <= 16) return LRB_V_M16;
+    if (m <= 32) return LRB_V_M32;
+    return LRB_V_M64;
+  }
+  return LRB_V_SQ;
+}
+
+int env_variant() {
+  const char* s = std::getenv("LRB_VARIANT");
+  if (!s || !*s) return -1;
+  return lrb_variant_from_name(s);
+}
+
+int choose_variant(const lrb_ctx* ctx, int64_t m, int64_t n) {
+  if (ctx && ctx->variant_override >= 0) return ctx->variant_override;
+  int v = env_variant();
+  if (v >= 0) return v;
+  return auto_variant(m, n);
+}
+
+// ============================================================ normalisation
+struct Gemm {  // column-major view
+  int a_t, b_t;
+  int64_t m, n, k;
+  const double* A;
+  int64_t lda, sA;
+  const double* B;
+  int64_t ldb, sB;
+  double* C;
+  int64_t ldc, sC;
+};
+
+bool is_order(char o) { return o == 'C' || o == 'c' || o == 'R' || o == 'r'; }
+bool is_op(char o) { return o == 'N' || o == 'n' || o == 'T' || o == 't'; }
+bool row_major(char o) { return o == 'R' || o == 'r'; }
+bool trans(char o) { return o == 'T' || o == 't'; }
+
+// stored shape (rows x cols, in the caller's order) of each operand
+struct Stored {
+  int64_t rows, cols;
+};
+Stored stored_a(char opA, int64_t m, int64_t k) { return trans(opA) ? Stored{k, m} : Stored{m, k}; }
+Stored stored_b(char opB, int64_t k, int64_t n) { return trans(opB) ? Stored{n, k} : Stored{k, n}; }
+
+int64_t min_ld(char order, Stored s) {
+  return std::max<int64_t>(1, row_major(order) ? s.cols : s.rows);
+}
+// elements spanned by one stored matrix with leading dimension ld
+int64_t footprint(char order, Stored s, int64_t ld) {
+  if (s.rows == 0 || s.cols == 0) return 0;
+  return row_major(order) ? (s.rows - 1) * ld + s.cols : (s.cols - 1) * ld + s.rows;
+}
+
+lrb_status validate(lrb_ctx* ctx, const char* fn, char order, char opA, char opB, int64_t m,
+                    int64_t n, int64_t k, double beta, const void* A, int64_t lda, int64_t sA,
+                    const void* B, int64_t ldb, int64_t sB, const void* C, int64_t ldc,
+                    int64_t sC, int64_t batch) {
+  if (!is_order(order))
+    return fail(ctx, LRB_ERR_ARG, "%s: order must be 'C' or 'R', got '%c'", fn, order);
+  if (!is_op(opA)) return fail(ctx, LRB_ERR_ARG, "%s: opA must be 'N' or 'T', got '%c'", fn, opA);
+  if (!is_op(opB)) return fail(ctx, LRB_ERR_ARG, "%s: opB must be 'N' or 'T', got '%c'", fn, opB);
+  if (m < 0 || n < 0 || k < 0 || batch < 0)
+    return fail(ctx, LRB_ERR_SHAPE,
+                "%s: m, n, k and batch must be >= 0, got m=%lld n=%lld k=%lld batch=%lld", fn,
+                (long long)m, (long long)n, (long long)k, (long long)batch);
+  if (!(beta == 0.0 || beta == 1.0))
+    return fail(ctx, LRB_ERR_UNSUPPORTED,
+                "%s: beta must be 0 or 1 (the reference 'accumulate' flag), got %g", fn, beta);
+  if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX)
+    return fail(ctx, LRB_ERR_UNSUPPORTED, "%s: dimensions above 2^31-1 are not supported", fn);
+  const char* om = row_major(order) ? "row" : "column";
+  const Stored a = stored_a(opA, m, k), b = stored_b(opB, k, n), c{m, n};
+  if (lda < min_ld(order, a))
+    return fail(ctx, LRB_ERR_SHAPE, "%s: lda is %lld but A is %lldx%lld (%s-major), needs >= %lld",
+                fn, (long long)lda, (long long)a.rows, (long long)a.cols, om,
+                (long long)min_ld(order, a));
+  if (ldb < min_ld(order, b))
+    return fail(ctx, LRB_ERR_SHAPE, "%s: ldb is %lld but B is %lldx%lld (%s-major), needs >= %lld",
+                fn, (long long)ldb, (long long)b.rows, (long long)b.cols, om,
+                (long long)min_ld(order, b));
+  if (ldc < min_ld(order, c))
+    return fail(ctx, LRB_ERR_SHAPE, "%s: ldc is %lld but C is %lldx%lld (%s-major), needs >= %lld",
+                fn, (long long)ldc, (long long)c.rows, (long long)c.cols, om,
+                (long long)min_ld(order, c));
+  if (sA < 0 || sB < 0 || sC < 0)
+    return fail(ctx, LRB_ERR_SHAPE, "%s: strides must be >= 0", fn);
+  const int64_t fc = footprint(order, c, ldc);
+  if (batch > 1 && fc > 0 && sC < fc)
+    return fail(ctx, LRB_ERR_SHAPE,
+                "%s: strideC is %lld but each C item spans %lld elements (items would overlap)", fn,
+                (long long)sC, (long long)fc);
+  if (batch > 0 && m > 0 && n > 0) {
+    if (!C) return fail(ctx, LRB_ERR_ARG, "%s: C is null", fn);
+    if (k > 0 && (!A || !B)) return fail(ctx, LRB_ERR_ARG, "%s: A or B is null", fn);
+  }
+  return LRB_OK;
+}
+
+Gemm normalize(char order, char opA, char opB, int64_t m, int64_t n, int64_t k, const double* A,
+               int64_t lda, int64_t sA, const double* B, int64_t ldb, int64_t sB, double* C,
+               int64_t ldc, int64_t sC) {
+  Gemm g;
+  if (!row_major(order)) {
+    g = Gemm{trans(opA) ? 1 : 0, trans(opB) ? 1 : 0, m, n, k, A, lda, sA, B, ldb, sB, C, ldc, sC};
+  } else {
+    // row-major C = op(A) op(B)  <=>  column-major C^T = op(B)^T op(A)^T
+    g = Gemm{trans(opB) ? 1 : 0, trans(opA) ? 1 : 0, n, m, k, B, ldb, sB, A, lda, sA, C, ldc, sC};
+  }
+  return g;
+}
+
+lrb_status run_strided(lrb_ctx* ctx, const Gemm& g, int64_t batch, int beta_one,
+                       cudaStream_t stream, int* variant_used) {
+  if (batch == 0 || g.m == 0 || g.n == 0) return LRB_OK;
+  if (g.k == 0 && beta_one) return LRB_OK;  // C = C
+  const int v = choose_variant(ctx, g.m, g.n);
+  const VariantMeta& vm = kVariants[v];
+  const int64_t ti = (g.m + vm.mb - 1) / vm.mb, tj = (g.n + vm.nb - 1) / vm.nb;
+  if (ti * tj > INT32_MAX || ti * tj * batch > (int64_t(1) << 62))
+    return fail(ctx, LRB_ERR_UNSUPPORTED, "lrb: too many tiles (%lld per item)", (long long)(ti * tj));
+  StridedProblem p;
+  p.A = g.A;
+  p.B = g.B;
+  p.C = g.C;
+  p.lda = g.lda;
+  p.ldb = g.ldb;
+  p.ldc = g.ldc;
+  p.sA = g.sA;
+  p.sB = g.sB;
+  p.sC = g.sC;
+  p.m = int(g.m);
+  p.n = int(g.n);
+  p.k = int(g.k);
+  p.tiles_i = int(ti);
+  p.tiles_per_item = int(ti * tj);
+  p.num_tiles = ti * tj * batch;
+  LaunchInfo info{0, 0};
+  cudaError_t e = kLaunch[v](g.a_t, g.b_t, &p, nullptr, beta_one, ctx->device, ctx->sm_count,
+                             stream, &info);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "lrb_gemm_kernel launch");
+  if (info.grid > 0) ctx->launches.fetch_add(1, std::memory_order_relaxed);
+  if (variant_used) *variant_used = v;
+  return LRB_OK;
+}
+
+}  // namespace lrb
+
+using namespace lrb;
+
+// ================================================================ context
+extern "C" const char* lrb_version(void) { return LRB_VERSION_STRING; }
+
+extern "C" int lrb_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+extern "C" lrb_status lrb_create(int device, lrb_ctx** out) {
+  if (!out) return fail(nullptr, LRB_ERR_ARG, "lrb_create: out is null");
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return fail(nullptr, LRB_ERR_NO_DEVICE, "lrb_create: no CUDA device (%s)",
+                e == cudaSuccess ? "device count 0" : cudaGetErrorString(e));
+  }
+  if (device < 0 || device >= n)
+    return fail(nullptr, LRB_ERR_NO_DEVICE, "lrb_create: device %d out of range [0,%d)", device, n);
+  cudaDeviceProp prop;
+  e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaGetDeviceProperties");
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(nullptr, LRB_ERR_NO_DEVICE,
+                "lrb_create: device %d is sm_%d%d; this build is sm_100a (B200) only", device,
+                prop.major, prop.minor);
+  lrb_ctx* ctx = new (std::nothrow) lrb_ctx;
+  if (!ctx) return fail(nullptr, LRB_ERR_CAPACITY, "lrb_create: out of host memory");
+  ctx->device = device;
+  ctx->sm_count = prop.multiProcessorCount;
+  ctx->l2_bytes = size_t(prop.l2CacheSize);
+  e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return cuda_fail(nullptr, e, "cudaSetDevice");
+  }
+  for (int i = 0; i < lrb_ctx::kLanes; ++i) {
+    e = cudaStreamCreateWithFlags(&ctx->lane_stream[i], cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      lrb_destroy(ctx);
+      return cuda_fail(nullptr, e, "cudaStreamCreate");
+    }
+  }
+  *out = ctx;
+  return LRB_OK;
+}
+
+extern "C" lrb_status lrb_destroy(lrb_ctx* ctx) {
+  if (!ctx) return LRB_OK;
+  cudaSetDevice(ctx->device);
+  for (int i = 0; i < lrb_ctx::kLanes; ++i) {
+    if (ctx->lane_stream[i]) {
+      cudaStreamSynchronize(ctx->lane_stream[i]);
+      cudaStreamDestroy(ctx->lane_stream[i]);
+    }
+    if (ctx->lane_buf[i]) cudaFree(ctx->lane_buf[i]);
+  }
+  if (ctx->flush_buf) cudaFree(ctx->flush_buf);
+  delete ctx;
+  return LRB_OK;
+}
+
+extern "C" const char* lrb_last_error(const lrb_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : t_last_error.c_str();
+}
+extern "C" int lrb_ctx_device(const lrb_ctx* ctx) { return ctx ? ctx->device : -1; }
+extern "C" int lrb_ctx_sm_count(const lrb_ctx* ctx) { return ctx ? ctx->sm_count : 0; }
+extern "C" uint64_t lrb_launch_count(const lrb_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
+
+// ===================================================== memory / streams / events
+extern "C" lrb_status lrb_malloc(lrb_ctx* ctx, size_t bytes, void** dptr) {
+  if (!dptr) return fail(ctx, LRB_ERR_ARG, "lrb_malloc: dptr is null");
+  *dptr = nullptr;
+  lrb_status st = bind(ctx);
+  if (st) return st;
+  if (bytes == 0) return LRB_OK;
+  LRB_CUDA_TRY(ctx, cudaMalloc(dptr, bytes));
+  return LRB_OK;
+}
+extern "C" lrb_status lrb_free(lrb_ctx* ctx, void* dptr) {
+  lrb_status st = bind(ctx);
+  if (st) return st;
+  if (dptr) LRB_CUDA_TRY(ctx, cudaFree(dptr));
+  return LRB_OK;
+}
+extern "C" lrb_status lrb_host_alloc(lrb_ctx* ctx, size_t bytes, void** hptr) {
+  if (!hptr) return fail(ctx, LRB_ERR_ARG, "lrb_host_alloc: hptr is null");
+  *hptr = nullptr;
+  lrb_status st = bind(ctx);
+  if (st) return st;
+  if (bytes == 0) return LRB_OK;
+  LRB_CUDA_TRY(ctx, cudaMallocHost(hptr, bytes));
+  return LRB_OK;
+}
+extern "C" lrb_status lrb_host_free(lrb_ctx* ctx, void* hptr) {
+  lrb_status st = bind(ctx);
+  if (st) return st;
+  if (hptr) LRB_CUDA_TRY(ctx, cudaFreeHost(hptr));
+  return LRB_OK;
+}
+extern "C" lrb_status lrb_memcpy_h2d(lrb_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  lrb_status st = bind(ctx);
+  if (st) return st;
+  if (bytes) LRB_CUDA_TRY(ctx, cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+  return LRB_OK;
+}
+extern "C" lrb_status lrb_memcpy_d2h(lrb_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  lrb_status st = bind(ctx);
+  if (st) return st;
+  if (bytes) LRB_CUDA_TRY(ctx, cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+  return LRB_OK;
+}
+extern "C" lrb_status lrb_memset(lrb_ctx* ctx, void* dptr, int value, size_t bytes) {
+  lrb_status st = bind(ctx);
+  if (st) return st;
+  if (bytes) LRB_CUDA_TRY(ctx, cudaMemset(dptr, value, bytes));
+  return LRB_OK;
+}
+extern "C" lrb_status lrb_stream_create(lrb_ctx* ctx, void** stream) {
+  if (!stream) return fail(ctx, LRB_ERR_ARG, "lrb_stream_create: stream is null");
+  lrb_status st = bind(ctx);
+  if (st) return st;
+  cudaStream_t s;
+  LRB_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  *stream = s;
+  return LRB_OK;
+}
+extern "C" lrb_status lrb_stream_destroy(lrb_ctx* ctx, void* stream) {
+  lrb_status st = bind(ctx);
+  if (st) return st;
+  if (stream) LRB_CUDA_TRY(ctx, cudaStreamDestroy(static_cast<cudaStream_t>(stream)));
+  return LRB_OK;
+}
+extern "C" lrb_status lrb_stream_sync(lrb_ctx* ctx, void* stream) {
+  lrb_status st = bind(ctx);
+  if (st) return st;
+  LRB_CUDA_TRY(ctx, cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  return LRB_OK;
+}
+extern "C" lrb_status lrb_device_sync(lrb_ctx* ctx) {
+  lrb_status st = bind(ctx);
+  if (st) return st;
+  LRB_CUDA_TRY(ctx, cudaDeviceSynchronize());
+  return LRB_OK;
+}
+extern "C" lrb_status lrb_mem_info(lrb_ctx* ctx, size_t* free_bytes, size_t* total_bytes) {
+  lrb_status st = bind(ctx);
+  if (st) return st;
+  size_t f = 0, t = 0;
+  LRB_CUDA_TRY(ctx, cudaMemGetInfo(&f, &t));
+  if (free_bytes) *free_bytes = f;
+  if (total_bytes) *total_bytes = t;
+  return LRB_OK;
+}
+extern "C" lrb_status lrb_event_create(lrb_ctx* ctx, void** ev) {
+  if (!ev) return fail(ctx, LRB_ERR_ARG, "lrb_event_create: ev is null");
+  lrb_status st = bind(ctx);
+  if (st) return st;
+  cudaEvent_t e;
+  LRB_CUDA_TRY(ctx, cudaEventCreate(&e));
+  *ev = e;
+  return LRB_OK;
+}
+extern "C" lrb_status lrb_event_destroy(lrb_ctx* ctx, void* ev) {
+  lrb_status st = bind(ctx);
+  if (st) return st;
+  if (ev) LRB_CUDA_TRY(ctx, cudaEventDestroy(static_cast<cudaEvent_t>(ev)));
+  return LRB_OK;
+}
+extern "C" lrb_status lrb_event_record(lrb_ctx* ctx, void* ev, void* stream) {
+  lrb_status st = bind(ctx);
+  if (st) return st;
+  LRB_CUDA_TRY(ctx, cudaEventRecord(static_cast<cudaEvent_t>(ev), static_cast<cudaStream_t>(stream)));
+  return LRB_OK;
+}
+extern "C" lrb_status lrb_event_elapsed_ms(lrb_ctx* ctx, void* e0, void* e1, float* ms) {
+  if (!ms) return fail(ctx, LRB_ERR_ARG, "lrb_event_elapsed_ms: ms is null");
+  lrb_status st = bind(ctx);
+  if (st) return st;
+  LRB_CUDA_TRY(ctx, cudaEventSynchronize(static_cast<cudaEvent_t>(e1)));
+  LRB_CUDA_TRY(ctx, cudaEventElapsedTime(ms, static_cast<cudaEvent_t>(e0), static_cast<cudaEvent_t>(e1)));
+  return LRB_OK;
+}
+extern "C" lrb_status lrb_l2_flush(lrb_ctx* ctx, void* stream) {
+  lrb_status st = bind(ctx);
+  if (st) return st;
+  if (!ctx->flush_buf) {
+    ctx->flush_bytes = std::max<size_t>(2 * ctx->l2_bytes, size_t(256) << 20);
+    LRB_CUDA_TRY(ctx, cudaMalloc(&ctx->flush_buf, ctx->flush_bytes));
+  }
+  LRB_CUDA_TRY(ctx, cudaMemsetAsync(ctx->flush_buf, 0, ctx->flush_bytes,
+                                    static_cast<cudaStream_t>(stream)));
+  return LRB_OK;
+}
+
+// ============================================================ selector / planner
+extern "C" int lrb_variant_count(void) { return LRB_NUM_VARIANTS; }
+extern "C" const char* lrb_variant_name(int v) {
+  return (v >= 0 && v < LRB_NUM_VARIANTS) ? kVariants[v].name : nullptr;
+}
+extern "C" int lrb_variant_from_name(const char* name) {
+  if (!name) return -1;
+  for (int v = 0; v < LRB_NUM_VARIANTS; ++v)
+    if (std::strcmp(name, kVariants[v].name) == 0) return v;
+  return -1;
+}
+extern "C" lrb_status lrb_set_variant_override(lrb_ctx* ctx, int variant) {
+  if (!ctx) return fail(nullptr, LRB_ERR_ARG, "lrb_set_variant_override: null ctx");
+  if (variant < -1 || variant >= LRB_NUM_VARIANTS)
+    return fail(ctx, LRB_ERR_ARG, "lrb_set_variant_override: variant %d out of range", variant);
+  ctx->variant_override = variant;
+  return LRB_OK;
+}
+
+extern "C" double lrb_item_flops(int64_t m, int64_t n, int64_t k) {
+  return 2.0 * double(m) * double(n) * double(k);
+}
+extern "C" double lrb_item_bytes(int64_t m, int64_t n, int64_t k, double beta) {
+  return 8.0 * (double(m) * k + double(k) * n + double(m) * n * (beta != 0.0 ? 2.0 : 1.0));
+}
+
+extern "C" lrb_status lrb_select(const lrb_ctx* ctx, char order, char opA, char opB, int64_t m,
+                                 int64_t n, int64_t k, int64_t batch, lrb_selection* out) {
+  lrb_ctx* mctx = const_cast<lrb_ctx*>(ctx);
+  if (!out) return fail(mctx, LRB_ERR_ARG, "lrb_select: out is null");
+  if (!is_order(order) || !is_op(opA) || !is_op(opB))
+    return fail(mctx, LRB_ERR_ARG, "lrb_select: bad order/op character");
+  if (m < 0 || n < 0 || k < 0 || batch < 0)
+    return fail(mctx, LRB_ERR_SHAPE, "lrb_select: negative dimension");
+  const int64_t cm = row_major(order) ? n : m, cn = row_major(order) ? m : n;
+  const int v = choose_variant(ctx, cm, cn);
+  const VariantMeta& vm = kVariants[v];
+  std::memset(out, 0, sizeof(*out));
+  out->variant = v;
+  out->tile_m = vm.mb;
+  out->tile_n = vm.nb;
+  out->tile_k = vm.kb;
+  out->stages = vm.stages;
+  out->threads = vm.threads;
+  out->ctas_per_sm = vm.minb;
+  const int64_t ti = cm ? (cm + vm.mb - 1) / vm.mb : 0, tj = cn ? (cn + vm.nb - 1) / vm.nb : 0;
+  out->tiles = ti * tj * batch;
+  const int64_t sms = ctx ? ctx->sm_count : 148;
+  out->grid = std::min<int64_t>(out->tiles, sms * vm.minb);
+  const double bytes = lrb_item_bytes(m, n, k, 0.0);
+  out->intensity = bytes > 0 ? lrb_item_flops(m, n, k) / bytes : 0.0;
+  out->fp64_bound = out->intensity >= kFp64PeakFlops / kHbmBytesPerS ? 1 : 0;
+  std::snprintf(out->name, sizeof(out->name), "%s", vm.name);
+  return LRB_OK;
+}
+
+extern "C" lrb_status lrb_shard_plan(int64_t batch, const double* cost, int nparts, int64_t* begin) {
+  if (!begin) return fail(nullptr, LRB_ERR_ARG, "lrb_shard_plan: begin is null");
+  if (batch < 0) return fail(nullptr, LRB_ERR_SHAPE, "lrb_shard_plan: batch must be >= 0");
+  if (nparts < 1) return fail(nullptr, LRB_ERR_ARG, "lrb_shard_plan: nparts must be >= 1");
+  if (!cost) {
+    // the reference's contiguous fan-out (bench.hpp:69-75): per = ceil(batch / parts)
+    const int64_t per = (batch + nparts - 1) / nparts;
+    for (int g = 0; g <= nparts; ++g) begin[g] = std::min<int64_t>(int64_t(g) * per, batch);
+    return LRB_OK;
+  }
+  double total = 0.0;
+  for (int64_t i = 0; i < batch; ++i) {
+    if (!(cost[i] >= 0.0) || !std::isfinite(cost[i]))
+      return fail(nullptr, LRB_ERR_ARG, "lrb_shard_plan: cost[%lld] is negative or not finite",
+                  (long long)i);
+    total += cost[i];
+  }
+  begin[0] = 0;
+  int64_t idx = 0;
+  double prefix = 0.0;
+  for (int g = 1; g < nparts; ++g) {
+    const double target = total * double(g) / double(nparts);
+    // first cut index whose prefix cost reaches the target (closest cut)
+    while (idx < batch && prefix + cost[idx] <= target) prefix += cost[idx++];
+    if (idx < batch && (target - prefix) > (prefix + cost[idx] - target)) prefix += cost[idx++];
+    begin[g] = std::max(idx, begin[g - 1]);
+  }
+  begin[nparts] = batch;
+  return LRB_OK;
+}
+
+// ================================================================ strided
+extern "C" lrb_status lrb_dgemm_strided_batched(lrb_ctx* ctx, char order, char opA, char opB,
+                                                int64_t m, int64_t n, int64_t k, double beta,
+                                                const double* A, int64_t lda, int64_t strideA,
+                                                const double* B, int64_t ldb, int64_t strideB,
+                                                double* C, int64_t ldc, int64_t strideC,
+                                                int64_t batch, void* stream) {
+  static const char* fn = "lrb_dgemm_strided_batched";
+  lrb_status st = validate(ctx, fn, order, opA, opB, m, n, k, beta, A, lda, strideA, B, ldb,
+                           strideB, C, ldc, strideC, batch);
+  if (st) return st;
+  if (!ctx) return fail(nullptr, LRB_ERR_ARG, "%s: null ctx", fn);
+  st = bind(ctx);
+  if (st) return st;
+  const Gemm g = normalize(order, opA, opB, m, n, k, A, lda, strideA, B, ldb, strideB, C, ldc, strideC);
+  return run_strided(ctx, g, batch, beta == 1.0, static_cast<cudaStream_t>(stream), nullptr);
+}
+
+// ========================================================== pointer array
+struct lrb_ptr_plan {
+  int device = 0;
+  int a_t = 0, b_t = 0, beta_one = 0;
+  int64_t batch = 0;
+  ItemDesc* d_items = nullptr;
+  uint64_t* d_tiles = nullptr;
+  struct Group {
+    int variant;
+    int64_t offset, count;
+  };
+  std::vector<Group> groups;
+};
+
+extern "C" lrb_status lrb_ptr_plan_create(lrb_ctx* ctx, char order, char opA, char opB,
+                                          int64_t batch, const int64_t* m, const int64_t* n,
+                                          const int64_t* k, const double* const* A,
+                                          const int64_t* lda, const double* const* B,
+                                          const int64_t* ldb, double* const* C,
+                                          const int64_t* ldc, double beta, lrb_ptr_plan** out) {
+  static const char* fn = "lrb_ptr_plan_create";
+  if (!ctx) return fail(nullptr, LRB_ERR_ARG, "%s: null ctx", fn);
+  if (!out) return fail(ctx, LRB_ERR_ARG, "%s: out is null", fn);
+  *out = nullptr;
+  if (batch < 0) return fail(ctx, LRB_ERR_SHAPE, "%s: batch must be >= 0", fn);
+  if (batch >= (int64_t(1) << 32)) return fail(ctx, LRB_ERR_UNSUPPORTED, "%s: batch >= 2^32", fn);
+  if (batch > 0 && (!m || !n || !k || !A || !B || !C || !lda || !ldb || !ldc))
+    return fail(ctx, LRB_ERR_ARG, "%s: a descriptor array is null", fn);
+  lrb_status st = bind(ctx);
+  if (st) return st;
+
+  std::vector<ItemDesc> items(static_cast<size_t>(batch));
+  std::vector<std::vector<int64_t>> per_variant(LRB_NUM_VARIANTS);  // item ids
+  int a_t = 0, b_t = 0;
+  for (int64_t i = 0; i < batch; ++i) {
+    char where[64];
+    std::snprintf(where, sizeof(where), "%s: item %lld", fn, (long long)i);
+    st = validate(ctx, where, order, opA, opB, m[i], n[i], k[i], beta, A[i], lda[i], 0, B[i],
+                  ldb[i], 0, C[i], ldc[i], 0, 1);
+    if (st) return st;
+    const Gemm g = normalize(order, opA, opB, m[i], n[i], k[i], A[i], lda[i], 0, B[i], ldb[i], 0,
+                             C[i], ldc[i], 0);
+    a_t = g.a_t;
+    b_t = g.b_t;
+    ItemDesc& d = items[size_t(i)];
+    d.A = g.A;
+    d.B = g.B;
+    d.C = g.C;
+    d.lda = g.lda;
+    d.ldb = g.ldb;
+    d.ldc = g.ldc;
+    d.m = int32_t(g.m);
+    d.n = int32_t(g.n);
+    d.k = int32_t(g.k);
+    d.pad = 0;
+    if (g.m == 0 || g.n == 0 || (g.k == 0 && beta == 1.0)) continue;
+    const int v = choose_variant(ctx, g.m, g.n);
+    const int64_t ti = (g.m + kVariants[v].mb - 1) / kVariants[v].mb;
+    const int64_t tj = (g.n + kVariants[v].nb - 1) / kVariants[v].nb;
+    if (ti > 0xFFFF || tj > 0xFFFF)
+      return fail(ctx, LRB_ERR_UNSUPPORTED, "%s: item %lld needs more than 65535 tiles per dim", fn,
+                  (long long)i);
+    per_variant[size_t(v)].push_back(i);
+  }
+  if (!is_order(order) || !is_op(opA) || !is_op(opB))
+    return fail(ctx, LRB_ERR_ARG, "%s: bad order/op character", fn);
+
+  auto* plan = new (std::nothrow) lrb_ptr_plan;
+  if (!plan) return fail(ctx, LRB_ERR_CAPACITY, "%s: out of host memory", fn);
+  plan->device = ctx->device;
+  plan->a_t = a_t;
+  plan->b_t = b_t;
+  plan->beta_one = beta == 1.0;
+  plan->batch = batch;
+  std::vector<uint64_t> tiles;
+  for (int v = 0; v < LRB_NUM_VARIANTS; ++v) {
+    auto& ids = per_variant[size_t(v)];
+    if (ids.empty()) continue;
+    // longest-k items first: the persistent grid then drains short tiles last
+    std::stable_sort(ids.begin(), ids.end(),
+                     [&](int64_t x, int64_t y) { return items[size_t(x)].k > items[size_t(y)].k; });
+    const int64_t off = int64_t(tiles.size());
+    for (int64_t id : ids) {
+      const ItemDesc& d = items[size_t(id)];
+      const int64_t ti = (d.m + kVariants[v].mb - 1) / kVariants[v].mb;
+      const int64_t tj = (d.n + kVariants[v].nb - 1) / kVariants[v].nb;
+      for (int64_t b = 0; b < tj; ++b)
+        for (int64_t a = 0; a < ti; ++a)
+          tiles.push_back((uint64_t(id) << 32) | (uint64_t(a) << 16) | uint64_t(b));
+    }
+    plan->groups.push_back({v, off, int64_t(tiles.size()) - off});
+  }
+  cudaError_t e;
+  if (batch > 0) {
+    e = cudaMalloc(&plan->d_items, sizeof(ItemDesc) * size_t(batch));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(plan->d_items, items.data(), sizeof(ItemDesc) * size_t(batch),
+                     cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      lrb_ptr_plan_destroy(ctx, plan);
+      return cuda_fail(ctx, e, "lrb_ptr_plan_create: descriptor upload");
+    }
+  }
+  if (!tiles.empty()) {
+    e = cudaMalloc(&plan->d_tiles, sizeof(uint64_t) * tiles.size());
+    if (e == cudaSuccess)
+      e = cudaMemcpy(plan->d_tiles, tiles.data(), sizeof(uint64_t) * tiles.size(),
+                     cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      lrb_ptr_plan_destroy(ctx, plan);
+      return cuda_fail(ctx, e, "lrb_ptr_plan_create: tile list upload");
+    }
+  }
+  *out = plan;
+  return LRB_OK;
+}
+
+extern "C" lrb_status lrb_ptr_plan_execute(lrb_ctx* ctx, const lrb_ptr_plan* plan, void* stream) {
+  if (!ctx || !plan) return fail(ctx, LRB_ERR_ARG, "lrb_ptr_plan_execute: null ctx or plan");
+  if (plan->device != ctx->device)
+    return fail(ctx, LRB_ERR_ARG, "lrb_ptr_plan_execute: plan built for device %d, ctx is device %d",
+                plan->device, ctx->device);
+  lrb_status st = bind(ctx);
+  if (st) return st;
+  for (const auto& grp : plan->groups) {
+    PtrProblem p{plan->d_items, plan->d_tiles + grp.offset, grp.count};
+    LaunchInfo info{0, 0};
+    cudaError_t e = kLaunch[grp.variant](plan->a_t, plan->b_t, nullptr, &p, plan->beta_one,
+                                         ctx->device, ctx->sm_count,
+                                         static_cast<cudaStream_t>(stream), &info);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "lrb_gemm_kernel (ptr) launch");
+    if (info.grid > 0) ctx->launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  return LRB_OK;
+}
+
+extern "C" int lrb_ptr_plan_launches(const lrb_ptr_plan* plan) {
+  return plan ? int(plan->groups.size()) : 0;
+}
+
+extern "C" lrb_status lrb_ptr_plan_destroy(lrb_ctx* ctx, lrb_ptr_plan* plan) {
+  if (!plan) return LRB_OK;
+  if (ctx) cudaSetDevice(ctx->device);
+  if (plan->d_items) cudaFree(plan->d_items);
+  if (plan->d_tiles) cudaFree(plan->d_tiles);
+  delete plan;
+  return LRB_OK;
+}
+
+extern "C" lrb_status lrb_dgemm_ptr_batched(lrb_ctx* ctx, char order, char opA, char opB,
+                                            int64_t batch, const int64_t* m, const int64_t* n,
+                                            const int64_t* k, const double* const* A,
+                                            const int64_t* lda, const double* const* B,
+                                            const int64_t* ldb, double* const* C,
+                                            const int64_t* ldc, double beta, void* stream) {
+  lrb_ptr_plan* plan = nullptr;
+  lrb_status st = lrb_ptr_plan_create(ctx, order, opA, opB, batch, m, n, k, A, lda, B, ldb, C, ldc,
+                                      beta, &plan);
+  if (st) return st;
+  st = lrb_ptr_plan_execute(ctx, plan, stream);
+  cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+  lrb_ptr_plan_destroy(ctx, plan);
+  if (st) return st;
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "lrb_dgemm_ptr_batched: stream sync");
+  return LRB_OK;
+}
+
+// ============================================================ host buffers
+namespace {
+int64_t span_elems(int64_t cnt, int64_t stride, int64_t fp) {
+  if (cnt <= 0 || fp == 0) return 0;
+  return (cnt - 1) * stride + fp;
+}
+int64_t round32(int64_t x) { return (x + 31) / 32 * 32; }
+}  // namespace
+
+extern "C" lrb_status lrb_dgemm_strided_batched_host(lrb_ctx* ctx, char order, char opA, char opB,
+                                                     int64_t m, int64_t n, int64_t k, double beta,
+                                                     const double* A, int64_t lda, int64_t sA,
+                                                     const double* B, int64_t ldb, int64_t sB,
+                                                     double* C, int64_t ldc, int64_t sC,
+                                                     int64_t batch) {
+  static const char* fn = "lrb_dgemm_strided_batched_host";
+  lrb_status st =
+      validate(ctx, fn, order, opA, opB, m, n, k, beta, A, lda, sA, B, ldb, sB, C, ldc, sC, batch);
+  if (st) return st;
+  if (!ctx) return fail(nullptr, LRB_ERR_ARG, "%s: null ctx", fn);
+  if (batch == 0 || m == 0 || n == 0) return LRB_OK;
+  const int beta_one = beta == 1.0;
+  if (k == 0 && beta_one) return LRB_OK;
+  st = bind(ctx);
+  if (st) return st;
+
+  const Stored sa = stored_a(opA, m, k), sb = stored_b(opB, k, n), sc{m, n};
+  const int64_t fA = footprint(order, sa, lda), fB = footprint(order, sb, ldb),
+                fC = footprint(order, sc, ldc);
+  // C must round-trip when it is read (beta = 1) or has gaps the kernel does not write
+  const bool c_dense = (fC == m * n) && (batch == 1 || sC == fC);
+  const bool upload_c = beta_one || !c_dense;
+
+  // chunk so that one lane's A + B + C spans stay near 256 MiB
+  const int64_t target = (int64_t(256) << 20) / 8;
+  const int64_t base = fA + fB + fC, incr = sA + sB + sC;
+  int64_t per_chunk = batch;
+  if (incr > 0) per_chunk = std::max<int64_t>(1, std::min<int64_t>(batch, (target - base) / incr + 1));
+  const int64_t need =
+      round32(span_elems(per_chunk, sA, fA)) + round32(span_elems(per_chunk, sB, fB)) +
+      round32(span_elems(per_chunk, sC, fC));
+  const int64_t nchunks = (batch + per_chunk - 1) / per_chunk;
+  const int lanes = int(std::min<int64_t>(lrb_ctx::kLanes, nchunks));
+  for (int l = 0; l < lanes; ++l) {
+    if (ctx->lane_bytes[l] < size_t(need) * 8) {
+      LRB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->lane_stream[l]));
+      if (ctx->lane_buf[l]) cudaFree(ctx->lane_buf[l]);
+      ctx->lane_buf[l] = nullptr;
+      ctx->lane_bytes[l] = 0;
+      LRB_CUDA_TRY(ctx, cudaMalloc(&ctx->lane_buf[l], size_t(need) * 8));
+      ctx->lane_bytes[l] = size_t(need) * 8;
+    }
+  }
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int l = int(c % lanes);
+    cudaStream_t s = ctx->lane_stream[l];
+    const int64_t c0 = c * per_chunk, cnt = std::min(per_chunk, batch - c0);
+    const int64_t nA = span_elems(cnt, sA, fA), nB = span_elems(cnt, sB, fB),
+                  nC = span_elems(cnt, sC, fC);
+    double* dA = ctx->lane_buf[l];
+    double* dB = dA + round32(span_elems(per_chunk, sA, fA));
+    double* dC = dB + round32(span_elems(per_chunk, sB, fB));
+    if (nA) LRB_CUDA_TRY(ctx, cudaMemcpyAsync(dA, A + c0 * sA, size_t(nA) * 8, cudaMemcpyHostToDevice, s));
+    if (nB) LRB_CUDA_TRY(ctx, cudaMemcpyAsync(dB, B + c0 * sB, size_t(nB) * 8, cudaMemcpyHostToDevice, s));
+    if (upload_c && nC)
+      LRB_CUDA_TRY(ctx, cudaMemcpyAsync(dC, C + c0 * sC, size_t(nC) * 8, cudaMemcpyHostToDevice, s));
+    const Gemm g = normalize(order, opA, opB, m, n, k, dA, lda, sA, dB, ldb, sB, dC, ldc, sC);
+    st = run_strided(ctx, g, cnt, beta_one, s, nullptr);
+    if (st) return st;
+    if (nC) LRB_CUDA_TRY(ctx, cudaMemcpyAsync(C + c0 * sC, dC, size_t(nC) * 8, cudaMemcpyDeviceToHost, s));
+  }
+  for (int l = 0; l < lanes; ++l) LRB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->lane_stream[l]));
+  return LRB_OK;
+}
+
+extern "C" lrb_status lrb_gemm_naive_raw(lrb_ctx* ctx, const double* a, const double* b, double* c,
+                                         size_t m, size_t k, size_t n, int accumulate,
+                                         uint64_t* flops) {
+  const int64_t lda = k ? int64_t(k) : 1, ldb = n ? int64_t(n) : 1, ldc = n ? int64_t(n) : 1;
+  lrb_status st = lrb_dgemm_strided_batched_host(ctx, 'R', 'N', 'N', int64_t(m), int64_t(n),
+                                                 int64_t(k), accumulate ? 1.0 : 0.0, a, lda, 0, b,
+                                                 ldb, 0, c, ldc, 0, 1);
+  if (st) return st;
+  if (flops) *flops += uint64_t(2) * m * n * k;  // the reference's in-loop count, dense.hpp:148
+  return LRB_OK;
+}

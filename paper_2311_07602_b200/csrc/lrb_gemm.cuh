@@ -1,0 +1,449 @@
+// lrb_gemm.cuh — the batched FP64 GEMM kernel family (sm_100a).
+//
+// C_i = op(A_i) * op(B_i) + beta * C_i, column-major, beta in {0, 1}.
+// Replaces the reference's per-item oracle loop nest
+//   for i: for j: sum = accumulate ? c : 0; for p: sum += a[i,p] * b[p,j]
+// (reference: proj/include/lrbatch/dense.hpp:43-56) over a batch.
+//
+// Structure (persistent CTAs, every warp computes):
+//   * The CTA walks a flattened sequence of (tile, k-chunk) pairs: tiles
+//     blockIdx.x, +gridDim.x, ...; each tile's k range in KB-wide chunks.
+//   * Operands reach shared memory only through TMA bulk copies
+//     (cp.async.bulk, SASS UBLKCP): one copy per contiguous column segment of
+//     the A and B tiles, completing on the stage's `full` mbarrier with
+//     expect_tx. A segment that is not 16-byte aligned / sized (odd ld, odd m
+//     at a ragged edge) is copied by the issuing lane with plain loads into
+//     the same stage under the same barrier, so there is one code path.
+//   * The ring has STAGES slots. Warp 0 issues chunks 0..STAGES-1 up front.
+//     After a warp has consumed a slot it bumps the slot's release counter;
+//     the LAST warp to release it immediately issues the next chunk of the
+//     sequence into it. No warp ever waits to issue, no producer warp holds
+//     registers, and refills are issued in chunk order.
+//   * Each warp owns a WI x WJ sub-tile of C in registers as DMMA 8x8x4
+//     fragments. The MMA computes C^T = op(B)^T op(A)^T so a lane's
+//     accumulator pair is two consecutive ROWS of column-major C: the
+//     epilogue is one 16-byte store per pair.
+//   * k is consumed in ascending order, 4 at a time by DMMA (each entry an
+//     in-order FMA chain, probed bitwise on B200) and a scalar fma() tail, so
+//     every C entry is exactly the reference's FMA chain.
+// Shared-memory operand layouts are padded so DMMA fragment loads are
+// conflict-free (2 wavefronts per 256 B warp load):
+//   K-rows   X_s[kk][o]  row pitch P = o_extent + pad, P == 8 (mod 16) doubles
+//   K-contig X_s[o][kk]  row pitch P = KB + pad,       P == 4 (mod 16) doubles
+// op(A)=N (A(i,k) at i + k*lda) and op(B)=T are K-rows; op(A)=T and op(B)=N
+// are K-contig. Each K-rows row / K-contig row is one bulk copy.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "lrb_device.cuh"
+
+namespace lrb {
+
+// ------------------------------------------------------------------ config
+__host__ __device__ constexpr int pad_krows(int extent) { return (8 - extent % 16 + 16) % 16; }
+__host__ __device__ constexpr int pad_kcontig(int kb) { return (4 - kb % 16 + 16) % 16; }
+__host__ __device__ constexpr int round_up_c(int x, int m) { return (x + m - 1) / m * m; }
+
+template <int WARPS_I_, int WARPS_J_, int WI_, int WJ_, int KB_, int STAGES_, int MINB_, bool A_T_,
+          bool B_T_>
+struct GemmCfg {
+  static constexpr int WARPS_I = WARPS_I_, WARPS_J = WARPS_J_, WI = WI_, WJ = WJ_;
+  static constexpr int KB = KB_, STAGES = STAGES_, MINB = MINB_;
+  static constexpr bool A_T = A_T_, B_T = B_T_;
+  static constexpr int MB = WARPS_I * WI, NB = WARPS_J * WJ;
+  static constexpr int FI = WI / 8, FJ = WJ / 8;
+  static constexpr int WARPS = WARPS_I * WARPS_J;
+  static constexpr int THREADS = WARPS * 32;
+  // operand pitches (doubles)
+  static constexpr int PMA = MB + pad_krows(MB);   // A K-rows  (op(A)=N): As[kk][i]
+  static constexpr int PKA = KB + pad_kcontig(KB); // A K-contig (op(A)=T): As[i][kk]
+  static constexpr int PNB = NB + pad_krows(NB);   // B K-rows  (op(B)=T): Bs[kk][j]
+  static constexpr int PKB = KB + pad_kcontig(KB); // B K-contig (op(B)=N): Bs[j][kk]
+  static constexpr int A_ELEMS = round_up_c(A_T ? MB * PKA : KB * PMA, 16);
+  static constexpr int B_ELEMS = round_up_c(B_T ? KB * PNB : NB * PKB, 16);
+  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
+  // stages + full barriers + release counters + issue state + base alignment slack
+  static constexpr size_t SMEM_BYTES =
+      size_t(STAGES) * STAGE_ELEMS * 8 + size_t(STAGES) * 8 + size_t(STAGES) * 4 + 16 + 128;
+  static_assert(WI % 8 == 0 && WJ % 8 == 0, "warp tile must be a multiple of the 8x8 fragment");
+  static_assert(KB % 4 == 0, "k chunk must be a multiple of the DMMA k (4)");
+  static_assert(WARPS % 4 == 0, "warps per CTA must fill all four SM sub-partitions");
+
+  // op(A)(i, kk) and op(B)(kk, j) inside a stage
+  __device__ __forceinline__ static double a_at(const double* As, int i, int kk) {
+    return A_T ? As[i * PKA + kk] : As[kk * PMA + i];
+  }
+  __device__ __forceinline__ static double b_at(const double* Bs, int kk, int j) {
+    return B_T ? Bs[kk * PNB + j] : Bs[j * PKB + kk];
+  }
+};
+
+// ---------------------------------------------------------------- problems
+struct TileView {
+  const double* A;
+  const double* B;
+  double* C;
+  int64_t lda, ldb, ldc;
+  int m, n, k;
+  int i0, j0;
+};
+
+// Fixed-stride batch: item i at base + i * stride (the reference's
+// LowRankBatch role arrays, low_rank.hpp:147-158).
+struct StridedProblem {
+  const double* A;
+  const double* B;
+  double* C;
+  int64_t lda, ldb, ldc, sA, sB, sC;
+  int m, n, k;
+  int tiles_i, tiles_per_item;
+  int64_t num_tiles;
+
+  template <int MB, int NB>
+  __device__ __forceinline__ TileView tile(int64_t t) const {
+    const int64_t item = t / tiles_per_item;
+    const int r = static_cast<int>(t - item * tiles_per_item);
+    TileView v;
+    v.A = A + item * sA;
+    v.B = B + item * sB;
+    v.C = C + item * sC;
+    v.lda = lda;
+    v.ldb = ldb;
+    v.ldc = ldc;
+    v.m = m;
+    v.n = n;
+    v.k = k;
+    v.i0 = (r % tiles_i) * MB;
+    v.j0 = (r / tiles_i) * NB;
+    return v;
+  }
+  __device__ __forceinline__ int tile_k(int64_t) const { return k; }
+};
+
+// Pointer-array / variable-size batch: per-item descriptors plus a host-built
+// tile list (item << 32 | ti << 16 | tj), largest k first.
+struct ItemDesc {
+  const double* A;
+  const double* B;
+  double* C;
+  int64_t lda, ldb, ldc;
+  int32_t m, n, k, pad;
+};
+static_assert(sizeof(ItemDesc) == 64, "ItemDesc is one 64-byte line");
+
+struct PtrProblem {
+  const ItemDesc* items;
+  const uint64_t* tiles;
+  int64_t num_tiles;
+
+  template <int MB, int NB>
+  __device__ __forceinline__ TileView tile(int64_t t) const {
+    const uint64_t e = tiles[t];
+    const ItemDesc d = items[e >> 32];
+    TileView v;
+    v.A = d.A;
+    v.B = d.B;
+    v.C = d.C;
+    v.lda = d.lda;
+    v.ldb = d.ldb;
+    v.ldc = d.ldc;
+    v.m = d.m;
+    v.n = d.n;
+    v.k = d.k;
+    v.i0 = static_cast<int>((e >> 16) & 0xFFFF) * MB;
+    v.j0 = static_cast<int>(e & 0xFFFF) * NB;
+    return v;
+  }
+  __device__ __forceinline__ int tile_k(int64_t t) const { return items[tiles[t] >> 32].k; }
+};
+
+// next chunk to issue, shared by the CTA's warps
+struct IssueState {
+  int64_t t;
+  int k0;
+  int pad;
+};
+
+// ------------------------------------------------------------------ kernel
+template <class Problem>
+__device__ __forceinline__ int64_t skip_empty_tiles(const Problem& prob, int64_t t) {
+  while (t < prob.num_tiles && prob.tile_k(t) == 0) t += gridDim.x;
+  return t;
+}
+
+// Issue the chunk described by *st into `stage` (whole warp), then advance *st.
+template <class Cfg, class Problem>
+__device__ __forceinline__ void issue_chunk(const Problem& prob, double* smem, uint64_t* full,
+                                            IssueState* st, int stage, int lane) {
+  constexpr int MB = Cfg::MB, NB = Cfg::NB, KB = Cfg::KB;
+  // lane 0 (which synchronised with the previous issuer through the release
+  // counter) reads the shared state and broadcasts it
+  long long t_ll = 0;
+  int k0 = 0;
+  if (lane == 0) {
+    t_ll = st->t;
+    k0 = st->k0;
+  }
+  const int64_t t = __shfl_sync(0xffffffffu, t_ll, 0);
+  k0 = __shfl_sync(0xffffffffu, k0, 0);
+  if (t >= prob.num_tiles) return;  // sequence exhausted (uniform across the warp)
+  const TileView v = prob.template tile<MB, NB>(t);
+  const int ivalid = min(MB, v.m - v.i0);
+  const int jvalid = min(NB, v.n - v.j0);
+  const int kvalid = min(KB, v.k - k0);
+  // A is streamed once when one column tile covers C; B once when one row tile does.
+  const uint64_t pol_a = (v.n <= NB) ? policy_evict_first() : policy_evict_last();
+  const uint64_t pol_b = (v.m <= MB) ? policy_evict_first() : policy_evict_last();
+  double* As = smem + size_t(stage) * Cfg::STAGE_ELEMS;
+  double* Bs = As + Cfg::A_ELEMS;
+  const int seg_a = Cfg::A_T ? ivalid : kvalid;
+  const int seg_b = Cfg::B_T ? kvalid : jvalid;
+  // order this warp's generic-proxy smem reads of the slot before the async-proxy refill
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  uint32_t bytes = 0;
+#pragma unroll 1
+  for (int s = lane; s < seg_a + seg_b; s += 32) {
+    const double* src;
+    double* dst;
+    int len;
+    uint64_t pol;
+    if (s < seg_a) {
+      if (Cfg::A_T) {
+        src = v.A + k0 + int64_t(v.i0 + s) * v.lda;
+        dst = As + s * Cfg::PKA;
+        len = kvalid;
+      } else {
+        src = v.A + v.i0 + int64_t(k0 + s) * v.lda;
+        dst = As + s * Cfg::PMA;
+        len = ivalid;
+      }
+      pol = pol_a;
+    } else {
+      const int q = s - seg_a;
+      if (Cfg::B_T) {
+        src = v.B + v.j0 + int64_t(k0 + q) * v.ldb;
+        dst = Bs + q * Cfg::PNB;
+        len = jvalid;
+      } else {
+        src = v.B + k0 + int64_t(v.j0 + q) * v.ldb;
+        dst = Bs + q * Cfg::PKB;
+        len = kvalid;
+      }
+      pol = pol_b;
+    }
+    const uint32_t nb = uint32_t(len) * 8u;
+    if (((reinterpret_cast<uintptr_t>(src) & 15) == 0) && ((nb & 15) == 0)) {
+      bulk_g2s(dst, src, nb, &full[stage], pol);
+      bytes += nb;
+    } else {
+#pragma unroll 4
+      for (int e = 0; e < len; ++e) dst[e] = __ldg(src + e);
+    }
+  }
+  bytes = __reduce_add_sync(0xffffffffu, bytes);
+  __syncwarp();
+  if (lane == 0) {
+    if (bytes)
+      mbar_arrive_expect_tx(&full[stage], bytes);
+    else
+      mbar_arrive(&full[stage]);
+    // advance the sequence
+    int nk0 = k0 + KB;
+    int64_t nt = t;
+    if (nk0 >= v.k) {
+      nk0 = 0;
+      nt = skip_empty_tiles(prob, t + gridDim.x);
+    }
+    st->t = nt;
+    st->k0 = nk0;
+  }
+  __syncwarp();
+}
+
+template <class Cfg>
+__device__ __forceinline__ void mma_kstep(double (&acc)[Cfg::FJ][Cfg::FI][2], const double* As,
+                                          const double* Bs, int ib, int jb, int kk) {
+  double af[Cfg::FJ], bf[Cfg::FI];
+#pragma unroll
+  for (int fj = 0; fj < Cfg::FJ; ++fj) af[fj] = Cfg::b_at(Bs, kk, jb + fj * 8);
+#pragma unroll
+  for (int fi = 0; fi < Cfg::FI; ++fi) bf[fi] = Cfg::a_at(As, ib + fi * 8, kk);
+#pragma unroll
+  for (int fj = 0; fj < Cfg::FJ; ++fj)
+#pragma unroll
+    for (int fi = 0; fi < Cfg::FI; ++fi) dmma_8x8x4(acc[fj][fi][0], acc[fj][fi][1], af[fj], bf[fi]);
+}
+
+template <class Cfg, class Problem>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
+    lrb_gemm_kernel(const Problem prob, const int beta_one) {
+  constexpr int MB = Cfg::MB, NB = Cfg::NB, KB = Cfg::KB, STAGES = Cfg::STAGES;
+  constexpr int FI = Cfg::FI, FJ = Cfg::FJ;
+  extern __shared__ unsigned char smem_raw[];
+  double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
+                                           ~uintptr_t(127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(STAGES) * Cfg::STAGE_ELEMS);
+  IssueState* st = reinterpret_cast<IssueState*>(full + STAGES);
+  int* released = reinterpret_cast<int*>(st + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+#pragma unroll 1
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      released[s] = 0;
+    }
+    st->t = skip_empty_tiles(prob, int64_t(blockIdx.x));
+    st->k0 = 0;
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll 1
+    for (int s = 0; s < STAGES; ++s) issue_chunk<Cfg>(prob, smem, full, st, s, lane);
+  }
+
+  const int wi = warp % Cfg::WARPS_I;
+  const int wj = warp / Cfg::WARPS_I;
+  const int g = lane >> 2;
+  const int tq = lane & 3;
+  // local (in-tile) coordinates of this lane's fragments:
+  //   B-operand rows (i) of fragment fi: wi*WI + fi*8 + g       (loads)
+  //   A-operand rows (j) of fragment fj: wj*WJ + fj*8 + g       (loads)
+  //   accumulator pair (fj, fi): C(i = wi*WI + fi*8 + 2tq + {0,1}, j = wj*WJ + fj*8 + g)
+  const int li_load = wi * Cfg::WI + g;
+  const int lj_load = wj * Cfg::WJ + g;
+  const int li_acc = wi * Cfg::WI + 2 * tq;
+  const int lj_acc = wj * Cfg::WJ + g;
+
+  int stage = 0;
+  uint32_t phase = 0;
+#pragma unroll 1
+  for (int64_t t = blockIdx.x; t < prob.num_tiles; t += gridDim.x) {
+    const TileView v = prob.template tile<MB, NB>(t);
+    const bool vec_ok = ((reinterpret_cast<uintptr_t>(v.C) & 15) == 0) && ((v.ldc & 1) == 0);
+
+    double acc[FJ][FI][2];
+#pragma unroll
+    for (int fj = 0; fj < FJ; ++fj)
+#pragma unroll
+      for (int fi = 0; fi < FI; ++fi) acc[fj][fi][0] = acc[fj][fi][1] = 0.0;
+    if (beta_one) {
+#pragma unroll
+      for (int fj = 0; fj < FJ; ++fj) {
+        const int j = v.j0 + lj_acc + fj * 8;
+        if (j < v.n) {
+          const double* cp = v.C + int64_t(j) * v.ldc;
+#pragma unroll
+          for (int fi = 0; fi < FI; ++fi) {
+            const int i = v.i0 + li_acc + fi * 8;
+            if (i < v.m) acc[fj][fi][0] = cp[i];
+            if (i + 1 < v.m) acc[fj][fi][1] = cp[i + 1];
+          }
+        }
+      }
+    }
+
+#pragma unroll 1
+    for (int k0 = 0; k0 < v.k; k0 += KB) {
+      const int kvalid = min(KB, v.k - k0);
+      mbar_wait(&full[stage], phase);
+      const double* As = smem + size_t(stage) * Cfg::STAGE_ELEMS;
+      const double* Bs = As + Cfg::A_ELEMS;
+      if (kvalid == KB) {
+#pragma unroll
+        for (int kq = 0; kq < KB / 4; ++kq) mma_kstep<Cfg>(acc, As, Bs, li_load, lj_load, kq * 4 + tq);
+      } else {
+        const int nq = kvalid >> 2;
+#pragma unroll 1
+        for (int kq = 0; kq < nq; ++kq) mma_kstep<Cfg>(acc, As, Bs, li_load, lj_load, kq * 4 + tq);
+        // scalar tail keeps the in-order FMA chain for k % 4 != 0
+#pragma unroll 1
+        for (int kk = nq * 4; kk < kvalid; ++kk) {
+#pragma unroll
+          for (int fj = 0; fj < FJ; ++fj) {
+            const double bv = Cfg::b_at(Bs, kk, lj_acc + fj * 8);
+#pragma unroll
+            for (int fi = 0; fi < FI; ++fi) {
+              acc[fj][fi][0] = fma(Cfg::a_at(As, li_acc + fi * 8, kk), bv, acc[fj][fi][0]);
+              acc[fj][fi][1] = fma(Cfg::a_at(As, li_acc + fi * 8 + 1, kk), bv, acc[fj][fi][1]);
+            }
+          }
+        }
+      }
+      // release the slot; the last warp out refills it with the next chunk
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) {
+        __threadfence_block();
+        last = (atomicAdd(&released[stage], 1) == Cfg::WARPS - 1);
+        if (last) released[stage] = 0;
+        __threadfence_block();
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) issue_chunk<Cfg>(prob, smem, full, st, stage, lane);
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+
+    // epilogue: lane pair = two consecutive rows of one column of C
+#pragma unroll
+    for (int fj = 0; fj < FJ; ++fj) {
+      const int j = v.j0 + lj_acc + fj * 8;
+      if (j < v.n) {
+        double* cp = v.C + int64_t(j) * v.ldc;
+#pragma unroll
+        for (int fi = 0; fi < FI; ++fi) {
+          const int i = v.i0 + li_acc + fi * 8;
+          if (vec_ok && i + 1 < v.m) {
+            st_global_v2(cp + i, acc[fj][fi][0], acc[fj][fi][1]);
+          } else {
+            if (i < v.m) cp[i] = acc[fj][fi][0];
+            if (i + 1 < v.m) cp[i + 1] = acc[fj][fi][1];
+          }
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ launch
+struct LaunchInfo {
+  int64_t grid;
+  int occupancy;
+};
+
+template <class Cfg, class Problem>
+cudaError_t launch_gemm(const Problem& prob, int beta_one, int device, int sm_count,
+                        cudaStream_t stream, LaunchInfo* info) {
+  auto kern = lrb_gemm_kernel<Cfg, Problem>;
+  // per-device one-time attribute + occupancy query
+  static int occ_cache[64] = {0};
+  int occ = (device >= 0 && device < 64) ? occ_cache[device] : 0;
+  if (occ == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(Cfg::SMEM_BYTES));
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::THREADS, Cfg::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    if (device >= 0 && device < 64) occ_cache[device] = occ;
+  }
+  int64_t grid = int64_t(sm_count) * occ;
+  if (prob.num_tiles < grid) grid = prob.num_tiles;
+  if (info) {
+    info->grid = grid;
+    info->occupancy = occ;
+  }
+  if (grid <= 0) return cudaSuccess;
+  kern<<<static_cast<unsigned>(grid), Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(prob, beta_one);
+  return cudaGetLastError();
+}
+
+}  // namespace lrb

@@ -1,0 +1,41 @@
+// lrb_variants.h — the kernel variant table shared by the selector (host) and
+// the per-variant instantiation units (device).
+//
+// A variant fixes the CTA tile of C (column-major view): MB = WARPS_I * WI rows
+// by NB = WARPS_J * WJ columns, computed by WARPS_I * WARPS_J consumer warps
+// (warp tile WI rows x WJ columns, DMMA 8x8x4 fragments) fed by one TMA
+// producer warp through a STAGES-deep shared-memory ring of KB-wide k chunks.
+//
+//   n*  : tall-skinny C (dense b x b times a b x r basis, r <= 64): the BLR
+//         diagonal shape (reference blr.hpp:149-153) in column-major — HBM
+//         streaming of the b x b block, two CTAs per SM.
+//   m*  : short-wide C, the same product issued row-major (swapped operands).
+//   sq  : 128 x 128 tiles for the low-rank expansion U * V^T (blr.hpp:75-78),
+//         write-dominated and at the FP64 ridge.
+#pragma once
+
+//            id  name  WARPS_I WARPS_J WI  WJ  KB  STAGES MINB
+#define LRB_VARIANT_LIST(X)            \
+  X(0, n8, 4, 1, 32, 8, 16, 5, 2)      \
+  X(1, n16, 4, 1, 32, 16, 16, 5, 2)    \
+  X(2, n32, 4, 1, 32, 32, 16, 4, 2)    \
+  X(3, n64, 4, 2, 32, 32, 16, 4, 2)    \
+  X(4, sq, 2, 4, 64, 32, 32, 3, 1)     \
+  X(5, m8, 1, 4, 8, 32, 16, 5, 2)      \
+  X(6, m16, 1, 4, 16, 32, 16, 5, 2)    \
+  X(7, m32, 1, 4, 32, 32, 16, 4, 2)    \
+  X(8, m64, 2, 4, 32, 32, 16, 4, 2)
+
+#define LRB_NUM_VARIANTS 9
+
+enum {
+  LRB_V_N8 = 0,
+  LRB_V_N16 = 1,
+  LRB_V_N32 = 2,
+  LRB_V_N64 = 3,
+  LRB_V_SQ = 4,
+  LRB_V_M8 = 5,
+  LRB_V_M16 = 6,
+  LRB_V_M32 = 7,
+  LRB_V_M64 = 8
+};

@@ -1,0 +1,219 @@
+"""BASELINE.json workloads as seeded synthetic batches.
+
+There is no public dataset for this path: the reference and BASELINE.json
+specify i.i.d. uniform[-1,1) entries per config seed, column-major, packed.
+Inputs are generated ON THE DEVICE with the counter RNG of include/lrb_rng.h
+(keyed by seed, role, GLOBAL item index and element), so every shard and
+chunk regenerates exactly its slice and the host oracle can regenerate any
+sampled item bit-for-bit.
+
+Per-item accounting (beta = 0): flops 2mnk, algorithmic bytes 8(mk+kn+mn).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+from . import _lib
+
+ROLE_A, ROLE_B, ROLE_C, ROLE_SHAPE_B, ROLE_SHAPE_R = 0, 1, 2, 3, 4
+GIB = 1 << 30
+
+# ------------------------------------------------------------------ RNG (host)
+_M64 = (1 << 64) - 1
+_GOLDEN = 0x9E3779B97F4A7C15
+_ROLE_MUL = 0xD1B54A32D192ED03
+_ROLE_ADD = 0x632BE59BD9B4E019
+
+
+def mix64(z: int) -> int:
+    z &= _M64
+    z ^= z >> 30
+    z = (z * 0xBF58476D1CE4E5B9) & _M64
+    z ^= z >> 27
+    z = (z * 0x94D049BB133111EB) & _M64
+    z ^= z >> 31
+    return z
+
+
+def stream_key(seed: int, role: int) -> int:
+    return mix64((seed * _GOLDEN + role * _ROLE_MUL + _ROLE_ADD) & _M64)
+
+
+def bits(key: int, item: int, elem: int) -> int:
+    return mix64((key + (((item << 32) | (elem & 0xFFFFFFFF)) & _M64) * _GOLDEN) & _M64)
+
+
+def below(key: int, item: int, n: int) -> int:
+    """lrb_below: uniform integer in [0, n) (include/lrb_rng.h)"""
+    return ((bits(key, item, 0) >> 32) * n) >> 32
+
+
+def uniform(key: int, item: int, elem: int) -> float:
+    return (bits(key, item, elem) >> 11) * (1.0 / 4503599627370496.0) - 1.0
+
+
+# ---------------------------------------------------------------- workloads
+@dataclass
+class Strided:
+    """fixed-stride column-major batch: C_i = op(A_i) op(B_i)"""
+
+    name: str
+    m: int
+    n: int
+    k: int
+    batch: int
+    seed: int
+    opA: str = "N"
+    opB: str = "N"
+    order: str = "C"
+    beta: float = 0.0
+
+    @property
+    def a_rows(self):
+        return self.k if self.opA == "T" else self.m
+
+    @property
+    def a_cols(self):
+        return self.m if self.opA == "T" else self.k
+
+    @property
+    def b_rows(self):
+        return self.n if self.opB == "T" else self.k
+
+    @property
+    def b_cols(self):
+        return self.k if self.opB == "T" else self.n
+
+    @property
+    def lda(self):
+        return self.a_rows
+
+    @property
+    def ldb(self):
+        return self.b_rows
+
+    @property
+    def ldc(self):
+        return self.m
+
+    @property
+    def sA(self):
+        return self.a_rows * self.a_cols
+
+    @property
+    def sB(self):
+        return self.b_rows * self.b_cols
+
+    @property
+    def sC(self):
+        return self.m * self.n
+
+    def item_flops(self) -> float:
+        return 2.0 * self.m * self.n * self.k
+
+    def item_bytes(self) -> float:
+        return 8.0 * (self.m * self.k + self.k * self.n + self.m * self.n)
+
+    def flops(self, items: Optional[int] = None) -> float:
+        return self.item_flops() * (self.batch if items is None else items)
+
+    def bytes(self, items: Optional[int] = None) -> float:
+        return self.item_bytes() * (self.batch if items is None else items)
+
+    def describe(self) -> dict:
+        return {"workload": self.name, "m": self.m, "n": self.n, "k": self.k,
+                "batch": self.batch, "opA": self.opA, "opB": self.opB, "order": self.order,
+                "seed": self.seed, "layout": "column-major, packed (stride = rows*cols)"}
+
+
+@dataclass
+class Variable:
+    """pointer-array batch: C_i = A_i (b_i x b_i) B_i (b_i x r_i), 256-B aligned bases"""
+
+    name: str
+    batch: int
+    seed: int
+    b_choices: tuple = (256, 512, 1024)
+    r_lo: int = 8
+    r_hi: int = 64
+    bs: List[int] = field(default_factory=list)
+    rs: List[int] = field(default_factory=list)
+
+    def __post_init__(self):
+        kb = stream_key(self.seed, ROLE_SHAPE_B)
+        kr = stream_key(self.seed, ROLE_SHAPE_R)
+        nr = self.r_hi - self.r_lo + 1
+        self.bs = [self.b_choices[below(kb, i, len(self.b_choices))] for i in range(self.batch)]
+        self.rs = [self.r_lo + below(kr, i, nr) for i in range(self.batch)]
+
+    def item_flops(self, i: int) -> float:
+        b, r = self.bs[i], self.rs[i]
+        return 2.0 * b * r * b
+
+    def item_bytes(self, i: int) -> float:
+        b, r = self.bs[i], self.rs[i]
+        return 8.0 * (b * b + b * r + b * r)
+
+    def flops(self, items=None) -> float:
+        ids = range(self.batch) if items is None else items
+        return sum(self.item_flops(i) for i in ids)
+
+    def bytes(self, items=None) -> float:
+        ids = range(self.batch) if items is None else items
+        return sum(self.item_bytes(i) for i in ids)
+
+    def describe(self) -> dict:
+        return {"workload": self.name, "batch": self.batch, "seed": self.seed,
+                "b": list(self.b_choices), "r": [self.r_lo, self.r_hi],
+                "layout": "column-major, pointer array, 256-B aligned independent bases"}
+
+
+def cfg3_batch(b: int, r: int, budget: int = 16 * GIB) -> int:
+    """items whose A + B + C total ~16 GiB (BASELINE cfg3)"""
+    return budget // (8 * (b * b + 2 * b * r))
+
+
+CFG3_B = (128, 256, 512, 1024, 2048)
+CFG3_R = (8, 16, 32, 64)
+
+
+def get(name: str):
+    """cfg1 | cfg2 | cfg3_b{B}_r{R} | cfg4 | cfg5"""
+    if name == "cfg1":
+        return Strided("cfg1", 256, 16, 256, 256, seed=0)
+    if name == "cfg2":
+        # low-rank expansion C = U V^T, U and V 512 x 32 column-major
+        return Strided("cfg2", 512, 512, 32, 4096, seed=1, opA="N", opB="T")
+    if name.startswith("cfg3"):
+        parts = dict(p[0:1] and (p[0], p[1:]) for p in name.split("_")[1:])
+        b, r = int(parts["b"]), int(parts["r"])
+        return Strided(name, b, r, b, cfg3_batch(b, r), seed=2)
+    if name == "cfg4":
+        return Variable("cfg4", 8192, seed=3)
+    if name == "cfg5":
+        return Strided("cfg5", 512, 32, 512, 131072, seed=4)
+    raise KeyError(name)
+
+
+def all_names() -> List[str]:
+    return (["cfg1", "cfg2"] + [f"cfg3_b{b}_r{r}" for b in CFG3_B for r in CFG3_R]
+            + ["cfg4", "cfg5"])
+
+
+def align256(x: int) -> int:
+    return (x + 255) // 256 * 256
+
+
+def variable_layout(w: Variable, items: List[int]):
+    """byte offsets of A_i, B_i, C_i inside three arenas, each base 256-B aligned"""
+    oa = ob = oc = 0
+    offs = []
+    for i in items:
+        b, r = w.bs[i], w.rs[i]
+        offs.append((oa, ob, oc))
+        oa = align256(oa + 8 * b * b)
+        ob = align256(ob + 8 * b * r)
+        oc = align256(oc + 8 * b * r)
+    return offs, (oa, ob, oc)

@@ -1,0 +1,221 @@
+"""GPU parity at BASELINE.json's own configs (device-generated inputs).
+
+cfg1 is checked in full; larger configs through deterministic samples (first,
+last and interior items of every shard/chunk, every (b, r) class of cfg4)
+regenerated on the host from the same counter RNG, plus size-independent
+properties: shard/chunk invariance and run-to-run determinism.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2311_07602_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def _device_batch(ctx, w, items0=0, count=None):
+    count = w.batch if count is None else count
+    A = ctx.empty(w.sA * count)
+    B = ctx.empty(w.sB * count)
+    Cd = ctx.empty(w.sC * count)
+    ctx.fill_uniform(A, w.a_rows, w.a_cols, w.lda, w.sA, count, w.seed, W.ROLE_A, items0)
+    ctx.fill_uniform(B, w.b_rows, w.b_cols, w.ldb, w.sB, count, w.seed, W.ROLE_B, items0)
+    return A, B, Cd
+
+
+def _run(ctx, w, A, B, Cd, count):
+    ctx.dgemm_strided_batched(w.order, w.opA, w.opB, w.m, w.n, w.k, 0.0, A, w.lda, w.sA, B,
+                              w.ldb, w.sB, Cd, w.ldc, w.sC, count)
+    ctx.synchronize()
+
+
+def _check_items(w, Cd, items, base=0):
+    """items are global indices; Cd holds items [base, base + len)"""
+    worst = 0.0
+    for it in items:
+        a = O.fill_uniform(w.a_rows, w.a_cols, w.lda, w.sA, 1, w.seed, W.ROLE_A, it)
+        b = O.fill_uniform(w.b_rows, w.b_cols, w.ldb, w.sB, 1, w.seed, W.ROLE_B, it)
+        got = Cd.download(w.sC, offset_bytes=8 * w.sC * (it - base))
+        fma = np.zeros(w.sC)
+        O.dgemm_strided("C", w.opA, w.opB, w.m, w.n, w.k, 0.0, a, w.lda, 0, b, w.ldb, 0, fma,
+                        w.ldc, 0, 1)
+        assert np.array_equal(got, fma), f"{w.name} item {it}: != FMA-chain oracle"
+        ref = np.zeros(w.sC)
+        O.dgemm_strided("C", w.opA, w.opB, w.m, w.n, w.k, 0.0, a, w.lda, 0, b, w.ldb, 0, ref,
+                        w.ldc, 0, 1, mode=O.REF_COMPILED)
+        bad, ratio = O.check_bound("C", w.opA, w.opB, w.m, w.n, w.k, 0.0, a, w.lda, b, w.ldb,
+                                   None, got, ref, w.ldc)
+        assert bad == 0, f"{w.name} item {it}: {bad} entries outside the FP64 bound"
+        worst = max(worst, ratio)
+    return worst
+
+
+def _sample(batch, extra=4):
+    s = {0, batch - 1, batch // 2}
+    rng = np.random.default_rng(batch)
+    s.update(int(x) for x in rng.integers(0, batch, extra))
+    return sorted(s)
+
+
+def test_cfg1_all_items(ctx):
+    w = W.get("cfg1")
+    A, B, Cd = _device_batch(ctx, w)
+    _run(ctx, w, A, B, Cd, w.batch)
+    hA = O.fill_uniform(w.a_rows, w.a_cols, w.lda, w.sA, w.batch, w.seed, W.ROLE_A)
+    hB = O.fill_uniform(w.b_rows, w.b_cols, w.ldb, w.sB, w.batch, w.seed, W.ROLE_B)
+    assert np.array_equal(A.download(hA.size), hA), "device RNG != host RNG"
+    got = Cd.download(w.sC * w.batch)
+    fma = np.zeros_like(got)
+    O.dgemm_strided("C", "N", "N", w.m, w.n, w.k, 0.0, hA, w.lda, w.sA, hB, w.ldb, w.sB, fma,
+                    w.ldc, w.sC, w.batch, threads=8)
+    assert np.array_equal(got, fma)
+    ref = np.zeros_like(got)
+    if O.ref_available():  # the reference binary itself
+        O.ref_dgemm_colmajor("N", "N", w.m, w.n, w.k, 0, hA, w.lda, w.sA, hB, w.ldb, w.sB, ref,
+                             w.ldc, w.sC, w.batch, threads=8)
+    else:
+        O.dgemm_strided("C", "N", "N", w.m, w.n, w.k, 0.0, hA, w.lda, w.sA, hB, w.ldb, w.sB, ref,
+                        w.ldc, w.sC, w.batch, threads=8, mode=O.REF_COMPILED)
+    for it in range(w.batch):
+        o = it * w.sC
+        bad, _ = O.check_bound("C", "N", "N", w.m, w.n, w.k, 0.0, hA[it * w.sA:], w.lda,
+                               hB[it * w.sB:], w.ldb, None, got[o:], ref[o:], w.ldc)
+        assert bad == 0
+
+
+def test_cfg2_low_rank_expansion_sampled(ctx):
+    w = W.get("cfg2")
+    A, B, Cd = _device_batch(ctx, w)
+    _run(ctx, w, A, B, Cd, w.batch)
+    _check_items(w, Cd, _sample(w.batch))
+
+
+@pytest.mark.parametrize("b", W.CFG3_B)
+@pytest.mark.parametrize("r", W.CFG3_R)
+def test_cfg3_sweep_sampled(ctx, b, r):
+    w = W.get(f"cfg3_b{b}_r{r}")
+    A, B, Cd = _device_batch(ctx, w)
+    _run(ctx, w, A, B, Cd, w.batch)
+    _check_items(w, Cd, _sample(w.batch, extra=1 if b >= 1024 else 3))
+
+
+def test_cfg5_shard_and_chunk_invariance(ctx):
+    # a 6000-item window of cfg5 (global items 60000..65999): one launch vs
+    # three shards regenerated from global indices must agree bitwise
+    w = W.get("cfg5")
+    base, count = 60000, 6000
+    A, B, Cd = _device_batch(ctx, w, base, count)
+    _run(ctx, w, A, B, Cd, count)
+    whole = Cd.download(w.sC * count)
+    from paper_2311_07602_b200 import shard_plan
+
+    bounds = shard_plan(count, 3)
+    parts = []
+    for g in range(3):
+        lo, hi = bounds[g], bounds[g + 1]
+        a, b, c = _device_batch(ctx, w, base + lo, hi - lo)
+        _run(ctx, w, a, b, c, hi - lo)
+        parts.append(c.download(w.sC * (hi - lo)))
+    assert np.array_equal(whole, np.concatenate(parts))
+    _check_items(w, Cd, [base, base + 1, base + count // 2, base + count - 1], base=base)
+
+
+def test_cfg4_pointer_array_sampled(ctx):
+    w = W.get("cfg4")
+    items = list(range(w.batch))
+    offs, (na, nb, nc) = W.variable_layout(w, items)
+    arena_a, arena_b, arena_c = ctx.malloc(na), ctx.malloc(nb), ctx.malloc(nc)
+    pa = [arena_a.ptr + o[0] for o in offs]
+    pb = [arena_b.ptr + o[1] for o in offs]
+    pc = [arena_c.ptr + o[2] for o in offs]
+    assert all(p % 256 == 0 for p in pa + pb + pc)
+    ctx.fill_uniform_ptr(pa, w.bs, w.bs, w.bs, w.seed, W.ROLE_A)
+    ctx.fill_uniform_ptr(pb, w.bs, w.rs, w.bs, w.seed, W.ROLE_B)
+    plan = ctx.ptr_plan("C", "N", "N", w.bs, w.rs, w.bs, pa, w.bs, pb, w.bs, pc, w.bs, 0.0)
+    plan.execute()
+    ctx.synchronize()
+    # one item of every (b, r-class) plus first/last
+    pick = {0, w.batch - 1}
+    seen = set()
+    for i in range(w.batch):
+        cls = (w.bs[i], (w.rs[i] - 1) // 16)
+        if cls not in seen:
+            seen.add(cls)
+            pick.add(i)
+    for i in sorted(pick):
+        b, r = w.bs[i], w.rs[i]
+        a = O.fill_uniform(b, b, b, b * b, 1, w.seed, W.ROLE_A, i)
+        bb = O.fill_uniform(b, r, b, b * r, 1, w.seed, W.ROLE_B, i)
+        got = arena_c.download(b * r, offset_bytes=offs[i][2])
+        fma = np.zeros(b * r)
+        O.dgemm_strided("C", "N", "N", b, r, b, 0.0, a, b, 0, bb, b, 0, fma, b, 0, 1)
+        assert np.array_equal(got, fma), f"cfg4 item {i} (b={b}, r={r})"
+        ref = np.zeros(b * r)
+        O.dgemm_strided("C", "N", "N", b, r, b, 0.0, a, b, 0, bb, b, 0, ref, b, 0, 1,
+                        mode=O.REF_COMPILED)
+        bad, _ = O.check_bound("C", "N", "N", b, r, b, 0.0, a, b, bb, b, None, got, ref, b)
+        assert bad == 0
+
+
+def test_pointer_array_mixed_ragged_full(ctx):
+    # every item checked: mixed variants, odd shapes, transposes, beta = 1
+    rng = np.random.default_rng(21)
+    for (opA, opB, beta) in [("N", "N", 0.0), ("N", "T", 1.0), ("T", "N", 0.0), ("T", "T", 1.0)]:
+        batch = 40
+        ms = rng.integers(1, 300, batch)
+        ns = rng.integers(1, 150, batch)
+        ks = rng.integers(0, 90, batch)
+        hostA, hostB, hostC, lda, ldb, ldc = [], [], [], [], [], []
+        for i in range(batch):
+            m, n, k = int(ms[i]), int(ns[i]), int(ks[i])
+            ar, ac = (k, m) if opA == "T" else (m, k)
+            br, bc = (n, k) if opB == "T" else (k, n)
+            la, lb, lc = max(1, ar) + (i % 3), max(1, br) + (i % 2), m + (i % 4)
+            hostA.append(rng.uniform(-1, 1, max(1, la * ac)))
+            hostB.append(rng.uniform(-1, 1, max(1, lb * bc)))
+            hostC.append(rng.uniform(-1, 1, max(1, lc * n)))
+            lda.append(la)
+            ldb.append(lb)
+            ldc.append(lc)
+        dA = [ctx.to_device(x) for x in hostA]
+        dB = [ctx.to_device(x) for x in hostB]
+        dC = [ctx.to_device(x) for x in hostC]
+        ctx.dgemm_ptr_batched("C", opA, opB, ms, ns, ks, dA, lda, dB, ldb, dC, ldc, beta)
+        expect = [x.copy() for x in hostC]
+        O.dgemm_ptr("C", opA, opB, ms, ns, ks, hostA, lda, hostB, ldb, expect, ldc, beta)
+        for i in range(batch):
+            got = dC[i].download(hostC[i].size)
+            assert np.array_equal(got, expect[i]), f"item {i} ({ms[i]}x{ns[i]}x{ks[i]})"
+
+
+def test_host_buffer_api_pinned_and_pageable(ctx):
+    # the e2e path: H2D + kernel + D2H pipelined over chunks (cfg1 shape, 3000 items)
+    w = W.Strided("host", 256, 16, 256, 3000, seed=22)
+    hA = O.fill_uniform(w.a_rows, w.a_cols, w.lda, w.sA, w.batch, w.seed, W.ROLE_A)
+    hB = O.fill_uniform(w.b_rows, w.b_cols, w.ldb, w.sB, w.batch, w.seed, W.ROLE_B)
+    out = np.zeros(w.sC * w.batch)
+    ctx.dgemm_strided_batched_host("C", "N", "N", w.m, w.n, w.k, 0.0, hA, w.lda, w.sA, hB,
+                                   w.ldb, w.sB, out, w.ldc, w.sC, w.batch)
+    pA, pB, pC = ctx.pinned(hA.size), ctx.pinned(hB.size), ctx.pinned(out.size)
+    pA.array[:] = hA
+    pB.array[:] = hB
+    ctx.dgemm_strided_batched_host("C", "N", "N", w.m, w.n, w.k, 0.0, pA.array, w.lda, w.sA,
+                                   pB.array, w.ldb, w.sB, pC.array, w.ldc, w.sC, w.batch)
+    assert np.array_equal(out, pC.array)
+    fma = np.zeros_like(out)
+    O.dgemm_strided("C", "N", "N", w.m, w.n, w.k, 0.0, hA, w.lda, w.sA, hB, w.ldb, w.sB, fma,
+                    w.ldc, w.sC, w.batch, threads=8)
+    assert np.array_equal(out, fma)
+
+
+def test_device_rng_matches_host(ctx):
+    for (rows, cols, ld, batch, seed, role, off) in [(5, 3, 7, 4, 9, 0, 0), (64, 16, 64, 3, 1, 1, 777),
+                                                     (1, 1, 1, 1, 0, 2, 5)]:
+        stride = ld * cols
+        d = ctx.empty(stride * batch)
+        d.fill_bytes(0)
+        ctx.fill_uniform(d, rows, cols, ld, stride, batch, seed, role, off)
+        host = O.fill_uniform(rows, cols, ld, stride, batch, seed, role, off)
+        got = d.download(host.size)
+        assert np.array_equal(got, host)
