@@ -190,6 +190,10 @@ int lrb_variant_count(void);
 const char* lrb_variant_name(int variant);
 int lrb_variant_from_name(const char* name); /* -1 if unknown */
 lrb_status lrb_set_variant_override(lrb_ctx* ctx, int variant); /* -1 = automatic */
+/* operand loader: -1 automatic (TMA tensor maps when the operands are 16-B
+ * aligned with even leading dimensions / strides), 0 force the per-segment
+ * bulk-copy loader, 1 TMA when eligible. Env LRB_LOADER=segment forces 0. */
+lrb_status lrb_set_loader_override(lrb_ctx* ctx, int mode);
 
 /*
  * Shard planner: split `batch` independent items into `nparts` contiguous

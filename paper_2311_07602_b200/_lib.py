@@ -105,6 +105,7 @@ SIGNATURES = {
     "lrb_variant_name": (C.c_char_p, [C.c_int]),
     "lrb_variant_from_name": (C.c_int, [C.c_char_p]),
     "lrb_set_variant_override": (C.c_int, [vp, C.c_int]),
+    "lrb_set_loader_override": (C.c_int, [vp, C.c_int]),
     "lrb_shard_plan": (C.c_int, [i64, P(dbl), C.c_int, P(i64)]),
     "lrb_item_flops": (dbl, [i64, i64, i64]),
     "lrb_item_bytes": (dbl, [i64, i64, i64, dbl]),

@@ -7,6 +7,8 @@
 //   dense_gemm_naive      proj/include/lrbatch/dense.hpp:58-77 (ShapeError text)
 //   make_packing_plan     proj/include/lrbatch/plan.hpp:66-100 (selector role)
 //   naive_multiply_batch  proj/include/lrbatch/bench.hpp:55-77 (contiguous split)
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -66,16 +68,82 @@ struct VariantMeta {
 };
 
 #define LRB_X(id, nm, ...)                                                                  \
-  {VariantTraits<id>::name, VariantTraits<id>::Cfg<false, false>::MB,                       \
-   VariantTraits<id>::Cfg<false, false>::NB, VariantTraits<id>::Cfg<false, false>::KB,      \
-   VariantTraits<id>::Cfg<false, false>::STAGES, VariantTraits<id>::Cfg<false, false>::THREADS, \
-   VariantTraits<id>::Cfg<false, false>::MINB, VariantTraits<id>::Cfg<false, false>::SMEM_BYTES},
+  {VariantTraits<id>::name, VariantTraits<id>::Cfg<false, false, true>::MB,                       \
+   VariantTraits<id>::Cfg<false, false, true>::NB, VariantTraits<id>::Cfg<false, false, true>::KB,      \
+   VariantTraits<id>::Cfg<false, false, true>::STAGES, VariantTraits<id>::Cfg<false, false, true>::THREADS, \
+   VariantTraits<id>::Cfg<false, false, true>::MINB, VariantTraits<id>::Cfg<false, false, true>::SMEM_BYTES},
 static const VariantMeta kVariants[LRB_NUM_VARIANTS] = {LRB_VARIANT_LIST(LRB_X)};
 #undef LRB_X
 
 #define LRB_X(id, ...) &launch_variant<id>,
 static const LaunchFn kLaunch[LRB_NUM_VARIANTS] = {LRB_VARIANT_LIST(LRB_X)};
 #undef LRB_X
+
+// ------------------------------------------------------------- tensor maps
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    cudaGetLastError();
+  });
+  return fn;
+}
+
+// (rows, cols, zdim) map of a column-major operand; box (box_in, box_out, 1).
+// Returns false when the operand does not meet TMA's alignment rules (16-B
+// base, 16-B multiple strides) — the caller then takes the segment loader.
+bool encode_operand(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld,
+                    int64_t stride, int64_t zdim, int box_in, int box_out) {
+  auto fn = encode_fn();
+  if (!fn || rows < 1 || cols < 1 || zdim < 1) return false;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || (ld & 1) != 0) return false;
+  if (zdim > 1 && (stride & 1) != 0) return false;
+  if (ld * 8 >= (int64_t(1) << 40) || stride * 8 >= (int64_t(1) << 40)) return false;
+  if (rows > UINT32_MAX || cols > UINT32_MAX || zdim > UINT32_MAX) return false;
+  const int64_t zstride = zdim > 1 ? stride : (ld * cols + 1) / 2 * 2;
+  cuuint64_t dims[3] = {cuuint64_t(rows), cuuint64_t(cols), cuuint64_t(zdim)};
+  cuuint64_t strides[2] = {cuuint64_t(ld * 8), cuuint64_t(zstride * 8)};
+  cuuint32_t box[3] = {cuuint32_t(box_in), cuuint32_t(box_out), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// loader choice: ctx override, else LRB_LOADER=segment|tma, else automatic
+int loader_mode(const lrb_ctx* ctx) {
+  if (ctx && ctx->loader_override >= 0) return ctx->loader_override;
+  const char* s = std::getenv("LRB_LOADER");
+  if (s && std::strcmp(s, "segment") == 0) return 0;
+  return 1;
+}
+
+// Encode both operand maps of a column-major view for variant v; false if the
+// operands are not TMA-eligible (then the segment loader is used).
+bool encode_pair(const VariantMeta& vm, int a_t, int b_t, int64_t m, int64_t n, int64_t k,
+                 const double* A, int64_t lda, int64_t sA, const double* B, int64_t ldb,
+                 int64_t sB, int64_t batch, CUtensorMap* mA, CUtensorMap* mB, int* a_batched,
+                 int* b_batched) {
+  if (k == 0) return false;
+  const int64_t za = (batch > 1 && sA > 0) ? batch : 1;
+  const int64_t zb = (batch > 1 && sB > 0) ? batch : 1;
+  *a_batched = za > 1;
+  *b_batched = zb > 1;
+  const bool okA = a_t ? encode_operand(mA, A, k, m, lda, sA, za, vm.kb + kPad, vm.mb)
+                       : encode_operand(mA, A, m, k, lda, sA, za, vm.mb + kPad, vm.kb);
+  if (!okA) return false;
+  const bool okB = b_t ? encode_operand(mB, B, n, k, ldb, sB, zb, vm.nb + kPad, vm.kb)
+                       : encode_operand(mB, B, k, n, ldb, sB, zb, vm.kb + kPad, vm.nb);
+  return okB;
+}
 
 // Measured on this pool's B200 (tools/microbench/fp64_peaks.cu, profiles/):
 // DFMA and DMMA both 36.9 TFLOP/s; HBM copy 6553.6 GB/s (MEASURED_PEAKS.json).
@@ -213,6 +281,13 @@ lrb_status run_strided(lrb_ctx* ctx, const Gemm& g, int64_t batch, int beta_one,
   if (ti * tj > INT32_MAX || ti * tj * batch > (int64_t(1) << 62))
     return fail(ctx, LRB_ERR_UNSUPPORTED, "lrb: too many tiles (%lld per item)", (long long)(ti * tj));
   StridedProblem p;
+  std::memset(&p, 0, sizeof(p));
+  int tma = 0;
+  if (loader_mode(ctx) == 1)
+    tma = encode_pair(vm, g.a_t, g.b_t, g.m, g.n, g.k, g.A, g.lda, g.sA, g.B, g.ldb, g.sB, batch,
+                      &p.tmA, &p.tmB, &p.a_batched, &p.b_batched)
+              ? 1
+              : 0;
   p.A = g.A;
   p.B = g.B;
   p.C = g.C;
@@ -229,8 +304,8 @@ lrb_status run_strided(lrb_ctx* ctx, const Gemm& g, int64_t batch, int beta_one,
   p.tiles_per_item = int(ti * tj);
   p.num_tiles = ti * tj * batch;
   LaunchInfo info{0, 0};
-  cudaError_t e = kLaunch[v](g.a_t, g.b_t, &p, nullptr, beta_one, ctx->device, ctx->sm_count,
-                             stream, &info);
+  cudaError_t e = kLaunch[v](g.a_t, g.b_t, tma, &p, nullptr, beta_one, ctx->device,
+                             ctx->sm_count, stream, &info);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "lrb_gemm_kernel launch");
   if (info.grid > 0) ctx->launches.fetch_add(1, std::memory_order_relaxed);
   if (variant_used) *variant_used = v;
@@ -460,6 +535,14 @@ extern "C" lrb_status lrb_set_variant_override(lrb_ctx* ctx, int variant) {
   return LRB_OK;
 }
 
+extern "C" lrb_status lrb_set_loader_override(lrb_ctx* ctx, int mode) {
+  if (!ctx) return fail(nullptr, LRB_ERR_ARG, "lrb_set_loader_override: null ctx");
+  if (mode < -1 || mode > 1)
+    return fail(ctx, LRB_ERR_ARG, "lrb_set_loader_override: mode %d not in {-1, 0, 1}", mode);
+  ctx->loader_override = mode;
+  return LRB_OK;
+}
+
 extern "C" double lrb_item_flops(int64_t m, int64_t n, int64_t k) {
   return 2.0 * double(m) * double(n) * double(k);
 }
@@ -553,9 +636,11 @@ struct lrb_ptr_plan {
   int64_t batch = 0;
   ItemDesc* d_items = nullptr;
   uint64_t* d_tiles = nullptr;
+  CUtensorMap* d_maps = nullptr;  // 2 per item on the TMA path
   struct Group {
     int variant;
     int64_t offset, count;
+    int tma;
   };
   std::vector<Group> groups;
 };
@@ -620,10 +705,24 @@ extern "C" lrb_status lrb_ptr_plan_create(lrb_ctx* ctx, char order, char opA, ch
   plan->b_t = b_t;
   plan->beta_one = beta == 1.0;
   plan->batch = batch;
+  // per-item 2-D maps (one item per map: z extent 1); a variant group takes
+  // the TMA path only if every one of its items is eligible
+  std::vector<CUtensorMap> maps;
+  const bool want_tma = loader_mode(ctx) == 1;
+  if (want_tma && batch > 0) maps.resize(2 * size_t(batch));
   std::vector<uint64_t> tiles;
   for (int v = 0; v < LRB_NUM_VARIANTS; ++v) {
     auto& ids = per_variant[size_t(v)];
     if (ids.empty()) continue;
+    int group_tma = want_tma ? 1 : 0;
+    for (int64_t id : ids) {
+      if (!group_tma) break;
+      const ItemDesc& d = items[size_t(id)];
+      int ab = 0, bb = 0;
+      if (!encode_pair(kVariants[v], a_t, b_t, d.m, d.n, d.k, d.A, d.lda, 0, d.B, d.ldb, 0, 1,
+                       &maps[2 * size_t(id)], &maps[2 * size_t(id) + 1], &ab, &bb))
+        group_tma = 0;
+    }
     // longest-k items first: the persistent grid then drains short tiles last
     std::stable_sort(ids.begin(), ids.end(),
                      [&](int64_t x, int64_t y) { return items[size_t(x)].k > items[size_t(y)].k; });
@@ -636,7 +735,7 @@ extern "C" lrb_status lrb_ptr_plan_create(lrb_ctx* ctx, char order, char opA, ch
         for (int64_t a = 0; a < ti; ++a)
           tiles.push_back((uint64_t(id) << 32) | (uint64_t(a) << 16) | uint64_t(b));
     }
-    plan->groups.push_back({v, off, int64_t(tiles.size()) - off});
+    plan->groups.push_back({v, off, int64_t(tiles.size()) - off, group_tma});
   }
   cudaError_t e;
   if (batch > 0) {
@@ -647,6 +746,18 @@ extern "C" lrb_status lrb_ptr_plan_create(lrb_ctx* ctx, char order, char opA, ch
     if (e != cudaSuccess) {
       lrb_ptr_plan_destroy(ctx, plan);
       return cuda_fail(ctx, e, "lrb_ptr_plan_create: descriptor upload");
+    }
+  }
+  bool any_tma = false;
+  for (const auto& grp : plan->groups) any_tma = any_tma || grp.tma;
+  if (any_tma) {
+    e = cudaMalloc(&plan->d_maps, sizeof(CUtensorMap) * maps.size());
+    if (e == cudaSuccess)
+      e = cudaMemcpy(plan->d_maps, maps.data(), sizeof(CUtensorMap) * maps.size(),
+                     cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      lrb_ptr_plan_destroy(ctx, plan);
+      return cuda_fail(ctx, e, "lrb_ptr_plan_create: tensor map upload");
     }
   }
   if (!tiles.empty()) {
@@ -671,9 +782,10 @@ extern "C" lrb_status lrb_ptr_plan_execute(lrb_ctx* ctx, const lrb_ptr_plan* pla
   lrb_status st = bind(ctx);
   if (st) return st;
   for (const auto& grp : plan->groups) {
-    PtrProblem p{plan->d_items, plan->d_tiles + grp.offset, grp.count};
+    PtrProblem p{plan->d_items, plan->d_tiles + grp.offset, grp.tma ? plan->d_maps : nullptr,
+                 grp.count};
     LaunchInfo info{0, 0};
-    cudaError_t e = kLaunch[grp.variant](plan->a_t, plan->b_t, nullptr, &p, plan->beta_one,
+    cudaError_t e = kLaunch[grp.variant](plan->a_t, plan->b_t, grp.tma, nullptr, &p, plan->beta_one,
                                          ctx->device, ctx->sm_count,
                                          static_cast<cudaStream_t>(stream), &info);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "lrb_gemm_kernel (ptr) launch");
@@ -691,6 +803,7 @@ extern "C" lrb_status lrb_ptr_plan_destroy(lrb_ctx* ctx, lrb_ptr_plan* plan) {
   if (ctx) cudaSetDevice(ctx->device);
   if (plan->d_items) cudaFree(plan->d_items);
   if (plan->d_tiles) cudaFree(plan->d_tiles);
+  if (plan->d_maps) cudaFree(plan->d_maps);
   delete plan;
   return LRB_OK;
 }

@@ -76,6 +76,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// global -> shared TMA tensor copy of a 3-D box (cp.async.bulk.tensor, SASS
+// UTMALDG). `tmap` is the generic address of a CUtensorMap in param or global
+// space; coordinates are element offsets (x innermost).
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int x, int y, int z,
+                                            uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
 // ------------------------------------------------------------ FP64 MMA
 // D(8x8) += A(8x4, row) * B(4x8, col). Lane l = 4g + t holds A[g][t], B[t][g],
 // D[g][2t], D[g][2t+1]. Each D entry is a k-ascending FMA chain (probed on

@@ -14,38 +14,43 @@ struct VariantTraits;
 #define LRB_X(id, nm, WARPS_I, WARPS_J, WI, WJ, KB, ST, MINB)                        \
   template <>                                                                        \
   struct VariantTraits<id> {                                                         \
-    template <bool AT, bool BT>                                                      \
-    using Cfg = GemmCfg<WARPS_I, WARPS_J, WI, WJ, KB, ST, MINB, AT, BT>;             \
+    template <bool AT, bool BT, bool TMA>                                            \
+    using Cfg = GemmCfg<WARPS_I, WARPS_J, WI, WJ, KB, ST, MINB, AT, BT, TMA>;        \
     static constexpr const char* name = #nm;                                         \
   };
 LRB_VARIANT_LIST(LRB_X)
 #undef LRB_X
 
-// a_t / b_t: op flags of the column-major view; exactly one of sp / pp non-null.
+// a_t / b_t: op flags of the column-major view; tma: operands loaded through
+// tensor maps (else per-segment bulk copies); exactly one of sp / pp non-null.
 template <int ID>
-cudaError_t launch_variant(int a_t, int b_t, const StridedProblem* sp, const PtrProblem* pp,
-                           int beta_one, int device, int sm_count, cudaStream_t stream,
-                           LaunchInfo* info) {
+cudaError_t launch_variant(int a_t, int b_t, int tma, const StridedProblem* sp,
+                           const PtrProblem* pp, int beta_one, int device, int sm_count,
+                           cudaStream_t stream, LaunchInfo* info) {
   using VT = VariantTraits<ID>;
-#define LRB_CASE(AT, BT)                                                                       \
-  if (a_t == AT && b_t == BT) {                                                                \
-    using C = typename VT::template Cfg<AT, BT>;                                               \
+#define LRB_CASE(AT, BT, TM)                                                                   \
+  if (a_t == AT && b_t == BT && (tma != 0) == TM) {                                            \
+    using C = typename VT::template Cfg<AT, BT, TM>;                                           \
     return sp ? launch_gemm<C>(*sp, beta_one, device, sm_count, stream, info)                  \
               : launch_gemm<C>(*pp, beta_one, device, sm_count, stream, info);                 \
   }
-  LRB_CASE(0, 0)
-  LRB_CASE(0, 1)
-  LRB_CASE(1, 0)
-  LRB_CASE(1, 1)
+  LRB_CASE(0, 0, true)
+  LRB_CASE(0, 1, true)
+  LRB_CASE(1, 0, true)
+  LRB_CASE(1, 1, true)
+  LRB_CASE(0, 0, false)
+  LRB_CASE(0, 1, false)
+  LRB_CASE(1, 0, false)
+  LRB_CASE(1, 1, false)
 #undef LRB_CASE
   return cudaErrorInvalidValue;
 }
 
-using LaunchFn = cudaError_t (*)(int, int, const StridedProblem*, const PtrProblem*, int, int, int,
-                                 cudaStream_t, LaunchInfo*);
+using LaunchFn = cudaError_t (*)(int, int, int, const StridedProblem*, const PtrProblem*, int, int,
+                                 int, cudaStream_t, LaunchInfo*);
 
 #define LRB_X(id, ...)                                                                         \
-  extern template cudaError_t launch_variant<id>(int, int, const StridedProblem*,              \
+  extern template cudaError_t launch_variant<id>(int, int, int, const StridedProblem*,         \
                                                  const PtrProblem*, int, int, int, cudaStream_t, \
                                                  LaunchInfo*);
 LRB_VARIANT_LIST(LRB_X)

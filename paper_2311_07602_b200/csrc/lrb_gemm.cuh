@@ -8,16 +8,20 @@
 // Structure (persistent CTAs, every warp computes):
 //   * The CTA walks a flattened sequence of (tile, k-chunk) pairs: tiles
 //     blockIdx.x, +gridDim.x, ...; each tile's k range in KB-wide chunks.
-//   * Operands reach shared memory only through TMA bulk copies
-//     (cp.async.bulk, SASS UBLKCP): one copy per contiguous column segment of
-//     the A and B tiles, completing on the stage's `full` mbarrier with
-//     expect_tx. A segment that is not 16-byte aligned / sized (odd ld, odd m
-//     at a ragged edge) is copied by the issuing lane with plain loads into
-//     the same stage under the same barrier, so there is one code path.
+//   * Operands reach shared memory only through TMA. TMA=true (the fast
+//     path): ONE cp.async.bulk.tensor.3d (SASS UTMALDG) per operand per stage
+//     from a (rows, cols, batch) tensor map; the box is 4 elements wider than
+//     the tile along its contiguous dimension, so the landed tile has a row
+//     pitch == 4 (mod 16) doubles and the DMMA fragment loads are
+//     bank-conflict free (64-bit loads are served per half-warp: lanes
+//     (g, tq) g<4 hit pitch*tq + g, 16 distinct bank pairs). Ragged edges are
+//     zero-filled by TMA. TMA=false (misaligned operands: odd ld, unaligned
+//     base): one cp.async.bulk per contiguous column segment, or per-lane
+//     plain loads where a segment is not 16-byte aligned/sized.
 //   * The ring has STAGES slots. Warp 0 issues chunks 0..STAGES-1 up front.
 //     After a warp has consumed a slot it bumps the slot's release counter;
 //     the LAST warp to release it immediately issues the next chunk of the
-//     sequence into it. No warp ever waits to issue, no producer warp holds
+//     sequence into it. No warp waits to issue, no producer warp holds
 //     registers, and refills are issued in chunk order.
 //   * Each warp owns a WI x WJ sub-tile of C in registers as DMMA 8x8x4
 //     fragments. The MMA computes C^T = op(B)^T op(A)^T so a lane's
@@ -26,14 +30,12 @@
 //   * k is consumed in ascending order, 4 at a time by DMMA (each entry an
 //     in-order FMA chain, probed bitwise on B200) and a scalar fma() tail, so
 //     every C entry is exactly the reference's FMA chain.
-// Shared-memory operand layouts are padded so DMMA fragment loads are
-// conflict-free (2 wavefronts per 256 B warp load):
-//   K-rows   X_s[kk][o]  row pitch P = o_extent + pad, P == 8 (mod 16) doubles
-//   K-contig X_s[o][kk]  row pitch P = KB + pad,       P == 4 (mod 16) doubles
-// op(A)=N (A(i,k) at i + k*lda) and op(B)=T are K-rows; op(A)=T and op(B)=N
-// are K-contig. Each K-rows row / K-contig row is one bulk copy.
+// Shared-memory operand layouts (doubles):
+//   K-rows   X_s[kk][o]  pitch = o_extent + 4   (op(A)=N, op(B)=T)
+//   K-contig X_s[o][kk]  pitch = KB + 4         (op(A)=T, op(B)=N)
 #pragma once
 
+#include <cuda.h>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -42,41 +44,46 @@
 namespace lrb {
 
 // ------------------------------------------------------------------ config
-__host__ __device__ constexpr int pad_krows(int extent) { return (8 - extent % 16 + 16) % 16; }
-__host__ __device__ constexpr int pad_kcontig(int kb) { return (4 - kb % 16 + 16) % 16; }
 __host__ __device__ constexpr int round_up_c(int x, int m) { return (x + m - 1) / m * m; }
+constexpr int kPad = 4;  // pitch == extent + 4 == 4 or 12 (mod 16) for extents multiple of 8
 
 template <int WARPS_I_, int WARPS_J_, int WI_, int WJ_, int KB_, int STAGES_, int MINB_, bool A_T_,
-          bool B_T_>
+          bool B_T_, bool TMA_>
 struct GemmCfg {
   static constexpr int WARPS_I = WARPS_I_, WARPS_J = WARPS_J_, WI = WI_, WJ = WJ_;
   static constexpr int KB = KB_, STAGES = STAGES_, MINB = MINB_;
-  static constexpr bool A_T = A_T_, B_T = B_T_;
+  static constexpr bool A_T = A_T_, B_T = B_T_, TMA = TMA_;
   static constexpr int MB = WARPS_I * WI, NB = WARPS_J * WJ;
   static constexpr int FI = WI / 8, FJ = WJ / 8;
   static constexpr int WARPS = WARPS_I * WARPS_J;
   static constexpr int THREADS = WARPS * 32;
   // operand pitches (doubles)
-  static constexpr int PMA = MB + pad_krows(MB);   // A K-rows  (op(A)=N): As[kk][i]
-  static constexpr int PKA = KB + pad_kcontig(KB); // A K-contig (op(A)=T): As[i][kk]
-  static constexpr int PNB = NB + pad_krows(NB);   // B K-rows  (op(B)=T): Bs[kk][j]
-  static constexpr int PKB = KB + pad_kcontig(KB); // B K-contig (op(B)=N): Bs[j][kk]
-  static constexpr int A_ELEMS = round_up_c(A_T ? MB * PKA : KB * PMA, 16);
-  static constexpr int B_ELEMS = round_up_c(B_T ? KB * PNB : NB * PKB, 16);
+  static constexpr int PMA = MB + kPad;  // A K-rows  (op(A)=N): As[kk][i]
+  static constexpr int PKA = KB + kPad;  // A K-contig (op(A)=T): As[i][kk]
+  static constexpr int PNB = NB + kPad;  // B K-rows  (op(B)=T): Bs[kk][j]
+  static constexpr int PKB = KB + kPad;  // B K-contig (op(B)=N): Bs[j][kk]
+  // TMA boxes (inner = contiguous dim incl. pad, outer) == the landed layout
+  static constexpr int A_BOX_IN = A_T ? PKA : PMA, A_BOX_OUT = A_T ? MB : KB;
+  static constexpr int B_BOX_IN = B_T ? PNB : PKB, B_BOX_OUT = B_T ? KB : NB;
+  static constexpr int A_BOX = A_BOX_IN * A_BOX_OUT, B_BOX = B_BOX_IN * B_BOX_OUT;
+  static constexpr int A_ELEMS = round_up_c(A_BOX, 16);  // 128-B aligned sub-buffers
+  static constexpr int B_ELEMS = round_up_c(B_BOX, 16);
   static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
-  // stages + full barriers + release counters + issue state + base alignment slack
+  // stages + full barriers + release counters + issue state
   static constexpr size_t SMEM_BYTES =
-      size_t(STAGES) * STAGE_ELEMS * 8 + size_t(STAGES) * 8 + size_t(STAGES) * 4 + 16 + 128;
+      size_t(STAGES) * STAGE_ELEMS * 8 + size_t(STAGES) * 8 + size_t(STAGES) * 4 + 32;
   static_assert(WI % 8 == 0 && WJ % 8 == 0, "warp tile must be a multiple of the 8x8 fragment");
   static_assert(KB % 4 == 0, "k chunk must be a multiple of the DMMA k (4)");
   static_assert(WARPS % 4 == 0, "warps per CTA must fill all four SM sub-partitions");
+  static_assert(A_BOX_IN <= 256 && A_BOX_OUT <= 256 && B_BOX_IN <= 256 && B_BOX_OUT <= 256,
+                "TMA box dimensions are limited to 256");
 
-  // op(A)(i, kk) and op(B)(kk, j) inside a stage
-  __device__ __forceinline__ static double a_at(const double* As, int i, int kk) {
-    return A_T ? As[i * PKA + kk] : As[kk * PMA + i];
+  // element offsets of op(A)(i, kk) and op(B)(kk, j) inside a stage
+  __device__ __forceinline__ static int a_off(int i, int kk) {
+    return A_T ? i * PKA + kk : kk * PMA + i;
   }
-  __device__ __forceinline__ static double b_at(const double* Bs, int kk, int j) {
-    return B_T ? Bs[kk * PNB + j] : Bs[j * PKB + kk];
+  __device__ __forceinline__ static int b_off(int kk, int j) {
+    return B_T ? kk * PNB + j : j * PKB + kk;
   }
 };
 
@@ -88,17 +95,23 @@ struct TileView {
   int64_t lda, ldb, ldc;
   int m, n, k;
   int i0, j0;
+  const void* tmA;  // tensor maps (TMA path)
+  const void* tmB;
+  int za, zb;  // batch coordinate inside the maps
 };
 
 // Fixed-stride batch: item i at base + i * stride (the reference's
 // LowRankBatch role arrays, low_rank.hpp:147-158).
 struct StridedProblem {
+  CUtensorMap tmA;  // (rows, cols, batch) maps of the stored operands
+  CUtensorMap tmB;
   const double* A;
   const double* B;
   double* C;
   int64_t lda, ldb, ldc, sA, sB, sC;
   int m, n, k;
   int tiles_i, tiles_per_item;
+  int a_batched, b_batched;  // 0 when the stride is 0 (one matrix broadcast)
   int64_t num_tiles;
 
   template <int MB, int NB>
@@ -117,13 +130,18 @@ struct StridedProblem {
     v.k = k;
     v.i0 = (r % tiles_i) * MB;
     v.j0 = (r / tiles_i) * NB;
+    v.tmA = &tmA;
+    v.tmB = &tmB;
+    v.za = a_batched ? static_cast<int>(item) : 0;
+    v.zb = b_batched ? static_cast<int>(item) : 0;
     return v;
   }
   __device__ __forceinline__ int tile_k(int64_t) const { return k; }
 };
 
-// Pointer-array / variable-size batch: per-item descriptors plus a host-built
-// tile list (item << 32 | ti << 16 | tj), largest k first.
+// Pointer-array / variable-size batch: per-item descriptors (and, on the TMA
+// path, a pair of 2-D tensor maps per item) plus a host-built tile list
+// (item << 32 | ti << 16 | tj), largest k first.
 struct ItemDesc {
   const double* A;
   const double* B;
@@ -136,12 +154,14 @@ static_assert(sizeof(ItemDesc) == 64, "ItemDesc is one 64-byte line");
 struct PtrProblem {
   const ItemDesc* items;
   const uint64_t* tiles;
+  const CUtensorMap* maps;  // 2 per item (A, B); null on the segment path
   int64_t num_tiles;
 
   template <int MB, int NB>
   __device__ __forceinline__ TileView tile(int64_t t) const {
     const uint64_t e = tiles[t];
-    const ItemDesc d = items[e >> 32];
+    const uint32_t item = static_cast<uint32_t>(e >> 32);
+    const ItemDesc d = items[item];
     TileView v;
     v.A = d.A;
     v.B = d.B;
@@ -154,6 +174,10 @@ struct PtrProblem {
     v.k = d.k;
     v.i0 = static_cast<int>((e >> 16) & 0xFFFF) * MB;
     v.j0 = static_cast<int>(e & 0xFFFF) * NB;
+    v.tmA = maps ? &maps[2 * size_t(item)] : nullptr;
+    v.tmB = maps ? &maps[2 * size_t(item) + 1] : nullptr;
+    v.za = 0;
+    v.zb = 0;
     return v;
   }
   __device__ __forceinline__ int tile_k(int64_t t) const { return items[tiles[t] >> 32].k; }
@@ -161,7 +185,7 @@ struct PtrProblem {
 
 // next chunk to issue, shared by the CTA's warps
 struct IssueState {
-  int64_t t;
+  long long t;
   int k0;
   int pad;
 };
@@ -190,66 +214,83 @@ __device__ __forceinline__ void issue_chunk(const Problem& prob, double* smem, u
   k0 = __shfl_sync(0xffffffffu, k0, 0);
   if (t >= prob.num_tiles) return;  // sequence exhausted (uniform across the warp)
   const TileView v = prob.template tile<MB, NB>(t);
-  const int ivalid = min(MB, v.m - v.i0);
-  const int jvalid = min(NB, v.n - v.j0);
-  const int kvalid = min(KB, v.k - k0);
-  // A is streamed once when one column tile covers C; B once when one row tile does.
-  const uint64_t pol_a = (v.n <= NB) ? policy_evict_first() : policy_evict_last();
-  const uint64_t pol_b = (v.m <= MB) ? policy_evict_first() : policy_evict_last();
   double* As = smem + size_t(stage) * Cfg::STAGE_ELEMS;
   double* Bs = As + Cfg::A_ELEMS;
-  const int seg_a = Cfg::A_T ? ivalid : kvalid;
-  const int seg_b = Cfg::B_T ? kvalid : jvalid;
-  // order this warp's generic-proxy smem reads of the slot before the async-proxy refill
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  uint32_t bytes = 0;
-#pragma unroll 1
-  for (int s = lane; s < seg_a + seg_b; s += 32) {
-    const double* src;
-    double* dst;
-    int len;
-    uint64_t pol;
-    if (s < seg_a) {
-      if (Cfg::A_T) {
-        src = v.A + k0 + int64_t(v.i0 + s) * v.lda;
-        dst = As + s * Cfg::PKA;
-        len = kvalid;
-      } else {
-        src = v.A + v.i0 + int64_t(k0 + s) * v.lda;
-        dst = As + s * Cfg::PMA;
-        len = ivalid;
-      }
-      pol = pol_a;
-    } else {
-      const int q = s - seg_a;
-      if (Cfg::B_T) {
-        src = v.B + v.j0 + int64_t(k0 + q) * v.ldb;
-        dst = Bs + q * Cfg::PNB;
-        len = jvalid;
-      } else {
-        src = v.B + k0 + int64_t(v.j0 + q) * v.ldb;
-        dst = Bs + q * Cfg::PKB;
-        len = kvalid;
-      }
-      pol = pol_b;
+  // order this CTA's generic-proxy reads of the slot before the async-proxy refill
+  fence_proxy_async_smem();
+  if constexpr (Cfg::TMA) {
+    if (lane == 0) {
+      // A is streamed once when one column tile covers C; B once when one row tile does
+      const uint64_t pol_a = (v.n <= NB) ? policy_evict_first() : policy_evict_last();
+      const uint64_t pol_b = (v.m <= MB) ? policy_evict_first() : policy_evict_last();
+      mbar_arrive_expect_tx(&full[stage], uint32_t(Cfg::A_BOX + Cfg::B_BOX) * 8u);
+      if (Cfg::A_T)
+        tma_load_3d(As, v.tmA, k0, v.i0, v.za, &full[stage], pol_a);
+      else
+        tma_load_3d(As, v.tmA, v.i0, k0, v.za, &full[stage], pol_a);
+      if (Cfg::B_T)
+        tma_load_3d(Bs, v.tmB, v.j0, k0, v.zb, &full[stage], pol_b);
+      else
+        tma_load_3d(Bs, v.tmB, k0, v.j0, v.zb, &full[stage], pol_b);
     }
-    const uint32_t nb = uint32_t(len) * 8u;
-    if (((reinterpret_cast<uintptr_t>(src) & 15) == 0) && ((nb & 15) == 0)) {
-      bulk_g2s(dst, src, nb, &full[stage], pol);
-      bytes += nb;
-    } else {
+  } else {
+    const int ivalid = min(MB, v.m - v.i0);
+    const int jvalid = min(NB, v.n - v.j0);
+    const int kvalid = min(KB, v.k - k0);
+    const uint64_t pol_a = (v.n <= NB) ? policy_evict_first() : policy_evict_last();
+    const uint64_t pol_b = (v.m <= MB) ? policy_evict_first() : policy_evict_last();
+    const int seg_a = Cfg::A_T ? ivalid : kvalid;
+    const int seg_b = Cfg::B_T ? kvalid : jvalid;
+    uint32_t bytes = 0;
+#pragma unroll 1
+    for (int s = lane; s < seg_a + seg_b; s += 32) {
+      const double* src;
+      double* dst;
+      int len;
+      uint64_t pol;
+      if (s < seg_a) {
+        if (Cfg::A_T) {
+          src = v.A + k0 + int64_t(v.i0 + s) * v.lda;
+          dst = As + s * Cfg::PKA;
+          len = kvalid;
+        } else {
+          src = v.A + v.i0 + int64_t(k0 + s) * v.lda;
+          dst = As + s * Cfg::PMA;
+          len = ivalid;
+        }
+        pol = pol_a;
+      } else {
+        const int q = s - seg_a;
+        if (Cfg::B_T) {
+          src = v.B + v.j0 + int64_t(k0 + q) * v.ldb;
+          dst = Bs + q * Cfg::PNB;
+          len = jvalid;
+        } else {
+          src = v.B + k0 + int64_t(v.j0 + q) * v.ldb;
+          dst = Bs + q * Cfg::PKB;
+          len = kvalid;
+        }
+        pol = pol_b;
+      }
+      const uint32_t nb = uint32_t(len) * 8u;
+      if (((reinterpret_cast<uintptr_t>(src) & 15) == 0) && ((nb & 15) == 0)) {
+        bulk_g2s(dst, src, nb, &full[stage], pol);
+        bytes += nb;
+      } else {
 #pragma unroll 4
-      for (int e = 0; e < len; ++e) dst[e] = __ldg(src + e);
+        for (int e = 0; e < len; ++e) dst[e] = __ldg(src + e);
+      }
+    }
+    bytes = __reduce_add_sync(0xffffffffu, bytes);
+    __syncwarp();
+    if (lane == 0) {
+      if (bytes)
+        mbar_arrive_expect_tx(&full[stage], bytes);
+      else
+        mbar_arrive(&full[stage]);
     }
   }
-  bytes = __reduce_add_sync(0xffffffffu, bytes);
-  __syncwarp();
-  if (lane == 0) {
-    if (bytes)
-      mbar_arrive_expect_tx(&full[stage], bytes);
-    else
-      mbar_arrive(&full[stage]);
-    // advance the sequence
+  if (lane == 0) {  // advance the sequence
     int nk0 = k0 + KB;
     int64_t nt = t;
     if (nk0 >= v.k) {
@@ -267,9 +308,9 @@ __device__ __forceinline__ void mma_kstep(double (&acc)[Cfg::FJ][Cfg::FI][2], co
                                           const double* Bs, int ib, int jb, int kk) {
   double af[Cfg::FJ], bf[Cfg::FI];
 #pragma unroll
-  for (int fj = 0; fj < Cfg::FJ; ++fj) af[fj] = Cfg::b_at(Bs, kk, jb + fj * 8);
+  for (int fj = 0; fj < Cfg::FJ; ++fj) af[fj] = Bs[Cfg::b_off(kk, jb + fj * 8)];
 #pragma unroll
-  for (int fi = 0; fi < Cfg::FI; ++fi) bf[fi] = Cfg::a_at(As, ib + fi * 8, kk);
+  for (int fi = 0; fi < Cfg::FI; ++fi) bf[fi] = As[Cfg::a_off(ib + fi * 8, kk)];
 #pragma unroll
   for (int fj = 0; fj < Cfg::FJ; ++fj)
 #pragma unroll
@@ -278,12 +319,12 @@ __device__ __forceinline__ void mma_kstep(double (&acc)[Cfg::FJ][Cfg::FI][2], co
 
 template <class Cfg, class Problem>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
-    lrb_gemm_kernel(const Problem prob, const int beta_one) {
+    lrb_gemm_kernel(const __grid_constant__ Problem prob, const int beta_one) {
   constexpr int MB = Cfg::MB, NB = Cfg::NB, KB = Cfg::KB, STAGES = Cfg::STAGES;
   constexpr int FI = Cfg::FI, FJ = Cfg::FJ;
-  extern __shared__ unsigned char smem_raw[];
-  double* smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
-                                           ~uintptr_t(127));
+  // dynamic shared memory starts 1024-B aligned (no static shared memory);
+  // keep every pointer derived from this array so loads stay LDS
+  extern __shared__ __align__(1024) double smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(STAGES) * Cfg::STAGE_ELEMS);
   IssueState* st = reinterpret_cast<IssueState*>(full + STAGES);
   int* released = reinterpret_cast<int*>(st + 1);
@@ -366,11 +407,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
         for (int kk = nq * 4; kk < kvalid; ++kk) {
 #pragma unroll
           for (int fj = 0; fj < FJ; ++fj) {
-            const double bv = Cfg::b_at(Bs, kk, lj_acc + fj * 8);
+            const double bv = Bs[Cfg::b_off(kk, lj_acc + fj * 8)];
 #pragma unroll
             for (int fi = 0; fi < FI; ++fi) {
-              acc[fj][fi][0] = fma(Cfg::a_at(As, li_acc + fi * 8, kk), bv, acc[fj][fi][0]);
-              acc[fj][fi][1] = fma(Cfg::a_at(As, li_acc + fi * 8 + 1, kk), bv, acc[fj][fi][1]);
+              acc[fj][fi][0] = fma(As[Cfg::a_off(li_acc + fi * 8, kk)], bv, acc[fj][fi][0]);
+              acc[fj][fi][1] = fma(As[Cfg::a_off(li_acc + fi * 8 + 1, kk)], bv, acc[fj][fi][1]);
             }
           }
         }
@@ -382,7 +423,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
         __threadfence_block();
         last = (atomicAdd(&released[stage], 1) == Cfg::WARPS - 1);
         if (last) released[stage] = 0;
-        __threadfence_block();
       }
       last = __shfl_sync(0xffffffffu, last, 0);
       if (last) issue_chunk<Cfg>(prob, smem, full, st, stage, lane);

@@ -343,6 +343,13 @@ class Context:
             raise ArgError(f"unknown kernel variant {name!r}; known: {variant_names()}")
         _check(lib.lrb_set_variant_override(self._h, v), self._h)
 
+    def set_loader(self, mode: Optional[str]) -> None:
+        """None/'auto', 'segment' (per-segment bulk copies) or 'tma' (tensor maps)"""
+        m = {None: -1, "auto": -1, "segment": 0, "tma": 1}.get(mode)
+        if m is None:
+            raise ArgError(f"unknown loader {mode!r}")
+        _check(lib.lrb_set_loader_override(self._h, m), self._h)
+
     # -- hot path
     def dgemm_strided_batched(self, order, opA, opB, m, n, k, beta, A, lda, strideA, B, ldb,
                               strideB, Cm, ldc, strideC, batch, stream: Optional[Stream] = None):

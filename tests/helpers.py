@@ -56,14 +56,16 @@ class Case:
         return (self.order, self.opA, self.opB, self.m, self.n, self.k, self.beta, A, self.lda,
                 self.strideA, B, self.ldb, self.strideB, Cm, self.ldc, self.strideC, self.batch)
 
-    def run_device(self, ctx, variant=None):
+    def run_device(self, ctx, variant=None, loader=None):
         dA, dB, dC = ctx.to_device(self.A), ctx.to_device(self.B), ctx.to_device(self.C0)
         ctx.set_variant_override(variant)
+        ctx.set_loader(loader)
         try:
             ctx.dgemm_strided_batched(*self.args(dA, dB, dC))
             ctx.synchronize()
         finally:
             ctx.set_variant_override(None)
+            ctx.set_loader(None)
         return dC.download(self.C0.size)
 
     def oracle(self, mode=O.FMA_CHAIN):

@@ -78,11 +78,20 @@ def test_beta_must_be_flag(ctx):
 
 
 # ------------------------------------------------------- variants x layouts
+@pytest.mark.parametrize("loader", ["tma", "segment"])
 @pytest.mark.parametrize("variant", variant_names())
 @pytest.mark.parametrize("ops", OPS)
-def test_every_variant_every_op_colmajor(ctx, variant, ops):
-    # ragged m and n, k with a tail (k % 4 == 1) across several k chunks
-    c = Case("C", ops[0], ops[1], 137, 23, 45, 3, seed=11)
+def test_every_variant_every_op_colmajor(ctx, variant, ops, loader):
+    # ragged m and n, k with a tail (k % 4 == 1) across several k chunks;
+    # both operand loaders (TMA tensor maps / per-segment bulk copies)
+    c = Case("C", ops[0], ops[1], 138, 23, 45, 3, seed=11)
+    c.check(c.run_device(ctx, variant, loader))
+
+
+@pytest.mark.parametrize("variant", variant_names())
+def test_every_variant_multi_tile_items(ctx, variant):
+    # several row and column tiles per item, ragged in both, multiple items
+    c = Case("C", "N", "N", 300, 150, 70, 3, seed=31)
     c.check(c.run_device(ctx, variant))
 
 
@@ -117,13 +126,16 @@ def test_beta_zero_never_reads_c(ctx):
     c.check(got)
 
 
-@pytest.mark.parametrize("pad", [(1, 0, 0), (0, 1, 0), (0, 0, 1), (3, 5, 7), (1, 1, 1)])
+@pytest.mark.parametrize("pad", [(1, 0, 0), (0, 1, 0), (0, 0, 1), (3, 5, 7), (1, 1, 1),
+                                 (2, 2, 2), (4, 6, 0)])
 def test_padded_and_odd_leading_dims(ctx, pad):
     # odd ld -> misaligned column segments take the per-lane copy path;
-    # gaps between columns / items must stay untouched (checked bitwise)
+    # even padding keeps the TMA path; gaps between columns / items must stay
+    # untouched (checked bitwise)
     for ops in OPS:
-        c = Case("C", ops[0], ops[1], 41, 19, 23, 3, pad=pad, spad=(3, 1, 5), seed=15)
-        c.check(c.run_device(ctx))
+        for spad in ((3, 1, 5), (2, 4, 6)):
+            c = Case("C", ops[0], ops[1], 41, 19, 23, 3, pad=pad, spad=spad, seed=15)
+            c.check(c.run_device(ctx))
 
 
 def test_broadcast_operand_stride_zero(ctx):
