@@ -150,7 +150,9 @@ bool encode_pair(const VariantMeta& vm, int a_t, int b_t, int64_t m, int64_t n, 
 constexpr double kFp64PeakFlops = 36.9e12;
 constexpr double kHbmBytesPerS = 6553.6e9;
 
-// Automatic choice on the column-major view (m x n output, inner k).
+// Automatic choice on the column-major view (m x n output, inner k); tile
+// sizes per shape class were chosen from the per-variant sweep in
+// profiles/sweep_variants_r01.jsonl.
 int auto_variant(int64_t m, int64_t n) {
   if (n <= 64 && n <= m) {
     if (n <= 8) return LRB_V_N8;
@@ -164,7 +166,7 @@ int auto_variant(int64_t m, int64_t n) {
     if (m <= 32) return LRB_V_M32;
     return LRB_V_M64;
   }
-  return LRB_V_SQ;
+  return LRB_V_N64;  // 128 x 64 tiles, two CTAs per SM
 }
 
 int env_variant() {
@@ -378,6 +380,14 @@ extern "C" lrb_status lrb_destroy(lrb_ctx* ctx) {
     }
     if (ctx->lane_buf[i]) cudaFree(ctx->lane_buf[i]);
   }
+  for (int i = 0; i < lrb_ctx::kAux; ++i) {
+    if (ctx->aux_stream[i]) {
+      cudaStreamSynchronize(ctx->aux_stream[i]);
+      cudaStreamDestroy(ctx->aux_stream[i]);
+    }
+    if (ctx->aux_done[i]) cudaEventDestroy(ctx->aux_done[i]);
+  }
+  if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
   if (ctx->flush_buf) cudaFree(ctx->flush_buf);
   delete ctx;
   return LRB_OK;
@@ -781,15 +791,39 @@ extern "C" lrb_status lrb_ptr_plan_execute(lrb_ctx* ctx, const lrb_ptr_plan* pla
                 plan->device, ctx->device);
   lrb_status st = bind(ctx);
   if (st) return st;
-  for (const auto& grp : plan->groups) {
+  cudaStream_t user = static_cast<cudaStream_t>(stream);
+  // several variant groups: fork them onto auxiliary streams so one group's
+  // tail overlaps the next group's ramp-up, then join back into `user`
+  const int ngroups = int(plan->groups.size());
+  const bool fork = ngroups > 1;
+  if (fork) {
+    if (!ctx->fork_ev) {
+      LRB_CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+      for (int i = 0; i < lrb_ctx::kAux; ++i) {
+        LRB_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->aux_stream[i], cudaStreamNonBlocking));
+        LRB_CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->aux_done[i], cudaEventDisableTiming));
+      }
+    }
+    LRB_CUDA_TRY(ctx, cudaEventRecord(ctx->fork_ev, user));
+    for (int i = 0; i < std::min(ngroups, int(lrb_ctx::kAux)); ++i)
+      LRB_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->aux_stream[i], ctx->fork_ev, 0));
+  }
+  for (int gi = 0; gi < ngroups; ++gi) {
+    const auto& grp = plan->groups[size_t(gi)];
     PtrProblem p{plan->d_items, plan->d_tiles + grp.offset, grp.tma ? plan->d_maps : nullptr,
                  grp.count};
     LaunchInfo info{0, 0};
-    cudaError_t e = kLaunch[grp.variant](plan->a_t, plan->b_t, grp.tma, nullptr, &p, plan->beta_one,
-                                         ctx->device, ctx->sm_count,
-                                         static_cast<cudaStream_t>(stream), &info);
+    cudaStream_t s = fork ? ctx->aux_stream[gi % lrb_ctx::kAux] : user;
+    cudaError_t e = kLaunch[grp.variant](plan->a_t, plan->b_t, grp.tma, nullptr, &p,
+                                         plan->beta_one, ctx->device, ctx->sm_count, s, &info);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "lrb_gemm_kernel (ptr) launch");
     if (info.grid > 0) ctx->launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  if (fork) {
+    for (int i = 0; i < std::min(ngroups, int(lrb_ctx::kAux)); ++i) {
+      LRB_CUDA_TRY(ctx, cudaEventRecord(ctx->aux_done[i], ctx->aux_stream[i]));
+      LRB_CUDA_TRY(ctx, cudaStreamWaitEvent(user, ctx->aux_done[i], 0));
+    }
   }
   return LRB_OK;
 }

@@ -103,8 +103,14 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 }
 
 // ------------------------------------------------------- streaming stores
+// C is written once and never re-read by the kernel: streaming (.cs) stores
+// keep the result stream from evicting the operands the neighbouring tiles
+// of the same item still need from L2.
 __device__ __forceinline__ void st_global_v2(double* p, double x, double y) {
-  asm volatile("st.global.v2.f64 [%0], {%1, %2};\n" ::"l"(p), "d"(x), "d"(y) : "memory");
+  asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};\n" ::"l"(p), "d"(x), "d"(y) : "memory");
+}
+__device__ __forceinline__ void st_global_cs(double* p, double x) {
+  asm volatile("st.global.cs.f64 [%0], %1;\n" ::"l"(p), "d"(x) : "memory");
 }
 
 }  // namespace lrb

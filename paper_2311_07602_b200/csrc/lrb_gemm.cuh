@@ -444,8 +444,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
           if (vec_ok && i + 1 < v.m) {
             st_global_v2(cp + i, acc[fj][fi][0], acc[fj][fi][1]);
           } else {
-            if (i < v.m) cp[i] = acc[fj][fi][0];
-            if (i + 1 < v.m) cp[i + 1] = acc[fj][fi][1];
+            if (i < v.m) st_global_cs(cp + i, acc[fj][fi][0]);
+            if (i + 1 < v.m) st_global_cs(cp + i + 1, acc[fj][fi][1]);
           }
         }
       }

@@ -25,6 +25,12 @@ struct lrb_ctx {
   cudaStream_t lane_stream[kLanes] = {nullptr, nullptr, nullptr};
   double* lane_buf[kLanes] = {nullptr, nullptr, nullptr};
   size_t lane_bytes[kLanes] = {0, 0, 0};
+  // pointer-array plans: one auxiliary stream per variant group so the groups'
+  // persistent grids overlap their tails (fork/join through events)
+  static constexpr int kAux = 4;
+  cudaStream_t aux_stream[kAux] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t aux_done[kAux] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t fork_ev = nullptr;
   // L2 flush buffer
   void* flush_buf = nullptr;
   size_t flush_bytes = 0;
