@@ -192,12 +192,16 @@ def cpu_sample_run(w, items, threads):
         B = O.fill_uniform(w.b_rows, w.b_cols, w.ldb, w.sB, n, w.seed, W.ROLE_B, first)
         Cm = np.zeros(w.sC * n)
         t0 = time.perf_counter()
-        if O.ref_available():
+        if O.ref_available() and w.order == "R" and w.opA == "N" and w.opB == "N":
+            # the reference's own row-major call, item by item
+            O.ref_rowmajor_batched(A, B, Cm, w.m, w.k, w.n, 0, n, threads=threads)
+            kind = "reference"
+        elif O.ref_available() and w.order == "C":
             O.ref_dgemm_colmajor(w.opA, w.opB, w.m, w.n, w.k, 0, A, w.lda, w.sA, B, w.ldb, w.sB,
                                  Cm, w.ldc, w.sC, n, threads=threads)
             kind = "reference"
         else:
-            O.dgemm_strided("C", w.opA, w.opB, w.m, w.n, w.k, 0.0, A, w.lda, w.sA, B, w.ldb,
+            O.dgemm_strided(w.order, w.opA, w.opB, w.m, w.n, w.k, 0.0, A, w.lda, w.sA, B, w.ldb,
                             w.sB, Cm, w.ldc, w.sC, n, threads=threads, mode=O.REF_COMPILED)
             kind = "port"
         dt = time.perf_counter() - t0
@@ -464,7 +468,7 @@ def run_gpu_arm(args, w, world, rank, local, pg):
     # ---- dominant kernel roofline (this rank, per launch)
     per_launch_ms = ms_rank / max(1, launches)
     launch_items = count if resident else chunk
-    sel = select("C", w.opA, w.opB, w.m, w.n, w.k, launch_items, ctx)
+    sel = select(w.order, w.opA, w.opB, w.m, w.n, w.k, launch_items, ctx)
     intensity = w.item_flops() / w.item_bytes()
     fp64_bound = intensity >= (fp64_peak * 1e12) / (hbm_peak * 1e9)
     if fp64_bound:

@@ -157,7 +157,11 @@ int auto_variant(int64_t m, int64_t n) {
   if (n <= 64 && n <= m) {
     if (n <= 8) return LRB_V_N8;
     if (n <= 16) return LRB_V_N16;
+    if (n <= 24) return LRB_V_N24;
     if (n <= 32) return LRB_V_N32;
+    if (n <= 40) return LRB_V_N40;
+    if (n <= 48) return LRB_V_N48;
+    if (n <= 56) return LRB_V_N56;
     return LRB_V_N64;
   }
   if (m <= 64 && m < n) {

@@ -15,25 +15,25 @@
 //   n64 : 128 x 64 tiles at two CTAs per SM — also the general-shape choice:
 //         one CTA's epilogue overlaps the other's MMAs (low-rank expansion
 //         U * V^T, blr.hpp:75-78, measured 1.17x over 128 x 128 tiles).
-//   n16s, n32s : 64-row tiles at three CTAs per SM for small batches.
-//   n16k16, n32x3 : KB = 16 alternatives kept for the selector sweep.
+//   n24, n40, n48, n56 : intermediate widths so a variable-rank batch
+//         (cfg4, r_i in 8..64) wastes less than one 8-column fragment.
 #pragma once
 
 //            id  name  WARPS_I WARPS_J WI  WJ  KB  STAGES MINB
-#define LRB_VARIANT_LIST(X)             \
-  X(0, n8, 4, 1, 32, 8, 32, 2, 2)       \
-  X(1, n16, 4, 1, 32, 16, 32, 2, 2)     \
-  X(2, n32, 4, 1, 32, 32, 32, 2, 2)     \
-  X(3, n64, 4, 2, 32, 32, 32, 2, 2)     \
-  X(4, sq, 2, 4, 64, 32, 32, 3, 1)      \
-  X(5, m8, 1, 4, 8, 32, 32, 2, 2)       \
-  X(6, m16, 1, 4, 16, 32, 32, 2, 2)     \
-  X(7, m32, 1, 4, 32, 32, 32, 2, 2)     \
-  X(8, m64, 2, 4, 32, 32, 32, 2, 2)     \
-  X(9, n16s, 4, 1, 16, 16, 32, 2, 3)    \
-  X(10, n32s, 4, 1, 16, 32, 32, 2, 3)   \
-  X(11, n16k16, 4, 1, 32, 16, 16, 5, 2) \
-  X(12, n32x3, 4, 1, 32, 32, 16, 3, 3)
+#define LRB_VARIANT_LIST(X)          \
+  X(0, n8, 4, 1, 32, 8, 32, 2, 2)    \
+  X(1, n16, 4, 1, 32, 16, 32, 2, 2)  \
+  X(2, n32, 4, 1, 32, 32, 32, 2, 2)  \
+  X(3, n64, 4, 2, 32, 32, 32, 2, 2)  \
+  X(4, sq, 2, 4, 64, 32, 32, 3, 1)   \
+  X(5, m8, 1, 4, 8, 32, 32, 2, 2)    \
+  X(6, m16, 1, 4, 16, 32, 32, 2, 2)  \
+  X(7, m32, 1, 4, 32, 32, 32, 2, 2)  \
+  X(8, m64, 2, 4, 32, 32, 32, 2, 2)  \
+  X(9, n24, 4, 1, 32, 24, 32, 2, 2)  \
+  X(10, n40, 4, 1, 32, 40, 32, 2, 2) \
+  X(11, n48, 4, 2, 32, 24, 32, 2, 2) \
+  X(12, n56, 8, 1, 16, 56, 32, 2, 2)
 
 #define LRB_NUM_VARIANTS 13
 
@@ -47,6 +47,8 @@ enum {
   LRB_V_M16 = 6,
   LRB_V_M32 = 7,
   LRB_V_M64 = 8,
-  LRB_V_N16S = 9,
-  LRB_V_N32S = 10
+  LRB_V_N24 = 9,
+  LRB_V_N40 = 10,
+  LRB_V_N48 = 11,
+  LRB_V_N56 = 12
 };

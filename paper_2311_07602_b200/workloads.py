@@ -70,21 +70,34 @@ class Strided:
     order: str = "C"
     beta: float = 0.0
 
+    # (rows, cols) of each stored operand in the caller's order
+    def _stored_a(self):
+        return (self.k, self.m) if self.opA == "T" else (self.m, self.k)
+
+    def _stored_b(self):
+        return (self.n, self.k) if self.opB == "T" else (self.k, self.n)
+
+    def _view(self, rc):
+        """column-major view of a stored matrix: row-major r x c == column-major c x r"""
+        return rc if self.order == "C" else (rc[1], rc[0])
+
+    # the properties below describe the COLUMN-MAJOR VIEW of each buffer
+    # (what lrb_fill_uniform fills); ld is the same number in either order
     @property
     def a_rows(self):
-        return self.k if self.opA == "T" else self.m
+        return self._view(self._stored_a())[0]
 
     @property
     def a_cols(self):
-        return self.m if self.opA == "T" else self.k
+        return self._view(self._stored_a())[1]
 
     @property
     def b_rows(self):
-        return self.n if self.opB == "T" else self.k
+        return self._view(self._stored_b())[0]
 
     @property
     def b_cols(self):
-        return self.k if self.opB == "T" else self.n
+        return self._view(self._stored_b())[1]
 
     @property
     def lda(self):
@@ -96,7 +109,7 @@ class Strided:
 
     @property
     def ldc(self):
-        return self.m
+        return self.m if self.order == "C" else self.n
 
     @property
     def sA(self):
@@ -187,9 +200,12 @@ def get(name: str):
         # low-rank expansion C = U V^T, U and V 512 x 32 column-major
         return Strided("cfg2", 512, 512, 32, 4096, seed=1, opA="N", opB="T")
     if name.startswith("cfg3"):
+        # cfg3_b{B}_r{R}: BASELINE's column-major sweep; cfg3r_...: the same
+        # shapes in the reference's own row-major storage (the drop-in case)
         parts = dict(p[0:1] and (p[0], p[1:]) for p in name.split("_")[1:])
         b, r = int(parts["b"]), int(parts["r"])
-        return Strided(name, b, r, b, cfg3_batch(b, r), seed=2)
+        order = "R" if name.startswith("cfg3r") else "C"
+        return Strided(name, b, r, b, cfg3_batch(b, r), seed=2, order=order)
     if name == "cfg4":
         return Variable("cfg4", 8192, seed=3)
     if name == "cfg5":

@@ -93,7 +93,7 @@ def main():
             roof = min(fp64 * 1e12, intensity * hbm * 1e9)
             from paper_2311_07602_b200 import select
 
-            sel = select("C", w.opA, w.opB, w.m, w.n, w.k, count, ctx)
+            sel = select(w.order, w.opA, w.opB, w.m, w.n, w.k, count, ctx)
             print(json.dumps({"config": name, "variant": sel["name"], "items": count,
                               "ms": round(med, 4), "ms_best": round(best, 4),
                               "gflops": round(fl / med / 1e6, 1), "gbs": round(by / med / 1e6, 1),
