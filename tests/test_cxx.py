@@ -1,0 +1,30 @@
+"""The C++ host mirror (include/lrbatch_b200.hpp) compiles against the C-ABI
+here and runs on the GPU."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = os.path.join(ROOT, "tests", "cxx", "test_wrapper.cpp")
+LIBDIR = os.path.join(ROOT, "paper_2311_07602_b200")
+
+
+def _build(out):
+    cmd = ["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"), SRC, "-o", out,
+           "-L", LIBDIR, "-llrb", f"-Wl,-rpath,{LIBDIR}"]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+
+
+def test_cxx_wrapper_compiles_and_links(tmp_path):
+    _build(str(tmp_path / "t"))
+    assert os.path.exists(tmp_path / "t")
+
+
+@pytest.mark.gpu
+def test_cxx_wrapper_runs(tmp_path):
+    exe = str(tmp_path / "t")
+    _build(exe)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failures" in r.stdout

@@ -1,0 +1,163 @@
+"""CPU: pin the oracle to the reference.
+
+* golden vectors produced by the reference binary (tests/golden/make_golden.py,
+  oracle/_ref built from /root/reference) — the C restatement must reproduce
+  them BITWISE in its reference-rounding mode, and its FMA-chain mode (the
+  device kernels' rounding) must sit inside BASELINE's componentwise bound;
+* the reference's own known-answer cases (tests/test_core.cpp:24-49);
+* the bound checker's negative control (tests/test_kernels.cpp:286-294);
+* the counter RNG (host C == host Python, values pinned).
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2311_07602_b200 import workloads as W
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLDEN = np.load(os.path.join(HERE, "golden", "gemm_golden.npz"))
+META = json.loads(bytes(GOLDEN["meta"]).decode())
+
+
+def stored(order, op, r, c):
+    s = (c, r) if op == "T" else (r, c)
+    return s if order == "C" else (s[1], s[0])
+
+
+def _inputs(order, opA, opB, m, n, k, batch, acc, seed):
+    ar, ac = stored(order, opA, m, k)
+    br, bc = stored(order, opB, k, n)
+    cr, cc = stored(order, "N", m, n)
+    A = O.fill_uniform(ar, ac, ar, ar * ac, batch, seed, 0)
+    B = O.fill_uniform(br, bc, br, br * bc, batch, seed, 1)
+    C0 = O.fill_uniform(cr, cc, cr, cr * cc, batch, seed, 2) if acc else np.zeros(cr * cc * batch)
+    return A, B, C0, (ar, ac), (br, bc), (cr, cc)
+
+
+def _oracle(mode, order, opA, opB, m, n, k, batch, acc, A, B, C0, sa, sb, sc):
+    out = C0.copy()
+    O.dgemm_strided(order, opA, opB, m, n, k, float(acc), A, sa[0], sa[0] * sa[1], B, sb[0],
+                    sb[0] * sb[1], out, sc[0], sc[0] * sc[1], batch, threads=4, mode=mode)
+    return out
+
+
+@pytest.mark.parametrize("case", META["small"], ids=[c[0] for c in META["small"]])
+def test_golden_small_cases(case):
+    name, order, opA, opB, m, n, k, batch, acc, seed = case
+    A, B, C0, sa, sb, sc = _inputs(order, opA, opB, m, n, k, batch, acc, seed)
+    # the inputs the reference saw are exactly what the counter RNG regenerates
+    assert np.array_equal(A, GOLDEN[f"{name}__A"])
+    assert np.array_equal(B, GOLDEN[f"{name}__B"])
+    assert np.array_equal(C0, GOLDEN[f"{name}__C0"])
+    want = GOLDEN[f"{name}__C"]
+    got = _oracle(O.REF_COMPILED, order, opA, opB, m, n, k, batch, acc, A, B, C0, sa, sb, sc)
+    assert np.array_equal(got, want), "oracle restatement != reference binary"
+    fma = _oracle(O.FMA_CHAIN, order, opA, opB, m, n, k, batch, acc, A, B, C0, sa, sb, sc)
+    for it in range(batch):
+        o = it * sc[0] * sc[1]
+        bad, ratio = O.check_bound(order, opA, opB, m, n, k, float(acc), A[it * sa[0] * sa[1]:],
+                                   sa[0], B[it * sb[0] * sb[1]:], sb[0],
+                                   C0[o:] if acc else None, fma[o:], want[o:], sc[0])
+        assert bad == 0, f"{name} item {it}: FMA chain outside the FP64 bound (ratio {ratio})"
+
+
+@pytest.mark.parametrize("case", META["digest"], ids=[c[0] for c in META["digest"]])
+def test_golden_baseline_digests(case):
+    name, order, opA, opB, m, n, k, batch, acc, seed, digest, first, last = case
+    A, B, C0, sa, sb, sc = _inputs(order, opA, opB, m, n, k, batch, acc, seed)
+    got = _oracle(O.REF_COMPILED, order, opA, opB, m, n, k, batch, acc, A, B, C0, sa, sb, sc)
+    assert got[0] == first and got[-1] == last
+    assert hashlib.sha256(got.tobytes()).hexdigest() == digest
+
+
+def test_golden_flops_counter():
+    f = META["flops"]
+    c = np.zeros(f["m"] * f["n"])
+    fl = np.zeros(1, dtype=np.uint64)
+    O.gemm_naive_raw(GOLDEN["flops__A"], GOLDEN["flops__B"], c, f["m"], f["k"], f["n"], False, fl)
+    assert int(fl[0]) == f["count"] == 2 * f["m"] * f["n"] * f["k"]
+    # the flops != NULL path is fully unfused in the reference binary
+    assert np.array_equal(c, GOLDEN["flops__C"])
+
+
+def test_known_answers_reference_tests():
+    # tests/test_core.cpp:24-39
+    ident = np.eye(3).ravel()
+    mm = np.arange(1, 10, dtype=np.float64)
+    c = np.zeros(9)
+    O.gemm_naive_raw(ident, mm, c, 3, 3, 3, False)
+    assert np.array_equal(c, mm)
+    c = np.zeros(8)
+    O.gemm_naive_raw(np.zeros(10), np.full(20, 3.25), c, 2, 5, 4, False)
+    assert np.all(c == 0.0)
+    c = np.zeros(4)
+    O.gemm_naive_raw(np.array([1., 2, 3, 4]), np.array([5., 6, 7, 8]), c, 2, 2, 2, False)
+    assert c.tolist() == [19, 22, 43, 50]
+    # :41-49 accumulate
+    c = np.full(4, 10.0)
+    O.gemm_naive_raw(np.array([1., 0, 0, 1]), np.array([1., 2, 3, 4]), c, 2, 2, 2, True)
+    assert c.tolist() == [11, 12, 13, 14]
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("shape", [(1, 1, 1), (2, 3, 4), (9, 7, 33), (31, 17, 64), (128, 16, 127)])
+@pytest.mark.parametrize("acc", [False, True])
+def test_restatement_equals_reference_binary(shape, acc):
+    m, k, n = shape
+    rng = np.random.default_rng(m * 100 + k)
+    a, b = rng.uniform(-1, 1, m * k), rng.uniform(-1, 1, k * n)
+    c0 = rng.uniform(-1, 1, m * n)
+    for with_flops in (False, True):
+        c1, c2 = c0.copy(), c0.copy()
+        f1 = np.zeros(1, np.uint64) if with_flops else None
+        f2 = np.zeros(1, np.uint64) if with_flops else None
+        O.ref_gemm_naive_raw(a, b, c1, m, k, n, acc, f1)
+        O.gemm_naive_raw(a, b, c2, m, k, n, acc, f2)
+        assert np.array_equal(c1, c2)
+        if with_flops:
+            assert f1[0] == f2[0] == 2 * m * n * k
+
+
+def test_bound_checker_negative_control():
+    m, n, k = 12, 6, 10
+    A = O.fill_uniform(m, k, m, m * k, 1, 7, 0)
+    B = O.fill_uniform(k, n, k, k * n, 1, 7, 1)
+    ref = np.zeros(m * n)
+    O.dgemm_strided("C", "N", "N", m, n, k, 0.0, A, m, 0, B, k, 0, ref, m, 0, 1,
+                    mode=O.REF_COMPILED)
+    good = np.zeros(m * n)
+    O.dgemm_strided("C", "N", "N", m, n, k, 0.0, A, m, 0, B, k, 0, good, m, 0, 1)
+    assert O.check_bound("C", "N", "N", m, n, k, 0.0, A, m, B, k, None, good, ref, m)[0] == 0
+    bad = good.copy()
+    bad[5] += 1e-9
+    nbad, ratio = O.check_bound("C", "N", "N", m, n, k, 0.0, A, m, B, k, None, bad, ref, m)
+    assert nbad == 1 and ratio > 1.0
+    nan = good.copy()
+    nan[3] = np.nan
+    assert O.check_bound("C", "N", "N", m, n, k, 0.0, A, m, B, k, None, nan, ref, m)[0] == 1
+
+
+def test_rng_c_matches_python_and_is_pinned():
+    x = O.fill_uniform(5, 3, 7, 21, 2, 9, 1, 100)
+    key = W.stream_key(9, 1)
+    for it in range(2):
+        for c in range(3):
+            for r in range(5):
+                assert x[it * 21 + c * 7 + r] == W.uniform(key, 100 + it, r + c * 5)
+    # pinned values (a change of generator breaks every stored golden vector)
+    assert W.uniform(W.stream_key(0, 0), 0, 0) == O.fill_uniform(1, 1, 1, 1, 1, 0, 0)[0]
+    v = O.fill_uniform(1000, 1, 1000, 1000, 1, 3, 0)
+    assert v.min() >= -1.0 and v.max() < 1.0 and abs(v.mean()) < 0.1
+
+
+def test_cfg4_shapes_are_deterministic():
+    w = W.get("cfg4")
+    assert len(w.bs) == 8192 and set(w.bs) == {256, 512, 1024}
+    assert min(w.rs) == 8 and max(w.rs) == 64
+    w2 = W.Variable("cfg4", 8192, seed=3)
+    assert w.bs == w2.bs and w.rs == w2.rs
+    assert 29.0 < w.bytes() / 2 ** 30 < 32.0  # ~30.6 GiB
