@@ -170,7 +170,13 @@ int auto_variant(int64_t m, int64_t n) {
     if (m <= 32) return LRB_V_M32;
     return LRB_V_M64;
   }
-  return LRB_V_N64;  // 128 x 64 tiles, two CTAs per SM
+  return LRB_V_Q64;  // 64 x 64 tiles, three CTAs per SM (U * V^T: profiles/sweep_*)
+}
+
+// debug-only kernel flags for probes (tools/probe_cfg2.py): bit 1 skips C stores
+int debug_flags() {
+  const char* s = std::getenv("LRB_DEBUG_FLAGS");
+  return s ? (std::atoi(s) & 6) : 0;
 }
 
 int env_variant() {
@@ -309,9 +315,10 @@ lrb_status run_strided(lrb_ctx* ctx, const Gemm& g, int64_t batch, int beta_one,
   p.tiles_i = int(ti);
   p.tiles_per_item = int(ti * tj);
   p.num_tiles = ti * tj * batch;
+  p.j_fastest = (debug_flags() & 4) ? 1 : 0;
   LaunchInfo info{0, 0};
-  cudaError_t e = kLaunch[v](g.a_t, g.b_t, tma, &p, nullptr, beta_one, ctx->device,
-                             ctx->sm_count, stream, &info);
+  cudaError_t e = kLaunch[v](g.a_t, g.b_t, tma, &p, nullptr, beta_one | debug_flags(),
+                             ctx->device, ctx->sm_count, stream, &info);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "lrb_gemm_kernel launch");
   if (info.grid > 0) ctx->launches.fetch_add(1, std::memory_order_relaxed);
   if (variant_used) *variant_used = v;

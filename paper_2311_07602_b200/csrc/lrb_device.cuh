@@ -109,6 +109,12 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 __device__ __forceinline__ void st_global_v2(double* p, double x, double y) {
   asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};\n" ::"l"(p), "d"(x), "d"(y) : "memory");
 }
+// 32-byte store (sm_100: STG.E.EF.256)
+__device__ __forceinline__ void st_global_v4(double* p, double x, double y, double z, double w) {
+  asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "d"(x), "d"(y), "d"(z),
+               "d"(w)
+               : "memory");
+}
 __device__ __forceinline__ void st_global_cs(double* p, double x) {
   asm volatile("st.global.cs.f64 [%0], %1;\n" ::"l"(p), "d"(x) : "memory");
 }

@@ -78,6 +78,28 @@ struct GemmCfg {
   static_assert(A_BOX_IN <= 256 && A_BOX_OUT <= 256 && B_BOX_IN <= 256 && B_BOX_OUT <= 256,
                 "TMA box dimensions are limited to 256");
 
+  // Fragment pairing: where the operand's tile dimension is contiguous in
+  // shared memory (K-rows layouts), fragments (2p, 2p+1) take the adjacent
+  // rows (2g, 2g+1): one conflict-free LDS.128 feeds two fragments, and (for
+  // the i side) a lane's accumulators become 4 consecutive rows of C, stored
+  // with one 32-byte st.global.v4 so each warp store covers whole 128-B lines.
+  static constexpr bool PAIR_I = !A_T && (FI % 2 == 0);
+  static constexpr bool PAIR_J = B_T && (FJ % 2 == 0);
+
+  // in-tile row (i) of B-operand fragment fi / n-index g (loads)
+  __device__ __forceinline__ static int load_row(int wi, int fi, int g) {
+    return PAIR_I ? wi * WI + 16 * (fi >> 1) + 2 * g + (fi & 1) : wi * WI + 8 * fi + g;
+  }
+  // in-tile column (j) of A-operand fragment fj / row g (loads and accumulators)
+  __device__ __forceinline__ static int load_col(int wj, int fj, int g) {
+    return PAIR_J ? wj * WJ + 16 * (fj >> 1) + 2 * g + (fj & 1) : wj * WJ + 8 * fj + g;
+  }
+  // in-tile row of accumulator acc[.][fi][c] of lane quad tq
+  __device__ __forceinline__ static int acc_row(int wi, int fi, int c, int tq) {
+    return PAIR_I ? wi * WI + 16 * (fi >> 1) + 2 * (2 * tq + c) + (fi & 1)
+                  : wi * WI + 8 * fi + 2 * tq + c;
+  }
+
   // element offsets of op(A)(i, kk) and op(B)(kk, j) inside a stage
   __device__ __forceinline__ static int a_off(int i, int kk) {
     return A_T ? i * PKA + kk : kk * PMA + i;
@@ -112,6 +134,7 @@ struct StridedProblem {
   int m, n, k;
   int tiles_i, tiles_per_item;
   int a_batched, b_batched;  // 0 when the stride is 0 (one matrix broadcast)
+  int j_fastest;             // tile order inside an item: column tiles vary fastest
   int64_t num_tiles;
 
   template <int MB, int NB>
@@ -128,8 +151,14 @@ struct StridedProblem {
     v.m = m;
     v.n = n;
     v.k = k;
-    v.i0 = (r % tiles_i) * MB;
-    v.j0 = (r / tiles_i) * NB;
+    if (j_fastest) {
+      const int tiles_j = tiles_per_item / tiles_i;
+      v.i0 = (r / tiles_j) * MB;
+      v.j0 = (r % tiles_j) * NB;
+    } else {
+      v.i0 = (r % tiles_i) * MB;
+      v.j0 = (r / tiles_i) * NB;
+    }
     v.tmA = &tmA;
     v.tmB = &tmB;
     v.za = a_batched ? static_cast<int>(item) : 0;
@@ -305,12 +334,32 @@ __device__ __forceinline__ void issue_chunk(const Problem& prob, double* smem, u
 
 template <class Cfg>
 __device__ __forceinline__ void mma_kstep(double (&acc)[Cfg::FJ][Cfg::FI][2], const double* As,
-                                          const double* Bs, int ib, int jb, int kk) {
+                                          const double* Bs, int wi, int wj, int g, int kk) {
   double af[Cfg::FJ], bf[Cfg::FI];
+  if constexpr (Cfg::PAIR_J) {
 #pragma unroll
-  for (int fj = 0; fj < Cfg::FJ; ++fj) af[fj] = Bs[Cfg::b_off(kk, jb + fj * 8)];
+    for (int q = 0; q < Cfg::FJ / 2; ++q) {
+      const double2 v =
+          *reinterpret_cast<const double2*>(&Bs[Cfg::b_off(kk, Cfg::load_col(wj, 2 * q, g))]);
+      af[2 * q] = v.x;
+      af[2 * q + 1] = v.y;
+    }
+  } else {
 #pragma unroll
-  for (int fi = 0; fi < Cfg::FI; ++fi) bf[fi] = As[Cfg::a_off(ib + fi * 8, kk)];
+    for (int fj = 0; fj < Cfg::FJ; ++fj) af[fj] = Bs[Cfg::b_off(kk, Cfg::load_col(wj, fj, g))];
+  }
+  if constexpr (Cfg::PAIR_I) {
+#pragma unroll
+    for (int p = 0; p < Cfg::FI / 2; ++p) {
+      const double2 v =
+          *reinterpret_cast<const double2*>(&As[Cfg::a_off(Cfg::load_row(wi, 2 * p, g), kk)]);
+      bf[2 * p] = v.x;
+      bf[2 * p + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int fi = 0; fi < Cfg::FI; ++fi) bf[fi] = As[Cfg::a_off(Cfg::load_row(wi, fi, g), kk)];
+  }
 #pragma unroll
   for (int fj = 0; fj < Cfg::FJ; ++fj)
 #pragma unroll
@@ -319,7 +368,10 @@ __device__ __forceinline__ void mma_kstep(double (&acc)[Cfg::FJ][Cfg::FI][2], co
 
 template <class Cfg, class Problem>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
-    lrb_gemm_kernel(const __grid_constant__ Problem prob, const int beta_one) {
+    lrb_gemm_kernel(const __grid_constant__ Problem prob, const int flags) {
+  // flags bit 0: beta = 1 (accumulate into C); bit 1: debug probe, skip the
+  // epilogue stores (LRB_DEBUG_FLAGS, never set by the library itself)
+  const int beta_one = flags & 1;
   constexpr int MB = Cfg::MB, NB = Cfg::NB, KB = Cfg::KB, STAGES = Cfg::STAGES;
   constexpr int FI = Cfg::FI, FJ = Cfg::FJ;
   // dynamic shared memory starts 1024-B aligned (no static shared memory);
@@ -352,14 +404,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   const int wj = warp / Cfg::WARPS_I;
   const int g = lane >> 2;
   const int tq = lane & 3;
-  // local (in-tile) coordinates of this lane's fragments:
-  //   B-operand rows (i) of fragment fi: wi*WI + fi*8 + g       (loads)
-  //   A-operand rows (j) of fragment fj: wj*WJ + fj*8 + g       (loads)
-  //   accumulator pair (fj, fi): C(i = wi*WI + fi*8 + 2tq + {0,1}, j = wj*WJ + fj*8 + g)
-  const int li_load = wi * Cfg::WI + g;
-  const int lj_load = wj * Cfg::WJ + g;
-  const int li_acc = wi * Cfg::WI + 2 * tq;
-  const int lj_acc = wj * Cfg::WJ + g;
+  // in-tile coordinates of this lane's fragments: Cfg::load_row / load_col /
+  // acc_row (accumulator acc[fj][fi][c] is C(acc_row(fi, c), load_col(fj)))
 
   int stage = 0;
   uint32_t phase = 0;
@@ -367,6 +413,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   for (int64_t t = blockIdx.x; t < prob.num_tiles; t += gridDim.x) {
     const TileView v = prob.template tile<MB, NB>(t);
     const bool vec_ok = ((reinterpret_cast<uintptr_t>(v.C) & 15) == 0) && ((v.ldc & 1) == 0);
+    const bool vec4_ok = ((reinterpret_cast<uintptr_t>(v.C) & 31) == 0) && ((v.ldc & 3) == 0);
 
     double acc[FJ][FI][2];
 #pragma unroll
@@ -376,15 +423,16 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     if (beta_one) {
 #pragma unroll
       for (int fj = 0; fj < FJ; ++fj) {
-        const int j = v.j0 + lj_acc + fj * 8;
+        const int j = v.j0 + Cfg::load_col(wj, fj, g);
         if (j < v.n) {
           const double* cp = v.C + int64_t(j) * v.ldc;
 #pragma unroll
-          for (int fi = 0; fi < FI; ++fi) {
-            const int i = v.i0 + li_acc + fi * 8;
-            if (i < v.m) acc[fj][fi][0] = cp[i];
-            if (i + 1 < v.m) acc[fj][fi][1] = cp[i + 1];
-          }
+          for (int fi = 0; fi < FI; ++fi)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              const int i = v.i0 + Cfg::acc_row(wi, fi, c, tq);
+              if (i < v.m) acc[fj][fi][c] = cp[i];
+            }
         }
       }
     }
@@ -397,22 +445,23 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
       const double* Bs = As + Cfg::A_ELEMS;
       if (kvalid == KB) {
 #pragma unroll
-        for (int kq = 0; kq < KB / 4; ++kq) mma_kstep<Cfg>(acc, As, Bs, li_load, lj_load, kq * 4 + tq);
+        for (int kq = 0; kq < KB / 4; ++kq) mma_kstep<Cfg>(acc, As, Bs, wi, wj, g, kq * 4 + tq);
       } else {
         const int nq = kvalid >> 2;
 #pragma unroll 1
-        for (int kq = 0; kq < nq; ++kq) mma_kstep<Cfg>(acc, As, Bs, li_load, lj_load, kq * 4 + tq);
+        for (int kq = 0; kq < nq; ++kq) mma_kstep<Cfg>(acc, As, Bs, wi, wj, g, kq * 4 + tq);
         // scalar tail keeps the in-order FMA chain for k % 4 != 0
 #pragma unroll 1
         for (int kk = nq * 4; kk < kvalid; ++kk) {
 #pragma unroll
           for (int fj = 0; fj < FJ; ++fj) {
-            const double bv = Bs[Cfg::b_off(kk, lj_acc + fj * 8)];
+            const double bv = Bs[Cfg::b_off(kk, Cfg::load_col(wj, fj, g))];
 #pragma unroll
-            for (int fi = 0; fi < FI; ++fi) {
-              acc[fj][fi][0] = fma(As[Cfg::a_off(li_acc + fi * 8, kk)], bv, acc[fj][fi][0]);
-              acc[fj][fi][1] = fma(As[Cfg::a_off(li_acc + fi * 8 + 1, kk)], bv, acc[fj][fi][1]);
-            }
+            for (int fi = 0; fi < FI; ++fi)
+#pragma unroll
+              for (int c = 0; c < 2; ++c)
+                acc[fj][fi][c] =
+                    fma(As[Cfg::a_off(Cfg::acc_row(wi, fi, c, tq), kk)], bv, acc[fj][fi][c]);
           }
         }
       }
@@ -432,20 +481,39 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
       }
     }
 
-    // epilogue: lane pair = two consecutive rows of one column of C
+    // epilogue: consecutive rows of one column of C per lane — 4 rows (one
+    // 32-B store) for paired fragments, else 2 rows (one 16-B store)
+    if (flags & 2) continue;
 #pragma unroll
     for (int fj = 0; fj < FJ; ++fj) {
-      const int j = v.j0 + lj_acc + fj * 8;
+      const int j = v.j0 + Cfg::load_col(wj, fj, g);
       if (j < v.n) {
         double* cp = v.C + int64_t(j) * v.ldc;
+        if constexpr (Cfg::PAIR_I) {
 #pragma unroll
-        for (int fi = 0; fi < FI; ++fi) {
-          const int i = v.i0 + li_acc + fi * 8;
-          if (vec_ok && i + 1 < v.m) {
-            st_global_v2(cp + i, acc[fj][fi][0], acc[fj][fi][1]);
-          } else {
-            if (i < v.m) st_global_cs(cp + i, acc[fj][fi][0]);
-            if (i + 1 < v.m) st_global_cs(cp + i + 1, acc[fj][fi][1]);
+          for (int p = 0; p < FI / 2; ++p) {
+            const int i = v.i0 + Cfg::acc_row(wi, 2 * p, 0, tq);  // rows i .. i+3
+            const double r0 = acc[fj][2 * p][0], r1 = acc[fj][2 * p + 1][0];
+            const double r2 = acc[fj][2 * p][1], r3 = acc[fj][2 * p + 1][1];
+            if (vec4_ok && i + 3 < v.m) {
+              st_global_v4(cp + i, r0, r1, r2, r3);
+            } else {
+              if (i < v.m) st_global_cs(cp + i, r0);
+              if (i + 1 < v.m) st_global_cs(cp + i + 1, r1);
+              if (i + 2 < v.m) st_global_cs(cp + i + 2, r2);
+              if (i + 3 < v.m) st_global_cs(cp + i + 3, r3);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int fi = 0; fi < FI; ++fi) {
+            const int i = v.i0 + Cfg::acc_row(wi, fi, 0, tq);  // rows i, i+1
+            if (vec_ok && i + 1 < v.m) {
+              st_global_v2(cp + i, acc[fj][fi][0], acc[fj][fi][1]);
+            } else {
+              if (i < v.m) st_global_cs(cp + i, acc[fj][fi][0]);
+              if (i + 1 < v.m) st_global_cs(cp + i + 1, acc[fj][fi][1]);
+            }
           }
         }
       }

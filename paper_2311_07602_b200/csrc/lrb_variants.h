@@ -12,9 +12,11 @@
 //   m*  : short-wide C, the same product issued row-major (swapped operands).
 //   sq  : 128 x 128 tiles for the low-rank expansion U * V^T (blr.hpp:75-78),
 //         write-dominated and at the FP64 ridge.
-//   n64 : 128 x 64 tiles at two CTAs per SM — also the general-shape choice:
-//         one CTA's epilogue overlaps the other's MMAs (low-rank expansion
-//         U * V^T, blr.hpp:75-78, measured 1.17x over 128 x 128 tiles).
+//   n64 : 128 x 64 tiles at two CTAs per SM (r in 57..64).
+//   q64 : 64 x 64 tiles at three CTAs per SM — the general-shape choice (the
+//         low-rank expansion U * V^T, blr.hpp:75-78): more independent CTAs
+//         overlap one CTA's epilogue and operand wait with the others' MMAs.
+//   n64s4 : KB = 16 alternative kept for the selector sweep.
 //   n24, n40, n48, n56 : intermediate widths so a variable-rank batch
 //         (cfg4, r_i in 8..64) wastes less than one 8-column fragment.
 #pragma once
@@ -33,9 +35,11 @@
   X(9, n24, 4, 1, 32, 24, 32, 2, 2)  \
   X(10, n40, 4, 1, 32, 40, 32, 2, 2) \
   X(11, n48, 4, 2, 32, 24, 32, 2, 2) \
-  X(12, n56, 8, 1, 16, 56, 32, 2, 2)
+  X(12, n56, 8, 1, 16, 56, 32, 2, 2) \
+  X(13, q64, 2, 2, 32, 32, 32, 2, 3) \
+  X(14, n64s4, 4, 2, 32, 32, 16, 4, 2)
 
-#define LRB_NUM_VARIANTS 13
+#define LRB_NUM_VARIANTS 15
 
 enum {
   LRB_V_N8 = 0,
@@ -50,5 +54,7 @@ enum {
   LRB_V_N24 = 9,
   LRB_V_N40 = 10,
   LRB_V_N48 = 11,
-  LRB_V_N56 = 12
+  LRB_V_N56 = 12,
+  LRB_V_Q64 = 13,
+  LRB_V_N64S4 = 14
 };
