@@ -139,8 +139,17 @@ struct StridedProblem {
 
   template <int MB, int NB>
   __device__ __forceinline__ TileView tile(int64_t t) const {
-    const int64_t item = t / tiles_per_item;
-    const int r = static_cast<int>(t - item * tiles_per_item);
+    int64_t item;
+    int r;
+    if (num_tiles <= int64_t(UINT32_MAX)) {  // 32-bit divide on the common path
+      const uint32_t tt = static_cast<uint32_t>(t), tpi = static_cast<uint32_t>(tiles_per_item);
+      const uint32_t it = tt / tpi;
+      item = it;
+      r = static_cast<int>(tt - it * tpi);
+    } else {
+      item = t / tiles_per_item;
+      r = static_cast<int>(t - item * tiles_per_item);
+    }
     TileView v;
     v.A = A + item * sA;
     v.B = B + item * sB;
@@ -469,8 +478,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
       __syncwarp();
       int last = 0;
       if (lane == 0) {
-        __threadfence_block();
-        last = (atomicAdd(&released[stage], 1) == Cfg::WARPS - 1);
+        // acq_rel: orders this warp's reads of the slot before the count, and
+        // lets the last warp see the issue state the previous issuer wrote
+        last = (atom_add_acq_rel_cta(&released[stage], 1) == Cfg::WARPS - 1);
         if (last) released[stage] = 0;
       }
       last = __shfl_sync(0xffffffffu, last, 0);
