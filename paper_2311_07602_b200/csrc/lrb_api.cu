@@ -153,8 +153,13 @@ constexpr double kHbmBytesPerS = 6553.6e9;
 // Automatic choice on the column-major view (m x n output, inner k); tile
 // sizes per shape class were chosen from the per-variant sweep in
 // profiles/sweep_variants_r01.jsonl.
-int auto_variant(int64_t m, int64_t n) {
+int auto_variant(int64_t m, int64_t n, int64_t batch, int sm_count) {
   if (n <= 64 && n <= m) {
+    // small batches of skinny products (cfg1: 256 items of 256 x 16) would
+    // fill fewer than two waves of 128-row tiles: 32-row tiles at five CTAs
+    // per SM balance the SMs better (0.66 -> 0.70 of HBM on cfg1)
+    if (n <= 16 && batch > 0 && batch * ((m + 127) / 128) < 2LL * 2 * sm_count)
+      return LRB_V_N16T;
     if (n <= 8) return LRB_V_N8;
     if (n <= 16) return LRB_V_N16;
     if (n <= 24) return LRB_V_N24;
@@ -185,11 +190,11 @@ int env_variant() {
   return lrb_variant_from_name(s);
 }
 
-int choose_variant(const lrb_ctx* ctx, int64_t m, int64_t n) {
+int choose_variant(const lrb_ctx* ctx, int64_t m, int64_t n, int64_t batch) {
   if (ctx && ctx->variant_override >= 0) return ctx->variant_override;
   int v = env_variant();
   if (v >= 0) return v;
-  return auto_variant(m, n);
+  return auto_variant(m, n, batch, ctx ? ctx->sm_count : 148);
 }
 
 // ============================================================ normalisation
@@ -287,7 +292,7 @@ lrb_status run_strided(lrb_ctx* ctx, const Gemm& g, int64_t batch, int beta_one,
                        cudaStream_t stream, int* variant_used) {
   if (batch == 0 || g.m == 0 || g.n == 0) return LRB_OK;
   if (g.k == 0 && beta_one) return LRB_OK;  // C = C
-  const int v = choose_variant(ctx, g.m, g.n);
+  const int v = choose_variant(ctx, g.m, g.n, batch);
   const VariantMeta& vm = kVariants[v];
   const int64_t ti = (g.m + vm.mb - 1) / vm.mb, tj = (g.n + vm.nb - 1) / vm.nb;
   if (ti * tj > INT32_MAX || ti * tj * batch > (int64_t(1) << 62))
@@ -580,7 +585,7 @@ extern "C" lrb_status lrb_select(const lrb_ctx* ctx, char order, char opA, char 
   if (m < 0 || n < 0 || k < 0 || batch < 0)
     return fail(mctx, LRB_ERR_SHAPE, "lrb_select: negative dimension");
   const int64_t cm = row_major(order) ? n : m, cn = row_major(order) ? m : n;
-  const int v = choose_variant(ctx, cm, cn);
+  const int v = choose_variant(ctx, cm, cn, batch);
   const VariantMeta& vm = kVariants[v];
   std::memset(out, 0, sizeof(*out));
   out->variant = v;
@@ -708,7 +713,7 @@ extern "C" lrb_status lrb_ptr_plan_create(lrb_ctx* ctx, char order, char opA, ch
     d.k = int32_t(g.k);
     d.pad = 0;
     if (g.m == 0 || g.n == 0 || (g.k == 0 && beta == 1.0)) continue;
-    const int v = choose_variant(ctx, g.m, g.n);
+    const int v = choose_variant(ctx, g.m, g.n, batch);
     const int64_t ti = (g.m + kVariants[v].mb - 1) / kVariants[v].mb;
     const int64_t tj = (g.n + kVariants[v].nb - 1) / kVariants[v].nb;
     if (ti > 0xFFFF || tj > 0xFFFF)

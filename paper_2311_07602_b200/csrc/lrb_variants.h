@@ -17,6 +17,8 @@
 //         low-rank expansion U * V^T, blr.hpp:75-78): more independent CTAs
 //         overlap one CTA's epilogue and operand wait with the others' MMAs.
 //   n64s4 : KB = 16 alternative kept for the selector sweep.
+//   n16t : 32-row tiles at five CTAs per SM for small skinny batches (cfg1).
+//   n16h : 64-row tiles, sweep candidate.
 //   n24, n40, n48, n56 : intermediate widths so a variable-rank batch
 //         (cfg4, r_i in 8..64) wastes less than one 8-column fragment.
 #pragma once
@@ -37,9 +39,11 @@
   X(11, n48, 4, 2, 32, 24, 32, 2, 2) \
   X(12, n56, 8, 1, 16, 56, 32, 2, 2) \
   X(13, q64, 2, 2, 32, 32, 32, 2, 3) \
-  X(14, n64s4, 4, 2, 32, 32, 16, 4, 2)
+  X(14, n64s4, 4, 2, 32, 32, 16, 4, 2) \
+  X(15, n16t, 4, 1, 8, 16, 32, 2, 5)   \
+  X(16, n16h, 4, 1, 16, 16, 32, 2, 4)
 
-#define LRB_NUM_VARIANTS 15
+#define LRB_NUM_VARIANTS 17
 
 enum {
   LRB_V_N8 = 0,
@@ -56,5 +60,7 @@ enum {
   LRB_V_N48 = 11,
   LRB_V_N56 = 12,
   LRB_V_Q64 = 13,
-  LRB_V_N64S4 = 14
+  LRB_V_N64S4 = 14,
+  LRB_V_N16T = 15,
+  LRB_V_N16H = 16
 };

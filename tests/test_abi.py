@@ -72,9 +72,16 @@ def test_no_device_here_fails_loudly():
     (512, 56, 512, "n56"), (16, 512, 512, "m16"), (8, 300, 7, "m8"), (64, 200, 64, "m64"),
 ])
 def test_selector_by_shape(m, n, k, want):
-    s = P.select("C", "N", "N", m, n, k, 10)
+    batch = 100000
+    s = P.select("C", "N", "N", m, n, k, batch)
     assert s["name"] == want
-    assert s["tiles"] == 10 * -(-m // s["tile_m"]) * -(-n // s["tile_n"])
+    assert s["tiles"] == batch * -(-m // s["tile_m"]) * -(-n // s["tile_n"])
+
+
+def test_selector_small_skinny_batches_use_short_tiles():
+    # cfg1: 256 items of 256 x 16 -> fewer than two waves of 128-row tiles
+    assert P.select("C", "N", "N", 256, 16, 256, 256)["name"] == "n16t"
+    assert P.select("C", "N", "N", 256, 16, 256, 100000)["name"] == "n16"
 
 
 def test_selector_row_major_swaps_roles():
