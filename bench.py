@@ -408,12 +408,23 @@ def run_gpu_arm(args, w, world, rank, local, pg):
     chunk = min(count, cap_items)
     nchunks = (count + chunk - 1) // chunk
     resident = nchunks == 1
-    A, B, Cd = alloc_inputs(ctx, w, first, chunk)
+    # a working set within 3x L2 (cfg1: 151 MB) rotates over identical copies
+    # of its inputs and outputs, so no step finds the previous step's data in L2
+    L2_BYTES = 132644864
+    copies = 1
+    if resident and per_item * count < 3 * L2_BYTES:
+        copies = min(int(-(-3 * L2_BYTES // (per_item * count))),
+                     max(1, int((free - (2 << 30)) // (per_item * count))))
+    bufs = [alloc_inputs(ctx, w, first, chunk) for _ in range(copies)]
+    A, B, Cd = bufs[0]
+    rot = [0]
 
     def step():
         """one pass over this rank's items; returns device ms of the GEMM launches"""
         if resident:
-            gemm(ctx, w, A, B, Cd, count, stream)
+            a, b, c = bufs[rot[0] % copies]
+            rot[0] += 1
+            gemm(ctx, w, a, b, c, count, stream)
             return None
         # chunked (cfg5 below 4 GPUs): regenerate each chunk (untimed), time GEMMs
         total = 0.0
@@ -436,6 +447,16 @@ def run_gpu_arm(args, w, world, rank, local, pg):
         step()
     stream.synchronize()
 
+    # resident batches: the K timed steps are captured once as a CUDA graph
+    # (lrb_graph_*) and replayed with one host call, so short steps (cfg1,
+    # ~35 us) are not separated by host enqueue gaps
+    graph = None
+    if resident and not args.no_graph:
+        with ctx.capture(stream) as cap:
+            for _ in range(args.steps):
+                step()
+        graph = cap.graph
+
     # ---- timed region
     sampler = ClockSampler(local)
     sampler.start()
@@ -445,10 +466,13 @@ def run_gpu_arm(args, w, world, rank, local, pg):
     t_start, t_end = ctx.event(), ctx.event()
     chunk_ms = 0.0
     t_start.record(stream)
-    for _ in range(args.steps):
-        r = step()
-        if r is not None:
-            chunk_ms += r
+    if graph is not None:
+        graph.launch(stream)
+    else:
+        for _ in range(args.steps):
+            r = step()
+            if r is not None:
+                chunk_ms += r
     t_end.record(stream)
     stream.synchronize()
     barrier(pg)
@@ -467,8 +491,9 @@ def run_gpu_arm(args, w, world, rank, local, pg):
 
     # ---- dominant kernel roofline (this rank, per launch)
     per_launch_ms = ms_rank / max(1, launches)
-    launch_items = count if resident else chunk
-    sel = select(w.order, w.opA, w.opB, w.m, w.n, w.k, launch_items, ctx)
+    # average items per launch (chunks may be unequal; algorithmic units per launch)
+    launch_items = count / nchunks
+    sel = select(w.order, w.opA, w.opB, w.m, w.n, w.k, chunk, ctx)
     intensity = w.item_flops() / w.item_bytes()
     fp64_bound = intensity >= (fp64_peak * 1e12) / (hbm_peak * 1e9)
     if fp64_bound:
@@ -490,6 +515,7 @@ def run_gpu_arm(args, w, world, rank, local, pg):
         min(fp64_peak * 1e12, intensity * hbm_peak * 1e9), 4)
 
     # ---- e2e through the host-buffer C-ABI (pinned host memory, copies timed)
+    del A, B, Cd, bufs
     e2e = run_e2e(args, ctx, w, first, count, pg) if args.e2e_steps > 0 else None
 
     # ---- CPU baseline on rank 0 at N = 1
@@ -506,10 +532,13 @@ def run_gpu_arm(args, w, world, rank, local, pg):
     if rank == 0:
         cfg = dict(w.describe())
         cfg.update({"items_per_rank": count, "global_items": int(items_all),
+                    "timed_launch": "CUDA graph of the K steps" if graph is not None
+                    else "eager launches",
                     "parallelism": f"shard{world} (independent items, no collective)",
                     "kernel_variant": sel["name"],
-                    "l2": "inputs larger than L2 (no flush)" if per_item * count > 3 * 132644864
-                          else "L2 flushed between steps",
+                    "l2": (f"{copies} rotating copies of inputs+outputs "
+                           f"({per_item * count * copies / 2**20:.0f} MiB) > 3x L2"
+                           if copies > 1 else "inputs larger than L2 (no flush)"),
                     "chunks_per_step": nchunks})
         line = {
             "metric": "batched FP64 GFLOP/s", "value": round(gflops, 2), "unit": "GFLOP/s",
@@ -527,7 +556,10 @@ def run_gpu_arm(args, w, world, rank, local, pg):
 def run_e2e(args, ctx, w, first, count, pg):
     """same metric through lrb_dgemm_strided_batched_host: pinned host inputs,
     H2D + kernels + D2H of the result inside the timed region"""
-    n = min(count, args.e2e_items) if args.e2e_items else count
+    # whole batch when it fits in 16 GiB of pinned host memory (cfg5's 288 GiB
+    # does not: its e2e runs on the largest prefix that does)
+    per_item = 8 * (w.sA + w.sB + w.sC)
+    n = min(count, args.e2e_items) if args.e2e_items else min(count, (16 << 30) // per_item)
     A, B, _ = alloc_inputs(ctx, w, first, n)
     hA, hB, hC = ctx.pinned(w.sA * n), ctx.pinned(w.sB * n), ctx.pinned(w.sC * n)
     from paper_2311_07602_b200.lrbatch import _check, lib  # noqa
@@ -569,6 +601,8 @@ def main():
                     help="CPU work per reference-arm step / cpu_baseline sample")
     ap.add_argument("--warmup-ref", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="launch the timed steps one by one instead of as a CUDA graph")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "lrb":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

@@ -162,6 +162,21 @@ lrb_status lrb_dgemm_strided_batched_host(lrb_ctx* ctx, char order, char opA, ch
                                           double* C, int64_t ldc, int64_t strideC,
                                           int64_t batch);
 
+/* ------------------------------------------------------------ CUDA graphs */
+/*
+ * Capture every lrb_* launch issued on `stream` (a non-default stream)
+ * between begin and end into a CUDA graph; replaying it issues the whole
+ * sequence with one host call (no per-launch validation, tensor-map encoding
+ * or driver overhead). Operand pointers are baked in at capture time.
+ */
+typedef struct lrb_graph lrb_graph;
+lrb_status lrb_graph_begin(lrb_ctx* ctx, void* stream);
+lrb_status lrb_graph_end(lrb_ctx* ctx, void* stream, lrb_graph** out);
+lrb_status lrb_graph_launch(lrb_ctx* ctx, const lrb_graph* graph, void* stream);
+lrb_status lrb_graph_destroy(lrb_ctx* ctx, lrb_graph* graph);
+/* kernel launches one replay performs */
+uint64_t lrb_graph_launches(const lrb_graph* graph);
+
 /* ---------------------------------------------------- selector / planner */
 typedef struct lrb_selection {
   int variant;        /* index into the variant table */

@@ -98,6 +98,11 @@ SIGNATURES = {
         [vp, C.c_char, C.c_char, C.c_char, i64, i64, i64, dbl, vp, i64, i64, vp, i64, i64, vp, i64,
          i64, i64],
     ),
+    "lrb_graph_begin": (C.c_int, [vp, vp]),
+    "lrb_graph_end": (C.c_int, [vp, vp, P(vp)]),
+    "lrb_graph_launch": (C.c_int, [vp, vp, vp]),
+    "lrb_graph_destroy": (C.c_int, [vp, vp]),
+    "lrb_graph_launches": (u64, [vp]),
     "lrb_select": (
         C.c_int, [vp, C.c_char, C.c_char, C.c_char, i64, i64, i64, i64, P(lrb_selection)]
     ),

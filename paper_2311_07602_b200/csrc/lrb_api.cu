@@ -909,9 +909,15 @@ extern "C" lrb_status lrb_dgemm_strided_batched_host(lrb_ctx* ctx, char order, c
   const bool c_dense = (fC == m * n) && (batch == 1 || sC == fC);
   const bool upload_c = beta_one || !c_dense;
 
-  // chunk so that one lane's A + B + C spans stay near 256 MiB
-  const int64_t target = (int64_t(256) << 20) / 8;
+  // chunk target ~1/8 of the batch, clamped to [16, 256] MiB per lane: small
+  // batches still get several chunks overlapping on the three streams, large
+  // ones keep few, large copies (measured: 64 MiB D2H chunks ran cfg2's 8 GiB
+  // result 2.3x slower than 256 MiB ones)
   const int64_t base = fA + fB + fC, incr = sA + sB + sC;
+  const int64_t total_elems = span_elems(batch, sA, fA) + span_elems(batch, sB, fB) +
+                              span_elems(batch, sC, fC);
+  const int64_t target = std::min<int64_t>(
+      (int64_t(256) << 20) / 8, std::max<int64_t>((int64_t(16) << 20) / 8, total_elems / 8));
   int64_t per_chunk = batch;
   if (incr > 0) per_chunk = std::max<int64_t>(1, std::min<int64_t>(batch, (target - base) / incr + 1));
   const int64_t need =
@@ -962,3 +968,62 @@ extern "C" lrb_status lrb_gemm_naive_raw(lrb_ctx* ctx, const double* a, const do
   if (flops) *flops += uint64_t(2) * m * n * k;  // the reference's in-loop count, dense.hpp:148
   return LRB_OK;
 }
+
+// ================================================================== graphs
+struct lrb_graph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  uint64_t launches = 0;
+  int device = 0;
+};
+
+extern "C" lrb_status lrb_graph_begin(lrb_ctx* ctx, void* stream) {
+  lrb_status st = bind(ctx);
+  if (st) return st;
+  if (!stream) return fail(ctx, LRB_ERR_ARG, "lrb_graph_begin: capture needs a non-default stream");
+  ctx->capture_launches0 = ctx->launches.load();
+  LRB_CUDA_TRY(ctx, cudaStreamBeginCapture(static_cast<cudaStream_t>(stream),
+                                           cudaStreamCaptureModeThreadLocal));
+  return LRB_OK;
+}
+
+extern "C" lrb_status lrb_graph_end(lrb_ctx* ctx, void* stream, lrb_graph** out) {
+  if (!out) return fail(ctx, LRB_ERR_ARG, "lrb_graph_end: out is null");
+  *out = nullptr;
+  lrb_status st = bind(ctx);
+  if (st) return st;
+  auto* g = new (std::nothrow) lrb_graph;
+  if (!g) return fail(ctx, LRB_ERR_CAPACITY, "lrb_graph_end: out of host memory");
+  cudaError_t e = cudaStreamEndCapture(static_cast<cudaStream_t>(stream), &g->graph);
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&g->exec, g->graph, 0);
+  if (e != cudaSuccess) {
+    lrb_graph_destroy(ctx, g);
+    return cuda_fail(ctx, e, "lrb_graph_end");
+  }
+  // captured launches did not execute: move them from the context to the graph
+  g->launches = ctx->launches.load() - ctx->capture_launches0;
+  ctx->launches.fetch_sub(g->launches);
+  g->device = ctx->device;
+  *out = g;
+  return LRB_OK;
+}
+
+extern "C" lrb_status lrb_graph_launch(lrb_ctx* ctx, const lrb_graph* g, void* stream) {
+  if (!g) return fail(ctx, LRB_ERR_ARG, "lrb_graph_launch: null graph");
+  lrb_status st = bind(ctx);
+  if (st) return st;
+  LRB_CUDA_TRY(ctx, cudaGraphLaunch(g->exec, static_cast<cudaStream_t>(stream)));
+  ctx->launches.fetch_add(g->launches, std::memory_order_relaxed);
+  return LRB_OK;
+}
+
+extern "C" lrb_status lrb_graph_destroy(lrb_ctx* ctx, lrb_graph* g) {
+  if (!g) return LRB_OK;
+  if (ctx) cudaSetDevice(ctx->device);
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  delete g;
+  return LRB_OK;
+}
+
+extern "C" uint64_t lrb_graph_launches(const lrb_graph* g) { return g ? g->launches : 0; }

@@ -20,6 +20,7 @@ struct lrb_ctx {
   int loader_override = -1;  // -1 auto, 0 segment copies, 1 TMA tensor maps (when eligible)
   std::string err;
   std::atomic<uint64_t> launches{0};
+  uint64_t capture_launches0 = 0;  // launch counter at lrb_graph_begin
   // host-buffer pipeline: per-lane stream and device staging buffers
   static constexpr int kLanes = 3;
   cudaStream_t lane_stream[kLanes] = {nullptr, nullptr, nullptr};

@@ -225,6 +225,49 @@ class Event:
             pass
 
 
+class Graph:
+    """A captured sequence of lrb launches (CUDA graph), replayed with one call."""
+
+    def __init__(self, ctx: "Context", handle: int):
+        self.ctx = ctx
+        self.handle = handle
+
+    @property
+    def launches(self) -> int:
+        return int(lib.lrb_graph_launches(self.handle))
+
+    def launch(self, stream: "Stream") -> None:
+        _check(lib.lrb_graph_launch(self.ctx._h, self.handle, stream.handle), self.ctx._h)
+
+    def destroy(self) -> None:
+        if self.handle and self.ctx._h:
+            lib.lrb_graph_destroy(self.ctx._h, self.handle)
+        self.handle = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+class _Capture:
+    def __init__(self, ctx: "Context", stream: "Stream"):
+        self.ctx, self.stream, self.graph = ctx, stream, None
+
+    def __enter__(self):
+        _check(lib.lrb_graph_begin(self.ctx._h, self.stream.handle), self.ctx._h)
+        return self
+
+    def __exit__(self, exc_type, exc, tb):
+        h = C.c_void_p()
+        st = lib.lrb_graph_end(self.ctx._h, self.stream.handle, C.byref(h))
+        if exc_type is None:
+            _check(st, self.ctx._h)
+            self.graph = Graph(self.ctx, h.value)
+        return False
+
+
 def _i64arr(xs, n: int, name: str):
     a = np.ascontiguousarray(np.asarray(xs, dtype=np.int64))
     if a.shape != (n,):
@@ -333,6 +376,11 @@ class Context:
 
     def synchronize(self) -> None:
         _check(lib.lrb_device_sync(self._h), self._h)
+
+    def capture(self, stream: Stream) -> _Capture:
+        """``with ctx.capture(s) as cap: ...`` records the launches on ``s`` into
+        ``cap.graph`` (a CUDA graph) instead of running them"""
+        return _Capture(self, stream)
 
     def l2_flush(self, stream: Optional[Stream] = None) -> None:
         _check(lib.lrb_l2_flush(self._h, stream.handle if stream else None), self._h)

@@ -183,3 +183,46 @@ def test_negative_control_detects_corruption():
                                 c.B[c.strideB:], c.ldb, None, bad[c.strideC:], ref[c.strideC:],
                                 c.ldc)
     assert nbad == 1 and ratio > 1.0
+
+
+def test_graph_capture_replays_bitwise(ctx):
+    # lrb_graph_*: captured launches replay with identical results, and the
+    # launch counter moves only on replay
+    c = Case("C", "N", "T", 96, 80, 40, 4, seed=41)
+    dA, dB, dC = ctx.to_device(c.A), ctx.to_device(c.B), ctx.to_device(c.C0)
+    s = ctx.stream()
+    ctx.dgemm_strided_batched(*c.args(dA, dB, dC), stream=s)  # warm (attributes)
+    s.synchronize()
+    dC.fill_bytes(0)
+    n0 = ctx.launch_count
+    with ctx.capture(s) as cap:
+        ctx.dgemm_strided_batched(*c.args(dA, dB, dC), stream=s)
+        ctx.dgemm_strided_batched(*c.args(dA, dB, dC), stream=s)
+    g = cap.graph
+    assert g.launches == 2 and ctx.launch_count == n0
+    g.launch(s)
+    s.synchronize()
+    assert ctx.launch_count == n0 + 2
+    c.check(dC.download(c.C0.size))
+
+
+def test_graph_capture_of_pointer_plan(ctx):
+    rng = np.random.default_rng(42)
+    ms, ns, ks = [70, 130, 33], [9, 40, 64], [50, 17, 96]
+    hA = [rng.uniform(-1, 1, m * k) for m, k in zip(ms, ks)]
+    hB = [rng.uniform(-1, 1, k * n) for k, n in zip(ks, ns)]
+    dA = [ctx.to_device(x) for x in hA]
+    dB = [ctx.to_device(x) for x in hB]
+    dC = [ctx.empty(m * n) for m, n in zip(ms, ns)]
+    plan = ctx.ptr_plan("C", "N", "N", ms, ns, ks, dA, ms, dB, ks, dC, ms, 0.0)
+    s = ctx.stream()
+    plan.execute(s)
+    s.synchronize()
+    with ctx.capture(s) as cap:
+        plan.execute(s)
+    cap.graph.launch(s)
+    s.synchronize()
+    expect = [np.zeros(m * n) for m, n in zip(ms, ns)]
+    O.dgemm_ptr("C", "N", "N", ms, ns, ks, hA, ms, hB, ks, expect, ms, 0.0)
+    for i in range(3):
+        assert np.array_equal(dC[i].download(ms[i] * ns[i]), expect[i])
