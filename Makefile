@@ -45,7 +45,7 @@ oracle/liblrb_oracle.so: oracle/lrb_oracle.c oracle/lrb_oracle.h include/lrb_rng
 
 oracle/_ref/liblrb_ref.so: oracle/ref_shim.cpp
 	@mkdir -p oracle/_ref
-	$(CXX) $(REF_FLAGS) -I$(REF_INC) -Iinclude $< -o $@
+	$(CXX) $(REF_FLAGS) -I$(REF_INC) -Iinclude -DLRBATCH_MACHINE_DIR=\"$(REFERENCE)/proj/machines\" $< -o $@
 
 clean:
 	rm -rf $(BUILD) $(LIB) oracle/liblrb_oracle.so oracle/_ref

@@ -162,6 +162,29 @@ lrb_status lrb_dgemm_strided_batched_host(lrb_ctx* ctx, char order, char opA, ch
                                           double* C, int64_t ldc, int64_t strideC,
                                           int64_t batch);
 
+/* ------------------------------------------- the paper's low-rank product */
+/*
+ * G_i = A_X_i (A_Vt_i B_U_i) B_X_i over a LowRankBatch (arXiv 2311.07602,
+ * Algorithm 1): all matrices row-major, each role packed contiguously with
+ * item i at base + i*rows*cols (reference low_rank.hpp:109-176):
+ *   a_vt: rank x block, b_u: block x rank, a_x, b_x, g: rank x rank.
+ * rank_a == rank_b == rank, as fused_multiply / packed_multiply require
+ * (kernels.hpp:133-135, 246-248). G is overwritten (stored once per item).
+ * Each product is an in-order FMA chain, i.e. the reference oracle
+ * low_rank_multiply_reference_raw (low_rank.hpp:73-87) with fused rounding.
+ * Replaces: fused_multiply (kernels.hpp:131-161), packed_multiply
+ * (kernels.hpp:243-349), naive_multiply_batch (bench.hpp:55-77).
+ */
+lrb_status lrb_lowrank_multiply(lrb_ctx* ctx, int64_t batch, int64_t block, int64_t rank,
+                                const double* a_vt, const double* b_u, const double* a_x,
+                                const double* b_x, double* g, void* stream);
+/* host-buffer form (synchronous; chunked H2D / kernel / D2H) */
+lrb_status lrb_lowrank_multiply_host(lrb_ctx* ctx, int64_t batch, int64_t block, int64_t rank,
+                                     const double* a_vt, const double* b_u, const double* a_x,
+                                     const double* b_x, double* g);
+/* the reference's accounting 4 r^3 + 2 r^2 b (flops_per_item, low_rank.hpp:66-68) */
+double lrb_lowrank_flops_per_item(int64_t rank, int64_t block);
+
 /* ------------------------------------------------------------ CUDA graphs */
 /*
  * Capture every lrb_* launch issued on `stream` (a non-default stream)

@@ -55,6 +55,8 @@ def oracle_lib() -> C.CDLL:
         L.oracle_check_bound.argtypes = [C.c_char, C.c_char, C.c_char, i64, i64, i64, dbl, vp, i64,
                                          vp, i64, vp, vp, vp, i64, P(dbl)]
         L.oracle_check_bound.restype = i64
+        L.oracle_lowrank_batch.argtypes = [C.c_int, i64, i64, i64, vp, vp, vp, vp, vp, C.c_int]
+        L.oracle_lowrank_batch.restype = C.c_int
         _oracle = L
     return _oracle
 
@@ -85,6 +87,11 @@ def ref_lib() -> C.CDLL:
         L.ref_dgemm_colmajor_ptr.restype = C.c_int
         L.ref_dense_gemm_naive_error.argtypes = [C.c_size_t] * 6 + [C.c_char_p, C.c_size_t]
         L.ref_dense_gemm_naive_error.restype = C.c_int
+        L.ref_lowrank_multiply.argtypes = [C.c_int, i64, i64, i64, vp, vp, vp, vp, vp, C.c_int,
+                                           C.c_char_p]
+        L.ref_lowrank_multiply.restype = C.c_int
+        L.ref_compare_to_reference.argtypes = [i64, i64, i64, vp, vp, vp, vp, vp, P(i64), P(i64)]
+        L.ref_compare_to_reference.restype = dbl
         _ref = L
     return _ref
 
@@ -187,3 +194,49 @@ def ref_dense_gemm_naive_error(ar, ac, br, bc, orow, ocol) -> Optional[str]:
     if ref_lib().ref_dense_gemm_naive_error(ar, ac, br, bc, orow, ocol, buf, 256):
         return buf.value.decode()
     return None
+
+
+# ------------------------------------------------------- low-rank product
+def lowrank(batch, block, rank, a_vt, b_u, a_x, b_x, threads=1, mode=FMA_CHAIN):
+    """G = A_X (A_Vt B_U) B_X per item (low_rank.hpp:73-87), rounded per `mode`"""
+    g = np.zeros(batch * rank * rank)
+    rc = oracle_lib().oracle_lowrank_batch(mode, batch, block, rank, _p(a_vt), _p(b_u), _p(a_x),
+                                           _p(b_x), _p(g), threads)
+    if rc != 0:
+        raise ValueError("oracle_lowrank_batch: bad arguments")
+    return g
+
+
+def ref_lowrank(which, batch, block, rank, a_vt, b_u, a_x, b_x, workers=1, machine=None):
+    """the reference's own drivers: 0 naive_multiply_batch, 1 fused_multiply,
+    2 packed_multiply (plan for `machine`)"""
+    g = np.zeros(batch * rank * rank)
+    rc = ref_lib().ref_lowrank_multiply(which, batch, block, rank, _p(a_vt), _p(b_u), _p(a_x),
+                                        _p(b_x), _p(g), workers,
+                                        machine.encode() if machine else None)
+    if rc != 0:
+        raise ValueError("ref_lowrank_multiply failed")
+    return g
+
+
+def ref_compare_to_reference(batch, block, rank, a_vt, b_u, a_x, b_x, g):
+    """the reference's compare_to_reference metric (verify.hpp:38-64):
+    (max relative error, worst item, worst entry)"""
+    wi, we = C.c_int64(0), C.c_int64(0)
+    err = ref_lib().ref_compare_to_reference(batch, block, rank, _p(a_vt), _p(b_u), _p(a_x),
+                                             _p(b_x), _p(g), C.byref(wi), C.byref(we))
+    return float(err), int(wi.value), int(we.value)
+
+
+def lowrank_bound_check(batch, block, rank, a_vt, b_u, a_x, b_x, g, g_ref):
+    """Componentwise bound for the chained product (three naive products):
+    |G - G_ref| <= 4 (b + 2r) 2^-52 (|A_X| |A_Vt| |B_U| |B_X|), evaluated with
+    the same chain on absolute values. Returns (violations, max ratio)."""
+    mags = lowrank(batch, block, rank, np.abs(a_vt), np.abs(b_u), np.abs(a_x), np.abs(b_x),
+                   threads=4)
+    bound = 4.0 * (block + 2 * rank) * 2.0 ** -52 * mags
+    err = np.abs(g - g_ref)
+    exact = bound == 0
+    bad = int(np.sum(err[~exact] > bound[~exact]) + np.sum(err[exact] != 0))
+    ratio = float(np.max(err[~exact] / bound[~exact])) if np.any(~exact) else 0.0
+    return bad, ratio

@@ -285,3 +285,72 @@ int64_t oracle_check_bound(char order, char opA, char opB, int64_t m, int64_t n,
   if (max_ratio) *max_ratio = worst;
   return bad;
 }
+
+/* ------------------------------------------------------------------------
+ * The paper's batched low-rank product (reference low_rank.hpp:73-87,
+ * reference_item :179-184, naive_multiply_batch bench.hpp:55-77):
+ *   C = A_Vt (r x b) B_U (b x r); E = A_X C; G = E B_X — three naive
+ *   row-major products with materialised intermediates, per item of a
+ *   LowRankBatch (roles packed contiguously, item i at base + i*rows*cols). */
+typedef struct {
+  int mode;
+  int64_t block, rank;
+  const double *a_vt, *b_u, *a_x, *b_x;
+  double* g;
+  int64_t begin, end;
+} lr_job_t;
+
+static void lr_gemm(int mode, const double* a, const double* b, double* c, int64_t m, int64_t k,
+                    int64_t n) {
+  /* gemm_naive_raw(a, b, c, m, k, n, false) (dense.hpp:43-56) in `mode` rounding */
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      double sum = 0.0;
+      if (mode == ORACLE_REF_COMPILED)
+        sum = ref_dot(a + i * k, 1, b + j, n, k, sum, 0);
+      else
+        for (int64_t p = 0; p < k; ++p) sum = fma(a[i * k + p], b[p * n + j], sum);
+      c[i * n + j] = sum;
+    }
+}
+
+static void* lr_worker(void* arg) {
+  const lr_job_t* j = (const lr_job_t*)arg;
+  const int64_t r = j->rank, b = j->block;
+  double* cs = (double*)malloc(sizeof(double) * (size_t)(r * r));
+  double* es = (double*)malloc(sizeof(double) * (size_t)(r * r));
+  for (int64_t it = j->begin; it < j->end; ++it) {
+    lr_gemm(j->mode, j->a_vt + it * r * b, j->b_u + it * b * r, cs, r, b, r);
+    lr_gemm(j->mode, j->a_x + it * r * r, cs, es, r, r, r);
+    lr_gemm(j->mode, es, j->b_x + it * r * r, j->g + it * r * r, r, r, r);
+  }
+  free(cs);
+  free(es);
+  return NULL;
+}
+
+int oracle_lowrank_batch(int mode, int64_t batch, int64_t block, int64_t rank, const double* a_vt,
+                         const double* b_u, const double* a_x, const double* b_x, double* g,
+                         int threads) {
+  if (batch < 0 || block < 1 || rank < 1) return -1;
+  if (mode != ORACLE_FMA_CHAIN && mode != ORACLE_REF_COMPILED) return -1;
+  if (threads < 1) threads = 1;
+  if (threads > batch) threads = (int)(batch > 0 ? batch : 1);
+  const int64_t per = (batch + threads - 1) / threads; /* bench.hpp:69-75 split */
+  lr_job_t* jobs = (lr_job_t*)malloc(sizeof(lr_job_t) * (size_t)threads);
+  pthread_t* tids = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)threads);
+  for (int w = 0; w < threads; ++w) {
+    int64_t bg = (int64_t)w * per;
+    if (bg > batch) bg = batch;
+    int64_t en = bg + per;
+    if (en > batch) en = batch;
+    lr_job_t jb = {mode, block, rank, a_vt, b_u, a_x, b_x, g, bg, en};
+    jobs[w] = jb;
+  }
+  for (int w = 1; w < threads; ++w) pthread_create(&tids[w], NULL, lr_worker, &jobs[w]);
+  lr_worker(&jobs[0]);
+  for (int w = 1; w < threads; ++w) pthread_join(tids[w], NULL);
+  free(jobs);
+  free(tids);
+  return 0;
+}

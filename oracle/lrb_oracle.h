@@ -66,6 +66,15 @@ int64_t oracle_check_bound(char order, char opA, char opB, int64_t m, int64_t n,
                            const double* C0, const double* C, const double* Cref, int64_t ldc,
                            double* max_ratio);
 
+/* The paper's batched low-rank product G = A_X (A_Vt B_U) B_X over a
+ * LowRankBatch (row-major roles packed contiguously; rank_a == rank_b), as the
+ * reference's oracle computes it: three naive products with materialised
+ * intermediates (low_rank.hpp:73-87), items split over `threads` like
+ * naive_multiply_batch (bench.hpp:55-77). Rounded per `mode`. */
+int oracle_lowrank_batch(int mode, int64_t batch, int64_t block, int64_t rank, const double* a_vt,
+                         const double* b_u, const double* a_x, const double* b_x, double* g,
+                         int threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -146,3 +146,63 @@ int ref_dense_gemm_naive_error(size_t ar, size_t ac, size_t br, size_t bc, size_
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// The paper's batched low-rank product through the reference's own drivers.
+#include <lrbatch/bench.hpp>
+#include <lrbatch/kernels.hpp>
+#include <lrbatch/machine.hpp>
+#include <lrbatch/verify.hpp>
+
+namespace {
+lrbatch::LowRankBatch make_batch(int64_t batch, int64_t block, int64_t rank, const double* a_vt,
+                                 const double* b_u, const double* a_x, const double* b_x) {
+  lrbatch::LowRankBatch lb{size_t(batch), size_t(block), size_t(rank), size_t(rank)};
+  std::memcpy(lb.a_vt_batch.data(), a_vt, sizeof(double) * lb.a_vt_batch.size());
+  std::memcpy(lb.b_u_batch.data(), b_u, sizeof(double) * lb.b_u_batch.size());
+  std::memcpy(lb.a_x_batch.data(), a_x, sizeof(double) * lb.a_x_batch.size());
+  std::memcpy(lb.b_x_batch.data(), b_x, sizeof(double) * lb.b_x_batch.size());
+  return lb;
+}
+}  // namespace
+
+extern "C" {
+
+// which: 0 naive_multiply_batch (the reference CPU baseline, bench.hpp:55-77),
+//        1 fused_multiply (kernels.hpp:131-161),
+//        2 packed_multiply with the plan for `machine` (kernels.hpp:243-349)
+int ref_lowrank_multiply(int which, int64_t batch, int64_t block, int64_t rank, const double* a_vt,
+                         const double* b_u, const double* a_x, const double* b_x, double* g,
+                         int workers, const char* machine) {
+  try {
+    lrbatch::LowRankBatch lb = make_batch(batch, block, rank, a_vt, b_u, a_x, b_x);
+    if (which == 0) {
+      lrbatch::naive_multiply_batch(lb, size_t(workers));
+    } else if (which == 1) {
+      lrbatch::fused_multiply(lb);
+    } else {
+      lrbatch::PackingPlan plan = lrbatch::make_packing_plan(
+          lrbatch::resolve_machine(machine ? machine : "skylake-x-6148"), size_t(rank),
+          size_t(block));
+      lrbatch::packed_multiply(lb, plan, size_t(workers));
+    }
+    std::memcpy(g, lb.g_xy_batch.data(), sizeof(double) * lb.g_xy_batch.size());
+  } catch (...) {
+    return -1;
+  }
+  return 0;
+}
+
+// compare_to_reference (verify.hpp:38-64) of `g` against the reference oracle
+double ref_compare_to_reference(int64_t batch, int64_t block, int64_t rank, const double* a_vt,
+                                const double* b_u, const double* a_x, const double* b_x,
+                                const double* g, int64_t* worst_item, int64_t* worst_entry) {
+  lrbatch::LowRankBatch lb = make_batch(batch, block, rank, a_vt, b_u, a_x, b_x);
+  std::memcpy(lb.g_xy_batch.data(), g, sizeof(double) * lb.g_xy_batch.size());
+  lrbatch::VerifyReport rep = lrbatch::compare_to_reference(lb, 1.0);
+  if (worst_item) *worst_item = int64_t(rep.worst_item);
+  if (worst_entry) *worst_entry = int64_t(rep.worst_entry);
+  return rep.max_rel_error;
+}
+
+}  // extern "C"

@@ -98,6 +98,9 @@ SIGNATURES = {
         [vp, C.c_char, C.c_char, C.c_char, i64, i64, i64, dbl, vp, i64, i64, vp, i64, i64, vp, i64,
          i64, i64],
     ),
+    "lrb_lowrank_multiply": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, vp]),
+    "lrb_lowrank_multiply_host": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp]),
+    "lrb_lowrank_flops_per_item": (dbl, [i64, i64]),
     "lrb_graph_begin": (C.c_int, [vp, vp]),
     "lrb_graph_end": (C.c_int, [vp, vp, P(vp)]),
     "lrb_graph_launch": (C.c_int, [vp, vp, vp]),

@@ -154,6 +154,9 @@ constexpr double kHbmBytesPerS = 6553.6e9;
 // sizes per shape class were chosen from the per-variant sweep in
 // profiles/sweep_variants_r01.jsonl.
 int auto_variant(int64_t m, int64_t n, int64_t batch, int sm_count) {
+  // small square-ish outputs (the r x r products of the low-rank product's
+  // three-GEMM path): one 64 x 64 tile covers them with the least padding
+  if (m <= 64 && n <= 64 && m > 32 && n > 32) return LRB_V_Q64;
   if (n <= 64 && n <= m) {
     // small batches of skinny products (cfg1: 256 items of 256 x 16) would
     // fill fewer than two waves of 128-row tiles: 32-row tiles at five CTAs
@@ -382,6 +385,20 @@ extern "C" lrb_status lrb_create(int device, lrb_ctx** out) {
       return cuda_fail(nullptr, e, "cudaStreamCreate");
     }
   }
+  {
+    cudaMemPoolProps props;
+    std::memset(&props, 0, sizeof(props));
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    if (cudaMemPoolCreate(&ctx->pool, &props) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    } else {
+      ctx->pool = nullptr;
+      cudaGetLastError();
+    }
+  }
   *out = ctx;
   return LRB_OK;
 }
@@ -404,6 +421,7 @@ extern "C" lrb_status lrb_destroy(lrb_ctx* ctx) {
     if (ctx->aux_done[i]) cudaEventDestroy(ctx->aux_done[i]);
   }
   if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+  if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
   if (ctx->flush_buf) cudaFree(ctx->flush_buf);
   delete ctx;
   return LRB_OK;
@@ -1027,3 +1045,14 @@ extern "C" lrb_status lrb_graph_destroy(lrb_ctx* ctx, lrb_graph* g) {
 }
 
 extern "C" uint64_t lrb_graph_launches(const lrb_graph* g) { return g ? g->launches : 0; }
+
+namespace lrb {
+// row-major packed batch C_i = A_i (m x k) B_i (k x n), beta 0 (for the
+// low-rank product's three-GEMM path)
+lrb_status run_strided_rowmajor(lrb_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
+                                int64_t sA, const double* B, int64_t sB, double* C, int64_t sC,
+                                int64_t batch, cudaStream_t stream) {
+  const Gemm g = normalize('R', 'N', 'N', m, n, k, A, k, sA, B, n, sB, C, n, sC);
+  return run_strided(ctx, g, batch, 0, stream, nullptr);
+}
+}  // namespace lrb

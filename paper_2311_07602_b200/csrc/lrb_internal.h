@@ -32,6 +32,9 @@ struct lrb_ctx {
   cudaStream_t aux_stream[kAux] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t aux_done[kAux] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t fork_ev = nullptr;
+  // stream-ordered scratch pool (keeps freed blocks for reuse instead of
+  // returning them to the driver at every synchronisation)
+  cudaMemPool_t pool = nullptr;
   // L2 flush buffer
   void* flush_buf = nullptr;
   size_t flush_bytes = 0;

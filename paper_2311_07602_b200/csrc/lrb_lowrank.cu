@@ -1,0 +1,504 @@
+// lrb_lowrank.cu — the paper's batched low-rank product on B200.
+//
+//   G_i = A_X_i (A_Vt_i B_U_i) B_X_i        (arXiv 2311.07602, Algorithm 1)
+//
+// over a LowRankBatch: every matrix row-major, each role packed
+// contiguously (item i at base + i*rows*cols), rank_a == rank_b == r
+// (reference low_rank.hpp:109-176; drivers fused_multiply / packed_multiply,
+// kernels.hpp:131-349; oracle low_rank_multiply_reference_raw,
+// low_rank.hpp:73-87). Each of the three products is an in-order FMA chain
+// over its inner index, so G is bitwise the reference oracle's three naive
+// products computed with fused multiply-adds.
+//
+// Fast path (r <= 32, even r and block, 16-B aligned roles): one warp per
+// item, four items per CTA, persistent CTAs.
+//   * C^T = B_U^T A_Vt^T on FP64 DMMA with k ascending; the A_Vt and B_U
+//     chunks of the CTA's four items arrive with ONE 3-D TMA box each
+//     (z = item), padded so fragment loads are bank-conflict free.
+//   * E = A_X C and G = E B_X straight from the accumulators: a lane's
+//     accumulator pair already shares the column the next product needs as an
+//     operand, so four quad-local shuffles per k-block turn accumulators into
+//     MMA operands — no shared-memory round trip; G is stored once.
+// r > 32: three batched GEMMs (lrb_dgemm_strided_batched's kernels) with the
+// intermediates in stream-ordered scratch. Other shapes: a plain per-item
+// kernel (same FMA chains).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "lrb_dispatch.cuh"
+#include "lrb_internal.h"
+
+namespace lrb {
+
+// declared in lrb_api.cu
+lrb_status run_strided_rowmajor(lrb_ctx* ctx, int64_t m, int64_t n, int64_t k, const double* A,
+                                int64_t sA, const double* B, int64_t sB, double* C, int64_t sC,
+                                int64_t batch, cudaStream_t stream);
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn();
+
+template <int R>
+struct LrCfg {
+  static constexpr int G = 4;  // items per CTA, one warp each
+  static constexpr int THREADS = 32 * G;
+  static constexpr int KB = (R >= 32) ? 16 : 32;
+  static constexpr int STAGES = (R <= 8) ? 4 : 2;
+  static constexpr int F = R / 8;
+  static constexpr int PK = KB + 4;  // A_Vt tile [m][kk]
+  static constexpr int PR = R + 4;   // B_U tile  [kk][n]
+  static constexpr int AV = PK * R;  // per item: box (KB+4, R, G)
+  static constexpr int BU = PR * KB; // per item: box (R+4, KB, G)
+  static constexpr int AV_ELEMS = round_up_c(AV * G, 16);
+  static constexpr int BU_ELEMS = round_up_c(BU * G, 16);
+  static constexpr int STAGE = AV_ELEMS + BU_ELEMS;
+  static constexpr size_t SMEM =
+      size_t(STAGES) * STAGE * 8 + size_t(STAGES) * 8 + size_t(STAGES) * 4 + 32;
+};
+
+struct LrProblem {
+  CUtensorMap tmAV;  // (b, r, batch) view of A_Vt
+  CUtensorMap tmBU;  // (r, b, batch) view of B_U
+  const double* a_vt;
+  const double* b_u;
+  const double* a_x;
+  const double* b_x;
+  double* g;
+  int64_t batch;
+  int block, rank;
+  int64_t groups;  // ceil(batch / G)
+};
+
+template <class Cf>
+__device__ __forceinline__ void lr_issue(const LrProblem& p, double* smem, uint64_t* full,
+                                         IssueState* st, int stage, int lane) {
+  long long t_ll = 0;
+  int k0 = 0;
+  if (lane == 0) {
+    t_ll = st->t;
+    k0 = st->k0;
+  }
+  const int64_t t = __shfl_sync(0xffffffffu, t_ll, 0);
+  k0 = __shfl_sync(0xffffffffu, k0, 0);
+  if (t >= p.groups) return;
+  if (lane == 0) {
+    double* av = smem + size_t(stage) * Cf::STAGE;
+    double* bu = av + Cf::AV_ELEMS;
+    fence_proxy_async_smem();
+    const uint64_t pol = policy_evict_first();  // A_Vt and B_U are read exactly once
+    mbar_arrive_expect_tx(&full[stage], uint32_t(Cf::AV + Cf::BU) * Cf::G * 8u);
+    const int z = static_cast<int>(t * Cf::G);
+    tma_load_3d(av, &p.tmAV, k0, 0, z, &full[stage], pol);
+    tma_load_3d(bu, &p.tmBU, 0, k0, z, &full[stage], pol);
+    int nk0 = k0 + Cf::KB;
+    int64_t nt = t;
+    if (nk0 >= p.block) {
+      nk0 = 0;
+      nt = t + gridDim.x;
+    }
+    st->t = nt;
+    st->k0 = nk0;
+  }
+  __syncwarp();
+}
+
+template <int R>
+__global__ void __launch_bounds__(LrCfg<R>::THREADS, 2)
+    lrb_lowrank_kernel(const __grid_constant__ LrProblem p) {
+  using Cf = LrCfg<R>;
+  constexpr int F = Cf::F, KB = Cf::KB, STAGES = Cf::STAGES;
+  extern __shared__ __align__(1024) double smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(STAGES) * Cf::STAGE);
+  IssueState* st = reinterpret_cast<IssueState*>(full + STAGES);
+  int* released = reinterpret_cast<int*>(st + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  const int r = p.rank;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      released[s] = 0;
+    }
+    st->t = blockIdx.x;
+    st->k0 = 0;
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == 0)
+    for (int s = 0; s < STAGES; ++s) lr_issue<Cf>(p, smem, full, st, s, lane);
+
+  int stage = 0;
+  uint32_t phase = 0;
+#pragma unroll 1
+  for (int64_t t = blockIdx.x; t < p.groups; t += gridDim.x) {
+    const int64_t item = t * Cf::G + warp;
+    // acc[fn][fm][c] = C[m = fm*8 + 2tq + c][n = fn*8 + g]   (D of C^T = B_U^T A_Vt^T)
+    double acc[F][F][2];
+#pragma unroll
+    for (int a = 0; a < F; ++a)
+#pragma unroll
+      for (int b = 0; b < F; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+#pragma unroll 1
+    for (int k0 = 0; k0 < p.block; k0 += KB) {
+      const int kvalid = min(KB, p.block - k0);
+      mbar_wait(&full[stage], phase);
+      const double* As = smem + size_t(stage) * Cf::STAGE + warp * Cf::AV;       // [m][kk]
+      const double* Bs = smem + size_t(stage) * Cf::STAGE + Cf::AV_ELEMS + warp * Cf::BU;  // [kk][n]
+      const int nq = kvalid >> 2;
+#pragma unroll 4
+      for (int kq = 0; kq < nq; ++kq) {
+        const int kk = kq * 4 + tq;
+        double af[F], bf[F];
+#pragma unroll
+        for (int fn = 0; fn < F; ++fn) af[fn] = Bs[kk * Cf::PR + fn * 8 + g];  // B_U[kk][n]
+#pragma unroll
+        for (int fm = 0; fm < F; ++fm) bf[fm] = As[(fm * 8 + g) * Cf::PK + kk];  // A_Vt[m][kk]
+#pragma unroll
+        for (int fn = 0; fn < F; ++fn)
+#pragma unroll
+          for (int fm = 0; fm < F; ++fm) dmma_8x8x4(acc[fn][fm][0], acc[fn][fm][1], af[fn], bf[fm]);
+      }
+#pragma unroll 1
+      for (int kk = nq * 4; kk < kvalid; ++kk) {
+#pragma unroll
+        for (int fn = 0; fn < F; ++fn) {
+          const double bv = Bs[kk * Cf::PR + fn * 8 + g];
+#pragma unroll
+          for (int fm = 0; fm < F; ++fm)
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+              acc[fn][fm][c] = fma(As[(fm * 8 + 2 * tq + c) * Cf::PK + kk], bv, acc[fn][fm][c]);
+        }
+      }
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) {
+        last = (atom_add_acq_rel_cta(&released[stage], 1) == Cf::G - 1);
+        if (last) released[stage] = 0;
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) lr_issue<Cf>(p, smem, full, st, stage, lane);
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    if (item >= p.batch) continue;  // warp-uniform
+
+    const double* ax = p.a_x + item * int64_t(r) * r;
+    const double* bx = p.b_x + item * int64_t(r) * r;
+    // quad-local source lane of k-block half h: C[m0 + tq][.] lives in lane
+    // (g, 2h + tq/2), element tq & 1
+    // ---- E = A_X C:  e[fx][fn][c] = E[x = fx*8 + g][n = fn*8 + 2tq + c]
+    double e[F][F][2];
+#pragma unroll
+    for (int a = 0; a < F; ++a)
+#pragma unroll
+      for (int b = 0; b < F; ++b) e[a][b][0] = e[a][b][1] = 0.0;
+#pragma unroll
+    for (int fn = 0; fn < F; ++fn)
+#pragma unroll
+      for (int fm = 0; fm < F; ++fm)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int src = g * 4 + 2 * h + (tq >> 1);
+          const double v0 = __shfl_sync(0xffffffffu, acc[fn][fm][0], src);
+          const double v1 = __shfl_sync(0xffffffffu, acc[fn][fm][1], src);
+          const double cb = (tq & 1) ? v1 : v0;  // B-operand C[m0 + tq][fn*8 + g]
+          const int mcol = fm * 8 + 4 * h + tq;  // m
+#pragma unroll
+          for (int fx = 0; fx < F; ++fx) {
+            const int x = fx * 8 + g;
+            const double a = (x < r && mcol < r) ? ax[x * r + mcol] : 0.0;  // A_X[x][m]
+            dmma_8x8x4(e[fx][fn][0], e[fx][fn][1], a, cb);
+          }
+        }
+    // ---- G = E B_X:  o[fx][fy][c] = G[x = fx*8 + g][y = fy*8 + 2tq + c]
+    double o[F][F][2];
+#pragma unroll
+    for (int a = 0; a < F; ++a)
+#pragma unroll
+      for (int b = 0; b < F; ++b) o[a][b][0] = o[a][b][1] = 0.0;
+#pragma unroll
+    for (int fx = 0; fx < F; ++fx)
+#pragma unroll
+      for (int fn = 0; fn < F; ++fn)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int src = g * 4 + 2 * h + (tq >> 1);
+          const double v0 = __shfl_sync(0xffffffffu, e[fx][fn][0], src);
+          const double v1 = __shfl_sync(0xffffffffu, e[fx][fn][1], src);
+          const double ea = (tq & 1) ? v1 : v0;  // A-operand E[fx*8 + g][n0 + tq]
+          const int nrow = fn * 8 + 4 * h + tq;  // n
+#pragma unroll
+          for (int fy = 0; fy < F; ++fy) {
+            const int y = fy * 8 + g;
+            const double b = (nrow < r && y < r) ? bx[nrow * r + y] : 0.0;  // B_X[n][y]
+            dmma_8x8x4(o[fx][fy][0], o[fx][fy][1], ea, b);
+          }
+        }
+    // ---- store G once (row-major r x r)
+    double* gp = p.g + item * int64_t(r) * r;
+    const bool vec = ((r & 1) == 0) && ((reinterpret_cast<uintptr_t>(gp) & 15) == 0);
+#pragma unroll
+    for (int fx = 0; fx < F; ++fx) {
+      const int x = fx * 8 + g;
+      if (x < r) {
+#pragma unroll
+        for (int fy = 0; fy < F; ++fy) {
+          const int y = fy * 8 + 2 * tq;
+          if (vec && y + 1 < r) {
+            st_global_v2(gp + x * r + y, o[fx][fy][0], o[fx][fy][1]);
+          } else {
+            if (y < r) st_global_cs(gp + x * r + y, o[fx][fy][0]);
+            if (y + 1 < r) st_global_cs(gp + x * r + y + 1, o[fx][fy][1]);
+          }
+        }
+      }
+    }
+  }
+}
+
+// Any shape: one CTA per item, entries spread over threads, the same three
+// in-order FMA chains; intermediates in shared memory (2 r^2 doubles).
+__global__ void lrb_lowrank_simple_kernel(const double* __restrict__ a_vt,
+                                          const double* __restrict__ b_u,
+                                          const double* __restrict__ a_x,
+                                          const double* __restrict__ b_x, double* __restrict__ g,
+                                          int64_t batch, int block, int rank) {
+  extern __shared__ double sm[];
+  double* cs = sm;
+  double* es = sm + size_t(rank) * rank;
+  const int rr = rank * rank;
+  for (int64_t item = blockIdx.x; item < batch; item += gridDim.x) {
+    const double* av = a_vt + item * int64_t(rank) * block;
+    const double* bu = b_u + item * int64_t(block) * rank;
+    const double* ax = a_x + item * int64_t(rr);
+    const double* bx = b_x + item * int64_t(rr);
+    for (int e = threadIdx.x; e < rr; e += blockDim.x) {
+      const int m = e / rank, n = e - m * rank;
+      double s = 0.0;
+      for (int k = 0; k < block; ++k) s = fma(av[int64_t(m) * block + k], bu[int64_t(k) * rank + n], s);
+      cs[e] = s;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < rr; e += blockDim.x) {
+      const int x = e / rank, n = e - x * rank;
+      double s = 0.0;
+      for (int m = 0; m < rank; ++m) s = fma(ax[x * rank + m], cs[m * rank + n], s);
+      es[e] = s;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < rr; e += blockDim.x) {
+      const int x = e / rank, y = e - x * rank;
+      double s = 0.0;
+      for (int n = 0; n < rank; ++n) s = fma(es[x * rank + n], bx[n * rank + y], s);
+      g[item * int64_t(rr) + e] = s;
+    }
+    __syncthreads();
+  }
+}
+
+namespace {
+
+bool encode3(CUtensorMap* map, const double* base, int64_t d0, int64_t d1, int64_t d2,
+             int64_t s1, int64_t s2, int b0, int b1, int b2) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (s1 & 1) || (d2 > 1 && (s2 & 1))) return false;
+  cuuint64_t dims[3] = {cuuint64_t(d0), cuuint64_t(d1), cuuint64_t(d2)};
+  cuuint64_t strides[2] = {cuuint64_t(s1 * 8), cuuint64_t((d2 > 1 ? s2 : s1 * d1 + (s1 * d1) % 2) * 8)};
+  cuuint32_t box[3] = {cuuint32_t(b0), cuuint32_t(b1), cuuint32_t(b2)};
+  cuuint32_t es[3] = {1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int R>
+cudaError_t launch_fast(const LrProblem& p, int device, int sm_count, cudaStream_t s,
+                        int64_t* grid_out) {
+  using Cf = LrCfg<R>;
+  auto kern = lrb_lowrank_kernel<R>;
+  static int occ_cache[64] = {0};
+  int occ = (device >= 0 && device < 64) ? occ_cache[device] : 0;
+  if (occ == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(Cf::SMEM));
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cf::THREADS, Cf::SMEM);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    if (device >= 0 && device < 64) occ_cache[device] = occ;
+  }
+  const int64_t grid = std::min<int64_t>(p.groups, int64_t(sm_count) * occ);
+  *grid_out = grid;
+  if (grid > 0) kern<<<unsigned(grid), Cf::THREADS, Cf::SMEM, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// 0 fast (TMA + DMMA), 1 three GEMMs, 2 simple kernel
+int lowrank_path(int64_t block, int64_t rank, const void* a_vt, const void* b_u) {
+  if (rank > 32) return 1;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(a_vt) | reinterpret_cast<uintptr_t>(b_u)) & 15) == 0;
+  if ((rank & 1) == 0 && (block & 1) == 0 && aligned && encode_fn()) return 0;
+  return 2;
+}
+
+lrb_status run_lowrank(lrb_ctx* ctx, int64_t batch, int64_t block, int64_t rank, const double* a_vt,
+                       const double* b_u, const double* a_x, const double* b_x, double* g,
+                       cudaStream_t s) {
+  if (batch == 0) return LRB_OK;
+  const int path = lowrank_path(block, rank, a_vt, b_u);
+  if (path == 0) {
+    LrProblem p;
+    std::memset(&p, 0, sizeof(p));
+    p.a_vt = a_vt;
+    p.b_u = b_u;
+    p.a_x = a_x;
+    p.b_x = b_x;
+    p.g = g;
+    p.batch = batch;
+    p.block = int(block);
+    p.rank = int(rank);
+    const int R = rank <= 8 ? 8 : rank <= 16 ? 16 : 32;
+    const int G = 4, KB = R >= 32 ? 16 : 32;
+    p.groups = (batch + G - 1) / G;
+    bool ok = encode3(&p.tmAV, a_vt, block, rank, batch, block, rank * block, KB + kPad, R, G) &&
+              encode3(&p.tmBU, b_u, rank, block, batch, rank, block * rank, R + kPad, KB, G);
+    if (ok) {
+      int64_t grid = 0;
+      cudaError_t e = R == 8    ? launch_fast<8>(p, ctx->device, ctx->sm_count, s, &grid)
+                      : R == 16 ? launch_fast<16>(p, ctx->device, ctx->sm_count, s, &grid)
+                                : launch_fast<32>(p, ctx->device, ctx->sm_count, s, &grid);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "lrb_lowrank_kernel launch");
+      if (grid > 0) ctx->launches.fetch_add(1, std::memory_order_relaxed);
+      return LRB_OK;
+    }
+  }
+  if (path == 1) {
+    // C = A_Vt B_U, E = A_X C, G = E B_X as three row-major batched GEMMs
+    double* scratch = nullptr;
+    const size_t bytes = size_t(batch) * size_t(rank * rank) * 2 * sizeof(double);
+    if (ctx->pool)
+      LRB_CUDA_TRY(ctx, cudaMallocFromPoolAsync(reinterpret_cast<void**>(&scratch), bytes,
+                                                ctx->pool, s));
+    else
+      LRB_CUDA_TRY(ctx, cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, s));
+    double* c = scratch;
+    double* e = scratch + size_t(batch) * size_t(rank * rank);
+    const int64_t rr = rank * rank;
+    lrb_status st = run_strided_rowmajor(ctx, rank, rank, block, a_vt, rank * block, b_u,
+                                         block * rank, c, rr, batch, s);
+    if (!st) st = run_strided_rowmajor(ctx, rank, rank, rank, a_x, rr, c, rr, e, rr, batch, s);
+    if (!st) st = run_strided_rowmajor(ctx, rank, rank, rank, e, rr, b_x, rr, g, rr, batch, s);
+    cudaFreeAsync(scratch, s);
+    return st;
+  }
+  const size_t smem = size_t(2) * rank * rank * sizeof(double);
+  if (smem > 200 * 1024)
+    return fail(ctx, LRB_ERR_UNSUPPORTED, "lrb_lowrank_multiply: rank %lld too large", (long long)rank);
+  if (smem > 48 * 1024)
+    LRB_CUDA_TRY(ctx, cudaFuncSetAttribute(lrb_lowrank_simple_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  const int64_t grid = std::min<int64_t>(batch, int64_t(ctx->sm_count) * 8);
+  lrb_lowrank_simple_kernel<<<unsigned(grid), 128, smem, s>>>(a_vt, b_u, a_x, b_x, g, batch,
+                                                             int(block), int(rank));
+  LRB_CUDA_TRY(ctx, cudaGetLastError());
+  ctx->launches.fetch_add(1, std::memory_order_relaxed);
+  return LRB_OK;
+}
+
+}  // namespace lrb
+
+using namespace lrb;
+
+static lrb_status validate_lowrank(lrb_ctx* ctx, const char* fn, int64_t batch, int64_t block,
+                                   int64_t rank, const void* a_vt, const void* b_u, const void* a_x,
+                                   const void* b_x, const void* g) {
+  // LowRankBatch invariants (low_rank.hpp:123-133, validate :162-175)
+  if (batch < 0) return fail(ctx, LRB_ERR_SHAPE, "%s: batch_size must be >= 0", fn);
+  if (block < 1) return fail(ctx, LRB_ERR_SHAPE, "%s: block_size must be >= 1", fn);
+  if (rank < 1) return fail(ctx, LRB_ERR_SHAPE, "%s: ranks must be >= 1", fn);
+  if (block > INT32_MAX || rank > 4096)
+    return fail(ctx, LRB_ERR_UNSUPPORTED, "%s: block or rank too large", fn);
+  if (batch > 0 && (!a_vt || !b_u || !a_x || !b_x || !g))
+    return fail(ctx, LRB_ERR_ARG, "%s: a role array is null", fn);
+  return LRB_OK;
+}
+
+extern "C" lrb_status lrb_lowrank_multiply(lrb_ctx* ctx, int64_t batch, int64_t block,
+                                           int64_t rank, const double* a_vt, const double* b_u,
+                                           const double* a_x, const double* b_x, double* g,
+                                           void* stream) {
+  static const char* fn = "lrb_lowrank_multiply";
+  lrb_status st = validate_lowrank(ctx, fn, batch, block, rank, a_vt, b_u, a_x, b_x, g);
+  if (st) return st;
+  if (!ctx) return fail(nullptr, LRB_ERR_ARG, "%s: null ctx", fn);
+  st = bind(ctx);
+  if (st) return st;
+  return run_lowrank(ctx, batch, block, rank, a_vt, b_u, a_x, b_x, g,
+                     static_cast<cudaStream_t>(stream));
+}
+
+extern "C" lrb_status lrb_lowrank_multiply_host(lrb_ctx* ctx, int64_t batch, int64_t block,
+                                                int64_t rank, const double* a_vt,
+                                                const double* b_u, const double* a_x,
+                                                const double* b_x, double* g) {
+  static const char* fn = "lrb_lowrank_multiply_host";
+  lrb_status st = validate_lowrank(ctx, fn, batch, block, rank, a_vt, b_u, a_x, b_x, g);
+  if (st) return st;
+  if (!ctx) return fail(nullptr, LRB_ERR_ARG, "%s: null ctx", fn);
+  if (batch == 0) return LRB_OK;
+  st = bind(ctx);
+  if (st) return st;
+  // chunk the batch; H2D of the four roles, kernel, D2H of G per chunk on the
+  // context's three pipeline streams
+  const int64_t per_item = 2 * rank * block + 3 * rank * rank;  // doubles
+  const int64_t target = (int64_t(128) << 20) / 8;
+  const int64_t per_chunk = std::max<int64_t>(1, std::min<int64_t>(batch, target / per_item));
+  const int64_t nchunks = (batch + per_chunk - 1) / per_chunk;
+  const int lanes = int(std::min<int64_t>(lrb_ctx::kLanes, nchunks));
+  const size_t need = size_t(per_item * per_chunk + 5 * 32) * 8;
+  for (int l = 0; l < lanes; ++l) {
+    if (ctx->lane_bytes[l] < need) {
+      LRB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->lane_stream[l]));
+      if (ctx->lane_buf[l]) cudaFree(ctx->lane_buf[l]);
+      ctx->lane_buf[l] = nullptr;
+      ctx->lane_bytes[l] = 0;
+      LRB_CUDA_TRY(ctx, cudaMalloc(&ctx->lane_buf[l], need));
+      ctx->lane_bytes[l] = need;
+    }
+  }
+  auto r32 = [](int64_t x) { return (x + 31) / 32 * 32; };
+  const int64_t rb = rank * block, rr = rank * rank;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int l = int(c % lanes);
+    cudaStream_t s = ctx->lane_stream[l];
+    const int64_t i0 = c * per_chunk, n = std::min(per_chunk, batch - i0);
+    double* dav = ctx->lane_buf[l];
+    double* dbu = dav + r32(rb * per_chunk);
+    double* dax = dbu + r32(rb * per_chunk);
+    double* dbx = dax + r32(rr * per_chunk);
+    double* dg = dbx + r32(rr * per_chunk);
+    LRB_CUDA_TRY(ctx, cudaMemcpyAsync(dav, a_vt + i0 * rb, size_t(n * rb) * 8, cudaMemcpyHostToDevice, s));
+    LRB_CUDA_TRY(ctx, cudaMemcpyAsync(dbu, b_u + i0 * rb, size_t(n * rb) * 8, cudaMemcpyHostToDevice, s));
+    LRB_CUDA_TRY(ctx, cudaMemcpyAsync(dax, a_x + i0 * rr, size_t(n * rr) * 8, cudaMemcpyHostToDevice, s));
+    LRB_CUDA_TRY(ctx, cudaMemcpyAsync(dbx, b_x + i0 * rr, size_t(n * rr) * 8, cudaMemcpyHostToDevice, s));
+    st = run_lowrank(ctx, n, block, rank, dav, dbu, dax, dbx, dg, s);
+    if (st) return st;
+    LRB_CUDA_TRY(ctx, cudaMemcpyAsync(g + i0 * rr, dg, size_t(n * rr) * 8, cudaMemcpyDeviceToHost, s));
+  }
+  for (int l = 0; l < lanes; ++l) LRB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->lane_stream[l]));
+  return LRB_OK;
+}
+
+extern "C" double lrb_lowrank_flops_per_item(int64_t rank, int64_t block) {
+  // the reference's accounting, flops_per_item (low_rank.hpp:66-68)
+  return 4.0 * double(rank) * rank * rank + 2.0 * double(rank) * rank * block;
+}

@@ -210,6 +210,8 @@ def get(name: str):
         return Variable("cfg4", 8192, seed=3)
     if name == "cfg5":
         return Strided("cfg5", 512, 32, 512, 131072, seed=4)
+    if name.startswith("lr_"):
+        return get_lowrank(name)
     raise KeyError(name)
 
 
@@ -233,3 +235,44 @@ def variable_layout(w: Variable, items: List[int]):
         ob = align256(ob + 8 * b * r)
         oc = align256(oc + 8 * b * r)
     return offs, (oa, ob, oc)
+
+
+@dataclass
+class LowRank:
+    """The paper's batched low-rank product over a LowRankBatch (row-major
+    roles): G = A_X (A_Vt B_U) B_X, paper Section 6 shapes (batch 20000)."""
+
+    name: str
+    batch: int
+    block: int
+    rank: int
+    seed: int = 7
+
+    def item_flops(self) -> float:  # reference flops_per_item (low_rank.hpp:66-68)
+        r, b = self.rank, self.block
+        return 4.0 * r ** 3 + 2.0 * r * r * b
+
+    def item_bytes(self) -> float:  # A_Vt, B_U, A_X, B_X read + G written
+        r, b = self.rank, self.block
+        return 8.0 * (2 * r * b + 3 * r * r)
+
+    def flops(self, items=None) -> float:
+        return self.item_flops() * (self.batch if items is None else items)
+
+    def bytes(self, items=None) -> float:
+        return self.item_bytes() * (self.batch if items is None else items)
+
+    def describe(self) -> dict:
+        return {"workload": self.name, "batch": self.batch, "block": self.block,
+                "rank": self.rank, "seed": self.seed,
+                "layout": "LowRankBatch: row-major roles packed contiguously"}
+
+
+LOWRANK_R = (8, 16, 32, 64, 128)
+LOWRANK_B = (512, 1024, 2048)
+
+
+def get_lowrank(name: str) -> LowRank:
+    """lr_r{R}_b{B}[_n{batch}]"""
+    parts = dict((p[0], p[1:]) for p in name.split("_")[1:])
+    return LowRank(name, int(parts.get("n", 20000)), int(parts["b"]), int(parts["r"]))

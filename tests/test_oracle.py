@@ -161,3 +161,36 @@ def test_cfg4_shapes_are_deterministic():
     w2 = W.Variable("cfg4", 8192, seed=3)
     assert w.bs == w2.bs and w.rs == w2.rs
     assert 29.0 < w.bytes() / 2 ** 30 < 32.0  # ~30.6 GiB
+
+
+# ------------------------------------------------ the paper's low-rank product
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("batch,block,rank", [(3, 16, 4), (7, 17, 3), (5, 256, 8), (4, 512, 16),
+                                              (2, 64, 32), (3, 1, 1), (2, 33, 40)])
+def test_lowrank_restatement_equals_reference_binary(batch, block, rank):
+    # the reference's own naive_multiply_batch (bench.hpp:55-77 -> low_rank.hpp:73-87)
+    from paper_2311_07602_b200 import lowrank as L
+
+    b = L.LowRankBatch.random(batch, block, rank, batch * 100 + rank)
+    args = (b.a_vt_batch, b.b_u_batch, b.a_x_batch, b.b_x_batch)
+    want = O.ref_lowrank(0, batch, block, rank, *args, workers=2)
+    got = O.lowrank(batch, block, rank, *args, threads=2, mode=O.REF_COMPILED)
+    assert np.array_equal(got, want)
+    fma = O.lowrank(batch, block, rank, *args, threads=2)
+    bad, ratio = O.lowrank_bound_check(batch, block, rank, *args, fma, want)
+    assert bad == 0
+    err, _, _ = O.ref_compare_to_reference(batch, block, rank, *args, fma)
+    assert err < 1e-12
+    # the reference's fused and packed drivers agree with its oracle to its own tolerance
+    for which in (1, 2):
+        other = O.ref_lowrank(which, batch, block, rank, *args, workers=2)
+        assert O.ref_compare_to_reference(batch, block, rank, *args, other)[0] < 1e-11
+
+
+def test_lowrank_flops_accounting():
+    from paper_2311_07602_b200 import lowrank as L
+    from paper_2311_07602_b200._lib import lib
+
+    # tests/test_core.cpp:95-99
+    for r, b, want in ((8, 512, 67584), (1, 1, 6), (32, 2048, 4325376)):
+        assert L.flops_per_item(r, b) == want == lib.lrb_lowrank_flops_per_item(r, b)
