@@ -56,7 +56,9 @@ typedef enum lrb_status {
   LRB_ERR_ARG = 3,         /* bad enum value, null pointer, bad handle */
   LRB_ERR_CUDA = 4,        /* CUDA runtime error (message carries cudaGetErrorString) */
   LRB_ERR_UNSUPPORTED = 5, /* valid request outside what this build implements */
-  LRB_ERR_NO_DEVICE = 6    /* no CUDA device / not sm_100 */
+  LRB_ERR_NO_DEVICE = 6,   /* no CUDA device / not sm_100 */
+  LRB_ERR_IO = 7,          /* file cannot be opened / written (reference IoError) */
+  LRB_ERR_PARSE = 8        /* malformed batch file (reference ParseError) */
 } lrb_status;
 
 typedef struct lrb_ctx lrb_ctx;           /* one per (host thread, device) */
@@ -184,6 +186,43 @@ lrb_status lrb_lowrank_multiply_host(lrb_ctx* ctx, int64_t batch, int64_t block,
                                      const double* b_x, double* g);
 /* the reference's accounting 4 r^3 + 2 r^2 b (flops_per_item, low_rank.hpp:66-68) */
 double lrb_lowrank_flops_per_item(int64_t rank, int64_t block);
+
+/* ------------------------------------------------- LRBATCH1 batch files */
+/*
+ * The reference's flat batch file (batch_io.hpp:11-77): "LRBATCH1", uint64
+ * batch_size, block_size, rank_a, rank_b, then a_vt, b_u, a_x, b_x as
+ * doubles (results not stored). Error texts follow save_batch / load_batch.
+ * hdr receives {batch_size, block_size, rank_a, rank_b}. With device_ptrs the
+ * role buffers are DEVICE pointers and the payload streams through pinned
+ * staging into HBM; otherwise they are host pointers.
+ */
+lrb_status lrb_batch_file_header(const char* path, int64_t* hdr);
+lrb_status lrb_batch_file_load(lrb_ctx* ctx, const char* path, double* a_vt, double* b_u,
+                               double* a_x, double* b_x, int device_ptrs);
+lrb_status lrb_batch_file_save(lrb_ctx* ctx, const char* path, int64_t batch, int64_t block,
+                               int64_t rank_a, int64_t rank_b, const double* a_vt,
+                               const double* b_u, const double* a_x, const double* b_x,
+                               int device_ptrs);
+
+/* --------------------------------------------- BLR multi-RHS matvec */
+/*
+ * Weakly admissible block low-rank matrix (reference BlrMatrix,
+ * blr.hpp:15-87) held on the device: n = tiles * block; host inputs in the
+ * reference's layout — diag: tiles dense block x block tiles; u, x, vt: the
+ * tiles*(tiles-1) off-diagonal factors in row-major (i, j != i) order, each
+ * row-major (u block x rank, x rank x rank, vt rank x block).
+ * lrb_blr_matvec: y = M rhs (blr_matvec, blr.hpp:141-175) for row-major
+ * n x nrhs HOST buffers; the _device form takes device buffers and is
+ * asynchronous. Four batched launches, every chain in the reference's order
+ * (y_i = D_i rhs_i, then += U_ij X_ij Vt_ij rhs_j for j ascending).
+ */
+typedef struct lrb_blr lrb_blr;
+lrb_status lrb_blr_create(lrb_ctx* ctx, int64_t n, int64_t block, int64_t rank, const double* diag,
+                          const double* u, const double* x, const double* vt, lrb_blr** out);
+lrb_status lrb_blr_matvec(lrb_ctx* ctx, lrb_blr* m, const double* rhs, int64_t nrhs, double* y);
+lrb_status lrb_blr_matvec_device(lrb_ctx* ctx, lrb_blr* m, const double* rhs, int64_t nrhs,
+                                 double* y, void* stream);
+lrb_status lrb_blr_destroy(lrb_ctx* ctx, lrb_blr* m);
 
 /* ------------------------------------------------------------ CUDA graphs */
 /*

@@ -57,6 +57,8 @@ def oracle_lib() -> C.CDLL:
         L.oracle_check_bound.restype = i64
         L.oracle_lowrank_batch.argtypes = [C.c_int, i64, i64, i64, vp, vp, vp, vp, vp, C.c_int]
         L.oracle_lowrank_batch.restype = C.c_int
+        L.oracle_blr_matvec.argtypes = [C.c_int, i64, i64, i64, vp, vp, vp, vp, vp, i64, vp]
+        L.oracle_blr_matvec.restype = C.c_int
         _oracle = L
     return _oracle
 
@@ -92,6 +94,9 @@ def ref_lib() -> C.CDLL:
         L.ref_lowrank_multiply.restype = C.c_int
         L.ref_compare_to_reference.argtypes = [i64, i64, i64, vp, vp, vp, vp, vp, P(i64), P(i64)]
         L.ref_compare_to_reference.restype = dbl
+        L.ref_blr_matvec.argtypes = [C.c_int, i64, i64, i64, vp, vp, vp, vp, vp, i64, vp, C.c_int,
+                                     C.c_char_p]
+        L.ref_blr_matvec.restype = C.c_int
         _ref = L
     return _ref
 
@@ -240,3 +245,30 @@ def lowrank_bound_check(batch, block, rank, a_vt, b_u, a_x, b_x, g, g_ref):
     bad = int(np.sum(err[~exact] > bound[~exact]) + np.sum(err[exact] != 0))
     ratio = float(np.max(err[~exact] / bound[~exact])) if np.any(~exact) else 0.0
     return bad, ratio
+
+
+# ------------------------------------------------------------ BLR matvec
+def blr_matvec(n, block, rank, diag, u, x, vt, rhs, nrhs, mode=FMA_CHAIN):
+    """blr_matvec_naive (blr.hpp:179-202) rounded per `mode`"""
+    y = np.zeros(n * nrhs)
+    rc = oracle_lib().oracle_blr_matvec(mode, n, block, rank, _p(diag), _p(u), _p(x), _p(vt),
+                                        _p(rhs), nrhs, _p(y))
+    if rc != 0:
+        raise ValueError("oracle_blr_matvec: bad arguments")
+    return y
+
+
+def ref_blr_matvec(which, n, block, rank, diag, u, x, vt, rhs, nrhs, workers=2, machine=None):
+    """the reference itself: 0 blr_matvec (packed), 1 blr_matvec_naive, 2 dense reconstruction"""
+    y = np.zeros(n * nrhs)
+    rc = ref_lib().ref_blr_matvec(which, n, block, rank, _p(diag), _p(u), _p(x), _p(vt), _p(rhs),
+                                  nrhs, _p(y), workers, machine.encode() if machine else None)
+    if rc != 0:
+        raise ValueError("ref_blr_matvec failed")
+    return y
+
+
+def ref_machines_available() -> bool:
+    """the reference's packed drivers resolve CPU machine files from its own
+    tree (LRBATCH_MACHINE_DIR); present only where /root/reference exists"""
+    return os.path.isdir("/root/reference/proj/machines")

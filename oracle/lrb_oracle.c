@@ -354,3 +354,45 @@ int oracle_lowrank_batch(int mode, int64_t batch, int64_t block, int64_t rank, c
   free(tids);
   return 0;
 }
+
+/* ------------------------------------------------------------------------
+ * BLR multi-RHS matvec, restating blr_matvec_naive (reference
+ * blr.hpp:179-202): y_i = D_i rhs_i for every tile, then for i, j != i
+ * ascending: vt_x = Vt_ij rhs_j; x_vt_x = X_ij vt_x; y_i += U_ij x_vt_x.
+ * Inputs in the reference layout (BlrMatrix: diagonal tiles, off-diagonal
+ * LowRankOperands row-major over (i, j != i)); rhs and y row-major n x nrhs. */
+static void gemm_acc(int mode, const double* a, const double* b, double* c, int64_t m, int64_t k,
+                     int64_t n, int acc) {
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      double sum = acc ? c[i * n + j] : 0.0;
+      if (mode == ORACLE_REF_COMPILED)
+        sum = ref_dot(a + i * k, 1, b + j, n, k, sum, 0);
+      else
+        for (int64_t p = 0; p < k; ++p) sum = fma(a[i * k + p], b[p * n + j], sum);
+      c[i * n + j] = sum;
+    }
+}
+
+int oracle_blr_matvec(int mode, int64_t n, int64_t block, int64_t rank, const double* diag,
+                      const double* u, const double* x, const double* vt, const double* rhs,
+                      int64_t nrhs, double* y) {
+  if (block < 1 || n % block || rank < 1 || nrhs < 1) return -1;
+  const int64_t T = n / block, b = block, r = rank;
+  memset(y, 0, sizeof(double) * (size_t)(n * nrhs));
+  for (int64_t i = 0; i < T; ++i)
+    gemm_acc(mode, diag + i * b * b, rhs + i * b * nrhs, y + i * b * nrhs, b, b, nrhs, 1);
+  double* vt_x = (double*)malloc(sizeof(double) * (size_t)(r * nrhs));
+  double* x_vt_x = (double*)malloc(sizeof(double) * (size_t)(r * nrhs));
+  for (int64_t i = 0; i < T; ++i)
+    for (int64_t j = 0; j < T; ++j) {
+      if (i == j) continue;
+      const int64_t o = i * (T - 1) + (j < i ? j : j - 1);
+      gemm_acc(mode, vt + o * r * b, rhs + j * b * nrhs, vt_x, r, b, nrhs, 0);
+      gemm_acc(mode, x + o * r * r, vt_x, x_vt_x, r, r, nrhs, 0);
+      gemm_acc(mode, u + o * b * r, x_vt_x, y + i * b * nrhs, b, r, nrhs, 1);
+    }
+  free(vt_x);
+  free(x_vt_x);
+  return 0;
+}

@@ -75,6 +75,11 @@ int oracle_lowrank_batch(int mode, int64_t batch, int64_t block, int64_t rank, c
                          const double* b_u, const double* a_x, const double* b_x, double* g,
                          int threads);
 
+/* BLR multi-RHS matvec, restating blr_matvec_naive (blr.hpp:179-202). */
+int oracle_blr_matvec(int mode, int64_t n, int64_t block, int64_t rank, const double* diag,
+                      const double* u, const double* x, const double* vt, const double* rhs,
+                      int64_t nrhs, double* y);
+
 #ifdef __cplusplus
 }
 #endif

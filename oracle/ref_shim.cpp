@@ -206,3 +206,77 @@ double ref_compare_to_reference(int64_t batch, int64_t block, int64_t rank, cons
 }
 
 }  // extern "C"
+
+#include <lrbatch/batch_io.hpp>
+
+extern "C" {
+// the reference's own save_batch / load_batch (batch_io.hpp:29-77)
+int ref_save_batch(const char* path, int64_t batch, int64_t block, int64_t rank, const double* a_vt,
+                   const double* b_u, const double* a_x, const double* b_x) {
+  try {
+    lrbatch::save_batch(make_batch(batch, block, rank, a_vt, b_u, a_x, b_x), path);
+  } catch (...) {
+    return -1;
+  }
+  return 0;
+}
+
+// returns 0 and the arrays, or 1 + the exception text in `err`
+int ref_load_batch(const char* path, int64_t* hdr, double* a_vt, double* b_u, double* a_x,
+                   double* b_x, char* err, size_t errlen) {
+  try {
+    lrbatch::LowRankBatch lb = lrbatch::load_batch(path);
+    hdr[0] = int64_t(lb.batch_size);
+    hdr[1] = int64_t(lb.block_size);
+    hdr[2] = int64_t(lb.rank_a);
+    hdr[3] = int64_t(lb.rank_b);
+    if (a_vt) std::memcpy(a_vt, lb.a_vt_batch.data(), lb.a_vt_batch.size() * 8);
+    if (b_u) std::memcpy(b_u, lb.b_u_batch.data(), lb.b_u_batch.size() * 8);
+    if (a_x) std::memcpy(a_x, lb.a_x_batch.data(), lb.a_x_batch.size() * 8);
+    if (b_x) std::memcpy(b_x, lb.b_x_batch.data(), lb.b_x_batch.size() * 8);
+  } catch (const std::exception& e) {
+    std::strncpy(err, e.what(), errlen - 1);
+    err[errlen - 1] = 0;
+    return 1;
+  }
+  return 0;
+}
+}  // extern "C"
+
+#include <lrbatch/blr.hpp>
+
+extern "C" {
+// which: 0 blr_matvec (packed path, plan for `machine`), 1 blr_matvec_naive,
+// 2 dense_gemm_naive(reconstruct_dense(), rhs) — blr.hpp:64-202
+int ref_blr_matvec(int which, int64_t n, int64_t block, int64_t rank, const double* diag,
+                   const double* u, const double* x, const double* vt, const double* rhs,
+                   int64_t nrhs, double* y, int workers, const char* machine) {
+  try {
+    lrbatch::BlrMatrix m{size_t(n), size_t(block), size_t(rank)};
+    const size_t T = m.tiles, b = size_t(block), r = size_t(rank);
+    for (size_t i = 0; i < T; ++i)
+      m.diagonal.emplace_back(b, b, std::vector<double>(diag + i * b * b, diag + (i + 1) * b * b));
+    for (size_t o = 0; o < T * (T - 1); ++o)
+      m.off_diagonal.emplace_back(b, b, r, std::vector<double>(u + o * b * r, u + (o + 1) * b * r),
+                                  std::vector<double>(x + o * r * r, x + (o + 1) * r * r),
+                                  std::vector<double>(vt + o * r * b, vt + (o + 1) * r * b));
+    lrbatch::DenseBlock rb{size_t(n), size_t(nrhs),
+                           std::vector<double>(rhs, rhs + size_t(n) * size_t(nrhs))};
+    lrbatch::DenseBlock out;
+    if (which == 0) {
+      lrbatch::PackingPlan plan = lrbatch::make_packing_plan(
+          lrbatch::resolve_machine(machine ? machine : "skylake-x-6148"),
+          std::max(r, size_t(nrhs)), b);
+      out = lrbatch::blr_matvec(m, rb, plan, size_t(workers));
+    } else if (which == 1) {
+      out = lrbatch::blr_matvec_naive(m, rb);
+    } else {
+      out = lrbatch::dense_gemm_naive(m.reconstruct_dense(), rb);
+    }
+    std::memcpy(y, out.data.data(), out.data.size() * sizeof(double));
+  } catch (...) {
+    return -1;
+  }
+  return 0;
+}
+}  // extern "C"

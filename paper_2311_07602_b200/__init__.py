@@ -12,7 +12,9 @@ from .lrbatch import (  # noqa: F401
     CudaError,
     DenseBlock,
     DeviceBuffer,
+    IoError,
     LrbError,
+    ParseError,
     NoDeviceError,
     PinnedBuffer,
     PtrPlan,

@@ -19,6 +19,8 @@ LRB_ERR_ARG = 3
 LRB_ERR_CUDA = 4
 LRB_ERR_UNSUPPORTED = 5
 LRB_ERR_NO_DEVICE = 6
+LRB_ERR_IO = 7
+LRB_ERR_PARSE = 8
 
 i64 = C.c_int64
 u64 = C.c_uint64
@@ -101,6 +103,13 @@ SIGNATURES = {
     "lrb_lowrank_multiply": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, vp]),
     "lrb_lowrank_multiply_host": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp]),
     "lrb_lowrank_flops_per_item": (dbl, [i64, i64]),
+    "lrb_batch_file_header": (C.c_int, [C.c_char_p, P(i64)]),
+    "lrb_batch_file_load": (C.c_int, [vp, C.c_char_p, vp, vp, vp, vp, C.c_int]),
+    "lrb_batch_file_save": (C.c_int, [vp, C.c_char_p, i64, i64, i64, i64, vp, vp, vp, vp, C.c_int]),
+    "lrb_blr_create": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, P(vp)]),
+    "lrb_blr_matvec": (C.c_int, [vp, vp, vp, i64, vp]),
+    "lrb_blr_matvec_device": (C.c_int, [vp, vp, vp, i64, vp, vp]),
+    "lrb_blr_destroy": (C.c_int, [vp, vp]),
     "lrb_graph_begin": (C.c_int, [vp, vp]),
     "lrb_graph_end": (C.c_int, [vp, vp, P(vp)]),
     "lrb_graph_launch": (C.c_int, [vp, vp, vp]),

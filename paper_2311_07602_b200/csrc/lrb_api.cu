@@ -1056,3 +1056,15 @@ lrb_status run_strided_rowmajor(lrb_ctx* ctx, int64_t m, int64_t n, int64_t k, c
   return run_strided(ctx, g, batch, 0, stream, nullptr);
 }
 }  // namespace lrb
+
+namespace lrb {
+// row-major strided batch with explicit leading dimensions and beta in {0,1}
+// (the BLR matvec's steps)
+lrb_status run_strided_rowmajor_beta(lrb_ctx* ctx, int64_t m, int64_t n, int64_t k,
+                                     const double* A, int64_t lda, int64_t sA, const double* B,
+                                     int64_t ldb, int64_t sB, double* C, int64_t ldc, int64_t sC,
+                                     int64_t batch, int beta_one, cudaStream_t stream) {
+  const Gemm g = normalize('R', 'N', 'N', m, n, k, A, lda, sA, B, ldb, sB, C, ldc, sC);
+  return run_strided(ctx, g, batch, beta_one, stream, nullptr);
+}
+}  // namespace lrb

@@ -1,0 +1,230 @@
+// lrb_blr.cu — block low-rank (BLR) multi-RHS matvec on the device.
+//
+// The reference's application caller of the batched path (proj/include/
+// lrbatch/blr.hpp): a weakly admissible BLR matrix with dense diagonal tiles
+// D_i (block x block) and low-rank off-diagonal tiles U_ij X_ij Vt_ij, and
+//   y = M rhs    (blr_matvec :141-175, oracle blr_matvec_naive :179-202)
+// with rhs, y row-major n x nrhs. Per row tile i the reference computes
+//   y_i  = D_i rhs_i,   then for j != i ascending:
+//   y_i += U_ij (X_ij (Vt_ij rhs_j))
+// each product a naive in-order chain. On the device this is four launches of
+// the batched GEMM kernels, every chain kept in the reference's order:
+//   1. y_i = D_i rhs_i                       strided batch over i
+//   2. W_.j = [Vt_0j; Vt_1j; ...] rhs_j       strided batch over j (the tiles of
+//                                            block column j stacked, one GEMM)
+//   3. Z_ij = X_ij W_ij                      pointer-array batch (gathers W by
+//                                            column, writes Z stacked by row)
+//   4. y_i += [U_i0 | U_i1 | ...] [Z_i0; Z_i1; ...]   strided batch over i,
+//      K = (tiles-1) rank, beta 1: the concatenated K runs j-major then p,
+//      exactly the reference's sequential per-j accumulation into y_i.
+// The device layout (stacked Vt by column, concatenated U by row) is built
+// once at lrb_blr_create.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "lrb_internal.h"
+
+struct lrb_blr {
+  int device = 0;
+  int64_t n = 0, block = 0, rank = 0, tiles = 0;
+  double* d_diag = nullptr;   // tiles x block^2, row-major tiles
+  double* d_vtcol = nullptr;  // per column j: (tiles-1) rank x block (i != j ascending)
+  double* d_x = nullptr;      // same (j, i) order: rank x rank each
+  double* d_ucat = nullptr;   // per row i: block x (tiles-1) rank, [U_i0 | U_i1 | ...]
+  // per-nrhs workspace and the step-3 plan
+  int64_t ws_nrhs = -1;
+  double* d_w = nullptr;
+  double* d_z = nullptr;
+  lrb_ptr_plan* plan3 = nullptr;
+};
+
+namespace lrb {
+lrb_status run_strided_rowmajor_beta(lrb_ctx* ctx, int64_t m, int64_t n, int64_t k,
+                                     const double* A, int64_t lda, int64_t sA, const double* B,
+                                     int64_t ldb, int64_t sB, double* C, int64_t ldc, int64_t sC,
+                                     int64_t batch, int beta_one, cudaStream_t stream);
+}
+
+using lrb::fail;
+
+namespace {
+
+void free_ws(lrb_ctx* ctx, lrb_blr* m) {
+  if (m->plan3) lrb_ptr_plan_destroy(ctx, m->plan3);
+  if (m->d_w) cudaFree(m->d_w);
+  if (m->d_z) cudaFree(m->d_z);
+  m->plan3 = nullptr;
+  m->d_w = m->d_z = nullptr;
+  m->ws_nrhs = -1;
+}
+
+lrb_status ensure_ws(lrb_ctx* ctx, lrb_blr* m, int64_t nrhs) {
+  if (m->ws_nrhs == nrhs) return LRB_OK;
+  free_ws(ctx, m);
+  const int64_t T = m->tiles, r = m->rank, items = T * (T - 1);
+  const size_t bytes = size_t(items * r * nrhs) * sizeof(double);
+  LRB_CUDA_TRY(ctx, cudaMalloc(&m->d_w, bytes));
+  LRB_CUDA_TRY(ctx, cudaMalloc(&m->d_z, bytes));
+  // step 3 items in W's (column j, row i) order
+  std::vector<int64_t> mm(items, r), nn(items, nrhs), kk(items, r), la(items, r), lb(items, nrhs),
+      lc(items, nrhs);
+  std::vector<const double*> pa(items), pb(items);
+  std::vector<double*> pc(items);
+  int64_t q = 0;
+  for (int64_t j = 0; j < T; ++j) {
+    for (int64_t i = 0; i < T; ++i) {
+      if (i == j) continue;
+      const int64_t jp = j < i ? j : j - 1;  // position of j among row i's tiles
+      pa[q] = m->d_x + q * r * r;
+      pb[q] = m->d_w + q * r * nrhs;
+      pc[q] = m->d_z + (i * (T - 1) + jp) * r * nrhs;
+      ++q;
+    }
+  }
+  lrb_status st = lrb_ptr_plan_create(ctx, 'R', 'N', 'N', items, mm.data(), nn.data(), kk.data(),
+                                      pa.data(), la.data(), pb.data(), lb.data(), pc.data(),
+                                      lc.data(), 0.0, &m->plan3);
+  if (st) return st;
+  m->ws_nrhs = nrhs;
+  return LRB_OK;
+}
+
+}  // namespace
+
+extern "C" lrb_status lrb_blr_create(lrb_ctx* ctx, int64_t n, int64_t block, int64_t rank,
+                                     const double* diag, const double* u, const double* x,
+                                     const double* vt, lrb_blr** out) {
+  static const char* fn = "lrb_blr_create";
+  if (!out) return fail(ctx, LRB_ERR_ARG, "%s: out is null", fn);
+  *out = nullptr;
+  // BlrMatrix constructor invariants (blr.hpp:23-31), with its messages
+  if (!(block >= 1 && n >= block)) return fail(ctx, LRB_ERR_SHAPE, "BlrMatrix: bad block size");
+  if (n % block != 0)
+    return fail(ctx, LRB_ERR_SHAPE, "BlrMatrix: n = %lld is not a multiple of block_size %lld",
+                (long long)n, (long long)block);
+  if (!(rank >= 1 && rank <= block))
+    return fail(ctx, LRB_ERR_SHAPE, "BlrMatrix: rank must be in [1, block]");
+  const int64_t T = n / block;
+  if (!diag || (T > 1 && (!u || !x || !vt)))
+    return fail(ctx, LRB_ERR_ARG, "%s: a tile array is null", fn);
+  if (!ctx) return fail(nullptr, LRB_ERR_ARG, "%s: null ctx", fn);
+  lrb_status st = lrb::bind(ctx);
+  if (st) return st;
+  auto* m = new (std::nothrow) lrb_blr;
+  if (!m) return fail(ctx, LRB_ERR_CAPACITY, "%s: out of host memory", fn);
+  m->device = ctx->device;
+  m->n = n;
+  m->block = block;
+  m->rank = rank;
+  m->tiles = T;
+  const int64_t b = block, r = rank, items = T * (T - 1);
+  auto upload = [&](double** dst, const std::vector<double>& h) -> cudaError_t {
+    cudaError_t e = cudaMalloc(dst, h.size() * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemcpy(*dst, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice);
+    return e;
+  };
+  cudaError_t e = cudaMalloc(&m->d_diag, size_t(T * b * b) * sizeof(double));
+  if (e == cudaSuccess)
+    e = cudaMemcpy(m->d_diag, diag, size_t(T * b * b) * sizeof(double), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && T > 1) {
+    // reference off-diagonal order: row-major over (i, j != i) (blr.hpp:33-35)
+    auto off = [&](int64_t i, int64_t j) { return i * (T - 1) + (j < i ? j : j - 1); };
+    std::vector<double> vtcol(size_t(items * r * b)), xs(size_t(items * r * r)),
+        ucat(size_t(T * b * (T - 1) * r));
+    int64_t q = 0;
+    for (int64_t j = 0; j < T; ++j)
+      for (int64_t i = 0; i < T; ++i) {
+        if (i == j) continue;
+        const int64_t o = off(i, j);
+        std::memcpy(&vtcol[size_t(q * r * b)], vt + o * r * b, size_t(r * b) * sizeof(double));
+        std::memcpy(&xs[size_t(q * r * r)], x + o * r * r, size_t(r * r) * sizeof(double));
+        ++q;
+      }
+    const int64_t K = (T - 1) * r;
+    for (int64_t i = 0; i < T; ++i)
+      for (int64_t j = 0; j < T; ++j) {
+        if (i == j) continue;
+        const int64_t jp = j < i ? j : j - 1;
+        const double* uij = u + off(i, j) * b * r;  // block x rank, row-major
+        for (int64_t row = 0; row < b; ++row)
+          std::memcpy(&ucat[size_t(i * b * K + row * K + jp * r)], uij + row * r,
+                      size_t(r) * sizeof(double));
+      }
+    e = upload(&m->d_vtcol, vtcol);
+    if (e == cudaSuccess) e = upload(&m->d_x, xs);
+    if (e == cudaSuccess) e = upload(&m->d_ucat, ucat);
+  }
+  if (e != cudaSuccess) {
+    lrb_blr_destroy(ctx, m);
+    return lrb::cuda_fail(ctx, e, "lrb_blr_create: upload");
+  }
+  *out = m;
+  return LRB_OK;
+}
+
+extern "C" lrb_status lrb_blr_matvec_device(lrb_ctx* ctx, lrb_blr* m, const double* rhs,
+                                            int64_t nrhs, double* y, void* stream) {
+  static const char* fn = "lrb_blr_matvec";
+  if (!ctx || !m) return fail(ctx, LRB_ERR_ARG, "%s: null ctx or matrix", fn);
+  if (nrhs < 1) return fail(ctx, LRB_ERR_SHAPE, "%s: nrhs must be >= 1", fn);
+  if (!rhs || !y) return fail(ctx, LRB_ERR_ARG, "%s: rhs or y is null", fn);
+  lrb_status st = lrb::bind(ctx);
+  if (st) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t T = m->tiles, b = m->block, r = m->rank, K = (T - 1) * r;
+  // 1. y_i = D_i rhs_i
+  st = lrb::run_strided_rowmajor_beta(ctx, b, nrhs, b, m->d_diag, b, b * b, rhs, nrhs, b * nrhs,
+                                      y, nrhs, b * nrhs, T, 0, s);
+  if (st || T == 1) return st;
+  st = ensure_ws(ctx, m, nrhs);
+  if (st) return st;
+  // 2. W_.j = [Vt_ij]_i rhs_j
+  st = lrb::run_strided_rowmajor_beta(ctx, K, nrhs, b, m->d_vtcol, b, K * b, rhs, nrhs, b * nrhs,
+                                      m->d_w, nrhs, K * nrhs, T, 0, s);
+  if (st) return st;
+  // 3. Z_ij = X_ij W_ij
+  st = lrb_ptr_plan_execute(ctx, m->plan3, stream);
+  if (st) return st;
+  // 4. y_i += [U_ij]_j [Z_ij]_j
+  return lrb::run_strided_rowmajor_beta(ctx, b, nrhs, K, m->d_ucat, K, b * K, m->d_z, nrhs,
+                                        K * nrhs, y, nrhs, b * nrhs, T, 1, s);
+}
+
+extern "C" lrb_status lrb_blr_matvec(lrb_ctx* ctx, lrb_blr* m, const double* rhs, int64_t nrhs,
+                                     double* y) {
+  if (!ctx || !m) return fail(ctx, LRB_ERR_ARG, "lrb_blr_matvec: null ctx or matrix");
+  if (nrhs < 1) return fail(ctx, LRB_ERR_SHAPE, "lrb_blr_matvec: nrhs must be >= 1");
+  if (!rhs || !y) return fail(ctx, LRB_ERR_ARG, "lrb_blr_matvec: rhs or y is null");
+  lrb_status st = lrb::bind(ctx);
+  if (st) return st;
+  const size_t bytes = size_t(m->n * nrhs) * sizeof(double);
+  double *d_rhs = nullptr, *d_y = nullptr;
+  cudaStream_t s = ctx->lane_stream[0];
+  LRB_CUDA_TRY(ctx, cudaMallocAsync(reinterpret_cast<void**>(&d_rhs), bytes, s));
+  LRB_CUDA_TRY(ctx, cudaMallocAsync(reinterpret_cast<void**>(&d_y), bytes, s));
+  cudaError_t e = cudaMemcpyAsync(d_rhs, rhs, bytes, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) {
+    st = lrb_blr_matvec_device(ctx, m, d_rhs, nrhs, d_y, s);
+    if (!st) e = cudaMemcpyAsync(y, d_y, bytes, cudaMemcpyDeviceToHost, s);
+  }
+  cudaFreeAsync(d_rhs, s);
+  cudaFreeAsync(d_y, s);
+  cudaError_t e2 = cudaStreamSynchronize(s);
+  if (st) return st;
+  if (e != cudaSuccess) return lrb::cuda_fail(ctx, e, "lrb_blr_matvec: copy");
+  if (e2 != cudaSuccess) return lrb::cuda_fail(ctx, e2, "lrb_blr_matvec: sync");
+  return LRB_OK;
+}
+
+extern "C" lrb_status lrb_blr_destroy(lrb_ctx* ctx, lrb_blr* m) {
+  if (!m) return LRB_OK;
+  if (ctx) cudaSetDevice(ctx->device);
+  free_ws(ctx, m);
+  if (m->d_diag) cudaFree(m->d_diag);
+  if (m->d_vtcol) cudaFree(m->d_vtcol);
+  if (m->d_x) cudaFree(m->d_x);
+  if (m->d_ucat) cudaFree(m->d_ucat);
+  delete m;
+  return LRB_OK;
+}

@@ -147,3 +147,43 @@ def lowrank_multiply_device(ctx: Context, batch: int, block: int, rank: int, a_v
     _check(lib.lrb_lowrank_multiply(ctx._h, batch, block, rank, _ptr(a_vt), _ptr(b_u), _ptr(a_x),
                                     _ptr(b_x), _ptr(g), stream.handle if stream else None),
            ctx._h)
+
+
+# ------------------------------------------------------ LRBATCH1 batch files
+def save_batch(batch: LowRankBatch, path: str) -> None:
+    """lrbatch::save_batch (batch_io.hpp:29-47)"""
+    import ctypes as C
+
+    batch.validate()
+    _check(lib.lrb_batch_file_save(None, path.encode(), batch.batch_size, batch.block_size,
+                                   batch.rank_a, batch.rank_b, batch.a_vt_batch.ctypes.data,
+                                   batch.b_u_batch.ctypes.data, batch.a_x_batch.ctypes.data,
+                                   batch.b_x_batch.ctypes.data, 0), None)
+
+
+def batch_file_header(path: str):
+    import ctypes as C
+
+    hdr = (C.c_int64 * 4)()
+    _check(lib.lrb_batch_file_header(path.encode(), hdr), None)
+    return tuple(int(x) for x in hdr)
+
+
+def load_batch(path: str) -> LowRankBatch:
+    """lrbatch::load_batch (batch_io.hpp:49-77): zeroed results"""
+    n, block, ra, rb = batch_file_header(path)
+    out = LowRankBatch(n, block, ra, rb)
+    _check(lib.lrb_batch_file_load(None, path.encode(), out.a_vt_batch.ctypes.data,
+                                   out.b_u_batch.ctypes.data, out.a_x_batch.ctypes.data,
+                                   out.b_x_batch.ctypes.data, 0), None)
+    return out
+
+
+def load_batch_device(ctx: Context, path: str):
+    """Stream a batch file into device memory: returns (header, [a_vt, b_u,
+    a_x, b_x] DeviceBuffers, g DeviceBuffer) ready for lowrank_multiply_device."""
+    n, block, ra, rb = batch_file_header(path)
+    bufs = [ctx.empty(n * ra * block), ctx.empty(n * block * rb), ctx.empty(n * ra * ra),
+            ctx.empty(n * rb * rb)]
+    _check(lib.lrb_batch_file_load(ctx._h, path.encode(), *[b.ptr for b in bufs], 1), ctx._h)
+    return (n, block, ra, rb), bufs, ctx.empty(n * ra * rb)

@@ -56,6 +56,18 @@ class NoDeviceError(LrbError):
     status = _lib.LRB_ERR_NO_DEVICE
 
 
+class IoError(LrbError):
+    """reference IoError (common.hpp:34-37)"""
+
+    status = _lib.LRB_ERR_IO
+
+
+class ParseError(LrbError):
+    """reference ParseError (common.hpp:29-32)"""
+
+    status = _lib.LRB_ERR_PARSE
+
+
 _EXC = {
     _lib.LRB_ERR_SHAPE: ShapeError,
     _lib.LRB_ERR_CAPACITY: CapacityError,
@@ -63,6 +75,8 @@ _EXC = {
     _lib.LRB_ERR_CUDA: CudaError,
     _lib.LRB_ERR_UNSUPPORTED: UnsupportedError,
     _lib.LRB_ERR_NO_DEVICE: NoDeviceError,
+    _lib.LRB_ERR_IO: IoError,
+    _lib.LRB_ERR_PARSE: ParseError,
 }
 
 

@@ -1,0 +1,98 @@
+"""GPU BLR multi-RHS matvec (reference blr.hpp:141-202; tests/test_blr.cpp).
+
+Bitwise equal to the FMA-chain restatement of blr_matvec_naive; against the
+reference binary's blr_matvec (packed path) and its dense reconstruction
+within the reference's own tolerance (max_rel < 1e-10, test_blr.cpp:12-22)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2311_07602_b200 import DenseBlock, ShapeError
+from paper_2311_07602_b200 import blr as B
+from paper_2311_07602_b200 import lowrank as L
+
+pytestmark = pytest.mark.gpu
+
+
+def max_rel(got, expect):
+    # tests/test_blr.cpp:12-22
+    rms = np.sqrt(np.mean(expect * expect))
+    floor = rms if rms > 0 else 1.0
+    return float(np.max(np.abs(got - expect) / np.maximum(np.abs(expect), floor)))
+
+
+def _rhs(n, nrhs, seed):
+    return DenseBlock(n, nrhs, L._uniform_vec(seed * 7919 + 1, 0, np.arange(n * nrhs, dtype=np.uint64)))
+
+
+def _check(m, rhs, y):
+    diag, u, x, vt = m.packed_arrays()
+    args = (m.n, m.block_size, m.rank, diag, u, x, vt, rhs.data, rhs.cols)
+    fma = O.blr_matvec(*args)
+    assert np.array_equal(y.data, fma), f"!= FMA-chain oracle ({np.abs(y.data - fma).max():.3e})"
+    if O.ref_available():
+        assert max_rel(y.data, O.ref_blr_matvec(1, *args)) < 1e-11  # blr_matvec_naive
+        if O.ref_machines_available():
+            assert max_rel(y.data, O.ref_blr_matvec(0, *args)) < 1e-10  # packed blr_matvec
+        assert max_rel(y.data, O.ref_blr_matvec(2, *args)) < 1e-10  # dense reconstruction
+    else:
+        assert max_rel(y.data, O.blr_matvec(*args, mode=O.REF_COMPILED)) < 1e-11
+
+
+def test_identity_like_maps_rhs_to_itself(ctx):
+    # test_blr.cpp "identity-like BLR maps rhs to itself"
+    block, tiles, rank = 16, 3, 4
+    m = B.BlrMatrix.random(block * tiles, block, rank, 5)
+    for t in range(tiles):
+        m.diagonal[t] = DenseBlock.identity(block)
+    for tile in m.off_diagonal:
+        tile.u[:] = 0.0
+        tile.x[:] = 0.0
+        tile.vt[:] = 0.0
+    rhs = _rhs(block * tiles, 2, 7)
+    y = B.blr_matvec(m, rhs, ctx=ctx)
+    assert np.array_equal(y.data, rhs.data)
+
+
+@pytest.mark.parametrize("tiles,rank,nrhs,block", [(2, 4, 8, 32), (4, 4, 1, 24), (4, 8, 8, 24),
+                                                   (16, 4, 1, 24), (16, 8, 8, 24), (5, 4, 6, 20),
+                                                   (3, 8, 11, 16), (1, 4, 3, 16), (8, 16, 16, 64)])
+def test_grids_match_reference(ctx, tiles, rank, nrhs, block):
+    m = B.BlrMatrix.random(tiles * block, block, rank, 100 + tiles + rank + nrhs)
+    rhs = _rhs(tiles * block, nrhs, 17 + nrhs)
+    _check(m, rhs, B.blr_matvec(m, rhs, ctx=ctx))
+
+
+def test_linearity_and_reuse(ctx):
+    # test_blr.cpp "linearity in the right-hand side" (+ nrhs changes reuse the upload)
+    block, tiles, rank, nrhs = 24, 4, 8, 3
+    m = B.BlrMatrix.random(tiles * block, block, rank, 23)
+    r1, r2 = _rhs(tiles * block, nrhs, 29), _rhs(tiles * block, nrhs, 30)
+    a, b = 1.75, -0.5
+    mix = DenseBlock(tiles * block, nrhs, a * r1.data + b * r2.data)
+    y_mix = B.blr_matvec(m, mix, ctx=ctx)
+    y1, y2 = B.blr_matvec(m, r1, ctx=ctx), B.blr_matvec(m, r2, ctx=ctx)
+    assert max_rel(y_mix.data, a * y1.data + b * y2.data) < 1e-10
+    _check(m, r1, y1)
+    r5 = _rhs(tiles * block, 5, 31)
+    _check(m, r5, B.blr_matvec(m, r5, ctx=ctx))
+
+
+def test_paper_scale_rank8_8rhs(ctx):
+    # the paper's BLR experiment shape (rank 8, 8 RHS), n = 8192, block 512
+    m = B.BlrMatrix.random(8192, 512, 8, 3)
+    rhs = _rhs(8192, 8, 4)
+    y = B.blr_matvec(m, rhs, ctx=ctx)
+    diag, u, x, vt = m.packed_arrays()
+    fma = O.blr_matvec(8192, 512, 8, diag, u, x, vt, rhs.data, 8)
+    assert np.array_equal(y.data, fma)
+
+
+def test_constraints():
+    with pytest.raises(ShapeError, match="not a multiple"):
+        B.BlrMatrix(100, 16, 4)
+    with pytest.raises(ShapeError, match="rank must be in"):
+        B.BlrMatrix(64, 16, 17)
+    m = B.BlrMatrix.random(64, 16, 4, 1)
+    with pytest.raises(ShapeError, match="rhs has"):
+        B.blr_matvec(m, DenseBlock(32, 2))

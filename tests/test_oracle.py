@@ -182,7 +182,7 @@ def test_lowrank_restatement_equals_reference_binary(batch, block, rank):
     err, _, _ = O.ref_compare_to_reference(batch, block, rank, *args, fma)
     assert err < 1e-12
     # the reference's fused and packed drivers agree with its oracle to its own tolerance
-    for which in (1, 2):
+    for which in ((1, 2) if O.ref_machines_available() else (1,)):
         other = O.ref_lowrank(which, batch, block, rank, *args, workers=2)
         assert O.ref_compare_to_reference(batch, block, rank, *args, other)[0] < 1e-11
 
