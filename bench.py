@@ -611,7 +611,20 @@ def main():
 
     w = W.get(args.config)
     world, rank, local, pg = dist_setup()
-    if args.impl == "reference":
+    import bench_rows as R
+
+    bench_mod = sys.modules[__name__]
+    if isinstance(w, W.LowRank):
+        if args.impl == "reference":
+            R.run_lowrank_reference(args, w, world, rank, bench_mod)
+        else:
+            R.run_lowrank_gpu(args, w, world, rank, local, pg, bench_mod)
+    elif isinstance(w, W.Blr):
+        if args.impl == "reference":
+            R.run_blr_reference(args, w, world, rank, bench_mod)
+        else:
+            R.run_blr_gpu(args, w, world, rank, local, pg, bench_mod)
+    elif args.impl == "reference":
         run_reference_arm(args, w, world, rank)
     else:
         run_gpu_arm(args, w, world, rank, local, pg)

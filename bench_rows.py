@@ -1,0 +1,295 @@
+"""bench.py legs for the widened §8(f) rows, same contract as the GEMM legs.
+
+  --config lr_r{R}_b{B}[_n{batch}]      the paper's batched low-rank product
+                                        (lrb_lowrank_multiply; reference arm:
+                                        the reference's naive_multiply_batch)
+  --config blr_n{N}_b{B}_r{R}_k{nrhs}   BLR multi-RHS matvec (lrb_blr_matvec;
+                                        reference arm: the reference's
+                                        blr_matvec / blr_matvec_naive)
+
+A step is one full product / matvec with inputs resident in HBM; the K timed
+steps replay as one CUDA graph. GFLOP/s follows the reference's accounting
+(4r^3 + 2r^2 b per low-rank item; 2mnk per product of the matvec).
+"""
+from __future__ import annotations
+
+import json
+import os
+import statistics
+import time
+
+import numpy as np
+
+
+def _roof(fl, by, ms, hbm, fp64, fsrc, hsrc):
+    intensity = fl / by
+    fp64_bound = intensity * hbm * 1e9 >= fp64 * 1e12
+    if fp64_bound:
+        ach = fl / (ms * 1e-3) / 1e12
+        r = {"bound": "tensor", "achieved": round(ach, 3), "peak": fp64, "unit": "TFLOP/s",
+             "frac": round(ach / fp64, 4), "peak_source": fsrc}
+    else:
+        ach = by / (ms * 1e-3) / 1e9
+        r = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+             "frac": round(ach / hbm, 4), "peak_source": hsrc}
+    r["roofline_frac"] = round(fl / (ms * 1e-3) / min(fp64 * 1e12, intensity * hbm * 1e9), 4)
+    r["algorithmic"] = by
+    r["traffic"] = None
+    return r
+
+
+def _timed(ctx, stream, step, steps, warmup, pg, B, clock_sampler):
+    for _ in range(warmup):
+        step()
+    stream.synchronize()
+    with ctx.capture(stream) as cap:
+        for _ in range(steps):
+            step()
+    graph = cap.graph
+    sampler = clock_sampler
+    sampler.start()
+    B.barrier(pg)
+    launches0 = ctx.launch_count
+    e0, e1 = ctx.event(), ctx.event()
+    e0.record(stream)
+    graph.launch(stream)
+    e1.record(stream)
+    stream.synchronize()
+    B.barrier(pg)
+    clocks = sampler.stop()
+    return e0.elapsed_ms(e1), ctx.launch_count - launches0, clocks
+
+
+# ------------------------------------------------------------ low-rank product
+def lowrank_inputs_host(w, items):
+    from paper_2311_07602_b200 import lowrank as L
+
+    b = L.LowRankBatch.random(items, w.block, w.rank, w.seed)
+    return b
+
+
+def run_lowrank_gpu(args, w, world, rank, local, pg, B):
+    from paper_2311_07602_b200 import Context
+    from paper_2311_07602_b200 import lowrank as L
+
+    hbm, hsrc, fp64, fsrc = B.load_peaks()
+    ctx = Context(local)
+    s = ctx.stream()
+    n, r, blk = w.batch, w.rank, w.block
+    bufs = [ctx.empty(n * r * blk), ctx.empty(n * blk * r), ctx.empty(n * r * r),
+            ctx.empty(n * r * r), ctx.empty(n * r * r)]
+    # roles as column-major views of the row-major items; global item offset per rank
+    first = rank * n
+    ctx.fill_uniform(bufs[0], blk, r, blk, r * blk, n, w.seed, 0, first)
+    ctx.fill_uniform(bufs[1], r, blk, r, blk * r, n, w.seed, 1, first)
+    ctx.fill_uniform(bufs[2], r, r, r, r * r, n, w.seed, 2, first)
+    ctx.fill_uniform(bufs[3], r, r, r, r * r, n, w.seed, 3, first)
+    ctx.synchronize()
+    step = lambda: L.lowrank_multiply_device(ctx, n, blk, r, *bufs, stream=s)  # noqa: E731
+    ms_rank, launches, clocks = _timed(ctx, s, step, args.steps, args.warmup, pg, B,
+                                       B.ClockSampler(local))
+    ms_step = B.all_max(pg, ms_rank) / args.steps
+    fl_all, by_all = B.all_sum(pg, w.flops()), B.all_sum(pg, w.bytes())
+    roof = _roof(w.flops(), w.bytes(), ms_rank / args.steps, hbm, fp64, fsrc, hsrc)
+    roof["kernel"] = "lrb_lowrank_kernel<R>" if r <= 32 else "lrb_gemm_kernel x3"
+    roof["kernel_ms"] = round(ms_rank / max(1, launches), 4)
+    e2e = None
+    if args.e2e_steps > 0:
+        hb = lowrank_inputs_host(w, n)
+        pins = [ctx.pinned(a.size) for a in (hb.a_vt_batch, hb.b_u_batch, hb.a_x_batch,
+                                            hb.b_x_batch, hb.g_xy_batch)]
+        for p, a in zip(pins, (hb.a_vt_batch, hb.b_u_batch, hb.a_x_batch, hb.b_x_batch)):
+            p.array[:] = a
+        from paper_2311_07602_b200.lrbatch import _check, lib
+
+        def once():
+            _check(lib.lrb_lowrank_multiply_host(ctx._h, n, blk, r, *[p.ptr for p in pins]),
+                   ctx._h)
+
+        once()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            once()
+        dt = B.all_max(pg, (time.perf_counter() - t0) / args.e2e_steps)
+        e2e = {"value": round(fl_all / dt / 1e9, 2), "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(8 * (2 * r * blk + 2 * r * r) * n),
+               "d2h_bytes_per_step": int(8 * r * r * n), "ms_per_step": round(dt * 1e3, 2),
+               "path": "lrb_lowrank_multiply_host (chunked H2D/kernel/D2H)"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = lowrank_cpu(w, os.cpu_count() or 1, args.ref_seconds)
+        cpu.pop("seconds", None)
+    if rank == 0:
+        cfg = dict(w.describe())
+        cfg.update({"parallelism": f"shard{world} (independent items, no collective)",
+                    "timed_launch": "CUDA graph of the K steps",
+                    "l2": "inputs larger than L2 (no flush)" if w.bytes() > 3 * 132644864
+                          else "inputs within 3x L2"})
+        print(json.dumps({
+            "metric": "batched FP64 GFLOP/s", "value": round(fl_all / (ms_step * 1e-3) / 1e9, 2),
+            "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (device counter RNG, uniform[-1,1))", "config": cfg,
+            "hbm_gbs": round(by_all / (ms_step * 1e-3) / 1e9, 1), "roofline": roof,
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches)}),
+            flush=True)
+    ctx.close()
+
+
+def lowrank_cpu(w, threads, target_s):
+    """the reference's naive_multiply_batch (bench.hpp:55-77) on a bounded sample"""
+    import oracle as O
+
+    probe = lowrank_inputs_host(w, max(1, threads))
+    args = (probe.a_vt_batch, probe.b_u_batch, probe.a_x_batch, probe.b_x_batch)
+    t0 = time.perf_counter()
+    if O.ref_available():
+        O.ref_lowrank(0, probe.batch_size, w.block, w.rank, *args, workers=threads)
+        kind = "reference"
+    else:
+        O.lowrank(probe.batch_size, w.block, w.rank, *args, threads=threads, mode=O.REF_COMPILED)
+        kind = "port"
+    per_item = (time.perf_counter() - t0) / probe.batch_size * threads
+    items = int(min(w.batch, max(threads, threads * target_s / max(per_item, 1e-9))))
+    b = lowrank_inputs_host(w, items)
+    args = (b.a_vt_batch, b.b_u_batch, b.a_x_batch, b.b_x_batch)
+    t0 = time.perf_counter()
+    if kind == "reference":
+        O.ref_lowrank(0, items, w.block, w.rank, *args, workers=threads)
+    else:
+        O.lowrank(items, w.block, w.rank, *args, threads=threads, mode=O.REF_COMPILED)
+    dt = time.perf_counter() - t0
+    return {"value": round(w.item_flops() * items / dt / 1e9, 3), "unit": "GFLOP/s",
+            "cores": threads, "kind": kind, "seconds": dt,
+            "sample": f"{items} of {w.batch} items ({dt:.1f} s), naive_multiply_batch"}
+
+
+def run_lowrank_reference(args, w, world, rank, B):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    for _ in range(max(0, args.warmup_ref)):
+        lowrank_cpu(w, threads, min(1.0, args.ref_seconds))
+    vals = [lowrank_cpu(w, threads, args.ref_seconds) for _ in range(args.steps)]
+    v = statistics.median(x["value"] for x in vals)
+    cb = dict(vals[0], value=v)
+    ms = 1e3 * statistics.median(x.pop("seconds") for x in vals)
+    cb.pop("seconds", None)
+    print(json.dumps({
+        "metric": "batched FP64 GFLOP/s", "value": v, "unit": "GFLOP/s", "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (counter RNG, uniform[-1,1))", "config": w.describe(),
+        "cpu_baseline": cb, "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                                    "d2h_bytes_per_step": 0}, "gpu_launches": 0}), flush=True)
+
+
+# ------------------------------------------------------------------ BLR matvec
+def blr_host(w):
+    from paper_2311_07602_b200 import DenseBlock
+    from paper_2311_07602_b200 import blr as BL
+    from paper_2311_07602_b200 import lowrank as L
+
+    m = BL.BlrMatrix.random(w.n, w.block, w.rank, w.seed)
+    rhs = DenseBlock(w.n, w.nrhs, L._uniform_vec(w.seed * 7919 + 1, 0,
+                                                 np.arange(w.n * w.nrhs, dtype=np.uint64)))
+    return m, rhs
+
+
+def run_blr_gpu(args, w, world, rank, local, pg, B):
+    from paper_2311_07602_b200 import Context
+    from paper_2311_07602_b200.lrbatch import _check, lib
+
+    hbm, hsrc, fp64, fsrc = B.load_peaks()
+    ctx = Context(local)
+    s = ctx.stream()
+    m, rhs = blr_host(w)
+    h = m.device_handle(ctx)
+    d_rhs, d_y = ctx.to_device(rhs.data), ctx.empty(w.n * w.nrhs)
+    step = lambda: _check(lib.lrb_blr_matvec_device(ctx._h, h, d_rhs.ptr, w.nrhs, d_y.ptr,  # noqa
+                                                     s.handle), ctx._h)
+    ms_rank, launches, clocks = _timed(ctx, s, step, args.steps, args.warmup, pg, B,
+                                       B.ClockSampler(local))
+    ms_step = B.all_max(pg, ms_rank) / args.steps
+    fl_all, by_all = B.all_sum(pg, w.flops()), B.all_sum(pg, w.bytes())
+    roof = _roof(w.flops(), w.bytes(), ms_rank / args.steps, hbm, fp64, fsrc, hsrc)
+    roof["kernel"] = "lrb_gemm_kernel x3 + blr_couple_kernel per matvec"
+    roof["kernel_ms"] = round(ms_rank / max(1, launches), 4)
+    e2e = None
+    if args.e2e_steps > 0:
+        y = np.zeros(w.n * w.nrhs)
+
+        def once():
+            _check(lib.lrb_blr_matvec(ctx._h, h, rhs.data.ctypes.data, w.nrhs, y.ctypes.data),
+                   ctx._h)
+
+        once()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            once()
+        dt = B.all_max(pg, (time.perf_counter() - t0) / args.e2e_steps)
+        e2e = {"value": round(fl_all / dt / 1e9, 2), "unit": "GFLOP/s",
+               "h2d_bytes_per_step": 8 * w.n * w.nrhs, "d2h_bytes_per_step": 8 * w.n * w.nrhs,
+               "ms_per_step": round(dt * 1e3, 3),
+               "path": "lrb_blr_matvec (matrix resident on the device, rhs/y host)"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = blr_cpu(w, m, rhs)
+        cpu.pop("seconds", None)
+    if rank == 0:
+        cfg = dict(w.describe())
+        cfg.update({"parallelism": f"replicas{world} (one matvec per GPU, no collective)",
+                    "timed_launch": "CUDA graph of the K steps"})
+        print(json.dumps({
+            "metric": "batched FP64 GFLOP/s", "value": round(fl_all / (ms_step * 1e-3) / 1e9, 2),
+            "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (counter RNG, uniform[-1,1))", "config": cfg,
+            "hbm_gbs": round(by_all / (ms_step * 1e-3) / 1e9, 1), "roofline": roof,
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches)}),
+            flush=True)
+    ctx.close()
+
+
+def blr_cpu(w, m, rhs, which=None):
+    """the reference's blr_matvec (packed path; naive when its machine files are absent)"""
+    import oracle as O
+
+    diag, u, x, vt = m.packed_arrays()
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    if O.ref_available():
+        which = 0 if O.ref_machines_available() else 1
+        O.ref_blr_matvec(which, w.n, w.block, w.rank, diag, u, x, vt, rhs.data, w.nrhs,
+                         workers=threads)
+        kind = "reference"
+        what = "blr_matvec (packed_multiply, all workers)" if which == 0 else "blr_matvec_naive"
+    else:
+        O.blr_matvec(w.n, w.block, w.rank, diag, u, x, vt, rhs.data, w.nrhs, mode=O.REF_COMPILED)
+        kind, what = "port", "blr_matvec_naive restatement"
+    dt = time.perf_counter() - t0
+    return {"value": round(w.flops() / dt / 1e9, 3), "unit": "GFLOP/s",
+            "cores": threads if (kind == "reference" and which == 0) else 1, "kind": kind,
+            "seconds": dt,
+            "sample": f"one full matvec ({dt:.2f} s): {what}"}
+
+
+def run_blr_reference(args, w, world, rank, B):
+    if rank != 0:
+        return
+    m, rhs = blr_host(w)
+    for _ in range(max(0, args.warmup_ref)):
+        blr_cpu(w, m, rhs)
+    vals = [blr_cpu(w, m, rhs) for _ in range(args.steps)]
+    v = statistics.median(x["value"] for x in vals)
+    ms = 1e3 * statistics.median(x.pop("seconds") for x in vals)
+    print(json.dumps({
+        "metric": "batched FP64 GFLOP/s", "value": v, "unit": "GFLOP/s", "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (counter RNG, uniform[-1,1))", "config": w.describe(),
+        "cpu_baseline": dict(vals[0], value=v),
+        "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0}), flush=True)

@@ -173,6 +173,10 @@ int auto_variant(int64_t m, int64_t n, int64_t batch, int sm_count) {
     return LRB_V_N64;
   }
   if (m <= 64 && m < n) {
+    // the same wave argument for short-wide C (BLR matvec: 64 row tiles of
+    // nrhs x block): 32-column tiles at five CTAs per SM
+    if (m <= 16 && batch > 0 && batch * ((n + 127) / 128) < 2LL * 2 * sm_count)
+      return m <= 8 ? LRB_V_M8T : LRB_V_M16T;
     if (m <= 8) return LRB_V_M8;
     if (m <= 16) return LRB_V_M16;
     if (m <= 32) return LRB_V_M32;
@@ -421,6 +425,11 @@ extern "C" lrb_status lrb_destroy(lrb_ctx* ctx) {
     if (ctx->aux_done[i]) cudaEventDestroy(ctx->aux_done[i]);
   }
   if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+  if (ctx->ws_ev) {
+    cudaEventSynchronize(ctx->ws_ev);
+    cudaEventDestroy(ctx->ws_ev);
+  }
+  if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
   if (ctx->flush_buf) cudaFree(ctx->flush_buf);
   delete ctx;
@@ -433,6 +442,51 @@ extern "C" const char* lrb_last_error(const lrb_ctx* ctx) {
 extern "C" int lrb_ctx_device(const lrb_ctx* ctx) { return ctx ? ctx->device : -1; }
 extern "C" int lrb_ctx_sm_count(const lrb_ctx* ctx) { return ctx ? ctx->sm_count : 0; }
 extern "C" uint64_t lrb_launch_count(const lrb_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
+
+// ===================================================== context workspace
+namespace lrb {
+
+lrb_status acquire_workspace(lrb_ctx* ctx, size_t bytes, cudaStream_t s, void** out,
+                             bool* temporary) {
+  *temporary = false;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  LRB_CUDA_TRY(ctx, cudaStreamIsCapturing(s, &cap));
+  if (cap != cudaStreamCaptureStatusNone) {
+    if (bytes <= ctx->ws_bytes) {
+      *out = ctx->ws;
+      return LRB_OK;
+    }
+    // not sized yet: a graph-owned allocation (correct; mapped per replay)
+    LRB_CUDA_TRY(ctx, pool_alloc(ctx, out, bytes, s));
+    *temporary = true;
+    return LRB_OK;
+  }
+  if (bytes > ctx->ws_bytes) {
+    if (ctx->ws_pending) LRB_CUDA_TRY(ctx, cudaEventSynchronize(ctx->ws_ev));
+    if (ctx->ws) cudaFree(ctx->ws);
+    ctx->ws = nullptr;
+    ctx->ws_bytes = 0;
+    ctx->ws_pending = false;
+    LRB_CUDA_TRY(ctx, cudaMalloc(&ctx->ws, bytes));
+    ctx->ws_bytes = bytes;
+  }
+  if (!ctx->ws_ev) LRB_CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->ws_ev, cudaEventDisableTiming));
+  if (ctx->ws_pending) LRB_CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ws_ev, 0));
+  *out = ctx->ws;
+  return LRB_OK;
+}
+
+void release_workspace(lrb_ctx* ctx, cudaStream_t s, void* p, bool temporary) {
+  if (temporary) {
+    cudaFreeAsync(p, s);
+    return;
+  }
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) return;
+  if (cudaEventRecord(ctx->ws_ev, s) == cudaSuccess) ctx->ws_pending = true;
+}
+
+}  // namespace lrb
 
 // ===================================================== memory / streams / events
 extern "C" lrb_status lrb_malloc(lrb_ctx* ctx, size_t bytes, void** dptr) {

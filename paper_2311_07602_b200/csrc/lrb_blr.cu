@@ -7,13 +7,15 @@
 // with rhs, y row-major n x nrhs. Per row tile i the reference computes
 //   y_i  = D_i rhs_i,   then for j != i ascending:
 //   y_i += U_ij (X_ij (Vt_ij rhs_j))
-// each product a naive in-order chain. On the device this is four launches of
-// the batched GEMM kernels, every chain kept in the reference's order:
+// each product a naive in-order chain. On the device this is three launches of
+// the batched GEMM kernels and one small coupling kernel, every chain kept in
+// the reference's order:
 //   1. y_i = D_i rhs_i                       strided batch over i
 //   2. W_.j = [Vt_0j; Vt_1j; ...] rhs_j       strided batch over j (the tiles of
 //                                            block column j stacked, one GEMM)
-//   3. Z_ij = X_ij W_ij                      pointer-array batch (gathers W by
-//                                            column, writes Z stacked by row)
+//   3. Z_ij = X_ij W_ij                      one thread per Z entry (an r-long
+//                                            FMA chain; reads W in column order,
+//                                            writes Z stacked by row)
 //   4. y_i += [U_i0 | U_i1 | ...] [Z_i0; Z_i1; ...]   strided batch over i,
 //      K = (tiles-1) rank, beta 1: the concatenated K runs j-major then p,
 //      exactly the reference's sequential per-j accumulation into y_i.
@@ -32,11 +34,10 @@ struct lrb_blr {
   double* d_vtcol = nullptr;  // per column j: (tiles-1) rank x block (i != j ascending)
   double* d_x = nullptr;      // same (j, i) order: rank x rank each
   double* d_ucat = nullptr;   // per row i: block x (tiles-1) rank, [U_i0 | U_i1 | ...]
-  // per-nrhs workspace and the step-3 plan
+  // per-nrhs workspace
   int64_t ws_nrhs = -1;
   double* d_w = nullptr;
   double* d_z = nullptr;
-  lrb_ptr_plan* plan3 = nullptr;
 };
 
 namespace lrb {
@@ -50,11 +51,9 @@ using lrb::fail;
 
 namespace {
 
-void free_ws(lrb_ctx* ctx, lrb_blr* m) {
-  if (m->plan3) lrb_ptr_plan_destroy(ctx, m->plan3);
+void free_ws(lrb_ctx*, lrb_blr* m) {
   if (m->d_w) cudaFree(m->d_w);
   if (m->d_z) cudaFree(m->d_z);
-  m->plan3 = nullptr;
   m->d_w = m->d_z = nullptr;
   m->ws_nrhs = -1;
 }
@@ -66,28 +65,36 @@ lrb_status ensure_ws(lrb_ctx* ctx, lrb_blr* m, int64_t nrhs) {
   const size_t bytes = size_t(items * r * nrhs) * sizeof(double);
   LRB_CUDA_TRY(ctx, cudaMalloc(&m->d_w, bytes));
   LRB_CUDA_TRY(ctx, cudaMalloc(&m->d_z, bytes));
-  // step 3 items in W's (column j, row i) order
-  std::vector<int64_t> mm(items, r), nn(items, nrhs), kk(items, r), la(items, r), lb(items, nrhs),
-      lc(items, nrhs);
-  std::vector<const double*> pa(items), pb(items);
-  std::vector<double*> pc(items);
-  int64_t q = 0;
-  for (int64_t j = 0; j < T; ++j) {
-    for (int64_t i = 0; i < T; ++i) {
-      if (i == j) continue;
-      const int64_t jp = j < i ? j : j - 1;  // position of j among row i's tiles
-      pa[q] = m->d_x + q * r * r;
-      pb[q] = m->d_w + q * r * nrhs;
-      pc[q] = m->d_z + (i * (T - 1) + jp) * r * nrhs;
-      ++q;
-    }
-  }
-  lrb_status st = lrb_ptr_plan_create(ctx, 'R', 'N', 'N', items, mm.data(), nn.data(), kk.data(),
-                                      pa.data(), la.data(), pb.data(), lb.data(), pc.data(),
-                                      lc.data(), 0.0, &m->plan3);
-  if (st) return st;
   m->ws_nrhs = nrhs;
   return LRB_OK;
+}
+
+// Step 3: Z_ij = X_ij W_ij for every off-diagonal tile. Item q runs in W's
+// (column j, row i != j) order; its Z block goes to row i's slot jp. Each
+// thread owns one entry Z[p][c] = sum_k X[p][k] W[k][c] as an in-order FMA
+// chain from zero (the order DMMA and the FMA-chain oracle use). Bytes: X
+// r^2 + W r*nrhs read, Z r*nrhs written per item — a few MB in total.
+__global__ void __launch_bounds__(256) blr_couple_kernel(const double* __restrict__ x,
+                                                         const double* __restrict__ w,
+                                                         double* __restrict__ z, int64_t tiles,
+                                                         int rank, int nrhs) {
+  const int64_t per = int64_t(rank) * nrhs;
+  const int64_t total = tiles * (tiles - 1) * per;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t q = e / per;
+    const int rem = int(e - q * per);
+    const int p = rem / nrhs, c = rem - p * nrhs;
+    const int64_t j = q / (tiles - 1), ip = q - j * (tiles - 1);
+    const int64_t i = ip < j ? ip : ip + 1;
+    const int64_t jp = j < i ? j : j - 1;
+    const double* xr = x + q * int64_t(rank) * rank + int64_t(p) * rank;
+    const double* wc = w + q * per + c;
+    double acc = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < rank; ++k) acc = fma(__ldg(xr + k), __ldg(wc + int64_t(k) * nrhs), acc);
+    z[(i * (tiles - 1) + jp) * per + rem] = acc;
+  }
 }
 
 }  // namespace
@@ -184,8 +191,14 @@ extern "C" lrb_status lrb_blr_matvec_device(lrb_ctx* ctx, lrb_blr* m, const doub
                                       m->d_w, nrhs, K * nrhs, T, 0, s);
   if (st) return st;
   // 3. Z_ij = X_ij W_ij
-  st = lrb_ptr_plan_execute(ctx, m->plan3, stream);
-  if (st) return st;
+  {
+    const int64_t total = T * (T - 1) * r * nrhs;
+    const int64_t blocks = std::min<int64_t>((total + 255) / 256, int64_t(ctx->sm_count) * 16);
+    blr_couple_kernel<<<unsigned(blocks), 256, 0, s>>>(m->d_x, m->d_w, m->d_z, T, int(r),
+                                                       int(nrhs));
+    LRB_CUDA_TRY(ctx, cudaGetLastError());
+    ctx->launches.fetch_add(1, std::memory_order_relaxed);
+  }
   // 4. y_i += [U_ij]_j [Z_ij]_j
   return lrb::run_strided_rowmajor_beta(ctx, b, nrhs, K, m->d_ucat, K, b * K, m->d_z, nrhs,
                                         K * nrhs, y, nrhs, b * nrhs, T, 1, s);
@@ -201,8 +214,8 @@ extern "C" lrb_status lrb_blr_matvec(lrb_ctx* ctx, lrb_blr* m, const double* rhs
   const size_t bytes = size_t(m->n * nrhs) * sizeof(double);
   double *d_rhs = nullptr, *d_y = nullptr;
   cudaStream_t s = ctx->lane_stream[0];
-  LRB_CUDA_TRY(ctx, cudaMallocAsync(reinterpret_cast<void**>(&d_rhs), bytes, s));
-  LRB_CUDA_TRY(ctx, cudaMallocAsync(reinterpret_cast<void**>(&d_y), bytes, s));
+  LRB_CUDA_TRY(ctx, lrb::pool_alloc(ctx, reinterpret_cast<void**>(&d_rhs), bytes, s));
+  LRB_CUDA_TRY(ctx, lrb::pool_alloc(ctx, reinterpret_cast<void**>(&d_y), bytes, s));
   cudaError_t e = cudaMemcpyAsync(d_rhs, rhs, bytes, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) {
     st = lrb_blr_matvec_device(ctx, m, d_rhs, nrhs, d_y, s);

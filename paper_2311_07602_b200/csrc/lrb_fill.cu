@@ -93,7 +93,7 @@ extern "C" lrb_status lrb_fill_uniform_ptr(lrb_ctx* ctx, double* const* dst, con
   if (st) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   FillDesc* d = nullptr;
-  LRB_CUDA_TRY(ctx, cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(FillDesc) * size_t(batch), s));
+  LRB_CUDA_TRY(ctx, lrb::pool_alloc(ctx, reinterpret_cast<void**>(&d), sizeof(FillDesc) * size_t(batch), s));
   LRB_CUDA_TRY(ctx, cudaMemcpyAsync(d, h.data(), sizeof(FillDesc) * size_t(batch),
                                     cudaMemcpyHostToDevice, s));
   const unsigned by = unsigned(std::min<int64_t>(batch, 65535));

@@ -35,6 +35,13 @@ struct lrb_ctx {
   // stream-ordered scratch pool (keeps freed blocks for reuse instead of
   // returning them to the driver at every synchronisation)
   cudaMemPool_t pool = nullptr;
+  // grow-only workspace for multi-launch paths (low-rank r > 32): allocated
+  // outside stream capture, so a captured graph references it instead of
+  // carrying alloc/free memory nodes; ws_ev orders consecutive eager users
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  cudaEvent_t ws_ev = nullptr;
+  bool ws_pending = false;
   // L2 flush buffer
   void* flush_buf = nullptr;
   size_t flush_bytes = 0;
@@ -46,6 +53,16 @@ void set_error(lrb_ctx* ctx, const char* fmt, ...);
 lrb_status fail(lrb_ctx* ctx, lrb_status st, const char* fmt, ...);
 lrb_status cuda_fail(lrb_ctx* ctx, cudaError_t e, const char* where);
 lrb_status bind(lrb_ctx* ctx);  // cudaSetDevice(ctx->device)
+// context workspace of >= bytes, ordered after its previous eager user on
+// another stream. It grows only outside stream capture; a capture that needs
+// more gets a stream-ordered (graph-owned) allocation instead (*temporary).
+lrb_status acquire_workspace(lrb_ctx* ctx, size_t bytes, cudaStream_t s, void** out,
+                             bool* temporary);
+void release_workspace(lrb_ctx* ctx, cudaStream_t s, void* p, bool temporary);
+// stream-ordered allocation from the context pool (blocks stay mapped)
+inline cudaError_t pool_alloc(lrb_ctx* ctx, void** p, size_t bytes, cudaStream_t s) {
+  return ctx->pool ? cudaMallocFromPoolAsync(p, bytes, ctx->pool, s) : cudaMallocAsync(p, bytes, s);
+}
 
 }  // namespace lrb
 

@@ -20,7 +20,7 @@
 //     operand, so four quad-local shuffles per k-block turn accumulators into
 //     MMA operands — no shared-memory round trip; G is stored once.
 // r > 32: three batched GEMMs (lrb_dgemm_strided_batched's kernels) with the
-// intermediates in stream-ordered scratch. Other shapes: a plain per-item
+// intermediates in the context workspace. Other shapes: a plain per-item
 // kernel (same FMA chains).
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -383,13 +383,13 @@ lrb_status run_lowrank(lrb_ctx* ctx, int64_t batch, int64_t block, int64_t rank,
   }
   if (path == 1) {
     // C = A_Vt B_U, E = A_X C, G = E B_X as three row-major batched GEMMs
+    // (the context workspace, not a stream-ordered allocation: inside a CUDA
+    // graph an allocation becomes a memory node that is mapped per replay)
     double* scratch = nullptr;
     const size_t bytes = size_t(batch) * size_t(rank * rank) * 2 * sizeof(double);
-    if (ctx->pool)
-      LRB_CUDA_TRY(ctx, cudaMallocFromPoolAsync(reinterpret_cast<void**>(&scratch), bytes,
-                                                ctx->pool, s));
-    else
-      LRB_CUDA_TRY(ctx, cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, s));
+    bool temp = false;
+    lrb_status wst = acquire_workspace(ctx, bytes, s, reinterpret_cast<void**>(&scratch), &temp);
+    if (wst) return wst;
     double* c = scratch;
     double* e = scratch + size_t(batch) * size_t(rank * rank);
     const int64_t rr = rank * rank;
@@ -397,7 +397,7 @@ lrb_status run_lowrank(lrb_ctx* ctx, int64_t batch, int64_t block, int64_t rank,
                                          block * rank, c, rr, batch, s);
     if (!st) st = run_strided_rowmajor(ctx, rank, rank, rank, a_x, rr, c, rr, e, rr, batch, s);
     if (!st) st = run_strided_rowmajor(ctx, rank, rank, rank, e, rr, b_x, rr, g, rr, batch, s);
-    cudaFreeAsync(scratch, s);
+    release_workspace(ctx, s, scratch, temp);
     return st;
   }
   const size_t smem = size_t(2) * rank * rank * sizeof(double);

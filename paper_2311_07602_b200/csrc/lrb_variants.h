@@ -19,6 +19,8 @@
 //   n64s4 : KB = 16 alternative kept for the selector sweep.
 //   n16t : 32-row tiles at five CTAs per SM for small skinny batches (cfg1).
 //   n16h : 64-row tiles, sweep candidate.
+//   m8t, m16t : 32-column tiles at five CTAs per SM, the m* shapes of small
+//         batches (the BLR matvec's per-row launches: 64 items of 8 x 512).
 //   n24, n40, n48, n56 : intermediate widths so a variable-rank batch
 //         (cfg4, r_i in 8..64) wastes less than one 8-column fragment.
 #pragma once
@@ -41,9 +43,11 @@
   X(13, q64, 2, 2, 32, 32, 32, 2, 3) \
   X(14, n64s4, 4, 2, 32, 32, 16, 4, 2) \
   X(15, n16t, 4, 1, 8, 16, 32, 2, 5)   \
-  X(16, n16h, 4, 1, 16, 16, 32, 2, 4)
+  X(16, n16h, 4, 1, 16, 16, 32, 2, 4)  \
+  X(17, m8t, 1, 4, 8, 8, 32, 2, 5)     \
+  X(18, m16t, 1, 4, 16, 8, 32, 2, 5)
 
-#define LRB_NUM_VARIANTS 17
+#define LRB_NUM_VARIANTS 19
 
 enum {
   LRB_V_N8 = 0,
@@ -62,5 +66,7 @@ enum {
   LRB_V_Q64 = 13,
   LRB_V_N64S4 = 14,
   LRB_V_N16T = 15,
-  LRB_V_N16H = 16
+  LRB_V_N16H = 16,
+  LRB_V_M8T = 17,
+  LRB_V_M16T = 18
 };

@@ -212,6 +212,8 @@ def get(name: str):
         return Strided("cfg5", 512, 32, 512, 131072, seed=4)
     if name.startswith("lr_"):
         return get_lowrank(name)
+    if name.startswith("blr_"):
+        return get_blr(name)
     raise KeyError(name)
 
 
@@ -276,3 +278,39 @@ def get_lowrank(name: str) -> LowRank:
     """lr_r{R}_b{B}[_n{batch}]"""
     parts = dict((p[0], p[1:]) for p in name.split("_")[1:])
     return LowRank(name, int(parts.get("n", 20000)), int(parts["b"]), int(parts["r"]))
+
+
+@dataclass
+class Blr:
+    """BLR multi-RHS matvec y = M rhs (reference blr.hpp:141-175): n = tiles *
+    block, dense diagonal tiles, rank-`rank` off-diagonal tiles, nrhs columns."""
+
+    name: str
+    n: int
+    block: int
+    rank: int
+    nrhs: int
+    seed: int = 11
+
+    @property
+    def tiles(self) -> int:
+        return self.n // self.block
+
+    def flops(self) -> float:
+        T, b, r, k = self.tiles, self.block, self.rank, self.nrhs
+        return T * 2.0 * b * b * k + T * (T - 1) * (4.0 * r * b * k + 2.0 * r * r * k)
+
+    def bytes(self) -> float:
+        T, b, r, k = self.tiles, self.block, self.rank, self.nrhs
+        return 8.0 * (T * b * b + T * (T - 1) * (2 * b * r + r * r) + 2 * self.n * k)
+
+    def describe(self) -> dict:
+        return {"workload": self.name, "n": self.n, "block": self.block, "rank": self.rank,
+                "nrhs": self.nrhs, "tiles": self.tiles, "seed": self.seed,
+                "layout": "BlrMatrix tiles (row-major), rhs/y row-major n x nrhs"}
+
+
+def get_blr(name: str) -> Blr:
+    """blr_n{N}_b{B}_r{R}_k{nrhs}"""
+    parts = dict((p[0], p[1:]) for p in name.split("_")[1:])
+    return Blr(name, int(parts["n"]), int(parts["b"]), int(parts["r"]), int(parts["k"]))

@@ -82,13 +82,18 @@ def test_selector_small_skinny_batches_use_short_tiles():
     # cfg1: 256 items of 256 x 16 -> fewer than two waves of 128-row tiles
     assert P.select("C", "N", "N", 256, 16, 256, 256)["name"] == "n16t"
     assert P.select("C", "N", "N", 256, 16, 256, 100000)["name"] == "n16"
+    # BLR matvec launches (64 row tiles, nrhs x block outputs): 32-column tiles
+    assert P.select("R", "N", "N", 512, 8, 504, 64)["name"] == "m8t"
+    assert P.select("R", "N", "N", 256, 16, 1008, 64)["name"] == "m16t"
+    assert P.select("R", "N", "N", 256, 16, 1008, 100000)["name"] == "m16"
 
 
 def test_selector_row_major_swaps_roles():
     # row-major C (m x n) is column-major C^T (n x m): the reference's BLR
     # diagonal step D(b x b) * rhs(b x r) lands on the short-wide m-variants
-    s = P.select("R", "N", "N", 1024, 16, 1024, 4)
+    s = P.select("R", "N", "N", 1024, 16, 1024, 10000)
     assert s["name"] == "m16"
+    assert P.select("R", "N", "N", 1024, 16, 1024, 4)["name"] == "m16t"  # < two waves
 
 
 def test_selector_intensity_and_bound():

@@ -80,6 +80,35 @@ def test_device_path_and_determinism(ctx):
     _check(b, r1)
 
 
+@pytest.mark.parametrize("eager_first", [False, True])
+def test_three_gemm_path_in_a_graph(eager_first):
+    # r > 32 inside stream capture: before the context workspace is sized the
+    # graph owns its scratch; afterwards it references the workspace
+    from paper_2311_07602_b200 import Context
+
+    c = Context(0)
+    try:
+        n, blk, r = 5, 256, 64
+        b = L.LowRankBatch.random(n, blk, r, 4242)
+        d = [c.to_device(x) for x in (b.a_vt_batch, b.b_u_batch, b.a_x_batch, b.b_x_batch)]
+        g_eager, g_graph = c.empty(n * r * r), c.empty(n * r * r)
+        s = c.stream()
+        if eager_first:
+            L.lowrank_multiply_device(c, n, blk, r, *d, g_eager, stream=s)
+        with c.capture(s) as cap:
+            L.lowrank_multiply_device(c, n, blk, r, *d, g_graph, stream=s)
+        assert cap.graph.launches == 3
+        for _ in range(3):
+            cap.graph.launch(s)
+        s.synchronize()
+        got = g_graph.download()
+        _check(b, got)
+        if eager_first:
+            assert np.array_equal(got, g_eager.download())
+    finally:
+        c.close()
+
+
 def test_poisoned_results_are_overwritten(ctx):
     # test_kernels.cpp:43-48 / 268-277: every entry written, stale values ignored
     b = L.LowRankBatch.random(4, 32, 8, 11)
