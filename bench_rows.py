@@ -21,7 +21,7 @@ import time
 import numpy as np
 
 
-def _roof(fl, by, ms, hbm, fp64, fsrc, hsrc):
+def _roof(fl, by, ms, hbm, fp64, fsrc, hsrc, name=None):
     intensity = fl / by
     fp64_bound = intensity * hbm * 1e9 >= fp64 * 1e12
     if fp64_bound:
@@ -35,6 +35,14 @@ def _roof(fl, by, ms, hbm, fp64, fsrc, hsrc):
     r["roofline_frac"] = round(fl / (ms * 1e-3) / min(fp64 * 1e12, intensity * hbm * 1e9), 4)
     r["algorithmic"] = by
     r["traffic"] = None
+    if name:
+        from bench import traffic_from_profiles
+
+        tr = traffic_from_profiles(name)
+        if isinstance(tr, dict):
+            # dram read + write of one step (summed over its launches), ncu --set full
+            r["traffic"] = tr.get("dram_bytes_per_launch")
+            r["traffic_launches"] = tr.get("launches")
     return r
 
 
@@ -90,7 +98,7 @@ def run_lowrank_gpu(args, w, world, rank, local, pg, B):
                                        B.ClockSampler(local))
     ms_step = B.all_max(pg, ms_rank) / args.steps
     fl_all, by_all = B.all_sum(pg, w.flops()), B.all_sum(pg, w.bytes())
-    roof = _roof(w.flops(), w.bytes(), ms_rank / args.steps, hbm, fp64, fsrc, hsrc)
+    roof = _roof(w.flops(), w.bytes(), ms_rank / args.steps, hbm, fp64, fsrc, hsrc, w.name)
     roof["kernel"] = "lrb_lowrank_kernel<R>" if r <= 32 else "lrb_gemm_kernel x3"
     roof["kernel_ms"] = round(ms_rank / max(1, launches), 4)
     e2e = None
@@ -137,41 +145,70 @@ def run_lowrank_gpu(args, w, world, rank, local, pg, B):
     ctx.close()
 
 
-def lowrank_cpu(w, threads, target_s):
-    """the reference's naive_multiply_batch (bench.hpp:55-77) on a bounded sample"""
+LOWRANK_DRIVERS = {0: "naive_multiply_batch", 2: "packed_multiply"}
+
+
+def _fastest(candidates, run):
+    """the candidate with the highest rate on a short probe (the reference
+    arm reports the reference at its best)"""
+    best, best_rate = candidates[0], -1.0
+    for c in candidates:
+        rate = run(c)
+        if rate > best_rate:
+            best, best_rate = c, rate
+    return best
+
+
+def lowrank_cpu(w, threads, target_s, which=None):
+    """The reference's own CPU driver on a bounded sample, timed inside the
+    reference call (oracle.ref_last_seconds: not the copy into LowRankBatch):
+    the faster on this host of packed_multiply (kernels.hpp:243-349, the
+    paper's optimised path, plan for oracle.DEFAULT_MACHINE) and
+    naive_multiply_batch (bench.hpp:55-77)."""
     import oracle as O
 
-    probe = lowrank_inputs_host(w, max(1, threads))
+    probe = lowrank_inputs_host(w, max(1, 4 * threads))
     args = (probe.a_vt_batch, probe.b_u_batch, probe.a_x_batch, probe.b_x_batch)
-    t0 = time.perf_counter()
     if O.ref_available():
-        O.ref_lowrank(0, probe.batch_size, w.block, w.rank, *args, workers=threads)
         kind = "reference"
+
+        def rate(c):
+            O.ref_lowrank(c, probe.batch_size, w.block, w.rank, *args, workers=threads)
+            return probe.batch_size / max(O.ref_last_seconds(), 1e-9)
+
+        which = _fastest((2, 0), rate) if which is None else which
+        what = LOWRANK_DRIVERS[which]
+        per_item = 1.0 / rate(which) * threads
     else:
+        kind, what = "port", "naive restatement"
+        t0 = time.perf_counter()
         O.lowrank(probe.batch_size, w.block, w.rank, *args, threads=threads, mode=O.REF_COMPILED)
-        kind = "port"
-    per_item = (time.perf_counter() - t0) / probe.batch_size * threads
+        per_item = (time.perf_counter() - t0) / probe.batch_size * threads
     items = int(min(w.batch, max(threads, threads * target_s / max(per_item, 1e-9))))
     b = lowrank_inputs_host(w, items)
     args = (b.a_vt_batch, b.b_u_batch, b.a_x_batch, b.b_x_batch)
     t0 = time.perf_counter()
     if kind == "reference":
-        O.ref_lowrank(0, items, w.block, w.rank, *args, workers=threads)
+        O.ref_lowrank(which, items, w.block, w.rank, *args, workers=threads)
+        dt = O.ref_last_seconds()
     else:
         O.lowrank(items, w.block, w.rank, *args, threads=threads, mode=O.REF_COMPILED)
-    dt = time.perf_counter() - t0
+        dt = time.perf_counter() - t0
+    plan = f", plan {O.DEFAULT_MACHINE}" if (kind == "reference" and which == 2) else ""
     return {"value": round(w.item_flops() * items / dt / 1e9, 3), "unit": "GFLOP/s",
-            "cores": threads, "kind": kind, "seconds": dt,
-            "sample": f"{items} of {w.batch} items ({dt:.1f} s), naive_multiply_batch"}
+            "cores": threads, "kind": kind, "seconds": dt, "driver": which,
+            "sample": f"{items} of {w.batch} items ({dt:.1f} s, driver call only), {what}{plan}"
+                      " (the faster of packed_multiply / naive_multiply_batch here)"}
 
 
 def run_lowrank_reference(args, w, world, rank, B):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    for _ in range(max(0, args.warmup_ref)):
-        lowrank_cpu(w, threads, min(1.0, args.ref_seconds))
-    vals = [lowrank_cpu(w, threads, args.ref_seconds) for _ in range(args.steps)]
+    driver = lowrank_cpu(w, threads, min(1.0, args.ref_seconds))["driver"]  # picks the driver
+    for _ in range(max(0, args.warmup_ref - 1)):
+        lowrank_cpu(w, threads, min(1.0, args.ref_seconds), driver)
+    vals = [lowrank_cpu(w, threads, args.ref_seconds, driver) for _ in range(args.steps)]
     v = statistics.median(x["value"] for x in vals)
     cb = dict(vals[0], value=v)
     ms = 1e3 * statistics.median(x.pop("seconds") for x in vals)
@@ -213,7 +250,7 @@ def run_blr_gpu(args, w, world, rank, local, pg, B):
                                        B.ClockSampler(local))
     ms_step = B.all_max(pg, ms_rank) / args.steps
     fl_all, by_all = B.all_sum(pg, w.flops()), B.all_sum(pg, w.bytes())
-    roof = _roof(w.flops(), w.bytes(), ms_rank / args.steps, hbm, fp64, fsrc, hsrc)
+    roof = _roof(w.flops(), w.bytes(), ms_rank / args.steps, hbm, fp64, fsrc, hsrc, w.name)
     roof["kernel"] = "lrb_gemm_kernel x3 + blr_couple_kernel per matvec"
     roof["kernel_ms"] = round(ms_rank / max(1, launches), 4)
     e2e = None
@@ -254,35 +291,45 @@ def run_blr_gpu(args, w, world, rank, local, pg, B):
 
 
 def blr_cpu(w, m, rhs, which=None):
-    """the reference's blr_matvec (packed path; naive when its machine files are absent)"""
+    """The reference's BLR matvec on the host, timed inside the reference
+    call (not building its BlrMatrix): the faster here of blr_matvec
+    (blr.hpp:141-175, packed per tile row, all workers, plan for
+    oracle.DEFAULT_MACHINE) and blr_matvec_naive (blr.hpp:179-202)."""
     import oracle as O
 
     diag, u, x, vt = m.packed_arrays()
     threads = os.cpu_count() or 1
-    t0 = time.perf_counter()
     if O.ref_available():
-        which = 0 if O.ref_machines_available() else 1
-        O.ref_blr_matvec(which, w.n, w.block, w.rank, diag, u, x, vt, rhs.data, w.nrhs,
-                         workers=threads)
         kind = "reference"
-        what = "blr_matvec (packed_multiply, all workers)" if which == 0 else "blr_matvec_naive"
+
+        def run(c):
+            O.ref_blr_matvec(c, w.n, w.block, w.rank, diag, u, x, vt, rhs.data, w.nrhs,
+                             workers=threads)
+            return O.ref_last_seconds()
+
+        which = _fastest((0, 1), lambda c: 1.0 / max(run(c), 1e-9)) if which is None else which
+        dt = run(which)
+        what = (f"blr_matvec (packed, plan {O.DEFAULT_MACHINE}, {threads} workers)" if which == 0
+                else "blr_matvec_naive (single thread)")
     else:
+        t0 = time.perf_counter()
         O.blr_matvec(w.n, w.block, w.rank, diag, u, x, vt, rhs.data, w.nrhs, mode=O.REF_COMPILED)
         kind, what = "port", "blr_matvec_naive restatement"
-    dt = time.perf_counter() - t0
+        dt = time.perf_counter() - t0
     return {"value": round(w.flops() / dt / 1e9, 3), "unit": "GFLOP/s",
             "cores": threads if (kind == "reference" and which == 0) else 1, "kind": kind,
-            "seconds": dt,
-            "sample": f"one full matvec ({dt:.2f} s): {what}"}
+            "seconds": dt, "driver": which,
+            "sample": f"one full matvec ({dt:.3f} s, driver call only): {what}"}
 
 
 def run_blr_reference(args, w, world, rank, B):
     if rank != 0:
         return
     m, rhs = blr_host(w)
-    for _ in range(max(0, args.warmup_ref)):
-        blr_cpu(w, m, rhs)
-    vals = [blr_cpu(w, m, rhs) for _ in range(args.steps)]
+    driver = blr_cpu(w, m, rhs)["driver"]  # picks the driver
+    for _ in range(max(0, args.warmup_ref - 1)):
+        blr_cpu(w, m, rhs, driver)
+    vals = [blr_cpu(w, m, rhs, driver) for _ in range(args.steps)]
     v = statistics.median(x["value"] for x in vals)
     ms = 1e3 * statistics.median(x.pop("seconds") for x in vals)
     print(json.dumps({

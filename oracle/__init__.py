@@ -14,6 +14,7 @@ Two libraries:
 from __future__ import annotations
 
 import ctypes as C
+import json
 import os
 from typing import Optional
 
@@ -90,13 +91,17 @@ def ref_lib() -> C.CDLL:
         L.ref_dense_gemm_naive_error.argtypes = [C.c_size_t] * 6 + [C.c_char_p, C.c_size_t]
         L.ref_dense_gemm_naive_error.restype = C.c_int
         L.ref_lowrank_multiply.argtypes = [C.c_int, i64, i64, i64, vp, vp, vp, vp, vp, C.c_int,
-                                           C.c_char_p]
+                                           C.c_char_p, P(i64)]
         L.ref_lowrank_multiply.restype = C.c_int
         L.ref_compare_to_reference.argtypes = [i64, i64, i64, vp, vp, vp, vp, vp, P(i64), P(i64)]
         L.ref_compare_to_reference.restype = dbl
         L.ref_blr_matvec.argtypes = [C.c_int, i64, i64, i64, vp, vp, vp, vp, vp, i64, vp, C.c_int,
-                                     C.c_char_p]
+                                     C.c_char_p, P(i64)]
         L.ref_blr_matvec.restype = C.c_int
+        L.ref_last_seconds.argtypes = []
+        L.ref_last_seconds.restype = dbl
+        L.ref_packing_plan.argtypes = [C.c_char_p, i64, i64, P(i64)]
+        L.ref_packing_plan.restype = C.c_int
         _ref = L
     return _ref
 
@@ -212,13 +217,60 @@ def lowrank(batch, block, rank, a_vt, b_u, a_x, b_x, threads=1, mode=FMA_CHAIN):
     return g
 
 
+# ------------------------------------------------- the reference's packing plans
+# the plan the GPU box's Xeon host runs fastest (tools/probe_cpu_ref.py: 2.4x
+# the epyc-7502 plan at r >= 32, equal at r = 8)
+DEFAULT_MACHINE = "skylake-x-6148"
+PLAN_FIELDS = ("b_small", "b_skinny", "m_pack", "n_pack", "x_pack", "y_pack", "tile", "llc_bytes",
+               "alignment_bytes", "dual_accumulator")
+_PLANS = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests",
+                      "golden", "packing_plans.json")
+_plan_cache = None
+
+
+def ref_last_seconds() -> float:
+    """wall time of the last ref_lowrank / ref_blr_matvec driver call alone
+    (excludes copying the inputs into the reference's containers)"""
+    return float(ref_lib().ref_last_seconds())
+
+
+def ref_packing_plan_live(machine, rank, block=0):
+    """make_packing_plan (plan.hpp:66-100) from the reference's machine files
+    (only where /root/reference exists); None if the reference rejects it"""
+    f = (C.c_int64 * 10)()
+    rc = ref_lib().ref_packing_plan(machine.encode(), rank, block, f)
+    return None if rc != 0 else [int(v) for v in f]
+
+
+def packing_plan(machine=None, rank=8, block=0):
+    """The reference's PackingPlan for (machine, rank) as 10 fields: live from
+    its machine files when present, else the committed fixture
+    tests/golden/packing_plans.json (made by tests/golden/make_plans.py from
+    the same call). The plan depends on rank only (plan.hpp:68)."""
+    global _plan_cache
+    machine = machine or DEFAULT_MACHINE
+    if ref_machines_available():
+        return ref_packing_plan_live(machine, rank, block)
+    if _plan_cache is None:
+        with open(_PLANS) as fh:
+            _plan_cache = json.load(fh)
+    return _plan_cache["plans"][machine].get(str(rank))
+
+
+def _plan_arg(machine, rank):
+    fields = packing_plan(machine, rank)
+    if fields is None:
+        raise ValueError(f"no packing plan for machine {machine or DEFAULT_MACHINE} rank {rank}")
+    return (C.c_int64 * 10)(*fields)
+
+
 def ref_lowrank(which, batch, block, rank, a_vt, b_u, a_x, b_x, workers=1, machine=None):
     """the reference's own drivers: 0 naive_multiply_batch, 1 fused_multiply,
-    2 packed_multiply (plan for `machine`)"""
+    2 packed_multiply (the reference's plan for `machine`, see packing_plan)"""
     g = np.zeros(batch * rank * rank)
+    plan = _plan_arg(machine, rank) if which == 2 else None
     rc = ref_lib().ref_lowrank_multiply(which, batch, block, rank, _p(a_vt), _p(b_u), _p(a_x),
-                                        _p(b_x), _p(g), workers,
-                                        machine.encode() if machine else None)
+                                        _p(b_x), _p(g), workers, None, plan)
     if rc != 0:
         raise ValueError("ref_lowrank_multiply failed")
     return g
@@ -259,10 +311,12 @@ def blr_matvec(n, block, rank, diag, u, x, vt, rhs, nrhs, mode=FMA_CHAIN):
 
 
 def ref_blr_matvec(which, n, block, rank, diag, u, x, vt, rhs, nrhs, workers=2, machine=None):
-    """the reference itself: 0 blr_matvec (packed), 1 blr_matvec_naive, 2 dense reconstruction"""
+    """the reference itself: 0 blr_matvec (packed; plan at rank max(rank, nrhs)
+    per blr.hpp), 1 blr_matvec_naive, 2 dense reconstruction"""
     y = np.zeros(n * nrhs)
+    plan = _plan_arg(machine, max(rank, nrhs)) if which == 0 else None
     rc = ref_lib().ref_blr_matvec(which, n, block, rank, _p(diag), _p(u), _p(x), _p(vt), _p(rhs),
-                                  nrhs, _p(y), workers, machine.encode() if machine else None)
+                                  nrhs, _p(y), workers, None, plan)
     if rc != 0:
         raise ValueError("ref_blr_matvec failed")
     return y

@@ -9,9 +9,11 @@
 #include <lrbatch/dense.hpp>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 namespace {
@@ -155,6 +157,61 @@ int ref_dense_gemm_naive_error(size_t ar, size_t ac, size_t br, size_t bc, size_
 #include <lrbatch/verify.hpp>
 
 namespace {
+// wall time of the last reference driver call alone (no marshalling into the
+// reference's containers), read back with ref_last_seconds()
+double g_last_seconds = 0.0;
+
+template <class F>
+auto timed(F&& f) {
+  const auto t0 = std::chrono::steady_clock::now();
+  auto finish = [&] {
+    g_last_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  };
+  if constexpr (std::is_void_v<decltype(f())>) {
+    f();
+    finish();
+  } else {
+    auto r = f();
+    finish();
+    return r;
+  }
+}
+
+// PackingPlan <-> 10 int64 fields (plan.hpp:21-31), so a plan the reference
+// derived here from its machine files can be replayed where they are absent
+constexpr int kPlanFields = 10;
+
+void plan_to_fields(const lrbatch::PackingPlan& p, int64_t* f) {
+  f[0] = int64_t(p.b_small);
+  f[1] = int64_t(p.b_skinny);
+  f[2] = int64_t(p.m_pack);
+  f[3] = int64_t(p.n_pack);
+  f[4] = int64_t(p.x_pack);
+  f[5] = int64_t(p.y_pack);
+  f[6] = int64_t(p.tile);
+  f[7] = int64_t(p.llc_bytes);
+  f[8] = int64_t(p.alignment_bytes);
+  f[9] = p.dual_accumulator ? 1 : 0;
+}
+
+lrbatch::PackingPlan plan_from(const int64_t* f, const char* machine, size_t rank, size_t block) {
+  if (!f)
+    return lrbatch::make_packing_plan(lrbatch::resolve_machine(machine ? machine : "skylake-x-6148"),
+                                      rank, block);
+  lrbatch::PackingPlan p;
+  p.b_small = size_t(f[0]);
+  p.b_skinny = size_t(f[1]);
+  p.m_pack = size_t(f[2]);
+  p.n_pack = size_t(f[3]);
+  p.x_pack = size_t(f[4]);
+  p.y_pack = size_t(f[5]);
+  p.tile = size_t(f[6]);
+  p.llc_bytes = size_t(f[7]);
+  p.alignment_bytes = size_t(f[8]);
+  p.dual_accumulator = f[9] != 0;
+  return p;
+}
+
 lrbatch::LowRankBatch make_batch(int64_t batch, int64_t block, int64_t rank, const double* a_vt,
                                  const double* b_u, const double* a_x, const double* b_x) {
   lrbatch::LowRankBatch lb{size_t(batch), size_t(block), size_t(rank), size_t(rank)};
@@ -168,23 +225,34 @@ lrbatch::LowRankBatch make_batch(int64_t batch, int64_t block, int64_t rank, con
 
 extern "C" {
 
+double ref_last_seconds() { return g_last_seconds; }
+
+// make_packing_plan (plan.hpp:66-100) for `machine` -> 10 fields; 0 on success
+int ref_packing_plan(const char* machine, int64_t rank, int64_t block, int64_t* fields) {
+  try {
+    plan_to_fields(plan_from(nullptr, machine, size_t(rank), size_t(block)), fields);
+  } catch (...) {
+    return -1;
+  }
+  return 0;
+}
+
 // which: 0 naive_multiply_batch (the reference CPU baseline, bench.hpp:55-77),
 //        1 fused_multiply (kernels.hpp:131-161),
-//        2 packed_multiply with the plan for `machine` (kernels.hpp:243-349)
+//        2 packed_multiply (kernels.hpp:243-349) with `plan` (10 fields) or,
+//          when plan is NULL, make_packing_plan for `machine`
 int ref_lowrank_multiply(int which, int64_t batch, int64_t block, int64_t rank, const double* a_vt,
                          const double* b_u, const double* a_x, const double* b_x, double* g,
-                         int workers, const char* machine) {
+                         int workers, const char* machine, const int64_t* plan) {
   try {
     lrbatch::LowRankBatch lb = make_batch(batch, block, rank, a_vt, b_u, a_x, b_x);
     if (which == 0) {
-      lrbatch::naive_multiply_batch(lb, size_t(workers));
+      timed([&] { lrbatch::naive_multiply_batch(lb, size_t(workers)); });
     } else if (which == 1) {
-      lrbatch::fused_multiply(lb);
+      timed([&] { lrbatch::fused_multiply(lb); });
     } else {
-      lrbatch::PackingPlan plan = lrbatch::make_packing_plan(
-          lrbatch::resolve_machine(machine ? machine : "skylake-x-6148"), size_t(rank),
-          size_t(block));
-      lrbatch::packed_multiply(lb, plan, size_t(workers));
+      const lrbatch::PackingPlan pp = plan_from(plan, machine, size_t(rank), size_t(block));
+      timed([&] { lrbatch::packed_multiply(lb, pp, size_t(workers)); });
     }
     std::memcpy(g, lb.g_xy_batch.data(), sizeof(double) * lb.g_xy_batch.size());
   } catch (...) {
@@ -246,11 +314,13 @@ int ref_load_batch(const char* path, int64_t* hdr, double* a_vt, double* b_u, do
 #include <lrbatch/blr.hpp>
 
 extern "C" {
-// which: 0 blr_matvec (packed path, plan for `machine`), 1 blr_matvec_naive,
+// which: 0 blr_matvec (packed path; `plan` fields, or the plan for `machine`
+// at rank max(rank, nrhs) when NULL), 1 blr_matvec_naive,
 // 2 dense_gemm_naive(reconstruct_dense(), rhs) — blr.hpp:64-202
 int ref_blr_matvec(int which, int64_t n, int64_t block, int64_t rank, const double* diag,
                    const double* u, const double* x, const double* vt, const double* rhs,
-                   int64_t nrhs, double* y, int workers, const char* machine) {
+                   int64_t nrhs, double* y, int workers, const char* machine,
+                   const int64_t* plan) {
   try {
     lrbatch::BlrMatrix m{size_t(n), size_t(block), size_t(rank)};
     const size_t T = m.tiles, b = size_t(block), r = size_t(rank);
@@ -264,14 +334,13 @@ int ref_blr_matvec(int which, int64_t n, int64_t block, int64_t rank, const doub
                            std::vector<double>(rhs, rhs + size_t(n) * size_t(nrhs))};
     lrbatch::DenseBlock out;
     if (which == 0) {
-      lrbatch::PackingPlan plan = lrbatch::make_packing_plan(
-          lrbatch::resolve_machine(machine ? machine : "skylake-x-6148"),
-          std::max(r, size_t(nrhs)), b);
-      out = lrbatch::blr_matvec(m, rb, plan, size_t(workers));
+      const lrbatch::PackingPlan pp = plan_from(plan, machine, std::max(r, size_t(nrhs)), b);
+      out = timed([&] { return lrbatch::blr_matvec(m, rb, pp, size_t(workers)); });
     } else if (which == 1) {
-      out = lrbatch::blr_matvec_naive(m, rb);
+      out = timed([&] { return lrbatch::blr_matvec_naive(m, rb); });
     } else {
-      out = lrbatch::dense_gemm_naive(m.reconstruct_dense(), rb);
+      const lrbatch::DenseBlock dense = m.reconstruct_dense();
+      out = timed([&] { return lrbatch::dense_gemm_naive(dense, rb); });
     }
     std::memcpy(y, out.data.data(), out.data.size() * sizeof(double));
   } catch (...) {

@@ -182,7 +182,7 @@ def test_lowrank_restatement_equals_reference_binary(batch, block, rank):
     err, _, _ = O.ref_compare_to_reference(batch, block, rank, *args, fma)
     assert err < 1e-12
     # the reference's fused and packed drivers agree with its oracle to its own tolerance
-    for which in ((1, 2) if O.ref_machines_available() else (1,)):
+    for which in (1, 2):  # packed: the reference's plan (live or tests/golden/packing_plans.json)
         other = O.ref_lowrank(which, batch, block, rank, *args, workers=2)
         assert O.ref_compare_to_reference(batch, block, rank, *args, other)[0] < 1e-11
 
@@ -194,3 +194,36 @@ def test_lowrank_flops_accounting():
     # tests/test_core.cpp:95-99
     for r, b, want in ((8, 512, 67584), (1, 1, 6), (32, 2048, 4325376)):
         assert L.flops_per_item(r, b) == want == lib.lrb_lowrank_flops_per_item(r, b)
+
+
+def test_packing_plan_fixture_matches_the_reference():
+    # tests/golden/packing_plans.json replays make_packing_plan where the
+    # machine files are absent (the GPU box); pin it against the live call
+    import json
+    import os
+
+    path = os.path.join(os.path.dirname(__file__), "golden", "packing_plans.json")
+    fx = json.load(open(path))
+    assert fx["fields"] == list(O.PLAN_FIELDS)
+    assert all(fx["plans"][O.DEFAULT_MACHINE][str(r)] is not None for r in range(1, 129))
+    if not (O.ref_available() and O.ref_machines_available()):
+        pytest.skip("the reference's machine files are not here")
+    for m, plans in fx["plans"].items():
+        for r in (1, 7, 8, 16, 31, 64, 128):
+            assert O.ref_packing_plan_live(m, r) == plans[str(r)], (m, r)
+
+
+def test_packed_drivers_replay_the_fixture_plan(monkeypatch):
+    # what the GPU box does: packed_multiply / blr_matvec with the committed plan
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    from paper_2311_07602_b200 import lowrank as L
+
+    b = L.LowRankBatch.random(5, 64, 8, 77)
+    args = (b.a_vt_batch, b.b_u_batch, b.a_x_batch, b.b_x_batch)
+    live = O.ref_lowrank(2, 5, 64, 8, *args, workers=2) if O.ref_machines_available() else None
+    monkeypatch.setattr(O, "ref_machines_available", lambda: False)
+    replay = O.ref_lowrank(2, 5, 64, 8, *args, workers=2)
+    assert O.ref_compare_to_reference(5, 64, 8, *args, replay)[0] < 1e-11
+    if live is not None:
+        assert np.array_equal(live, replay)

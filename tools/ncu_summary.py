@@ -53,7 +53,8 @@ def traffic(csv_path, order_path, out_path):
     rows = list(csv.DictReader(io.StringIO(text[start:])))
     per = {}
     for r in rows:
-        if "lrb_gemm_kernel" not in r["Kernel Name"]:
+        kn = r["Kernel Name"]
+        if "fill_" in kn or not ("lrb_" in kn or "blr_" in kn):
             continue
         key = int(r["ID"])
         per.setdefault(key, {"kernel": r["Kernel Name"][:120]})

@@ -14,6 +14,49 @@ from paper_2311_07602_b200 import Context, workloads as W  # noqa: E402
 
 CONFIGS = ["cfg1", "cfg2"] + [f"cfg3_b{b}_r{r}" for b in W.CFG3_B for r in W.CFG3_R] + [
     "cfg4", "cfg5"]
+# the widened rows (bench.py --config): low-rank product and BLR matvec
+LOWRANK = ["lr_r8_b1024", "lr_r16_b1024", "lr_r32_b2048", "lr_r64_b2048", "lr_r128_b1024"]
+BLR = ["blr_n32768_b512_r8_k8", "blr_n16384_b256_r16_k16"]
+
+
+def lowrank_one(ctx, name):
+    from paper_2311_07602_b200 import lowrank as L
+
+    w = W.get_lowrank(name)
+    n, r, blk = w.batch, w.rank, w.block
+    bufs = [ctx.empty(n * r * blk), ctx.empty(n * blk * r), ctx.empty(n * r * r),
+            ctx.empty(n * r * r), ctx.empty(n * r * r)]
+    for i, (rows, cols) in enumerate(((blk, r), (r, blk), (r, r), (r, r))):
+        ctx.fill_uniform(bufs[i], rows, cols, rows, rows * cols, n, w.seed, i, 0)
+    n0 = ctx.launch_count
+    L.lowrank_multiply_device(ctx, n, blk, r, *bufs)  # sizes the workspace (r > 32)
+    ctx.synchronize()
+    print(f"{name}_warm launches={ctx.launch_count - n0}", flush=True)
+    n0 = ctx.launch_count
+    L.lowrank_multiply_device(ctx, n, blk, r, *bufs)
+    ctx.synchronize()
+    print(f"{name} launches={ctx.launch_count - n0}", flush=True)
+
+
+def blr_one(ctx, name):
+    import bench_rows as R
+    from paper_2311_07602_b200.lrbatch import _check, lib
+
+    w = W.get_blr(name)
+    m, rhs = R.blr_host(w)
+    h = m.device_handle(ctx)
+    d_rhs, d_y = ctx.to_device(rhs.data), ctx.empty(w.n * w.nrhs)
+    run = lambda: _check(lib.lrb_blr_matvec_device(ctx._h, h, d_rhs.ptr, w.nrhs, d_y.ptr, None),  # noqa
+                         ctx._h)
+    n0 = ctx.launch_count
+    run()
+    ctx.synchronize()
+    print(f"{name}_warm launches={ctx.launch_count - n0}", flush=True)
+    n0 = ctx.launch_count
+    run()
+    ctx.synchronize()
+    print(f"{name} launches={ctx.launch_count - n0}", flush=True)
+    m.invalidate()
 
 
 def main():
@@ -46,6 +89,10 @@ def main():
         ctx.synchronize()
         print(f"{name} launches=1 items={count}", flush=True)
         del A, B, Cd
+    for name in LOWRANK:
+        lowrank_one(ctx, name)
+    for name in BLR:
+        blr_one(ctx, name)
 
 
 if __name__ == "__main__":
