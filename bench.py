@@ -624,6 +624,11 @@ def main():
             R.run_blr_reference(args, w, world, rank, bench_mod)
         else:
             R.run_blr_gpu(args, w, world, rank, local, pg, bench_mod)
+    elif isinstance(w, (W.LrExpand, W.BlrDense)):
+        if args.impl == "reference":
+            R.run_expand_reference(args, w, world, rank, bench_mod)
+        else:
+            R.run_expand_gpu(args, w, world, rank, local, pg, bench_mod)
     elif args.impl == "reference":
         run_reference_arm(args, w, world, rank)
     else:

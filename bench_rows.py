@@ -340,3 +340,186 @@ def run_blr_reference(args, w, world, rank, B):
         "cpu_baseline": dict(vals[0], value=v),
         "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0}), flush=True)
+
+
+# ------------------------------------------- low-rank expansion / BLR dense
+def _expand_host(w, items, first=0):
+    """seeded U, X, Vt host arrays for items [first, first+items) (counter RNG)"""
+    from paper_2311_07602_b200 import lowrank as L
+    from paper_2311_07602_b200 import workloads as W
+
+    m, r = w.m, w.rank
+    out = []
+    for role, per in ((0, m * r), (1, r * r), (2, r * m)):
+        key = W.stream_key(w.seed, role)
+        idx = np.arange(per, dtype=np.uint64)
+        out.append(np.concatenate([L._uniform_vec(key, first + it, idx) for it in range(items)]))
+    return out
+
+
+def expand_cpu(w, threads, target_s):
+    """the reference's expansion on the host: (U X) Vt per item through its
+    gemm_naive_raw (dense_gemm_naive's arithmetic), items split over all
+    threads; or reconstruct_dense itself (single-threaded, as the reference
+    has it). Timed inside the reference call."""
+    import oracle as O
+    from paper_2311_07602_b200 import blr as BL
+    from paper_2311_07602_b200 import workloads as W
+
+    if isinstance(w, W.BlrDense):
+        m = BL.BlrMatrix.random(w.n, w.block, w.rank, w.seed)
+        args = (w.n, w.block, w.rank) + m.packed_arrays()
+        if O.ref_available():
+            O.ref_blr_reconstruct(*args)
+            dt, kind = O.ref_last_seconds(), "reference"
+        else:
+            t0 = time.perf_counter()
+            O.blr_reconstruct(*args, mode=O.REF_COMPILED)
+            dt, kind = time.perf_counter() - t0, "port"
+        return {"value": round(w.flops() / dt / 1e9, 3), "unit": "GFLOP/s", "cores": 1,
+                "kind": kind, "seconds": dt,
+                "sample": f"one full reconstruct_dense ({dt:.2f} s, single-threaded as in the"
+                          " reference)"}
+    probe = max(threads, 2 * threads)
+    u, x, vt = _expand_host(w, probe)
+    if not O.ref_available():
+        t0 = time.perf_counter()
+        O.lowrank_expand(probe, w.m, w.m, w.rank, u, x, vt, mode=O.REF_COMPILED)
+        per_item = (time.perf_counter() - t0) / probe * threads
+        kind = "port"
+    else:
+        O.ref_lowrank_expand(probe, w.m, w.m, w.rank, u, x, vt, workers=threads)
+        per_item = O.ref_last_seconds() / probe * threads
+        kind = "reference"
+    items = int(min(w.batch, max(threads, threads * target_s / max(per_item, 1e-9))))
+    u, x, vt = _expand_host(w, items)
+    t0 = time.perf_counter()
+    if kind == "reference":
+        O.ref_lowrank_expand(items, w.m, w.m, w.rank, u, x, vt, workers=threads)
+        dt = O.ref_last_seconds()
+    else:
+        O.lowrank_expand(items, w.m, w.m, w.rank, u, x, vt, mode=O.REF_COMPILED)
+        dt = time.perf_counter() - t0
+    return {"value": round(w.item_flops() * items / dt / 1e9, 3), "unit": "GFLOP/s",
+            "cores": threads if kind == "reference" else 1, "kind": kind, "seconds": dt,
+            "sample": f"{items} of {w.batch} items ({dt:.1f} s, products only): (U X) Vt via"
+                      " the reference's gemm_naive_raw, contiguous split over threads"}
+
+
+def run_expand_gpu(args, w, world, rank, local, pg, B):
+    from paper_2311_07602_b200 import Context
+    from paper_2311_07602_b200 import blr as BL
+    from paper_2311_07602_b200 import workloads as W
+
+    hbm, hsrc, fp64, fsrc = B.load_peaks()
+    ctx = Context(local)
+    s = ctx.stream()
+    dense = isinstance(w, W.BlrDense)
+    if dense:
+        mat = BL.BlrMatrix.random(w.n, w.block, w.rank, w.seed)
+        mat.device_handle(ctx)
+        out = ctx.empty(w.n * w.n)
+        step = lambda: mat.reconstruct_dense_device(ctx, out, stream=s)  # noqa: E731
+        fl, by = w.flops(), w.bytes()
+        kernel = "blr_diag_kernel + blr_ux_kernel + lrb_gemm_kernel<q64> (ptr plan)"
+    else:
+        m, r, n = w.m, w.rank, w.batch
+        bufs = [ctx.empty(n * m * r), ctx.empty(n * r * r), ctx.empty(n * r * m)]
+        first = rank * n
+        ctx.fill_uniform(bufs[0], r, m, r, m * r, n, w.seed, 0, first)
+        ctx.fill_uniform(bufs[1], r, r, r, r * r, n, w.seed, 1, first)
+        ctx.fill_uniform(bufs[2], m, r, m, r * m, n, w.seed, 2, first)
+        out = ctx.empty(n * m * m)
+        ctx.synchronize()
+        step = lambda: BL.lowrank_expand_device(ctx, n, m, m, r, *bufs, out, stream=s)  # noqa
+        fl, by = w.flops(), w.bytes()
+        kernel = "lrb_gemm_kernel x2 (UX, then (UX) Vt on q64)"
+    ms_rank, launches, clocks = _timed(ctx, s, step, args.steps, args.warmup, pg, B,
+                                       B.ClockSampler(local))
+    ms_step = B.all_max(pg, ms_rank) / args.steps
+    fl_all, by_all = B.all_sum(pg, fl), B.all_sum(pg, by)
+    roof = _roof(fl, by, ms_rank / args.steps, hbm, fp64, fsrc, hsrc, w.name)
+    roof["kernel"] = kernel
+    roof["kernel_ms"] = round(ms_rank / max(1, launches), 4)
+    e2e = None
+    if args.e2e_steps > 0:
+        from paper_2311_07602_b200.lrbatch import _check, lib
+
+        if dense:
+            host = np.zeros(w.n * w.n)
+            h = mat.device_handle(ctx)
+
+            def once():
+                _check(lib.lrb_blr_reconstruct_dense(ctx._h, h, host.ctypes.data, 0, None),
+                       ctx._h)
+
+            hb, ob = 0, 8 * w.n * w.n
+            path = "lrb_blr_reconstruct_dense (host out; matrix resident on the device)"
+            ratio = 1.0
+        else:
+            items = min(w.batch, args.e2e_items or 1024)
+            hu, hx, hvt = _expand_host(w, items, rank * w.batch)
+            pins = [ctx.pinned(a.size) for a in (hu, hx, hvt)] + [ctx.pinned(items * w.m * w.m)]
+            for p_, a in zip(pins, (hu, hx, hvt)):
+                p_.array[:] = a
+            dbu = [ctx.empty(a.size) for a in (hu, hx, hvt)]
+            dout = ctx.empty(items * w.m * w.m)
+            e2s = ctx.stream()
+
+            def once():
+                for p_, d in zip(pins, dbu):  # synchronous copies from pinned memory
+                    _check(lib.lrb_memcpy_h2d(ctx._h, d.ptr, p_.ptr, p_.nbytes), ctx._h)
+                BL.lowrank_expand_device(ctx, items, w.m, w.m, w.rank, *dbu, dout, stream=e2s)
+                e2s.synchronize()
+                _check(lib.lrb_memcpy_d2h(ctx._h, pins[3].ptr, dout.ptr, pins[3].nbytes), ctx._h)
+
+            hb = 8 * (hu.size + hx.size + hvt.size)
+            ob = 8 * items * w.m * w.m
+            path = f"H2D (pinned) + lrb_lowrank_expand + D2H, {items} items per step"
+            ratio = items / w.batch
+        once()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            once()
+        dt = B.all_max(pg, (time.perf_counter() - t0) / args.e2e_steps)
+        e2e = {"value": round(fl_all * ratio / dt / 1e9, 2), "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(hb), "d2h_bytes_per_step": int(ob),
+               "ms_per_step": round(dt * 1e3, 3), "path": path}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = expand_cpu(w, os.cpu_count() or 1, args.ref_seconds)
+        cpu.pop("seconds", None)
+    if rank == 0:
+        cfg = dict(w.describe())
+        cfg.update({"parallelism": (f"replicas{world}" if dense else f"shard{world}")
+                    + " (no collective)", "timed_launch": "CUDA graph of the K steps",
+                    "l2": "output larger than L2 (no flush)"})
+        print(json.dumps({
+            "metric": "batched FP64 GFLOP/s", "value": round(fl_all / (ms_step * 1e-3) / 1e9, 2),
+            "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (counter RNG, uniform[-1,1))", "config": cfg,
+            "hbm_gbs": round(by_all / (ms_step * 1e-3) / 1e9, 1), "roofline": roof,
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches)}),
+            flush=True)
+    ctx.close()
+
+
+def run_expand_reference(args, w, world, rank, B):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    for _ in range(max(0, args.warmup_ref)):
+        expand_cpu(w, threads, min(1.0, args.ref_seconds))
+    vals = [expand_cpu(w, threads, args.ref_seconds) for _ in range(args.steps)]
+    v = statistics.median(x["value"] for x in vals)
+    ms = 1e3 * statistics.median(x.pop("seconds") for x in vals)
+    print(json.dumps({
+        "metric": "batched FP64 GFLOP/s", "value": v, "unit": "GFLOP/s", "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (counter RNG, uniform[-1,1))", "config": w.describe(),
+        "cpu_baseline": dict(vals[0], value=v),
+        "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0}), flush=True)

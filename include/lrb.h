@@ -187,6 +187,21 @@ lrb_status lrb_lowrank_multiply_host(lrb_ctx* ctx, int64_t batch, int64_t block,
 /* the reference's accounting 4 r^3 + 2 r^2 b (flops_per_item, low_rank.hpp:66-68) */
 double lrb_lowrank_flops_per_item(int64_t rank, int64_t block);
 
+/*
+ * Low-rank expansion of a batch of LowRankOperands (low_rank.hpp:16-63):
+ *   out_i = (U_i X_i) Vt_i        U m x rank, X rank x rank, Vt rank x n,
+ * all row-major, item i at base + i*stride; out_i m x n with leading
+ * dimension ldo >= n. The reference's per-tile expansion inside
+ * BlrMatrix::reconstruct_dense (blr.hpp:75-78: dense_gemm_naive(U, X), then
+ * dense_gemm_naive(UX, Vt)) in the same order: UX is formed (rounded) first,
+ * each entry an in-order FMA chain. UX lives in the context workspace.
+ * Device pointers, asynchronous on `stream`.
+ */
+lrb_status lrb_lowrank_expand(lrb_ctx* ctx, int64_t batch, int64_t m, int64_t n, int64_t rank,
+                              const double* u, int64_t su, const double* x, int64_t sx,
+                              const double* vt, int64_t svt, double* out, int64_t ldo,
+                              int64_t so, void* stream);
+
 /* ------------------------------------------------- LRBATCH1 batch files */
 /*
  * The reference's flat batch file (batch_io.hpp:11-77): "LRBATCH1", uint64
@@ -223,6 +238,15 @@ lrb_status lrb_blr_matvec(lrb_ctx* ctx, lrb_blr* m, const double* rhs, int64_t n
 lrb_status lrb_blr_matvec_device(lrb_ctx* ctx, lrb_blr* m, const double* rhs, int64_t nrhs,
                                  double* y, void* stream);
 lrb_status lrb_blr_destroy(lrb_ctx* ctx, lrb_blr* m);
+/*
+ * Exact dense assembly of the whole n x n matrix, row-major
+ * (BlrMatrix::reconstruct_dense, blr.hpp:62-86): diagonal tiles copied,
+ * off-diagonal tiles expanded as (U X) Vt in the reference's order. `out` is a
+ * device buffer (asynchronous on `stream`) when on_device, else a host buffer
+ * (synchronous).
+ */
+lrb_status lrb_blr_reconstruct_dense(lrb_ctx* ctx, lrb_blr* m, double* out, int on_device,
+                                     void* stream);
 
 /* ------------------------------------------------------------ CUDA graphs */
 /*

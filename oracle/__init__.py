@@ -59,6 +59,11 @@ def oracle_lib() -> C.CDLL:
         L.oracle_lowrank_batch.argtypes = [C.c_int, i64, i64, i64, vp, vp, vp, vp, vp, C.c_int]
         L.oracle_lowrank_batch.restype = C.c_int
         L.oracle_blr_matvec.argtypes = [C.c_int, i64, i64, i64, vp, vp, vp, vp, vp, i64, vp]
+        L.oracle_lowrank_expand.argtypes = [C.c_int, i64, i64, i64, i64, vp, i64, vp, i64, vp,
+                                            i64, vp, i64, i64]
+        L.oracle_lowrank_expand.restype = C.c_int
+        L.oracle_blr_reconstruct.argtypes = [C.c_int, i64, i64, i64, vp, vp, vp, vp, vp]
+        L.oracle_blr_reconstruct.restype = C.c_int
         L.oracle_blr_matvec.restype = C.c_int
         _oracle = L
     return _oracle
@@ -98,6 +103,10 @@ def ref_lib() -> C.CDLL:
         L.ref_blr_matvec.argtypes = [C.c_int, i64, i64, i64, vp, vp, vp, vp, vp, i64, vp, C.c_int,
                                      C.c_char_p, P(i64)]
         L.ref_blr_matvec.restype = C.c_int
+        L.ref_blr_reconstruct.argtypes = [i64, i64, i64, vp, vp, vp, vp, vp]
+        L.ref_blr_reconstruct.restype = C.c_int
+        L.ref_lowrank_expand.argtypes = [i64, i64, i64, i64, vp, vp, vp, vp, C.c_int]
+        L.ref_lowrank_expand.restype = C.c_int
         L.ref_last_seconds.argtypes = []
         L.ref_last_seconds.restype = dbl
         L.ref_packing_plan.argtypes = [C.c_char_p, i64, i64, P(i64)]
@@ -320,6 +329,49 @@ def ref_blr_matvec(which, n, block, rank, diag, u, x, vt, rhs, nrhs, workers=2, 
     if rc != 0:
         raise ValueError("ref_blr_matvec failed")
     return y
+
+
+def lowrank_expand(batch, m, n, r, u, x, vt, mode=FMA_CHAIN, su=None, sx=None, svt=None,
+                   ldo=None, so=None, out=None):
+    """out_i = (U_i X_i) Vt_i (blr.hpp:75-78 per tile) rounded per `mode`"""
+    su = m * r if su is None else su
+    sx = r * r if sx is None else sx
+    svt = r * n if svt is None else svt
+    ldo = n if ldo is None else ldo
+    so = m * ldo if so is None else so
+    if out is None:
+        out = np.zeros(max(1, (batch - 1) * so + max(0, (m - 1) * ldo + n)))
+    rc = oracle_lib().oracle_lowrank_expand(mode, batch, m, n, r, _p(u), su, _p(x), sx, _p(vt),
+                                            svt, _p(out), ldo, so)
+    if rc != 0:
+        raise ValueError("oracle_lowrank_expand: bad arguments")
+    return out
+
+
+def blr_reconstruct(n, block, rank, diag, u, x, vt, mode=FMA_CHAIN):
+    """BlrMatrix::reconstruct_dense (blr.hpp:62-86) rounded per `mode`"""
+    out = np.zeros(n * n)
+    rc = oracle_lib().oracle_blr_reconstruct(mode, n, block, rank, _p(diag), _p(u), _p(x),
+                                             _p(vt), _p(out))
+    if rc != 0:
+        raise ValueError("oracle_blr_reconstruct: bad arguments")
+    return out
+
+
+def ref_blr_reconstruct(n, block, rank, diag, u, x, vt):
+    """the reference's own reconstruct_dense"""
+    out = np.zeros(n * n)
+    if ref_lib().ref_blr_reconstruct(n, block, rank, _p(diag), _p(u), _p(x), _p(vt), _p(out)):
+        raise ValueError("ref_blr_reconstruct failed")
+    return out
+
+
+def ref_lowrank_expand(batch, m, n, r, u, x, vt, workers=1):
+    """the reference's (U X) Vt per item through its gemm_naive_raw"""
+    out = np.zeros(batch * m * n)
+    if ref_lib().ref_lowrank_expand(batch, m, n, r, _p(u), _p(x), _p(vt), _p(out), workers):
+        raise ValueError("ref_lowrank_expand failed")
+    return out
 
 
 def ref_machines_available() -> bool:

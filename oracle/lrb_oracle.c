@@ -396,3 +396,48 @@ int oracle_blr_matvec(int mode, int64_t n, int64_t block, int64_t rank, const do
   free(x_vt_x);
   return 0;
 }
+
+/* ------------------------------------------------------------------------
+ * Low-rank expansion out_i = (U_i X_i) Vt_i of a batch of LowRankOperands
+ * (low_rank.hpp:16-63), restating the per-tile expansion inside
+ * BlrMatrix::reconstruct_dense (blr.hpp:75-78): UX = dense_gemm_naive(U, X),
+ * then tile = dense_gemm_naive(UX, Vt), each gemm_naive_raw without a flop
+ * counter (dense.hpp:58-77). Items row-major at base + it*stride; out_i has
+ * leading dimension ldo. */
+int oracle_lowrank_expand(int mode, int64_t batch, int64_t m, int64_t n, int64_t r,
+                          const double* u, int64_t su, const double* x, int64_t sx,
+                          const double* vt, int64_t svt, double* out, int64_t ldo, int64_t so) {
+  if (batch < 0 || m < 0 || n < 0 || r < 1 || ldo < n) return -1;
+  double* ux = (double*)malloc(sizeof(double) * (size_t)(m * r + 1));
+  double* tile = (double*)malloc(sizeof(double) * (size_t)(m * n + 1));
+  for (int64_t it = 0; it < batch; ++it) {
+    gemm_acc(mode, u + it * su, x + it * sx, ux, m, r, r, 0);
+    gemm_acc(mode, ux, vt + it * svt, tile, m, r, n, 0);
+    for (int64_t row = 0; row < m; ++row)
+      memcpy(out + it * so + row * ldo, tile + row * n, sizeof(double) * (size_t)n);
+  }
+  free(ux);
+  free(tile);
+  return 0;
+}
+
+/* BlrMatrix::reconstruct_dense (blr.hpp:62-86): the n x n row-major matrix,
+ * diagonal tiles copied, off-diagonal tiles (U X) Vt. */
+int oracle_blr_reconstruct(int mode, int64_t n, int64_t block, int64_t rank, const double* diag,
+                           const double* u, const double* x, const double* vt, double* out) {
+  if (block < 1 || n % block || rank < 1) return -1;
+  const int64_t T = n / block, b = block, r = rank;
+  for (int64_t ti = 0; ti < T; ++ti)
+    for (int64_t tj = 0; tj < T; ++tj) {
+      double* dst = out + ti * b * n + tj * b;
+      if (ti == tj) {
+        for (int64_t row = 0; row < b; ++row)
+          memcpy(dst + row * n, diag + ti * b * b + row * b, sizeof(double) * (size_t)b);
+      } else {
+        const int64_t o = ti * (T - 1) + (tj < ti ? tj : tj - 1);
+        oracle_lowrank_expand(mode, 1, b, b, r, u + o * b * r, 0, x + o * r * r, 0,
+                              vt + o * r * b, 0, dst, n, 0);
+      }
+    }
+  return 0;
+}

@@ -79,6 +79,11 @@ int oracle_lowrank_batch(int mode, int64_t batch, int64_t block, int64_t rank, c
 int oracle_blr_matvec(int mode, int64_t n, int64_t block, int64_t rank, const double* diag,
                       const double* u, const double* x, const double* vt, const double* rhs,
                       int64_t nrhs, double* y);
+int oracle_lowrank_expand(int mode, int64_t batch, int64_t m, int64_t n, int64_t r,
+                          const double* u, int64_t su, const double* x, int64_t sx,
+                          const double* vt, int64_t svt, double* out, int64_t ldo, int64_t so);
+int oracle_blr_reconstruct(int mode, int64_t n, int64_t block, int64_t rank, const double* diag,
+                           const double* u, const double* x, const double* vt, double* out);
 
 #ifdef __cplusplus
 }

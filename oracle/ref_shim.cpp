@@ -349,3 +349,46 @@ int ref_blr_matvec(int which, int64_t n, int64_t block, int64_t rank, const doub
   return 0;
 }
 }  // extern "C"
+
+extern "C" {
+// BlrMatrix::reconstruct_dense (blr.hpp:62-86) -> out (n x n, row-major)
+int ref_blr_reconstruct(int64_t n, int64_t block, int64_t rank, const double* diag,
+                        const double* u, const double* x, const double* vt, double* out) {
+  try {
+    lrbatch::BlrMatrix m{size_t(n), size_t(block), size_t(rank)};
+    const size_t T = m.tiles, b = size_t(block), r = size_t(rank);
+    for (size_t i = 0; i < T; ++i)
+      m.diagonal.emplace_back(b, b, std::vector<double>(diag + i * b * b, diag + (i + 1) * b * b));
+    for (size_t o = 0; o < T * (T - 1); ++o)
+      m.off_diagonal.emplace_back(b, b, r, std::vector<double>(u + o * b * r, u + (o + 1) * b * r),
+                                  std::vector<double>(x + o * r * r, x + (o + 1) * r * r),
+                                  std::vector<double>(vt + o * r * b, vt + (o + 1) * r * b));
+    const lrbatch::DenseBlock full = timed([&] { return m.reconstruct_dense(); });
+    std::memcpy(out, full.data.data(), full.data.size() * sizeof(double));
+  } catch (...) {
+    return -1;
+  }
+  return 0;
+}
+
+// the per-tile expansion of reconstruct_dense (blr.hpp:75-78) over a batch of
+// contiguous LowRankOperands: out_i = (U_i X_i) Vt_i through the reference's
+// gemm_naive_raw (what dense_gemm_naive runs after its shape checks,
+// dense.hpp:58-77), items split over `workers` threads like
+// naive_multiply_batch; ref_last_seconds() covers the products alone.
+int ref_lowrank_expand(int64_t batch, int64_t m, int64_t n, int64_t rank, const double* u,
+                       const double* x, const double* vt, double* out, int workers) {
+  if (batch < 0 || m < 1 || n < 1 || rank < 1) return -1;
+  const size_t M = size_t(m), N = size_t(n), R = size_t(rank);
+  timed([&] {
+    fan_out(batch, workers, [&](int64_t b0, int64_t e0) {
+      std::vector<double> ux(M * R);
+      for (int64_t it = b0; it < e0; ++it) {
+        lrbatch::gemm_naive_raw(u + it * M * R, x + it * R * R, ux.data(), M, R, R, false);
+        lrbatch::gemm_naive_raw(ux.data(), vt + it * R * N, out + it * M * N, M, R, N, false);
+      }
+    });
+  });
+  return 0;
+}
+}  // extern "C"

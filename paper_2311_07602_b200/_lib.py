@@ -102,6 +102,8 @@ SIGNATURES = {
     ),
     "lrb_lowrank_multiply": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, vp]),
     "lrb_lowrank_multiply_host": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp]),
+    "lrb_lowrank_expand": (C.c_int, [vp, i64, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64,
+                                     i64, vp]),
     "lrb_lowrank_flops_per_item": (dbl, [i64, i64]),
     "lrb_batch_file_header": (C.c_int, [C.c_char_p, P(i64)]),
     "lrb_batch_file_load": (C.c_int, [vp, C.c_char_p, vp, vp, vp, vp, C.c_int]),
@@ -110,6 +112,7 @@ SIGNATURES = {
     "lrb_blr_matvec": (C.c_int, [vp, vp, vp, i64, vp]),
     "lrb_blr_matvec_device": (C.c_int, [vp, vp, vp, i64, vp, vp]),
     "lrb_blr_destroy": (C.c_int, [vp, vp]),
+    "lrb_blr_reconstruct_dense": (C.c_int, [vp, vp, vp, C.c_int, vp]),
     "lrb_graph_begin": (C.c_int, [vp, vp]),
     "lrb_graph_end": (C.c_int, [vp, vp, P(vp)]),
     "lrb_graph_launch": (C.c_int, [vp, vp, vp]),

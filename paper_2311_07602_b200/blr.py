@@ -104,6 +104,24 @@ class BlrMatrix:
         self._dev = (ctx, h.value)
         return h.value
 
+    def reconstruct_dense(self, ctx: Optional[Context] = None) -> DenseBlock:
+        """Exact dense n x n assembly (BlrMatrix::reconstruct_dense,
+        blr.hpp:62-86) on the GPU: diagonal tiles copied, off-diagonal tiles
+        expanded as (U X) Vt in the reference's order."""
+        ctx = ctx or default_context()
+        h = self.device_handle(ctx)
+        out = DenseBlock(self.n, self.n)
+        _check(lib.lrb_blr_reconstruct_dense(ctx._h, h, out.data.ctypes.data, 0, None), ctx._h)
+        return out
+
+    def reconstruct_dense_device(self, ctx: Context, out, stream=None) -> None:
+        """device form: `out` is a DeviceBuffer of n*n doubles (asynchronous)"""
+        from .lrbatch import _ptr
+
+        h = self.device_handle(ctx)
+        _check(lib.lrb_blr_reconstruct_dense(ctx._h, h, _ptr(out), 1,
+                                             stream.handle if stream else None), ctx._h)
+
     def __del__(self):
         try:
             self.invalidate()
@@ -122,3 +140,31 @@ def blr_matvec(m: BlrMatrix, rhs: DenseBlock, plan=None, workers: int = 1,
     _check(lib.lrb_blr_matvec(ctx._h, h, rhs.data.ctypes.data, rhs.cols, y.data.ctypes.data),
            ctx._h)
     return y
+
+
+def lowrank_expand(u, x, vt, batch: int, m: int, n: int, rank: int,
+                   ctx: Optional[Context] = None) -> np.ndarray:
+    """out_i = (U_i X_i) Vt_i for a uniform batch of LowRankOperands held as
+    contiguous row-major host arrays (the per-tile expansion of
+    reconstruct_dense, blr.hpp:75-78), computed on the GPU; returns
+    batch * m * n doubles."""
+    ctx = ctx or default_context()
+    du, dx, dvt = ctx.to_device(u), ctx.to_device(x), ctx.to_device(vt)
+    dout = ctx.empty(max(1, batch * m * n))
+    lowrank_expand_device(ctx, batch, m, n, rank, du, dx, dvt, dout)
+    ctx.synchronize()
+    return dout.download()[: batch * m * n]
+
+
+def lowrank_expand_device(ctx: Context, batch: int, m: int, n: int, rank: int, u, x, vt, out,
+                          su: Optional[int] = None, sx: Optional[int] = None,
+                          svt: Optional[int] = None, ldo: Optional[int] = None,
+                          so: Optional[int] = None, stream=None) -> None:
+    """device form of lrb_lowrank_expand (strides default to packed items)"""
+    from .lrbatch import _ptr
+
+    ldo = n if ldo is None else ldo
+    _check(lib.lrb_lowrank_expand(
+        ctx._h, batch, m, n, rank, _ptr(u), m * rank if su is None else su, _ptr(x),
+        rank * rank if sx is None else sx, _ptr(vt), rank * n if svt is None else svt, _ptr(out),
+        ldo, m * ldo if so is None else so, stream.handle if stream else None), ctx._h)

@@ -185,10 +185,11 @@ int auto_variant(int64_t m, int64_t n, int64_t batch, int sm_count) {
   return LRB_V_Q64;  // 64 x 64 tiles, three CTAs per SM (U * V^T: profiles/sweep_*)
 }
 
-// debug-only kernel flags for probes (tools/probe_cfg2.py): bit 1 skips C stores
+// debug-only kernel flags for probes (tools/probe_cfg2.py): bit 1 skips C
+// stores, bit 2 orders tiles j-fastest, bit 3 uses default-policy stores
 int debug_flags() {
   const char* s = std::getenv("LRB_DEBUG_FLAGS");
-  return s ? (std::atoi(s) & 6) : 0;
+  return s ? (std::atoi(s) & 14) : 0;
 }
 
 int env_variant() {

@@ -38,6 +38,11 @@ struct lrb_blr {
   int64_t ws_nrhs = -1;
   double* d_w = nullptr;
   double* d_z = nullptr;
+  // reconstruct_dense: UX tiles in Vt's (j, i) order and the tile plan for
+  // the last output buffer
+  double* d_ux = nullptr;
+  const double* recon_out = nullptr;
+  lrb_ptr_plan* recon_plan = nullptr;
 };
 
 namespace lrb {
@@ -50,6 +55,14 @@ lrb_status run_strided_rowmajor_beta(lrb_ctx* ctx, int64_t m, int64_t n, int64_t
 using lrb::fail;
 
 namespace {
+
+void free_recon(lrb_ctx* ctx, lrb_blr* m) {
+  if (m->recon_plan) lrb_ptr_plan_destroy(ctx, m->recon_plan);
+  if (m->d_ux) cudaFree(m->d_ux);
+  m->recon_plan = nullptr;
+  m->recon_out = nullptr;
+  m->d_ux = nullptr;
+}
 
 void free_ws(lrb_ctx*, lrb_blr* m) {
   if (m->d_w) cudaFree(m->d_w);
@@ -76,24 +89,104 @@ lrb_status ensure_ws(lrb_ctx* ctx, lrb_blr* m, int64_t nrhs) {
 // r^2 + W r*nrhs read, Z r*nrhs written per item — a few MB in total.
 __global__ void __launch_bounds__(256) blr_couple_kernel(const double* __restrict__ x,
                                                          const double* __restrict__ w,
-                                                         double* __restrict__ z, int64_t tiles,
+                                                         double* __restrict__ z, int tiles,
                                                          int rank, int nrhs) {
-  const int64_t per = int64_t(rank) * nrhs;
-  const int64_t total = tiles * (tiles - 1) * per;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
-       e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t q = e / per;
-    const int rem = int(e - q * per);
-    const int p = rem / nrhs, c = rem - p * nrhs;
-    const int64_t j = q / (tiles - 1), ip = q - j * (tiles - 1);
-    const int64_t i = ip < j ? ip : ip + 1;
-    const int64_t jp = j < i ? j : j - 1;
-    const double* xr = x + q * int64_t(rank) * rank + int64_t(p) * rank;
-    const double* wc = w + q * per + c;
-    double acc = 0.0;
+  // items per block pass; every index below is 32-bit (Q = tiles*(tiles-1)
+  // items of r*nrhs entries each), decomposed once per item
+  const int per = rank * nrhs;
+  const int ipb = max(1, int(blockDim.x) / per);
+  const int Q = tiles * (tiles - 1);
+  for (int q0 = int(blockIdx.x) * ipb; q0 < Q; q0 += int(gridDim.x) * ipb) {
+    for (int t = threadIdx.x; t < ipb * per; t += blockDim.x) {
+      const int qi = t / per, rem = t - qi * per;
+      const int q = q0 + qi;
+      if (q >= Q) break;
+      const int p = rem / nrhs, c = rem - p * nrhs;
+      const int j = q / (tiles - 1), ip = q - j * (tiles - 1);
+      const int i = ip < j ? ip : ip + 1;
+      const int jp = j < i ? j : j - 1;
+      const double* xr = x + int64_t(q) * rank * rank + int64_t(p) * rank;
+      const double* wc = w + int64_t(q) * per + c;
+      double acc = 0.0;
 #pragma unroll 4
-    for (int k = 0; k < rank; ++k) acc = fma(__ldg(xr + k), __ldg(wc + int64_t(k) * nrhs), acc);
-    z[(i * (tiles - 1) + jp) * per + rem] = acc;
+      for (int k = 0; k < rank; ++k) acc = fma(__ldg(xr + k), __ldg(wc + int64_t(k) * nrhs), acc);
+      z[(int64_t(i) * (tiles - 1) + jp) * per + rem] = acc;
+    }
+  }
+}
+
+// reconstruct_dense step 1: UX_p = U_ij X_ij for every off-diagonal tile, p
+// in Vt's (column j, row i != j) order, U_ij read from the concatenated row
+// layout [U_i0 | U_i1 | ...]. One block per item (32-bit indices within it).
+// A thread owns a 4-row x CP-column block of UX (CP = 2 when rank is even):
+// per step q it loads four U values and one X pair for 4*CP FMAs. Every
+// entry is still one r-long FMA chain over q ascending.
+template <int CP>
+__global__ void __launch_bounds__(256) blr_ux_kernel(const double* __restrict__ ucat,
+                                                     const double* __restrict__ x,
+                                                     double* __restrict__ ux, int tiles,
+                                                     int block, int rank) {
+  constexpr int RP = 4;
+  const int Q = tiles * (tiles - 1);
+  const int64_t K = int64_t(tiles - 1) * rank;
+  const int row_groups = (block + RP - 1) / RP, col_groups = rank / CP;
+  const int work = row_groups * col_groups;
+  for (int p = blockIdx.x; p < Q; p += gridDim.x) {
+    const int j = p / (tiles - 1), ip = p - j * (tiles - 1);
+    const int i = ip < j ? ip : ip + 1;
+    const int jp = j < i ? j : j - 1;
+    const double* ub = ucat + int64_t(i) * block * K + int64_t(jp) * rank;
+    const double* xb = x + int64_t(p) * rank * rank;
+    double* out = ux + int64_t(p) * block * rank;
+    for (int wkr = threadIdx.x; wkr < work; wkr += blockDim.x) {
+      const int rg = wkr / col_groups, cg = wkr - rg * col_groups;
+      const int r0 = rg * RP, c0 = cg * CP;
+      double acc[RP][CP];
+#pragma unroll
+      for (int a = 0; a < RP; ++a)
+#pragma unroll
+        for (int c = 0; c < CP; ++c) acc[a][c] = 0.0;
+      const double* ur[RP];
+#pragma unroll
+      for (int a = 0; a < RP; ++a) ur[a] = ub + int64_t(min(r0 + a, block - 1)) * K;
+#pragma unroll 2
+      for (int q = 0; q < rank; ++q) {
+        double xv[CP];
+        if constexpr (CP == 2) {
+          const double2 t = __ldg(reinterpret_cast<const double2*>(xb + q * rank + c0));
+          xv[0] = t.x;
+          xv[1] = t.y;
+        } else {
+          xv[0] = __ldg(xb + q * rank + c0);
+        }
+#pragma unroll
+        for (int a = 0; a < RP; ++a) {
+          const double u = __ldg(ur[a] + q);
+#pragma unroll
+          for (int c = 0; c < CP; ++c) acc[a][c] = fma(u, xv[c], acc[a][c]);
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < RP; ++a)
+        if (r0 + a < block) {
+#pragma unroll
+          for (int c = 0; c < CP; ++c) out[(r0 + a) * rank + c0 + c] = acc[a][c];
+        }
+    }
+  }
+}
+
+// reconstruct_dense: the diagonal tiles into the n x n row-major output, one
+// block per tile row
+__global__ void __launch_bounds__(256) blr_diag_kernel(const double* __restrict__ diag,
+                                                       double* __restrict__ out, int tiles,
+                                                       int block) {
+  const int64_t n = int64_t(tiles) * block;
+  for (int g = blockIdx.x; g < tiles * block; g += gridDim.x) {
+    const int t = g / block, row = g - t * block;
+    const double* src = diag + int64_t(g) * block;
+    double* dst = out + (int64_t(t) * block + row) * n + int64_t(t) * block;
+    for (int c = threadIdx.x; c < block; c += blockDim.x) dst[c] = __ldg(src + c);
   }
 }
 
@@ -113,6 +206,8 @@ extern "C" lrb_status lrb_blr_create(lrb_ctx* ctx, int64_t n, int64_t block, int
   if (!(rank >= 1 && rank <= block))
     return fail(ctx, LRB_ERR_SHAPE, "BlrMatrix: rank must be in [1, block]");
   const int64_t T = n / block;
+  if (n >= (int64_t(1) << 31))
+    return fail(ctx, LRB_ERR_UNSUPPORTED, "%s: n = %lld exceeds 2^31 - 1", fn, (long long)n);
   if (!diag || (T > 1 && (!u || !x || !vt)))
     return fail(ctx, LRB_ERR_ARG, "%s: a tile array is null", fn);
   if (!ctx) return fail(nullptr, LRB_ERR_ARG, "%s: null ctx", fn);
@@ -192,9 +287,10 @@ extern "C" lrb_status lrb_blr_matvec_device(lrb_ctx* ctx, lrb_blr* m, const doub
   if (st) return st;
   // 3. Z_ij = X_ij W_ij
   {
-    const int64_t total = T * (T - 1) * r * nrhs;
-    const int64_t blocks = std::min<int64_t>((total + 255) / 256, int64_t(ctx->sm_count) * 16);
-    blr_couple_kernel<<<unsigned(blocks), 256, 0, s>>>(m->d_x, m->d_w, m->d_z, T, int(r),
+    const int64_t per = r * nrhs, ipb = std::max<int64_t>(1, 256 / per);
+    const int64_t blocks = std::min<int64_t>((T * (T - 1) + ipb - 1) / ipb,
+                                             int64_t(ctx->sm_count) * 16);
+    blr_couple_kernel<<<unsigned(blocks), 256, 0, s>>>(m->d_x, m->d_w, m->d_z, int(T), int(r),
                                                        int(nrhs));
     LRB_CUDA_TRY(ctx, cudaGetLastError());
     ctx->launches.fetch_add(1, std::memory_order_relaxed);
@@ -234,10 +330,83 @@ extern "C" lrb_status lrb_blr_destroy(lrb_ctx* ctx, lrb_blr* m) {
   if (!m) return LRB_OK;
   if (ctx) cudaSetDevice(ctx->device);
   free_ws(ctx, m);
+  free_recon(ctx, m);
   if (m->d_diag) cudaFree(m->d_diag);
   if (m->d_vtcol) cudaFree(m->d_vtcol);
   if (m->d_x) cudaFree(m->d_x);
   if (m->d_ucat) cudaFree(m->d_ucat);
   delete m;
   return LRB_OK;
+}
+
+// BlrMatrix::reconstruct_dense (blr.hpp:62-86) on the device: diagonal tiles
+// copied; off-diagonal tiles (U X) Vt in the reference's order — UX by
+// blr_ux_kernel, then the b x b tiles by a pointer-array plan of the batched
+// GEMM (K = rank, q64 tiles) writing straight into the n x n output.
+extern "C" lrb_status lrb_blr_reconstruct_dense(lrb_ctx* ctx, lrb_blr* m, double* out,
+                                                int on_device, void* stream) {
+  static const char* fn = "lrb_blr_reconstruct_dense";
+  if (!ctx || !m) return fail(ctx, LRB_ERR_ARG, "%s: null ctx or matrix", fn);
+  if (!out) return fail(ctx, LRB_ERR_ARG, "%s: out is null", fn);
+  lrb_status st = lrb::bind(ctx);
+  if (st) return st;
+  const int64_t T = m->tiles, b = m->block, r = m->rank, n = m->n;
+  if (!on_device) {
+    // host destination: through a pooled device buffer, synchronously
+    cudaStream_t s = ctx->lane_stream[0];
+    double* d = nullptr;
+    const size_t bytes = size_t(n) * size_t(n) * sizeof(double);
+    LRB_CUDA_TRY(ctx, lrb::pool_alloc(ctx, reinterpret_cast<void**>(&d), bytes, s));
+    st = lrb_blr_reconstruct_dense(ctx, m, d, 1, s);
+    cudaError_t e = cudaSuccess;
+    if (!st) e = cudaMemcpyAsync(out, d, bytes, cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(d, s);
+    cudaError_t e2 = cudaStreamSynchronize(s);
+    if (st) return st;
+    if (e != cudaSuccess) return lrb::cuda_fail(ctx, e, "lrb_blr_reconstruct_dense: copy");
+    if (e2 != cudaSuccess) return lrb::cuda_fail(ctx, e2, "lrb_blr_reconstruct_dense: sync");
+    return LRB_OK;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  {
+    const int64_t blocks = std::min<int64_t>(T * b, int64_t(ctx->sm_count) * 32);
+    blr_diag_kernel<<<unsigned(blocks), 256, 0, s>>>(m->d_diag, out, int(T), int(b));
+    LRB_CUDA_TRY(ctx, cudaGetLastError());
+    ctx->launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  if (T == 1) return LRB_OK;
+  const int64_t items = T * (T - 1);
+  if (!m->d_ux) LRB_CUDA_TRY(ctx, cudaMalloc(&m->d_ux, size_t(items * b * r) * sizeof(double)));
+  if (m->recon_out != out) {
+    if (m->recon_plan) lrb_ptr_plan_destroy(ctx, m->recon_plan);
+    m->recon_plan = nullptr;
+    m->recon_out = nullptr;
+    std::vector<int64_t> mm(items, b), nn(items, b), kk(items, r), la(items, r), lb(items, b),
+        lc(items, n);
+    std::vector<const double*> pa(items), pb(items);
+    std::vector<double*> pc(items);
+    for (int64_t p = 0; p < items; ++p) {
+      const int64_t j = p / (T - 1), ip = p - j * (T - 1), i = ip < j ? ip : ip + 1;
+      pa[p] = m->d_ux + p * b * r;
+      pb[p] = m->d_vtcol + p * r * b;
+      pc[p] = out + i * b * n + j * b;
+    }
+    st = lrb_ptr_plan_create(ctx, 'R', 'N', 'N', items, mm.data(), nn.data(), kk.data(),
+                             pa.data(), la.data(), pb.data(), lb.data(), pc.data(), lc.data(),
+                             0.0, &m->recon_plan);
+    if (st) return st;
+    m->recon_out = out;
+  }
+  {
+    const int64_t blocks = std::min<int64_t>(items, int64_t(ctx->sm_count) * 16);
+    if (r % 2 == 0)
+      blr_ux_kernel<2><<<unsigned(blocks), 256, 0, s>>>(m->d_ucat, m->d_x, m->d_ux, int(T),
+                                                        int(b), int(r));
+    else
+      blr_ux_kernel<1><<<unsigned(blocks), 256, 0, s>>>(m->d_ucat, m->d_x, m->d_ux, int(T),
+                                                        int(b), int(r));
+    LRB_CUDA_TRY(ctx, cudaGetLastError());
+    ctx->launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  return lrb_ptr_plan_execute(ctx, m->recon_plan, stream);
 }

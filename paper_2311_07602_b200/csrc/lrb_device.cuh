@@ -124,6 +124,13 @@ __device__ __forceinline__ void st_global_v4(double* p, double x, double y, doub
                "d"(w)
                : "memory");
 }
+// default-policy 32-byte store (probe alternative to .cs)
+__device__ __forceinline__ void st_global_v4_wb(double* p, double x, double y, double z,
+                                                double w) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "d"(x), "d"(y), "d"(z),
+               "d"(w)
+               : "memory");
+}
 __device__ __forceinline__ void st_global_cs(double* p, double x) {
   asm volatile("st.global.cs.f64 [%0], %1;\n" ::"l"(p), "d"(x) : "memory");
 }

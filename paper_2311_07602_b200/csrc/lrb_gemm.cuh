@@ -378,8 +378,9 @@ __device__ __forceinline__ void mma_kstep(double (&acc)[Cfg::FJ][Cfg::FI][2], co
 template <class Cfg, class Problem>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     lrb_gemm_kernel(const __grid_constant__ Problem prob, const int flags) {
-  // flags bit 0: beta = 1 (accumulate into C); bit 1: debug probe, skip the
-  // epilogue stores (LRB_DEBUG_FLAGS, never set by the library itself)
+  // flags bit 0: beta = 1 (accumulate into C); debug probes (LRB_DEBUG_FLAGS,
+  // never set by the library itself): bit 1 skips the epilogue stores, bit 3
+  // uses default-policy instead of streaming stores (bit 2 is host-side)
   const int beta_one = flags & 1;
   constexpr int MB = Cfg::MB, NB = Cfg::NB, KB = Cfg::KB, STAGES = Cfg::STAGES;
   constexpr int FI = Cfg::FI, FJ = Cfg::FJ;
@@ -506,7 +507,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
             const double r0 = acc[fj][2 * p][0], r1 = acc[fj][2 * p + 1][0];
             const double r2 = acc[fj][2 * p][1], r3 = acc[fj][2 * p + 1][1];
             if (vec4_ok && i + 3 < v.m) {
-              st_global_v4(cp + i, r0, r1, r2, r3);
+              if (flags & 8)
+                st_global_v4_wb(cp + i, r0, r1, r2, r3);
+              else
+                st_global_v4(cp + i, r0, r1, r2, r3);
             } else {
               if (i < v.m) st_global_cs(cp + i, r0);
               if (i + 1 < v.m) st_global_cs(cp + i + 1, r1);

@@ -502,3 +502,55 @@ extern "C" double lrb_lowrank_flops_per_item(int64_t rank, int64_t block) {
   // the reference's accounting, flops_per_item (low_rank.hpp:66-68)
   return 4.0 * double(rank) * rank * rank + 2.0 * double(rank) * rank * block;
 }
+
+// ------------------------------------------------------ low-rank expansion
+namespace lrb {
+lrb_status run_strided_rowmajor_beta(lrb_ctx* ctx, int64_t m, int64_t n, int64_t k,
+                                     const double* A, int64_t lda, int64_t sA, const double* B,
+                                     int64_t ldb, int64_t sB, double* C, int64_t ldc, int64_t sC,
+                                     int64_t batch, int beta_one, cudaStream_t stream);
+}
+
+// out_i = (U_i X_i) Vt_i, the reference's per-tile expansion (blr.hpp:75-78):
+// UX (m x r, K = r) into the context workspace, then UX Vt (m x n, K = r) —
+// the cfg2 shape (U V^T with an r x r core), q64 tiles.
+extern "C" lrb_status lrb_lowrank_expand(lrb_ctx* ctx, int64_t batch, int64_t m, int64_t n,
+                                         int64_t rank, const double* u, int64_t su,
+                                         const double* x, int64_t sx, const double* vt,
+                                         int64_t svt, double* out, int64_t ldo, int64_t so,
+                                         void* stream) {
+  static const char* fn = "lrb_lowrank_expand";
+  // LowRankOperand invariants and messages (low_rank.hpp:56-61)
+  if (rank < 1) return fail(ctx, LRB_ERR_SHAPE, "LowRankOperand: rank must be >= 1");
+  if (m < rank || n < rank)
+    return fail(ctx, LRB_ERR_SHAPE,
+                "LowRankOperand: need m >= rank and n >= rank, got (%lld, %lld, %lld)",
+                (long long)m, (long long)n, (long long)rank);
+  if (batch < 0) return fail(ctx, LRB_ERR_SHAPE, "%s: batch must be >= 0", fn);
+  if (ldo < n)
+    return fail(ctx, LRB_ERR_SHAPE, "%s: ldo is %lld but out is %lldx%lld", fn, (long long)ldo,
+                (long long)m, (long long)n);
+  if (su < 0 || sx < 0 || svt < 0)
+    return fail(ctx, LRB_ERR_SHAPE, "%s: input strides must be >= 0", fn);
+  if (batch > 1 && so < (m - 1) * ldo + n)
+    return fail(ctx, LRB_ERR_SHAPE, "%s: stride %lld < %lld: output items would overlap", fn,
+                (long long)so, (long long)((m - 1) * ldo + n));
+  if (!u || !x || !vt || !out) return fail(ctx, LRB_ERR_ARG, "%s: null operand", fn);
+  if (!ctx) return fail(nullptr, LRB_ERR_ARG, "%s: null ctx", fn);
+  if (batch == 0) return LRB_OK;
+  lrb_status st = bind(ctx);
+  if (st) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* ux = nullptr;
+  bool temp = false;
+  const size_t bytes = size_t(batch) * size_t(m * rank) * sizeof(double);
+  st = acquire_workspace(ctx, bytes, s, reinterpret_cast<void**>(&ux), &temp);
+  if (st) return st;
+  st = run_strided_rowmajor_beta(ctx, m, rank, rank, u, rank, su, x, rank, sx, ux, rank, m * rank,
+                                 batch, 0, s);
+  if (!st)
+    st = run_strided_rowmajor_beta(ctx, m, n, rank, ux, rank, m * rank, vt, n, svt, out, ldo, so,
+                                   batch, 0, s);
+  release_workspace(ctx, s, ux, temp);
+  return st;
+}

@@ -214,6 +214,10 @@ def get(name: str):
         return get_lowrank(name)
     if name.startswith("blr_"):
         return get_blr(name)
+    if name.startswith("lrx_"):
+        return get_expand(name)
+    if name.startswith("blrd_"):
+        return get_blr_dense(name)
     raise KeyError(name)
 
 
@@ -314,3 +318,77 @@ def get_blr(name: str) -> Blr:
     """blr_n{N}_b{B}_r{R}_k{nrhs}"""
     parts = dict((p[0], p[1:]) for p in name.split("_")[1:])
     return Blr(name, int(parts["n"]), int(parts["b"]), int(parts["r"]), int(parts["k"]))
+
+
+@dataclass
+class LrExpand:
+    """Low-rank expansion out_i = (U_i X_i) Vt_i of `batch` m x m
+    LowRankOperands of rank r (the per-tile expansion of reconstruct_dense,
+    blr.hpp:75-78), all row-major and packed."""
+
+    name: str
+    batch: int
+    m: int
+    rank: int
+    seed: int = 13
+
+    def item_flops(self) -> float:  # UX: 2 m r^2, (UX) Vt: 2 m^2 r
+        m, r = self.m, self.rank
+        return 2.0 * m * r * r + 2.0 * m * m * r
+
+    def item_bytes(self) -> float:  # U, X, Vt read, out written
+        m, r = self.m, self.rank
+        return 8.0 * (2 * m * r + r * r + m * m)
+
+    def flops(self, items=None) -> float:
+        return self.item_flops() * (self.batch if items is None else items)
+
+    def bytes(self, items=None) -> float:
+        return self.item_bytes() * (self.batch if items is None else items)
+
+    def describe(self) -> dict:
+        return {"workload": self.name, "batch": self.batch, "m": self.m, "n": self.m,
+                "rank": self.rank, "seed": self.seed,
+                "layout": "LowRankOperand roles row-major, packed; out m x m per item"}
+
+
+def get_expand(name: str) -> LrExpand:
+    """lrx_m{M}_r{R}[_b{batch}] (default batch: 8 GiB of output, like cfg2)"""
+    parts = dict((p[0], p[1:]) for p in name.split("_")[1:])
+    m = int(parts["m"])
+    return LrExpand(name, int(parts.get("b", max(1, (8 << 30) // (8 * m * m)))), m,
+                    int(parts["r"]))
+
+
+@dataclass
+class BlrDense:
+    """BlrMatrix::reconstruct_dense (blr.hpp:62-86): the n x n dense matrix."""
+
+    name: str
+    n: int
+    block: int
+    rank: int
+    seed: int = 11
+
+    @property
+    def tiles(self) -> int:
+        return self.n // self.block
+
+    def flops(self) -> float:
+        T, b, r = self.tiles, self.block, self.rank
+        return T * (T - 1) * (2.0 * b * r * r + 2.0 * b * b * r)
+
+    def bytes(self) -> float:  # diag + factors read, n^2 written
+        T, b, r = self.tiles, self.block, self.rank
+        return 8.0 * (T * b * b + T * (T - 1) * (2 * b * r + r * r) + self.n * self.n)
+
+    def describe(self) -> dict:
+        return {"workload": self.name, "n": self.n, "block": self.block, "rank": self.rank,
+                "tiles": self.tiles, "seed": self.seed,
+                "layout": "BlrMatrix tiles in; n x n row-major out"}
+
+
+def get_blr_dense(name: str) -> BlrDense:
+    """blrd_n{N}_b{B}_r{R}"""
+    parts = dict((p[0], p[1:]) for p in name.split("_")[1:])
+    return BlrDense(name, int(parts["n"]), int(parts["b"]), int(parts["r"]))

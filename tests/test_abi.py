@@ -199,3 +199,22 @@ def test_item_accounting():
     assert P.item_flops(256, 16, 256) == 2 * 256 * 16 * 256
     assert P.item_bytes(256, 16, 256) == 8 * (256 * 256 + 256 * 16 + 256 * 16)
     assert P.item_bytes(2, 2, 2, 1.0) == 8 * (4 + 4 + 8)
+
+
+@pytest.mark.parametrize("args,status,text", [
+    (dict(rank=0), _lib.LRB_ERR_SHAPE, "LowRankOperand: rank must be >= 1"),
+    (dict(m=3), _lib.LRB_ERR_SHAPE, "need m >= rank and n >= rank, got (3, 8, 4)"),
+    (dict(ldo=7), _lib.LRB_ERR_SHAPE, "ldo is 7 but out is 8x8"),
+    (dict(so=10), _lib.LRB_ERR_SHAPE, "output items would overlap"),
+    (dict(ptr=0), _lib.LRB_ERR_ARG, "null operand"),
+    (dict(), _lib.LRB_ERR_ARG, "null ctx"),
+])
+def test_lowrank_expand_validation(args, status, text):
+    # LowRankOperand's invariants and messages (low_rank.hpp:56-61), before any device work
+    a = dict(batch=2, m=8, n=8, rank=4, ldo=8, so=64, ptr=16)
+    a.update(args)
+    p = a["ptr"]
+    st = lib.lrb_lowrank_expand(None, a["batch"], a["m"], a["n"], a["rank"], 16, a["m"] * a["rank"],
+                                16, 16, 16, 32, p, a["ldo"], a["so"], None)
+    assert st == status
+    assert text in (lib.lrb_last_error(None) or b"").decode()

@@ -227,3 +227,28 @@ def test_packed_drivers_replay_the_fixture_plan(monkeypatch):
     assert O.ref_compare_to_reference(5, 64, 8, *args, replay)[0] < 1e-11
     if live is not None:
         assert np.array_equal(live, replay)
+
+
+@pytest.mark.parametrize("batch,m,n,r", [(3, 17, 13, 5), (2, 64, 64, 8), (1, 33, 40, 33),
+                                         (2, 9, 9, 1)])
+def test_expand_restatement_equals_reference_binary(batch, m, n, r):
+    # dense_gemm_naive(dense_gemm_naive(U, X), Vt) per item (blr.hpp:75-78)
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(batch * 100 + m + r)
+    u, x, vt = (rng.uniform(-1, 1, s) for s in (batch * m * r, batch * r * r, batch * r * n))
+    want = O.ref_lowrank_expand(batch, m, n, r, u, x, vt)
+    assert np.array_equal(O.lowrank_expand(batch, m, n, r, u, x, vt, mode=O.REF_COMPILED), want)
+
+
+@pytest.mark.parametrize("n,block,rank", [(96, 32, 6), (40, 8, 3), (64, 64, 4)])
+def test_reconstruct_restatement_equals_reference_binary(n, block, rank):
+    # BlrMatrix::reconstruct_dense (blr.hpp:62-86)
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    from paper_2311_07602_b200 import blr as B
+
+    m = B.BlrMatrix.random(n, block, rank, n + block)
+    args = (n, block, rank) + m.packed_arrays()
+    assert np.array_equal(O.blr_reconstruct(*args, mode=O.REF_COMPILED),
+                          O.ref_blr_reconstruct(*args))

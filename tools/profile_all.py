@@ -17,6 +17,32 @@ CONFIGS = ["cfg1", "cfg2"] + [f"cfg3_b{b}_r{r}" for b in W.CFG3_B for r in W.CFG
 # the widened rows (bench.py --config): low-rank product and BLR matvec
 LOWRANK = ["lr_r8_b1024", "lr_r16_b1024", "lr_r32_b2048", "lr_r64_b2048", "lr_r128_b1024"]
 BLR = ["blr_n32768_b512_r8_k8", "blr_n16384_b256_r16_k16"]
+EXPAND = ["lrx_m512_r8", "lrx_m512_r32", "blrd_n16384_b512_r16"]
+
+
+def expand_one(ctx, name):
+    from paper_2311_07602_b200 import blr as BL
+
+    w = W.get(name)
+    if isinstance(w, W.BlrDense):
+        mat = BL.BlrMatrix.random(w.n, w.block, w.rank, w.seed)
+        out = ctx.empty(w.n * w.n)
+        run = lambda: mat.reconstruct_dense_device(ctx, out)  # noqa: E731
+    else:
+        m, r, n = w.m, w.rank, w.batch
+        bufs = [ctx.empty(n * m * r), ctx.empty(n * r * r), ctx.empty(n * r * m)]
+        for b_ in bufs:
+            b_.fill_bytes(0)
+        out = ctx.empty(n * m * m)
+        run = lambda: BL.lowrank_expand_device(ctx, n, m, m, r, *bufs, out)  # noqa: E731
+    n0 = ctx.launch_count
+    run()
+    ctx.synchronize()
+    print(f"{name}_warm launches={ctx.launch_count - n0}", flush=True)
+    n0 = ctx.launch_count
+    run()
+    ctx.synchronize()
+    print(f"{name} launches={ctx.launch_count - n0}", flush=True)
 
 
 def lowrank_one(ctx, name):
@@ -93,6 +119,8 @@ def main():
         lowrank_one(ctx, name)
     for name in BLR:
         blr_one(ctx, name)
+    for name in EXPAND:
+        expand_one(ctx, name)
 
 
 if __name__ == "__main__":
