@@ -107,6 +107,14 @@ def ref_lib() -> C.CDLL:
         L.ref_blr_reconstruct.restype = C.c_int
         L.ref_lowrank_expand.argtypes = [i64, i64, i64, i64, vp, vp, vp, vp, C.c_int]
         L.ref_lowrank_expand.restype = C.c_int
+        L.ref_bench_csv_header.argtypes = [C.c_char_p, C.c_size_t]
+        L.ref_bench_csv_header.restype = C.c_int
+        L.ref_bench_csv_row.argtypes = [vp, C.c_char_p, C.c_size_t]
+        L.ref_bench_csv_row.restype = C.c_int
+        L.ref_bench_rates.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, dbl, vp]
+        L.ref_bench_rates.restype = C.c_int
+        L.ref_median_of.argtypes = [vp, i64]
+        L.ref_median_of.restype = dbl
         L.ref_last_seconds.argtypes = []
         L.ref_last_seconds.restype = dbl
         L.ref_packing_plan.argtypes = [C.c_char_p, i64, i64, P(i64)]
@@ -372,6 +380,36 @@ def ref_lowrank_expand(batch, m, n, r, u, x, vt, workers=1):
     if ref_lib().ref_lowrank_expand(batch, m, n, r, _p(u), _p(x), _p(vt), _p(out), workers):
         raise ValueError("ref_lowrank_expand failed")
     return out
+
+
+def ref_bench_csv_header() -> str:
+    """lrbatch::bench_csv_header (bench.hpp:125-129)"""
+    buf = C.create_string_buffer(1024)
+    if ref_lib().ref_bench_csv_header(buf, 1024):
+        raise ValueError("ref_bench_csv_header failed")
+    return buf.value.decode()
+
+
+def ref_bench_csv_row(values) -> str:
+    """lrbatch::bench_csv_row (bench.hpp:131-141) of 17 column values"""
+    v = np.asarray(values, dtype=np.float64)
+    buf = C.create_string_buffer(1024)
+    if ref_lib().ref_bench_csv_row(_p(v), buf, 1024):
+        raise ValueError("ref_bench_csv_row failed")
+    return buf.value.decode()
+
+
+def ref_bench_rates(batch, rank, block, seconds):
+    """(gflops, bandwidth_overlapped_gib_s, bandwidth_nonoverlapped_gib_s), or None on ShapeError"""
+    out = np.zeros(3)
+    if ref_lib().ref_bench_rates(batch, rank, block, seconds, _p(out)):
+        return None
+    return tuple(float(x) for x in out)
+
+
+def ref_median_of(values) -> float:
+    v = np.asarray(values, dtype=np.float64)
+    return float(ref_lib().ref_median_of(_p(v), v.size))
 
 
 def ref_machines_available() -> bool:

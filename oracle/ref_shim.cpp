@@ -392,3 +392,56 @@ int ref_lowrank_expand(int64_t batch, int64_t m, int64_t n, int64_t rank, const 
   return 0;
 }
 }  // extern "C"
+
+extern "C" {
+// bench.hpp:125-170: the reference's CSV header / row for 17 values
+// (7 integers then 10 doubles, in column order); 0 on success
+int ref_bench_csv_header(char* out, size_t len) {
+  const std::string h = lrbatch::bench_csv_header();
+  if (h.size() + 1 > len) return -1;
+  std::memcpy(out, h.c_str(), h.size() + 1);
+  return 0;
+}
+
+int ref_bench_csv_row(const double* v, char* out, size_t len) {
+  lrbatch::BenchResult r;
+  r.batch_size = size_t(v[0]);
+  r.block_size = size_t(v[1]);
+  r.rank = size_t(v[2]);
+  r.workers = size_t(v[3]);
+  r.repetitions = size_t(v[4]);
+  r.warmup_reps = size_t(v[5]);
+  r.seed = uint64_t(v[6]);
+  r.wall_seconds = v[7];
+  r.gflops_rate = v[8];
+  r.bandwidth_overlapped = v[9];
+  r.bandwidth_nonoverlapped = v[10];
+  r.pack_small_seconds = v[11];
+  r.pack_skinny_seconds = v[12];
+  r.kernel_seconds = v[13];
+  r.other_seconds = v[14];
+  r.baseline_seconds = v[15];
+  r.speedup = v[16];
+  const std::string row = lrbatch::bench_csv_row(r);
+  if (row.size() + 1 > len) return -1;
+  std::memcpy(out, row.c_str(), row.size() + 1);
+  return 0;
+}
+
+// gflops / bandwidth_overlapped_gib_s / bandwidth_nonoverlapped_gib_s and
+// median_of (bench.hpp:21-88)
+int ref_bench_rates(uint64_t batch, uint64_t rank, uint64_t block, double seconds, double* out) {
+  try {
+    out[0] = lrbatch::gflops(batch, rank, block, seconds);
+    out[1] = lrbatch::bandwidth_overlapped_gib_s(batch, rank, block, seconds);
+    out[2] = lrbatch::bandwidth_nonoverlapped_gib_s(batch, rank, block, seconds);
+  } catch (...) {
+    return -1;
+  }
+  return 0;
+}
+
+double ref_median_of(const double* v, int64_t n) {
+  return lrbatch::median_of(std::vector<double>(v, v + n));
+}
+}  // extern "C"
