@@ -2,6 +2,7 @@
 // reference's known-answer tests (proj/tests/test_core.cpp:24-57) plus a
 // batched device call checked bitwise against an in-order FMA chain.
 // Exit 0 = all pass; prints one line per check.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -83,6 +84,119 @@ int main() {
     threw = true;
   }
   CHECK(threw, "lda < m raises ShapeError");
+
+  // ------------------------------------------------- the low-rank product
+  // all-ones factors (test_core.cpp:59-67): block 1 -> 1, block 4 -> 4
+  {
+    LowRankBatch one(1, 1, 1, 1), four(1, 4, 1, 1);
+    for (LowRankBatch* b : {&one, &four}) {
+      std::fill(b->a_vt_batch.begin(), b->a_vt_batch.end(), 1.0);
+      std::fill(b->b_u_batch.begin(), b->b_u_batch.end(), 1.0);
+      std::fill(b->a_x_batch.begin(), b->a_x_batch.end(), 1.0);
+      std::fill(b->b_x_batch.begin(), b->b_x_batch.end(), 1.0);
+    }
+    fused_multiply(one);
+    packed_multiply(four);
+    CHECK(one.g_xy_batch[0] == 1.0 && four.g_xy_batch[0] == 4.0, "all-ones low-rank product");
+  }
+  // random batch: G = A_X (A_Vt B_U) B_X bitwise vs three FMA chains
+  {
+    const std::size_t n = 9, blk = 256, r = 16;
+    LowRankBatch lb = LowRankBatch::random(n, blk, r, 7);
+    MultiplyStats stats;
+    packed_multiply(lb, /*plan=*/0, 4, &stats);
+    bool same = true;
+    std::vector<double> c(r * r), e(r * r);
+    for (std::size_t it = 0; it < n; ++it) {
+      const double *av = lb.a_vt(it), *bu = lb.b_u(it), *ax = lb.a_x(it), *bx = lb.b_x(it);
+      for (std::size_t i = 0; i < r; ++i)
+        for (std::size_t j = 0; j < r; ++j) {
+          double s = 0.0;
+          for (std::size_t p = 0; p < blk; ++p) s = std::fma(av[i * blk + p], bu[p * r + j], s);
+          c[i * r + j] = s;
+        }
+      for (std::size_t i = 0; i < r; ++i)
+        for (std::size_t j = 0; j < r; ++j) {
+          double s = 0.0;
+          for (std::size_t p = 0; p < r; ++p) s = std::fma(ax[i * r + p], c[p * r + j], s);
+          e[i * r + j] = s;
+        }
+      for (std::size_t i = 0; i < r; ++i)
+        for (std::size_t j = 0; j < r; ++j) {
+          double s = 0.0;
+          for (std::size_t p = 0; p < r; ++p) s = std::fma(e[i * r + p], bx[p * r + j], s);
+          same = same && s == lb.g_xy(it)[i * r + j];
+        }
+    }
+    CHECK(same, "packed_multiply == FMA-chain product (bitwise)");
+    CHECK(stats.g_entry_stores == n * r * r, "g_entry_stores");
+    LowRankBatch again = LowRankBatch::random(n, blk, r, 7);
+    naive_multiply_batch(again, 3);
+    CHECK(again.g_xy_batch == lb.g_xy_batch, "naive_multiply_batch == packed_multiply");
+  }
+  threw = false;
+  try {
+    LowRankBatch bad(2, 16, 4, 8);
+    fused_multiply(bad);
+  } catch (const ShapeError& ex) {
+    threw = std::string(ex.what()).find("rank_a must equal rank_b") != std::string::npos;
+  }
+  CHECK(threw, "rank mismatch raises ShapeError");
+
+  // ------------------------------------------------------ LRBATCH1 files
+  {
+    LowRankBatch lb = LowRankBatch::random(5, 32, 4, 11);
+    const std::string path = "/tmp/lrb_cxx_test.lrb";
+    save_batch(lb, path);
+    LowRankBatch back = load_batch(path);
+    CHECK(back.batch_size == 5 && back.block_size == 32 && back.rank_a == 4 &&
+              back.a_vt_batch == lb.a_vt_batch && back.b_x_batch == lb.b_x_batch,
+          "save_batch / load_batch round trip");
+    bool io = false, parse = false;
+    try {
+      load_batch("/tmp/definitely/not/here.lrb");
+    } catch (const IoError&) {
+      io = true;
+    }
+    {
+      FILE* f = std::fopen(path.c_str(), "wb");
+      std::fputs("NOTABATCHFILE...", f);
+      std::fclose(f);
+    }
+    try {
+      load_batch(path);
+    } catch (const ParseError&) {
+      parse = true;
+    }
+    std::remove(path.c_str());
+    CHECK(io && parse, "IoError / ParseError");
+  }
+
+  // ---------------------------------------------------------- BLR matvec
+  {
+    BlrMatrix m = BlrMatrix::random(192, 32, 6, 5);
+    DenseBlock rhs(192, 3);
+    NormalSource src(9);
+    src.fill(rhs.data.data(), rhs.data.size());
+    DenseBlock y = blr_matvec(m, rhs, /*plan=*/0, 2);
+    DenseBlock expect = dense_gemm_naive(m.reconstruct_dense(), rhs);
+    double rms = 0.0;
+    for (double v : expect.data) rms += v * v;
+    rms = std::sqrt(rms / double(expect.data.size()));
+    double worst = 0.0;
+    for (std::size_t i = 0; i < y.data.size(); ++i)
+      worst = std::max(worst, std::fabs(y.data[i] - expect.data[i]) /
+                                  std::max(std::fabs(expect.data[i]), rms));
+    CHECK(worst < 1e-10, "blr_matvec == reconstruct_dense * rhs");
+    CHECK(blr_matvec_naive(m, rhs).data == y.data, "blr_matvec_naive == blr_matvec");
+    bool shape = false;
+    try {
+      blr_matvec(m, DenseBlock(100, 2));
+    } catch (const ShapeError&) {
+      shape = true;
+    }
+    CHECK(shape, "rhs row mismatch raises ShapeError");
+  }
   std::printf("%d failures\n", failures);
   return failures ? 1 : 0;
 }

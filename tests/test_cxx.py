@@ -28,3 +28,17 @@ def test_cxx_wrapper_runs(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failures" in r.stdout
+
+
+def test_cxx_random_inputs_equal_the_reference(tmp_path):
+    # LowRankBatch::random / BlrMatrix::random of the mirror == the reference's
+    ref_inc = "/root/reference/proj/include"
+    if not os.path.isdir(ref_inc):
+        pytest.skip("the reference headers are not here")
+    exe = str(tmp_path / "rp")
+    src = os.path.join(ROOT, "tests", "cxx", "test_random_parity.cpp")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", ref_inc, "-I", os.path.join(ROOT, "include"),
+                    src, "-o", exe, "-L", LIBDIR, "-llrb", f"-Wl,-rpath,{LIBDIR}"], check=True,
+                   capture_output=True, text=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0 and "0 mismatches" in r.stdout, r.stdout + r.stderr
