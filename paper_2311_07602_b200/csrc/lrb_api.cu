@@ -489,6 +489,18 @@ void release_workspace(lrb_ctx* ctx, cudaStream_t s, void* p, bool temporary) {
 
 }  // namespace lrb
 
+namespace lrb {
+lrb_status ensure_aux(lrb_ctx* ctx) {
+  if (ctx->fork_ev) return LRB_OK;
+  for (int i = 0; i < lrb_ctx::kAux; ++i) {
+    LRB_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->aux_stream[i], cudaStreamNonBlocking));
+    LRB_CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->aux_done[i], cudaEventDisableTiming));
+  }
+  LRB_CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+  return LRB_OK;
+}
+}  // namespace lrb
+
 // ===================================================== memory / streams / events
 extern "C" lrb_status lrb_malloc(lrb_ctx* ctx, size_t bytes, void** dptr) {
   if (!dptr) return fail(ctx, LRB_ERR_ARG, "lrb_malloc: dptr is null");
@@ -886,13 +898,8 @@ extern "C" lrb_status lrb_ptr_plan_execute(lrb_ctx* ctx, const lrb_ptr_plan* pla
   const int ngroups = int(plan->groups.size());
   const bool fork = ngroups > 1;
   if (fork) {
-    if (!ctx->fork_ev) {
-      LRB_CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
-      for (int i = 0; i < lrb_ctx::kAux; ++i) {
-        LRB_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->aux_stream[i], cudaStreamNonBlocking));
-        LRB_CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->aux_done[i], cudaEventDisableTiming));
-      }
-    }
+    st = ensure_aux(ctx);
+    if (st) return st;
     LRB_CUDA_TRY(ctx, cudaEventRecord(ctx->fork_ev, user));
     for (int i = 0; i < std::min(ngroups, int(lrb_ctx::kAux)); ++i)
       LRB_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->aux_stream[i], ctx->fork_ev, 0));

@@ -87,31 +87,61 @@ lrb_status ensure_ws(lrb_ctx* ctx, lrb_blr* m, int64_t nrhs) {
 // thread owns one entry Z[p][c] = sum_k X[p][k] W[k][c] as an in-order FMA
 // chain from zero (the order DMMA and the FMA-chain oracle use). Bytes: X
 // r^2 + W r*nrhs read, Z r*nrhs written per item — a few MB in total.
+template <int CP>
 __global__ void __launch_bounds__(256) blr_couple_kernel(const double* __restrict__ x,
                                                          const double* __restrict__ w,
                                                          double* __restrict__ z, int tiles,
                                                          int rank, int nrhs) {
-  // items per block pass; every index below is 32-bit (Q = tiles*(tiles-1)
-  // items of r*nrhs entries each), decomposed once per item
-  const int per = rank * nrhs;
-  const int ipb = max(1, int(blockDim.x) / per);
+  // a thread owns a 4-row x CP-column block of one Z_q (CP = 2 when nrhs is
+  // even): per step k it loads four X values and one W pair for 4*CP FMAs;
+  // every entry is still one r-long chain over k ascending. 32-bit indices:
+  // Q = tiles*(tiles-1) items of r*nrhs entries.
+  constexpr int RP = 4;
+  const int rg_n = (rank + RP - 1) / RP, cg_n = nrhs / CP;
+  const int per_item = rg_n * cg_n, per = rank * nrhs;
   const int Q = tiles * (tiles - 1);
-  for (int q0 = int(blockIdx.x) * ipb; q0 < Q; q0 += int(gridDim.x) * ipb) {
-    for (int t = threadIdx.x; t < ipb * per; t += blockDim.x) {
-      const int qi = t / per, rem = t - qi * per;
-      const int q = q0 + qi;
-      if (q >= Q) break;
-      const int p = rem / nrhs, c = rem - p * nrhs;
-      const int j = q / (tiles - 1), ip = q - j * (tiles - 1);
-      const int i = ip < j ? ip : ip + 1;
-      const int jp = j < i ? j : j - 1;
-      const double* xr = x + int64_t(q) * rank * rank + int64_t(p) * rank;
-      const double* wc = w + int64_t(q) * per + c;
-      double acc = 0.0;
-#pragma unroll 4
-      for (int k = 0; k < rank; ++k) acc = fma(__ldg(xr + k), __ldg(wc + int64_t(k) * nrhs), acc);
-      z[(int64_t(i) * (tiles - 1) + jp) * per + rem] = acc;
+  const int total = Q * per_item;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int q = t / per_item, rem = t - q * per_item;
+    const int rg = rem / cg_n, cg = rem - rg * cg_n;
+    const int p0 = rg * RP, c0 = cg * CP;
+    const int j = q / (tiles - 1), ip = q - j * (tiles - 1);
+    const int i = ip < j ? ip : ip + 1;
+    const int jp = j < i ? j : j - 1;
+    const double* xq = x + int64_t(q) * rank * rank;
+    const double* wq = w + int64_t(q) * per + c0;
+    const double* xr[RP];
+#pragma unroll
+    for (int a = 0; a < RP; ++a) xr[a] = xq + min(p0 + a, rank - 1) * rank;
+    double acc[RP][CP];
+#pragma unroll
+    for (int a = 0; a < RP; ++a)
+#pragma unroll
+      for (int c = 0; c < CP; ++c) acc[a][c] = 0.0;
+#pragma unroll 2
+    for (int k = 0; k < rank; ++k) {
+      double wv[CP];
+      if constexpr (CP == 2) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(wq + k * nrhs));
+        wv[0] = v.x;
+        wv[1] = v.y;
+      } else {
+        wv[0] = __ldg(wq + k * nrhs);
+      }
+#pragma unroll
+      for (int a = 0; a < RP; ++a) {
+        const double xv = __ldg(xr[a] + k);
+#pragma unroll
+        for (int c = 0; c < CP; ++c) acc[a][c] = fma(xv, wv[c], acc[a][c]);
+      }
     }
+    double* zq = z + (int64_t(i) * (tiles - 1) + jp) * per + c0;
+#pragma unroll
+    for (int a = 0; a < RP; ++a)
+      if (p0 + a < rank) {
+#pragma unroll
+        for (int c = 0; c < CP; ++c) zq[(p0 + a) * nrhs + c] = acc[a][c];
+      }
   }
 }
 
@@ -275,27 +305,44 @@ extern "C" lrb_status lrb_blr_matvec_device(lrb_ctx* ctx, lrb_blr* m, const doub
   if (st) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t T = m->tiles, b = m->block, r = m->rank, K = (T - 1) * r;
-  // 1. y_i = D_i rhs_i
-  st = lrb::run_strided_rowmajor_beta(ctx, b, nrhs, b, m->d_diag, b, b * b, rhs, nrhs, b * nrhs,
-                                      y, nrhs, b * nrhs, T, 0, s);
-  if (st || T == 1) return st;
+  if (T == 1)  // 1. y = D rhs only
+    return lrb::run_strided_rowmajor_beta(ctx, b, nrhs, b, m->d_diag, b, b * b, rhs, nrhs,
+                                          b * nrhs, y, nrhs, b * nrhs, T, 0, s);
   st = ensure_ws(ctx, m, nrhs);
   if (st) return st;
+  // steps 1 and 2 are independent: step 1 runs forked on an auxiliary stream
+  // so the two launches' ramps and tails overlap; joined before step 4
+  st = lrb::ensure_aux(ctx);
+  if (st) return st;
+  cudaStream_t aux = ctx->aux_stream[lrb_ctx::kAux - 1];
+  cudaEvent_t done = ctx->aux_done[lrb_ctx::kAux - 1];
+  LRB_CUDA_TRY(ctx, cudaEventRecord(ctx->fork_ev, s));
+  LRB_CUDA_TRY(ctx, cudaStreamWaitEvent(aux, ctx->fork_ev, 0));
+  // 1. y_i = D_i rhs_i
+  st = lrb::run_strided_rowmajor_beta(ctx, b, nrhs, b, m->d_diag, b, b * b, rhs, nrhs, b * nrhs,
+                                      y, nrhs, b * nrhs, T, 0, aux);
+  if (st) return st;
+  LRB_CUDA_TRY(ctx, cudaEventRecord(done, aux));
   // 2. W_.j = [Vt_ij]_i rhs_j
   st = lrb::run_strided_rowmajor_beta(ctx, K, nrhs, b, m->d_vtcol, b, K * b, rhs, nrhs, b * nrhs,
                                       m->d_w, nrhs, K * nrhs, T, 0, s);
   if (st) return st;
   // 3. Z_ij = X_ij W_ij
   {
-    const int64_t per = r * nrhs, ipb = std::max<int64_t>(1, 256 / per);
-    const int64_t blocks = std::min<int64_t>((T * (T - 1) + ipb - 1) / ipb,
-                                             int64_t(ctx->sm_count) * 16);
-    blr_couple_kernel<<<unsigned(blocks), 256, 0, s>>>(m->d_x, m->d_w, m->d_z, int(T), int(r),
-                                                       int(nrhs));
+    const int cp = (nrhs % 2 == 0) ? 2 : 1;
+    const int64_t work = T * (T - 1) * ((r + 3) / 4) * (nrhs / cp);
+    const int64_t blocks = std::min<int64_t>((work + 255) / 256, int64_t(ctx->sm_count) * 16);
+    if (cp == 2)
+      blr_couple_kernel<2><<<unsigned(blocks), 256, 0, s>>>(m->d_x, m->d_w, m->d_z, int(T),
+                                                            int(r), int(nrhs));
+    else
+      blr_couple_kernel<1><<<unsigned(blocks), 256, 0, s>>>(m->d_x, m->d_w, m->d_z, int(T),
+                                                            int(r), int(nrhs));
     LRB_CUDA_TRY(ctx, cudaGetLastError());
     ctx->launches.fetch_add(1, std::memory_order_relaxed);
   }
-  // 4. y_i += [U_ij]_j [Z_ij]_j
+  // 4. y_i += [U_ij]_j [Z_ij]_j (after step 1's y)
+  LRB_CUDA_TRY(ctx, cudaStreamWaitEvent(s, done, 0));
   return lrb::run_strided_rowmajor_beta(ctx, b, nrhs, K, m->d_ucat, K, b * K, m->d_z, nrhs,
                                         K * nrhs, y, nrhs, b * nrhs, T, 1, s);
 }

@@ -59,6 +59,8 @@ lrb_status bind(lrb_ctx* ctx);  // cudaSetDevice(ctx->device)
 lrb_status acquire_workspace(lrb_ctx* ctx, size_t bytes, cudaStream_t s, void** out,
                              bool* temporary);
 void release_workspace(lrb_ctx* ctx, cudaStream_t s, void* p, bool temporary);
+// the auxiliary streams / fork-join events, created on first use
+lrb_status ensure_aux(lrb_ctx* ctx);
 // stream-ordered allocation from the context pool (blocks stay mapped)
 inline cudaError_t pool_alloc(lrb_ctx* ctx, void** p, size_t bytes, cudaStream_t s) {
   return ctx->pool ? cudaMallocFromPoolAsync(p, bytes, ctx->pool, s) : cudaMallocAsync(p, bytes, s);
