@@ -186,10 +186,11 @@ int auto_variant(int64_t m, int64_t n, int64_t batch, int sm_count) {
 }
 
 // debug-only kernel flags for probes (tools/probe_cfg2.py): bit 1 skips C
-// stores, bit 2 orders tiles j-fastest, bit 3 uses default-policy stores
+// stores, bit 2 orders tiles j-fastest, bit 3 uses default-policy stores,
+// bit 4 stops the operand refills after the prologue (stale data)
 int debug_flags() {
   const char* s = std::getenv("LRB_DEBUG_FLAGS");
-  return s ? (std::atoi(s) & 14) : 0;
+  return s ? (std::atoi(s) & 30) : 0;
 }
 
 int env_variant() {

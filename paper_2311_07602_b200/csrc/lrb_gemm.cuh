@@ -380,7 +380,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     lrb_gemm_kernel(const __grid_constant__ Problem prob, const int flags) {
   // flags bit 0: beta = 1 (accumulate into C); debug probes (LRB_DEBUG_FLAGS,
   // never set by the library itself): bit 1 skips the epilogue stores, bit 3
-  // uses default-policy instead of streaming stores (bit 2 is host-side)
+  // uses default-policy instead of streaming stores, bit 4 stops refilling the
+  // ring after the prologue (MMAs on stale data; bit 2 is host-side)
   const int beta_one = flags & 1;
   constexpr int MB = Cfg::MB, NB = Cfg::NB, KB = Cfg::KB, STAGES = Cfg::STAGES;
   constexpr int FI = Cfg::FI, FJ = Cfg::FJ;
@@ -419,6 +420,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
 
   int stage = 0;
   uint32_t phase = 0;
+  int consumed = 0;  // debug probe bit 4: after the prologue, compute on stale data
 #pragma unroll 1
   for (int64_t t = blockIdx.x; t < prob.num_tiles; t += gridDim.x) {
     const TileView v = prob.template tile<MB, NB>(t);
@@ -450,7 +452,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
 #pragma unroll 1
     for (int k0 = 0; k0 < v.k; k0 += KB) {
       const int kvalid = min(KB, v.k - k0);
-      mbar_wait(&full[stage], phase);
+      if (!(flags & 16) || consumed < STAGES) mbar_wait(&full[stage], phase);
+      ++consumed;
       const double* As = smem + size_t(stage) * Cfg::STAGE_ELEMS;
       const double* Bs = As + Cfg::A_ELEMS;
       if (kvalid == KB) {
@@ -485,7 +488,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
         if (last) released[stage] = 0;
       }
       last = __shfl_sync(0xffffffffu, last, 0);
-      if (last) issue_chunk<Cfg>(prob, smem, full, st, stage, lane);
+      if (last && !(flags & 16)) issue_chunk<Cfg>(prob, smem, full, st, stage, lane);
       if (++stage == STAGES) {
         stage = 0;
         phase ^= 1;
