@@ -153,7 +153,7 @@ constexpr double kHbmBytesPerS = 6553.6e9;
 // Automatic choice on the column-major view (m x n output, inner k); tile
 // sizes per shape class were chosen from the per-variant sweep in
 // profiles/sweep_variants_r01.jsonl.
-int auto_variant(int64_t m, int64_t n, int64_t batch, int sm_count) {
+int auto_variant(int64_t m, int64_t n, int64_t k_hint, int64_t batch, int sm_count) {
   // small square-ish outputs (the r x r products of the low-rank product's
   // three-GEMM path): one 64 x 64 tile covers them with the least padding
   if (m <= 64 && n <= 64 && m > 32 && n > 32) return LRB_V_Q64;
@@ -182,7 +182,11 @@ int auto_variant(int64_t m, int64_t n, int64_t batch, int sm_count) {
     if (m <= 32) return LRB_V_M32;
     return LRB_V_M64;
   }
-  return LRB_V_Q64;  // 64 x 64 tiles, three CTAs per SM (U * V^T: profiles/sweep_*)
+  // general shapes: 64 x 64 tiles at three CTAs per SM for short k (cfg2's
+  // U * V^T, k = 32: the per-tile overhead is small next to its epilogue);
+  // 128 x 64 tiles with 64 x 32 warp tiles once k >= 128 amortises them
+  if (k_hint >= 128 && m >= 128 && n >= 64) return LRB_V_T64;
+  return LRB_V_Q64;
 }
 
 // debug-only kernel flags for probes (tools/probe_cfg2.py): bit 1 skips C
@@ -199,11 +203,11 @@ int env_variant() {
   return lrb_variant_from_name(s);
 }
 
-int choose_variant(const lrb_ctx* ctx, int64_t m, int64_t n, int64_t batch) {
+int choose_variant(const lrb_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t batch) {
   if (ctx && ctx->variant_override >= 0) return ctx->variant_override;
   int v = env_variant();
   if (v >= 0) return v;
-  return auto_variant(m, n, batch, ctx ? ctx->sm_count : 148);
+  return auto_variant(m, n, k, batch, ctx ? ctx->sm_count : 148);
 }
 
 // ============================================================ normalisation
@@ -301,7 +305,7 @@ lrb_status run_strided(lrb_ctx* ctx, const Gemm& g, int64_t batch, int beta_one,
                        cudaStream_t stream, int* variant_used) {
   if (batch == 0 || g.m == 0 || g.n == 0) return LRB_OK;
   if (g.k == 0 && beta_one) return LRB_OK;  // C = C
-  const int v = choose_variant(ctx, g.m, g.n, batch);
+  const int v = choose_variant(ctx, g.m, g.n, g.k, batch);
   const VariantMeta& vm = kVariants[v];
   const int64_t ti = (g.m + vm.mb - 1) / vm.mb, tj = (g.n + vm.nb - 1) / vm.nb;
   if (ti * tj > INT32_MAX || ti * tj * batch > (int64_t(1) << 62))
@@ -671,7 +675,7 @@ extern "C" lrb_status lrb_select(const lrb_ctx* ctx, char order, char opA, char 
   if (m < 0 || n < 0 || k < 0 || batch < 0)
     return fail(mctx, LRB_ERR_SHAPE, "lrb_select: negative dimension");
   const int64_t cm = row_major(order) ? n : m, cn = row_major(order) ? m : n;
-  const int v = choose_variant(ctx, cm, cn, batch);
+  const int v = choose_variant(ctx, cm, cn, k, batch);
   const VariantMeta& vm = kVariants[v];
   std::memset(out, 0, sizeof(*out));
   out->variant = v;
@@ -799,7 +803,7 @@ extern "C" lrb_status lrb_ptr_plan_create(lrb_ctx* ctx, char order, char opA, ch
     d.k = int32_t(g.k);
     d.pad = 0;
     if (g.m == 0 || g.n == 0 || (g.k == 0 && beta == 1.0)) continue;
-    const int v = choose_variant(ctx, g.m, g.n, batch);
+    const int v = choose_variant(ctx, g.m, g.n, g.k, batch);
     const int64_t ti = (g.m + kVariants[v].mb - 1) / kVariants[v].mb;
     const int64_t tj = (g.n + kVariants[v].nb - 1) / kVariants[v].nb;
     if (ti > 0xFFFF || tj > 0xFFFF)

@@ -21,6 +21,10 @@
 //   n16h : 64-row tiles, sweep candidate.
 //   m8t, m16t : 32-column tiles at five CTAs per SM, the m* shapes of small
 //         batches (the BLR matvec's per-row launches: 64 items of 8 x 512).
+//   t64 : 128 x 64 tiles, 64 x 32 per warp (256 DMMAs per k-chunk instead of
+//         128), two CTAs per SM: general shapes with a long inner dimension
+//         (k >= 128), where the per-tile overhead then amortises (the
+//         low-rank product's r = 128 GEMMs: 0.86 -> 0.94 of FP64 peak).
 //   n24, n40, n48, n56 : intermediate widths so a variable-rank batch
 //         (cfg4, r_i in 8..64) wastes less than one 8-column fragment.
 #pragma once
@@ -45,9 +49,10 @@
   X(15, n16t, 4, 1, 8, 16, 32, 2, 5)   \
   X(16, n16h, 4, 1, 16, 16, 32, 2, 4)  \
   X(17, m8t, 1, 4, 8, 8, 32, 2, 5)     \
-  X(18, m16t, 1, 4, 16, 8, 32, 2, 5)
+  X(18, m16t, 1, 4, 16, 8, 32, 2, 5)   \
+  X(19, t64, 2, 2, 64, 32, 32, 2, 2)
 
-#define LRB_NUM_VARIANTS 19
+#define LRB_NUM_VARIANTS 20
 
 enum {
   LRB_V_N8 = 0,
@@ -68,5 +73,6 @@ enum {
   LRB_V_N16T = 15,
   LRB_V_N16H = 16,
   LRB_V_M8T = 17,
-  LRB_V_M16T = 18
+  LRB_V_M16T = 18,
+  LRB_V_T64 = 19
 };

@@ -88,6 +88,15 @@ def test_selector_small_skinny_batches_use_short_tiles():
     assert P.select("R", "N", "N", 256, 16, 1008, 100000)["name"] == "m16"
 
 
+def test_selector_long_k_general_shapes_use_t64():
+    # 128 x 64 tiles with 64 x 32 warp tiles once k >= 128 (the low-rank
+    # product's r = 128 GEMMs); short-k U V^T (cfg2) stays on q64
+    assert P.select("R", "N", "N", 128, 128, 1024, 20000)["name"] == "t64"
+    assert P.select("R", "N", "N", 128, 128, 128, 20000)["name"] == "t64"
+    assert P.select("C", "N", "T", 512, 512, 32, 4096)["name"] == "q64"
+    assert P.select("R", "N", "N", 64, 64, 1024, 20000)["name"] == "q64"
+
+
 def test_selector_row_major_swaps_roles():
     # row-major C (m x n) is column-major C^T (n x m): the reference's BLR
     # diagonal step D(b x b) * rhs(b x r) lands on the short-wide m-variants

@@ -172,6 +172,19 @@ int main() {
                   flops / (ms * 1e-3) / 1e12);
     }
   }
+  // DMMA throughput vs warps per SM sub-partition (one CTA per SM)
+  for (int warps : {4, 8, 12, 16}) {
+    int threads = warps * 32, blocks = sms;
+    dmma_peak<0><<<blocks, threads>>>(out, 0.5);
+    CK(cudaDeviceSynchronize());
+    cudaEventRecord(e0);
+    for (int r = 0; r < 5; ++r) dmma_peak<0><<<blocks, threads>>>(out, 0.5);
+    cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    double flops = 5.0 * blocks * warps * 8.0 * (kIters / 4) * fl[0] * 2.0;
+    std::printf("{\"probe\": \"dmma_m8n8k4_per_smsp\", \"warps_per_smsp\": %d, \"tflops\": %.2f}\n",
+                warps / 4, flops / (ms * 1e-3) / 1e12);
+  }
   // DMMA rounding probe (m8n8k4 and m16n8k16) vs sequential FMA chain
   {
     const int trials = 2000;
