@@ -70,6 +70,8 @@ lrb_status lrb_destroy(lrb_ctx* ctx);
 const char* lrb_last_error(const lrb_ctx* ctx); /* ctx may be NULL: thread-local last error */
 const char* lrb_version(void);
 int lrb_device_count(void); /* 0 when no driver / no device; never fails */
+/* the device's name (cudaGetDeviceProperties), NUL-terminated into buf */
+lrb_status lrb_device_name(int device, char* buf, size_t len);
 int lrb_ctx_device(const lrb_ctx* ctx);
 int lrb_ctx_sm_count(const lrb_ctx* ctx);
 /* number of kernels this context has launched so far (GEMM + fill + flush) */

@@ -54,6 +54,7 @@ SIGNATURES = {
     "lrb_last_error": (C.c_char_p, [vp]),
     "lrb_version": (C.c_char_p, []),
     "lrb_device_count": (C.c_int, []),
+    "lrb_device_name": (C.c_int, [C.c_int, C.c_char_p, C.c_size_t]),
     "lrb_ctx_device": (C.c_int, [vp]),
     "lrb_ctx_sm_count": (C.c_int, [vp]),
     "lrb_launch_count": (u64, [vp]),

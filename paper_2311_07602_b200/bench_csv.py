@@ -176,14 +176,14 @@ def parse_bench_csv_row(line: str) -> BenchResult:
     return r
 
 
-def _device_name() -> str:
-    try:
-        import torch
+def _device_name(ctx: Context) -> str:
+    import ctypes
 
-        if torch.cuda.is_available():
-            return torch.cuda.get_device_name(0)
-    except Exception:
-        pass
+    from .lrbatch import lib
+
+    buf = ctypes.create_string_buffer(256)
+    if lib.lrb_device_name(lib.lrb_ctx_device(ctx._h), buf, 256) == 0:
+        return buf.value.decode()
     return "cuda"
 
 
@@ -193,7 +193,8 @@ def run_bench(config: BenchConfig, ctx: Optional[Context] = None,
     median of `repetitions` host calls of packed_multiply; the device-resident
     kernel time, H2D and D2H are measured separately (module docstring).
     `baseline(batch, workers)` runs the comparison (the reference's
-    naive_multiply_batch) when config.run_baseline."""
+    naive_multiply_batch) when config.run_baseline; when it returns a float,
+    that is taken as its time."""
     config.validate()
     ctx = ctx or default_context()
     res = BenchResult(config.batch_size, config.block_size, config.rank, config.workers,
@@ -251,15 +252,17 @@ def run_bench(config: BenchConfig, ctx: Optional[Context] = None,
     res.other_seconds = max(0.0, wall - res.kernel_seconds)
     res.h2d_seconds = median_of(h2d)
     res.d2h_seconds = median_of(d2h)
-    res.device = _device_name()
+    res.device = _device_name(ctx)
     if config.run_baseline and baseline is not None:
         for _ in range(config.warmup_reps):
             baseline(batch, config.workers)
         bw = []
         for _ in range(config.repetitions):
             t0 = time.perf_counter()
-            baseline(batch, config.workers)
-            bw.append(time.perf_counter() - t0)
+            t = baseline(batch, config.workers)
+            # a callable may report its own time (e.g. the driver alone,
+            # without marshalling into the reference's containers)
+            bw.append(float(t) if isinstance(t, float) else time.perf_counter() - t0)
         res.baseline_seconds = median_of(bw)
         res.speedup = res.baseline_seconds / res.wall_seconds
     return res

@@ -350,6 +350,15 @@ using namespace lrb;
 // ================================================================ context
 extern "C" const char* lrb_version(void) { return LRB_VERSION_STRING; }
 
+extern "C" lrb_status lrb_device_name(int device, char* buf, size_t len) {
+  if (!buf || len == 0) return fail(nullptr, LRB_ERR_ARG, "lrb_device_name: empty buffer");
+  cudaDeviceProp prop;
+  cudaError_t e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "lrb_device_name");
+  std::snprintf(buf, len, "%s", prop.name);
+  return LRB_OK;
+}
+
 extern "C" int lrb_device_count(void) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) {
@@ -422,6 +431,10 @@ extern "C" lrb_status lrb_destroy(lrb_ctx* ctx) {
       cudaStreamDestroy(ctx->lane_stream[i]);
     }
     if (ctx->lane_buf[i]) cudaFree(ctx->lane_buf[i]);
+    if (ctx->lane_hin[i]) cudaFreeHost(ctx->lane_hin[i]);
+    if (ctx->lane_hout[i]) cudaFreeHost(ctx->lane_hout[i]);
+    if (ctx->lane_h2d[i]) cudaEventDestroy(ctx->lane_h2d[i]);
+    if (ctx->lane_d2h[i]) cudaEventDestroy(ctx->lane_d2h[i]);
   }
   for (int i = 0; i < lrb_ctx::kAux; ++i) {
     if (ctx->aux_stream[i]) {
@@ -1020,6 +1033,12 @@ extern "C" lrb_status lrb_dgemm_strided_batched_host(lrb_ctx* ctx, char order, c
       ctx->lane_bytes[l] = size_t(need) * 8;
     }
   }
+  // pageable host buffers go through pinned staging (HostPipe)
+  HostPipe pipe(ctx, lanes);
+  const bool page_in = !host_pinned(A) || !host_pinned(B) || (upload_c && !host_pinned(C));
+  const bool page_out = !host_pinned(C);
+  st = pipe.prepare(page_in ? size_t(need) * 8 + 3 * 256 : 0, page_out ? size_t(need) * 8 : 0);
+  if (st) return st;
   for (int64_t c = 0; c < nchunks; ++c) {
     const int l = int(c % lanes);
     cudaStream_t s = ctx->lane_stream[l];
@@ -1029,17 +1048,18 @@ extern "C" lrb_status lrb_dgemm_strided_batched_host(lrb_ctx* ctx, char order, c
     double* dA = ctx->lane_buf[l];
     double* dB = dA + round32(span_elems(per_chunk, sA, fA));
     double* dC = dB + round32(span_elems(per_chunk, sB, fB));
-    if (nA) LRB_CUDA_TRY(ctx, cudaMemcpyAsync(dA, A + c0 * sA, size_t(nA) * 8, cudaMemcpyHostToDevice, s));
-    if (nB) LRB_CUDA_TRY(ctx, cudaMemcpyAsync(dB, B + c0 * sB, size_t(nB) * 8, cudaMemcpyHostToDevice, s));
-    if (upload_c && nC)
-      LRB_CUDA_TRY(ctx, cudaMemcpyAsync(dC, C + c0 * sC, size_t(nC) * 8, cudaMemcpyHostToDevice, s));
+    if ((st = pipe.begin(l))) return st;
+    if ((st = pipe.h2d(l, dA, A + c0 * sA, size_t(nA) * 8))) return st;
+    if ((st = pipe.h2d(l, dB, B + c0 * sB, size_t(nB) * 8))) return st;
+    if (upload_c && (st = pipe.h2d(l, dC, C + c0 * sC, size_t(nC) * 8))) return st;
+    if ((st = pipe.inputs_done(l))) return st;
     const Gemm g = normalize(order, opA, opB, m, n, k, dA, lda, sA, dB, ldb, sB, dC, ldc, sC);
     st = run_strided(ctx, g, cnt, beta_one, s, nullptr);
     if (st) return st;
-    if (nC) LRB_CUDA_TRY(ctx, cudaMemcpyAsync(C + c0 * sC, dC, size_t(nC) * 8, cudaMemcpyDeviceToHost, s));
+    if ((st = pipe.d2h(l, C + c0 * sC, dC, size_t(nC) * 8))) return st;
+    if ((st = pipe.outputs_done(l))) return st;
   }
-  for (int l = 0; l < lanes; ++l) LRB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->lane_stream[l]));
-  return LRB_OK;
+  return pipe.finish();
 }
 
 extern "C" lrb_status lrb_gemm_naive_raw(lrb_ctx* ctx, const double* a, const double* b, double* c,

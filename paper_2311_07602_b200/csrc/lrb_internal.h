@@ -26,6 +26,14 @@ struct lrb_ctx {
   cudaStream_t lane_stream[kLanes] = {nullptr, nullptr, nullptr};
   double* lane_buf[kLanes] = {nullptr, nullptr, nullptr};
   size_t lane_bytes[kLanes] = {0, 0, 0};
+  // pageable host buffers: per-lane pinned staging (inputs / outputs) and the
+  // events that say when a lane's staging can be reused
+  void* lane_hin[kLanes] = {nullptr, nullptr, nullptr};
+  size_t lane_hin_bytes[kLanes] = {0, 0, 0};
+  void* lane_hout[kLanes] = {nullptr, nullptr, nullptr};
+  size_t lane_hout_bytes[kLanes] = {0, 0, 0};
+  cudaEvent_t lane_h2d[kLanes] = {nullptr, nullptr, nullptr};
+  cudaEvent_t lane_d2h[kLanes] = {nullptr, nullptr, nullptr};
   // pointer-array plans: one auxiliary stream per variant group so the groups'
   // persistent grids overlap their tails (fork/join through events)
   static constexpr int kAux = 4;
@@ -61,6 +69,36 @@ lrb_status acquire_workspace(lrb_ctx* ctx, size_t bytes, cudaStream_t s, void** 
 void release_workspace(lrb_ctx* ctx, cudaStream_t s, void* p, bool temporary);
 // the auxiliary streams / fork-join events, created on first use
 lrb_status ensure_aux(lrb_ctx* ctx);
+// Host side of the host-buffer pipelines. Pinned buffers are copied with
+// cudaMemcpyAsync directly; pageable ones through the lane's pinned staging
+// with a multi-threaded memcpy (the driver's own pageable path runs ~10 GB/s).
+// Per call: begin(l) before reusing lane l, h2d/d2h for each operand, then
+// inputs_done(l) / outputs_done(l), and finish() at the end.
+class HostPipe {
+ public:
+  HostPipe(lrb_ctx* ctx, int lanes) : ctx_(ctx), lanes_(lanes) {}
+  // staging sizes per lane (bytes); only allocated when a buffer is pageable
+  lrb_status prepare(size_t in_bytes, size_t out_bytes);
+  lrb_status begin(int lane);
+  lrb_status h2d(int lane, void* dev, const void* host, size_t bytes);
+  lrb_status inputs_done(int lane);
+  lrb_status d2h(int lane, void* host, const void* dev, size_t bytes);
+  lrb_status outputs_done(int lane);
+  lrb_status finish();
+
+ private:
+  struct Pending {
+    void* dst;
+    size_t off, bytes;
+  };
+  lrb_ctx* ctx_;
+  int lanes_;
+  size_t in_off_[lrb_ctx::kLanes] = {0, 0, 0}, out_off_[lrb_ctx::kLanes] = {0, 0, 0};
+  bool used_in_[lrb_ctx::kLanes] = {false, false, false};
+  std::vector<Pending> pend_[lrb_ctx::kLanes];
+};
+bool host_pinned(const void* p);
+void par_memcpy(void* dst, const void* src, size_t bytes);
 // stream-ordered allocation from the context pool (blocks stay mapped)
 inline cudaError_t pool_alloc(lrb_ctx* ctx, void** p, size_t bytes, cudaStream_t s) {
   return ctx->pool ? cudaMallocFromPoolAsync(p, bytes, ctx->pool, s) : cudaMallocAsync(p, bytes, s);

@@ -477,6 +477,14 @@ extern "C" lrb_status lrb_lowrank_multiply_host(lrb_ctx* ctx, int64_t batch, int
   }
   auto r32 = [](int64_t x) { return (x + 31) / 32 * 32; };
   const int64_t rb = rank * block, rr = rank * rank;
+  // pageable host buffers go through pinned staging (HostPipe)
+  HostPipe pipe(ctx, lanes);
+  const bool page_in = !host_pinned(a_vt) || !host_pinned(b_u) || !host_pinned(a_x) ||
+                       !host_pinned(b_x);
+  const bool page_out = !host_pinned(g);
+  st = pipe.prepare(page_in ? size_t(per_item * per_chunk) * 8 + 4 * 256 : 0,
+                    page_out ? size_t(rr * per_chunk) * 8 : 0);
+  if (st) return st;
   for (int64_t c = 0; c < nchunks; ++c) {
     const int l = int(c % lanes);
     cudaStream_t s = ctx->lane_stream[l];
@@ -486,16 +494,18 @@ extern "C" lrb_status lrb_lowrank_multiply_host(lrb_ctx* ctx, int64_t batch, int
     double* dax = dbu + r32(rb * per_chunk);
     double* dbx = dax + r32(rr * per_chunk);
     double* dg = dbx + r32(rr * per_chunk);
-    LRB_CUDA_TRY(ctx, cudaMemcpyAsync(dav, a_vt + i0 * rb, size_t(n * rb) * 8, cudaMemcpyHostToDevice, s));
-    LRB_CUDA_TRY(ctx, cudaMemcpyAsync(dbu, b_u + i0 * rb, size_t(n * rb) * 8, cudaMemcpyHostToDevice, s));
-    LRB_CUDA_TRY(ctx, cudaMemcpyAsync(dax, a_x + i0 * rr, size_t(n * rr) * 8, cudaMemcpyHostToDevice, s));
-    LRB_CUDA_TRY(ctx, cudaMemcpyAsync(dbx, b_x + i0 * rr, size_t(n * rr) * 8, cudaMemcpyHostToDevice, s));
+    if ((st = pipe.begin(l))) return st;
+    if ((st = pipe.h2d(l, dav, a_vt + i0 * rb, size_t(n * rb) * 8))) return st;
+    if ((st = pipe.h2d(l, dbu, b_u + i0 * rb, size_t(n * rb) * 8))) return st;
+    if ((st = pipe.h2d(l, dax, a_x + i0 * rr, size_t(n * rr) * 8))) return st;
+    if ((st = pipe.h2d(l, dbx, b_x + i0 * rr, size_t(n * rr) * 8))) return st;
+    if ((st = pipe.inputs_done(l))) return st;
     st = run_lowrank(ctx, n, block, rank, dav, dbu, dax, dbx, dg, s);
     if (st) return st;
-    LRB_CUDA_TRY(ctx, cudaMemcpyAsync(g + i0 * rr, dg, size_t(n * rr) * 8, cudaMemcpyDeviceToHost, s));
+    if ((st = pipe.d2h(l, g + i0 * rr, dg, size_t(n * rr) * 8))) return st;
+    if ((st = pipe.outputs_done(l))) return st;
   }
-  for (int l = 0; l < lanes; ++l) LRB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->lane_stream[l]));
-  return LRB_OK;
+  return pipe.finish();
 }
 
 extern "C" double lrb_lowrank_flops_per_item(int64_t rank, int64_t block) {

@@ -12,6 +12,7 @@ pytestmark = pytest.mark.gpu
 def _ref_naive(batch, workers):
     O.ref_lowrank(0, batch.batch_size, batch.block_size, batch.rank_a, batch.a_vt_batch,
                   batch.b_u_batch, batch.a_x_batch, batch.b_x_batch, workers=workers)
+    return O.ref_last_seconds()  # the driver alone
 
 
 def test_run_bench_produces_a_consistent_result_row(ctx):

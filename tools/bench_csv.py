@@ -30,6 +30,7 @@ def main():
     def naive(batch, workers):
         O.ref_lowrank(0, batch.batch_size, batch.block_size, batch.rank_a, batch.a_vt_batch,
                       batch.b_u_batch, batch.a_x_batch, batch.b_x_batch, workers=workers)
+        return O.ref_last_seconds()  # the driver alone
 
     rows = []
     for r in map(int, args.ranks.split(",")):
