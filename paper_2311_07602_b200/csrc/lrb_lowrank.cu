@@ -134,6 +134,17 @@ __global__ void __launch_bounds__(LrCfg<R>::THREADS, 2)
 #pragma unroll 1
   for (int64_t t = blockIdx.x; t < p.groups; t += gridDim.x) {
     const int64_t item = t * Cf::G + warp;
+    if (item < p.batch) {
+      // the epilogue reads this item's A_X and B_X (2 r^2 doubles) with its
+      // latency exposed: start them towards L2 while the main loop runs
+      const char* pax = reinterpret_cast<const char*>(p.a_x + item * int64_t(r) * r);
+      const char* pbx = reinterpret_cast<const char*>(p.b_x + item * int64_t(r) * r);
+      const int bytes = r * r * 8;
+      for (int off = lane * 128; off < bytes; off += 32 * 128) {
+        prefetch_l2(pax + off);
+        prefetch_l2(pbx + off);
+      }
+    }
     // acc[fn][fm][c] = C[m = fm*8 + 2tq + c][n = fn*8 + g]   (D of C^T = B_U^T A_Vt^T)
     double acc[F][F][2];
 #pragma unroll
@@ -212,7 +223,7 @@ __global__ void __launch_bounds__(LrCfg<R>::THREADS, 2)
 #pragma unroll
           for (int fx = 0; fx < F; ++fx) {
             const int x = fx * 8 + g;
-            const double a = (x < r && mcol < r) ? ax[x * r + mcol] : 0.0;  // A_X[x][m]
+            const double a = (x < r && mcol < r) ? __ldg(ax + x * r + mcol) : 0.0;  // A_X[x][m]
             dmma_8x8x4(e[fx][fn][0], e[fx][fn][1], a, cb);
           }
         }
@@ -236,7 +247,7 @@ __global__ void __launch_bounds__(LrCfg<R>::THREADS, 2)
 #pragma unroll
           for (int fy = 0; fy < F; ++fy) {
             const int y = fy * 8 + g;
-            const double b = (nrow < r && y < r) ? bx[nrow * r + y] : 0.0;  // B_X[n][y]
+            const double b = (nrow < r && y < r) ? __ldg(bx + nrow * r + y) : 0.0;  // B_X[n][y]
             dmma_8x8x4(o[fx][fy][0], o[fx][fy][1], ea, b);
           }
         }
