@@ -182,11 +182,22 @@ int auto_variant(int64_t m, int64_t n, int64_t k_hint, int64_t batch, int sm_cou
     if (m <= 32) return LRB_V_M32;
     return LRB_V_M64;
   }
-  // general shapes: 64 x 64 tiles at three CTAs per SM for short k (cfg2's
-  // U * V^T, k = 32: the per-tile overhead is small next to its epilogue);
-  // 128 x 64 tiles with 64 x 32 warp tiles once k >= 128 amortises them
-  if (k_hint >= 128 && m >= 128 && n >= 64) return LRB_V_T64;
-  return LRB_V_Q64;
+  // general shapes: the tile with the least padded area among 64 x 64 (q64,
+  // three CTAs per SM), 96 x 96 (s96) and, once k >= 128 amortises its
+  // per-tile overhead, 128 x 64 with 64 x 32 warp tiles (t64). Ties keep t64
+  // for long k, else q64 (cfg2's U * V^T, k = 32). r = 96 products: s96 fits
+  // exactly where the others pad 96 to 128 (0.48 -> 0.93 of FP64 peak).
+  auto padded = [&](int64_t mb, int64_t nb) {
+    return double((m + mb - 1) / mb * mb) * double((n + nb - 1) / nb * nb);
+  };
+  int best = (k_hint >= 128 && m >= 128 && n >= 64) ? LRB_V_T64 : LRB_V_Q64;
+  double best_area = best == LRB_V_T64 ? padded(128, 64) : padded(64, 64);
+  if (padded(64, 64) < best_area) {
+    best = LRB_V_Q64;
+    best_area = padded(64, 64);
+  }
+  if (padded(96, 96) < best_area) best = LRB_V_S96;
+  return best;
 }
 
 // debug-only kernel flags for probes (tools/probe_cfg2.py): bit 1 skips C

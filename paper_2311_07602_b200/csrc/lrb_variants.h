@@ -25,6 +25,9 @@
 //         128), two CTAs per SM: general shapes with a long inner dimension
 //         (k >= 128), where the per-tile overhead then amortises (the
 //         low-rank product's r = 128 GEMMs: 0.86 -> 0.94 of FP64 peak).
+//   s96 : 96 x 96 tiles (48 x 48 per warp), two CTAs per SM: outputs whose
+//         sides are (multiples of) 96, where 64- and 128-wide tiles pad 96 to
+//         128 (the paper's rank-96 low-rank products: 0.48 -> 0.93).
 //   n24, n40, n48, n56 : intermediate widths so a variable-rank batch
 //         (cfg4, r_i in 8..64) wastes less than one 8-column fragment.
 #pragma once
@@ -50,9 +53,10 @@
   X(16, n16h, 4, 1, 16, 16, 32, 2, 4)  \
   X(17, m8t, 1, 4, 8, 8, 32, 2, 5)     \
   X(18, m16t, 1, 4, 16, 8, 32, 2, 5)   \
-  X(19, t64, 2, 2, 64, 32, 32, 2, 2)
+  X(19, t64, 2, 2, 64, 32, 32, 2, 2)   \
+  X(20, s96, 2, 2, 48, 48, 32, 2, 2)
 
-#define LRB_NUM_VARIANTS 20
+#define LRB_NUM_VARIANTS 21
 
 enum {
   LRB_V_N8 = 0,
@@ -74,5 +78,6 @@ enum {
   LRB_V_N16H = 16,
   LRB_V_M8T = 17,
   LRB_V_M16T = 18,
-  LRB_V_T64 = 19
+  LRB_V_T64 = 19,
+  LRB_V_S96 = 20
 };

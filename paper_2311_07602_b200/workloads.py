@@ -274,7 +274,7 @@ class LowRank:
                 "layout": "LowRankBatch: row-major roles packed contiguously"}
 
 
-LOWRANK_R = (8, 16, 32, 64, 128)
+LOWRANK_R = (8, 16, 32, 64, 96, 128)
 LOWRANK_B = (512, 1024, 2048)
 
 

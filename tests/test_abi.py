@@ -97,6 +97,14 @@ def test_selector_long_k_general_shapes_use_t64():
     assert P.select("R", "N", "N", 64, 64, 1024, 20000)["name"] == "q64"
 
 
+def test_selector_rank96_uses_s96():
+    # 96 x 96 outputs: s96 fits exactly where q64 / t64 pad to 128 x 128
+    assert P.select("R", "N", "N", 96, 96, 1024, 20000)["name"] == "s96"
+    assert P.select("R", "N", "N", 96, 96, 96, 20000)["name"] == "s96"
+    assert P.select("C", "N", "N", 80, 80, 64, 1000)["name"] == "s96"
+    assert P.select("C", "N", "T", 512, 512, 32, 4096)["name"] == "q64"
+
+
 def test_selector_row_major_swaps_roles():
     # row-major C (m x n) is column-major C^T (n x m): the reference's BLR
     # diagonal step D(b x b) * rhs(b x r) lands on the short-wide m-variants

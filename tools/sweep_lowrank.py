@@ -22,7 +22,7 @@ from paper_2311_07602_b200 import workloads as W  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--ranks", default="8,16,32,64,128")
+    ap.add_argument("--ranks", default="8,16,32,64,96,128")
     ap.add_argument("--blocks", default="512,1024,2048")
     ap.add_argument("--batch", type=int, default=20000)
     ap.add_argument("--reps", type=int, default=7)
