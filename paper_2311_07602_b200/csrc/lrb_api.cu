@@ -118,6 +118,31 @@ bool encode_operand(CUtensorMap* map, const double* base, int64_t rows, int64_t 
   return r == CUDA_SUCCESS;
 }
 
+// (m, n, batch) map of column-major C for the TMA-store epilogue: box 16
+// rows x nb columns, 128-byte swizzle (matches stage_c_tile's layout). False
+// when C does not meet TMA's alignment rules (the register epilogue is used).
+bool encode_c_map(CUtensorMap* map, double* C, int64_t m, int64_t n, int64_t ldc, int64_t sC,
+                  int64_t batch, int nb) {
+  auto fn = encode_fn();
+  if (!fn || m < 1 || n < 1 || batch < 1) return false;
+  // the TMA store writes 16-byte granules: an odd m would spill one element
+  // past each column's last row (into the ld gap or the next column)
+  if ((m & 1) != 0) return false;
+  if ((reinterpret_cast<uintptr_t>(C) & 15) != 0 || (ldc & 1) != 0) return false;
+  if (batch > 1 && (sC & 1) != 0) return false;
+  if (ldc * 8 >= (int64_t(1) << 40) || sC * 8 >= (int64_t(1) << 40)) return false;
+  if (m > UINT32_MAX || n > UINT32_MAX || batch > INT32_MAX) return false;
+  const int64_t zstride = batch > 1 ? sC : (ldc * n + 1) / 2 * 2;
+  cuuint64_t dims[3] = {cuuint64_t(m), cuuint64_t(n), cuuint64_t(batch)};
+  cuuint64_t strides[2] = {cuuint64_t(ldc * 8), cuuint64_t(zstride * 8)};
+  cuuint32_t box[3] = {16, cuuint32_t(nb), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, C, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // loader choice: ctx override, else LRB_LOADER=segment|tma, else automatic
 int loader_mode(const lrb_ctx* ctx) {
   if (ctx && ctx->loader_override >= 0) return ctx->loader_override;
@@ -202,10 +227,11 @@ int auto_variant(int64_t m, int64_t n, int64_t k_hint, int64_t batch, int sm_cou
 
 // debug-only kernel flags for probes (tools/probe_cfg2.py): bit 1 skips C
 // stores, bit 2 orders tiles j-fastest, bit 3 uses default-policy stores,
-// bit 4 stops the operand refills after the prologue (stale data)
+// bit 4 stops the operand refills after the prologue (stale data), bit 6
+// keeps C on the register epilogue (no TMA store)
 int debug_flags() {
   const char* s = std::getenv("LRB_DEBUG_FLAGS");
-  return s ? (std::atoi(s) & 30) : 0;
+  return s ? (std::atoi(s) & 94) : 0;
 }
 
 int env_variant() {
@@ -345,6 +371,15 @@ lrb_status run_strided(lrb_ctx* ctx, const Gemm& g, int64_t batch, int beta_one,
   p.tiles_per_item = int(ti * tj);
   p.num_tiles = ti * tj * batch;
   p.j_fastest = (debug_flags() & 4) ? 1 : 0;
+  // C through the TMA engine when it is write-only here (beta = 0), the
+  // inner dimension is short (k <= 16: write-bound tiles, e.g. the low-rank
+  // expansion at small rank: 0.73 -> 0.83 of HBM) and C is TMA-aligned; the
+  // kernel uses it for variants whose tile fits a stage. At k = 32 (cfg2) the
+  // synchronous slot hand-back costs more than the register epilogue.
+  p.c_tma = (tma && !beta_one && g.k >= 1 && g.k <= 16 && !(debug_flags() & 64) &&
+             encode_c_map(&p.tmC, g.C, g.m, g.n, g.ldc, g.sC, batch, vm.nb))
+                ? 1
+                : 0;
   LaunchInfo info{0, 0};
   cudaError_t e = kLaunch[v](g.a_t, g.b_t, tma, &p, nullptr, beta_one | debug_flags(),
                              ctx->device, ctx->sm_count, stream, &info);

@@ -72,6 +72,11 @@ struct GemmCfg {
   // stages + full barriers + release counters + issue state
   static constexpr size_t SMEM_BYTES =
       size_t(STAGES) * STAGE_ELEMS * 8 + size_t(STAGES) * 8 + size_t(STAGES) * 4 + 32;
+  // TMA-store epilogue: the C tile is staged in the stage its last chunk just
+  // used, as MB/16 boxes of 16 rows x NB columns in the 128-byte swizzle
+  // (1024-byte aligned boxes), and written by the TMA engine
+  static constexpr bool EPI_FITS = TMA_ && (MB % 16 == 0) && (MB * NB <= STAGE_ELEMS) &&
+                                   (STAGE_ELEMS % 128 == 0) && (NB <= 256);
   static_assert(WI % 8 == 0 && WJ % 8 == 0, "warp tile must be a multiple of the 8x8 fragment");
   static_assert(KB % 4 == 0, "k chunk must be a multiple of the DMMA k (4)");
   static_assert(WARPS % 4 == 0, "warps per CTA must fill all four SM sub-partitions");
@@ -119,7 +124,8 @@ struct TileView {
   int i0, j0;
   const void* tmA;  // tensor maps (TMA path)
   const void* tmB;
-  int za, zb;  // batch coordinate inside the maps
+  const void* tmC;  // C map for the TMA-store epilogue (strided problems)
+  int za, zb, zc;   // batch coordinate inside the maps
 };
 
 // Fixed-stride batch: item i at base + i * stride (the reference's
@@ -127,6 +133,7 @@ struct TileView {
 struct StridedProblem {
   CUtensorMap tmA;  // (rows, cols, batch) maps of the stored operands
   CUtensorMap tmB;
+  CUtensorMap tmC;  // (m, n, batch) map of C, box 16 x NB, 128-B swizzle (when c_tma)
   const double* A;
   const double* B;
   double* C;
@@ -135,7 +142,10 @@ struct StridedProblem {
   int tiles_i, tiles_per_item;
   int a_batched, b_batched;  // 0 when the stride is 0 (one matrix broadcast)
   int j_fastest;             // tile order inside an item: column tiles vary fastest
+  int c_tma;                 // tmC is valid: beta = 0, k >= 1, C TMA-aligned
   int64_t num_tiles;
+
+  __device__ __forceinline__ bool tma_store() const { return c_tma != 0; }
 
   template <int MB, int NB>
   __device__ __forceinline__ TileView tile(int64_t t) const {
@@ -170,8 +180,10 @@ struct StridedProblem {
     }
     v.tmA = &tmA;
     v.tmB = &tmB;
+    v.tmC = &tmC;
     v.za = a_batched ? static_cast<int>(item) : 0;
     v.zb = b_batched ? static_cast<int>(item) : 0;
+    v.zc = static_cast<int>(item);
     return v;
   }
   __device__ __forceinline__ int tile_k(int64_t) const { return k; }
@@ -195,6 +207,8 @@ struct PtrProblem {
   const CUtensorMap* maps;  // 2 per item (A, B); null on the segment path
   int64_t num_tiles;
 
+  __device__ __forceinline__ bool tma_store() const { return false; }
+
   template <int MB, int NB>
   __device__ __forceinline__ TileView tile(int64_t t) const {
     const uint64_t e = tiles[t];
@@ -214,8 +228,10 @@ struct PtrProblem {
     v.j0 = static_cast<int>(e & 0xFFFF) * NB;
     v.tmA = maps ? &maps[2 * size_t(item)] : nullptr;
     v.tmB = maps ? &maps[2 * size_t(item) + 1] : nullptr;
+    v.tmC = nullptr;
     v.za = 0;
     v.zb = 0;
+    v.zc = 0;
     return v;
   }
   __device__ __forceinline__ int tile_k(int64_t t) const { return items[tiles[t] >> 32].k; }
@@ -375,6 +391,38 @@ __device__ __forceinline__ void mma_kstep(double (&acc)[Cfg::FJ][Cfg::FI][2], co
     for (int fi = 0; fi < Cfg::FI; ++fi) dmma_8x8x4(acc[fj][fi][0], acc[fj][fi][1], af[fj], bf[fi]);
 }
 
+// Stage a warp's accumulators as C-tile boxes for the TMA store: box q holds
+// tile rows 16q..16q+15 of all NB columns, column j a 128-byte row with its
+// 16-byte chunks XOR-swizzled by (j & 7) (CU_TENSOR_MAP_SWIZZLE_128B).
+template <class Cfg>
+__device__ __forceinline__ int c_stage_off(int i, int j) {
+  const int q = i >> 4, il = i & 15;
+  return q * 16 * Cfg::NB + j * 16 + ((((il >> 1) ^ (j & 7))) << 1) + (il & 1);
+}
+
+template <class Cfg>
+__device__ __forceinline__ void stage_c_tile(double* cs, const double (&acc)[Cfg::FJ][Cfg::FI][2],
+                                             int wi, int wj, int g, int tq) {
+#pragma unroll
+  for (int fj = 0; fj < Cfg::FJ; ++fj) {
+    const int j = Cfg::load_col(wj, fj, g);
+    if constexpr (Cfg::PAIR_I) {
+#pragma unroll
+      for (int p = 0; p < Cfg::FI / 2; ++p) {
+        const int i = Cfg::acc_row(wi, 2 * p, 0, tq);  // rows i .. i+3, i % 4 == 0
+        sts128(cs + c_stage_off<Cfg>(i, j), acc[fj][2 * p][0], acc[fj][2 * p + 1][0]);
+        sts128(cs + c_stage_off<Cfg>(i + 2, j), acc[fj][2 * p][1], acc[fj][2 * p + 1][1]);
+      }
+    } else {
+#pragma unroll
+      for (int fi = 0; fi < Cfg::FI; ++fi) {
+        const int i = Cfg::acc_row(wi, fi, 0, tq);  // rows i, i+1 (i even)
+        sts128(cs + c_stage_off<Cfg>(i, j), acc[fj][fi][0], acc[fj][fi][1]);
+      }
+    }
+  }
+}
+
 template <class Cfg, class Problem>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     lrb_gemm_kernel(const __grid_constant__ Problem prob, const int flags) {
@@ -383,6 +431,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   // uses default-policy instead of streaming stores, bit 4 stops refilling the
   // ring after the prologue (MMAs on stale data; bit 2 is host-side)
   const int beta_one = flags & 1;
+  // C leaves through the TMA engine from shared memory (strided problems with
+  // beta = 0 and a TMA-aligned C, variants whose C tile fits one stage)
+  const bool epi_tma = Cfg::EPI_FITS && prob.tma_store();
   constexpr int MB = Cfg::MB, NB = Cfg::NB, KB = Cfg::KB, STAGES = Cfg::STAGES;
   constexpr int FI = Cfg::FI, FJ = Cfg::FJ;
   // dynamic shared memory starts 1024-B aligned (no static shared memory);
@@ -478,23 +529,50 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
           }
         }
       }
-      // release the slot; the last warp out refills it with the next chunk
-      __syncwarp();
-      int last = 0;
-      if (lane == 0) {
-        // acq_rel: orders this warp's reads of the slot before the count, and
-        // lets the last warp see the issue state the previous issuer wrote
-        last = (atom_add_acq_rel_cta(&released[stage], 1) == Cfg::WARPS - 1);
-        if (last) released[stage] = 0;
+      if (epi_tma && k0 + KB >= v.k) {
+        // TMA-store epilogue: once every warp is done with the slot, stage C
+        // there (swizzled), hand it to the TMA engine, and refill the slot as
+        // soon as the engine has read it. The named barriers also order the
+        // issue state between this issuer and the previous one.
+        named_barrier_sync(1, Cfg::THREADS);
+        double* cs = smem + size_t(stage) * Cfg::STAGE_ELEMS;
+        stage_c_tile<Cfg>(cs, acc, wi, wj, g, tq);
+        fence_proxy_async_shared_cta();
+        named_barrier_sync(1, Cfg::THREADS);
+        if (warp == 0) {
+          if (lane == 0) {
+            if (!(flags & 2)) {
+#pragma unroll 1
+              for (int q = 0; q < MB / 16; ++q)
+                if (v.i0 + 16 * q < v.m)
+                  tma_store_3d(v.tmC, cs + q * 16 * NB, v.i0 + 16 * q, v.j0, v.zc);
+            }
+            bulk_commit_group();
+            bulk_wait_group_read0();
+          }
+          __syncwarp();
+          if (!(flags & 16)) issue_chunk<Cfg>(prob, smem, full, st, stage, lane);
+        }
+      } else {
+        // release the slot; the last warp out refills it with the next chunk
+        __syncwarp();
+        int last = 0;
+        if (lane == 0) {
+          // acq_rel: orders this warp's reads of the slot before the count, and
+          // lets the last warp see the issue state the previous issuer wrote
+          last = (atom_add_acq_rel_cta(&released[stage], 1) == Cfg::WARPS - 1);
+          if (last) released[stage] = 0;
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last && !(flags & 16)) issue_chunk<Cfg>(prob, smem, full, st, stage, lane);
       }
-      last = __shfl_sync(0xffffffffu, last, 0);
-      if (last && !(flags & 16)) issue_chunk<Cfg>(prob, smem, full, st, stage, lane);
       if (++stage == STAGES) {
         stage = 0;
         phase ^= 1;
       }
     }
 
+    if (epi_tma) continue;  // C was stored from shared memory at the last chunk
     // epilogue: consecutive rows of one column of C per lane — 4 rows (one
     // 32-B store) for paired fragments, else 2 rows (one 16-B store)
     if (flags & 2) continue;
@@ -536,6 +614,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
       }
     }
   }
+  // the TMA stores this CTA issued must land before the grid completes
+  if (epi_tma && threadIdx.x == 0) bulk_wait_group0();
 }
 
 // ------------------------------------------------------------------ launch

@@ -226,3 +226,19 @@ def test_graph_capture_of_pointer_plan(ctx):
     O.dgemm_ptr("C", "N", "N", ms, ns, ks, hA, ms, hB, ks, expect, ms, 0.0)
     for i in range(3):
         assert np.array_equal(dC[i].download(ms[i] * ns[i]), expect[i])
+
+
+@pytest.mark.parametrize("variant", ["q64", "n32", "n64", "m32", "s96", "n16t", None])
+@pytest.mark.parametrize("k", [4, 8, 13, 16])
+def test_tma_store_epilogue_short_k(ctx, variant, k):
+    # beta = 0 with k <= 16 stores C through the TMA engine from shared memory
+    # (variants whose C tile fits a stage): ragged tiles, even/odd m (odd m
+    # keeps the register epilogue), padded ld and item gaps that must stay
+    # NaN, every op combination, row-major too
+    for m, n in ((70, 45), (130, 96), (41, 19)):
+        for ops in OPS:
+            for pad, spad in (((0, 0, 0), (0, 0, 0)), ((2, 4, 6), (2, 2, 4))):
+                c = Case("C", ops[0], ops[1], m, n, k, 3, pad=pad, spad=spad, seed=m + k)
+                c.check(c.run_device(ctx, variant=variant))
+    r = Case("R", "N", "N", 64, 48, k, 2, seed=k)
+    r.check(r.run_device(ctx, variant=variant))
