@@ -26,7 +26,9 @@
 //   * Each warp owns a WI x WJ sub-tile of C in registers as DMMA 8x8x4
 //     fragments. The MMA computes C^T = op(B)^T op(A)^T so a lane's
 //     accumulator pair is two consecutive ROWS of column-major C: the
-//     epilogue is one 16-byte store per pair.
+//     epilogue is one 16-byte (32-byte for paired fragments) store per lane
+//     and column. Write-bound strided tiles (beta = 0, k <= 16) instead stage
+//     C in the consumed stage and leave through TMA stores (stage_c_tile).
 //   * k is consumed in ascending order, 4 at a time by DMMA (each entry an
 //     in-order FMA chain, probed bitwise on B200) and a scalar fma() tail, so
 //     every C entry is exactly the reference's FMA chain.

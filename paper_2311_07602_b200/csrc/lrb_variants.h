@@ -2,9 +2,10 @@
 // the per-variant instantiation units (device).
 //
 // A variant fixes the CTA tile of C (column-major view): MB = WARPS_I * WI rows
-// by NB = WARPS_J * WJ columns, computed by WARPS_I * WARPS_J consumer warps
-// (warp tile WI rows x WJ columns, DMMA 8x8x4 fragments) fed by one TMA
-// producer warp through a STAGES-deep shared-memory ring of KB-wide k chunks.
+// by NB = WARPS_J * WJ columns, computed by WARPS_I * WARPS_J warps (warp tile
+// WI rows x WJ columns, DMMA 8x8x4 fragments) fed through a STAGES-deep
+// shared-memory ring of KB-wide k chunks that the warps refill themselves
+// (lrb_gemm.cuh), MINB CTAs per SM.
 //
 //   n*  : tall-skinny C (dense b x b times a b x r basis, r <= 64): the BLR
 //         diagonal shape (reference blr.hpp:149-153) in column-major — HBM
