@@ -198,8 +198,12 @@ int auto_variant(int64_t m, int64_t n, int64_t k_hint, int64_t batch, int sm_cou
     return LRB_V_N64;
   }
   if (m <= 64 && m < n) {
-    // the same wave argument for short-wide C (BLR matvec: 64 row tiles of
-    // nrhs x block): 32-column tiles at five CTAs per SM
+    // short-wide C with a long inner dimension (the reference's row-major
+    // drop-in, the BLR matvec steps): the big operand is contiguous along k,
+    // so 64-deep chunks (512-byte TMA segments) over 64-column tiles
+    if (m <= 16 && k_hint >= 64) return m <= 8 ? LRB_V_M8K64 : LRB_V_M16K64;
+    // the same wave argument as for tall-skinny C: 32-column tiles at five
+    // CTAs per SM for small batches
     if (m <= 16 && batch > 0 && batch * ((n + 127) / 128) < 2LL * 2 * sm_count)
       return m <= 8 ? LRB_V_M8T : LRB_V_M16T;
     if (m <= 8) return LRB_V_M8;

@@ -69,7 +69,8 @@ def test_no_device_here_fails_loudly():
 @pytest.mark.parametrize("m,n,k,want", [
     (256, 16, 256, "n16"), (512, 512, 32, "q64"), (512, 32, 512, "n32"), (1024, 8, 1024, "n8"),
     (2048, 64, 2048, "n64"), (512, 24, 512, "n24"), (512, 40, 512, "n40"), (512, 48, 512, "n48"),
-    (512, 56, 512, "n56"), (16, 512, 512, "m16"), (8, 300, 7, "m8"), (64, 200, 64, "m64"),
+    (512, 56, 512, "n56"), (16, 512, 512, "m16k64"), (16, 512, 32, "m16"), (8, 300, 7, "m8"),
+    (8, 300, 300, "m8k64"), (64, 200, 64, "m64"),
 ])
 def test_selector_by_shape(m, n, k, want):
     batch = 100000
@@ -82,10 +83,18 @@ def test_selector_small_skinny_batches_use_short_tiles():
     # cfg1: 256 items of 256 x 16 -> fewer than two waves of 128-row tiles
     assert P.select("C", "N", "N", 256, 16, 256, 256)["name"] == "n16t"
     assert P.select("C", "N", "N", 256, 16, 256, 100000)["name"] == "n16"
-    # BLR matvec launches (64 row tiles, nrhs x block outputs): 32-column tiles
-    assert P.select("R", "N", "N", 512, 8, 504, 64)["name"] == "m8t"
-    assert P.select("R", "N", "N", 256, 16, 1008, 64)["name"] == "m16t"
-    assert P.select("R", "N", "N", 256, 16, 1008, 100000)["name"] == "m16"
+    # short-wide C with a short k and a small batch: 32-column tiles
+    assert P.select("R", "N", "N", 512, 8, 32, 64)["name"] == "m8t"
+    assert P.select("R", "N", "N", 256, 16, 48, 64)["name"] == "m16t"
+    assert P.select("R", "N", "N", 256, 16, 48, 100000)["name"] == "m16"
+
+
+def test_selector_row_major_long_k_uses_k64_tiles():
+    # the row-major drop-in's big block is contiguous along k: 64-deep chunks
+    assert P.select("R", "N", "N", 512, 8, 504, 64)["name"] == "m8k64"
+    assert P.select("R", "N", "N", 256, 16, 1008, 64)["name"] == "m16k64"
+    assert P.select("R", "N", "N", 1024, 16, 1024, 10000)["name"] == "m16k64"
+    assert P.select("R", "N", "N", 512, 32, 512, 10000)["name"] == "m32"
 
 
 def test_selector_long_k_general_shapes_use_t64():
@@ -109,8 +118,8 @@ def test_selector_row_major_swaps_roles():
     # row-major C (m x n) is column-major C^T (n x m): the reference's BLR
     # diagonal step D(b x b) * rhs(b x r) lands on the short-wide m-variants
     s = P.select("R", "N", "N", 1024, 16, 1024, 10000)
-    assert s["name"] == "m16"
-    assert P.select("R", "N", "N", 1024, 16, 1024, 4)["name"] == "m16t"  # < two waves
+    assert s["name"] == "m16k64"
+    assert P.select("R", "N", "N", 1024, 16, 32, 4)["name"] == "m16t"  # short k, < two waves
 
 
 def test_selector_intensity_and_bound():
