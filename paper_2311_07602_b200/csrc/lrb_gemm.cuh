@@ -256,7 +256,7 @@ __device__ __forceinline__ int64_t skip_empty_tiles(const Problem& prob, int64_t
 // Issue the chunk described by *st into `stage` (whole warp), then advance *st.
 template <class Cfg, class Problem>
 __device__ __forceinline__ void issue_chunk(const Problem& prob, double* smem, uint64_t* full,
-                                            IssueState* st, int stage, int lane) {
+                                            IssueState* st, int stage, int lane, int flags) {
   constexpr int MB = Cfg::MB, NB = Cfg::NB, KB = Cfg::KB;
   // lane 0 (which synchronised with the previous issuer through the release
   // counter) reads the shared state and broadcasts it
@@ -276,9 +276,16 @@ __device__ __forceinline__ void issue_chunk(const Problem& prob, double* smem, u
   fence_proxy_async_smem();
   if constexpr (Cfg::TMA) {
     if (lane == 0) {
-      // A is streamed once when one column tile covers C; B once when one row tile does
-      const uint64_t pol_a = (v.n <= NB) ? policy_evict_first() : policy_evict_last();
-      const uint64_t pol_b = (v.m <= MB) ? policy_evict_first() : policy_evict_last();
+      // A is streamed once when one column tile covers C; B once when one row tile does.
+      // A k-contiguous box (A_T for A, !B_T for B) reads kPad k-rows of the
+      // next chunk as its pitch pad: those must survive in L2 until that
+      // chunk's load, so such streams are not marked evict-first
+      const uint64_t pol_a = (v.n <= NB) ? ((Cfg::A_T && !(flags & 128)) ? policy_evict_normal()
+                                                                        : policy_evict_first())
+                                         : policy_evict_last();
+      const uint64_t pol_b = (v.m <= MB) ? ((!Cfg::B_T && !(flags & 128)) ? policy_evict_normal()
+                                                                         : policy_evict_first())
+                                         : policy_evict_last();
       mbar_arrive_expect_tx(&full[stage], uint32_t(Cfg::A_BOX + Cfg::B_BOX) * 8u);
       if (Cfg::A_T)
         tma_load_3d(As, v.tmA, k0, v.i0, v.za, &full[stage], pol_a);
@@ -461,7 +468,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   __syncthreads();
   if (warp == 0) {
 #pragma unroll 1
-    for (int s = 0; s < STAGES; ++s) issue_chunk<Cfg>(prob, smem, full, st, s, lane);
+    for (int s = 0; s < STAGES; ++s) issue_chunk<Cfg>(prob, smem, full, st, s, lane, flags);
   }
 
   const int wi = warp % Cfg::WARPS_I;
@@ -553,7 +560,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
             bulk_wait_group_read0();
           }
           __syncwarp();
-          if (!(flags & 16)) issue_chunk<Cfg>(prob, smem, full, st, stage, lane);
+          if (!(flags & 16)) issue_chunk<Cfg>(prob, smem, full, st, stage, lane, flags);
         }
       } else {
         // release the slot; the last warp out refills it with the next chunk
@@ -566,7 +573,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
           if (last) released[stage] = 0;
         }
         last = __shfl_sync(0xffffffffu, last, 0);
-        if (last && !(flags & 16)) issue_chunk<Cfg>(prob, smem, full, st, stage, lane);
+        if (last && !(flags & 16)) issue_chunk<Cfg>(prob, smem, full, st, stage, lane, flags);
       }
       if (++stage == STAGES) {
         stage = 0;
