@@ -86,11 +86,16 @@ __device__ __forceinline__ void lr_issue(const LrProblem& p, double* smem, uint6
     double* av = smem + size_t(stage) * Cf::STAGE;
     double* bu = av + Cf::AV_ELEMS;
     fence_proxy_async_smem();
-    const uint64_t pol = policy_evict_first();  // A_Vt and B_U are read exactly once
+    // A_Vt and B_U are read once, but A_Vt's box is k-contiguous: its pitch
+    // pad reads the next chunk's first k-columns, which must stay in L2
+    // (measured: r = 16/32 rows +3-6%; r = 8, where the pad is 1/9 of the
+    // box and the ring is 4 deep, stays evict-first)
+    const uint64_t pol_av = (Cf::F >= 2) ? policy_evict_normal() : policy_evict_first();
+    const uint64_t pol_bu = policy_evict_first();
     mbar_arrive_expect_tx(&full[stage], uint32_t(Cf::AV + Cf::BU) * Cf::G * 8u);
     const int z = static_cast<int>(t * Cf::G);
-    tma_load_3d(av, &p.tmAV, k0, 0, z, &full[stage], pol);
-    tma_load_3d(bu, &p.tmBU, 0, k0, z, &full[stage], pol);
+    tma_load_3d(av, &p.tmAV, k0, 0, z, &full[stage], pol_av);
+    tma_load_3d(bu, &p.tmBU, 0, k0, z, &full[stage], pol_bu);
     int nk0 = k0 + Cf::KB;
     int64_t nt = t;
     if (nk0 >= p.block) {
