@@ -232,11 +232,10 @@ int auto_variant(int64_t m, int64_t n, int64_t k_hint, int64_t batch, int sm_cou
 // debug-only kernel flags for probes (tools/probe_cfg2.py): bit 1 skips C
 // stores, bit 2 orders tiles j-fastest, bit 3 uses default-policy stores,
 // bit 4 stops the operand refills after the prologue (stale data), bit 6
-// keeps C on the register epilogue (no TMA store), bit 7 restores evict-first
-// for k-contiguous single-use operand streams
+// keeps C on the register epilogue (no TMA store)
 int debug_flags() {
   const char* s = std::getenv("LRB_DEBUG_FLAGS");
-  return s ? (std::atoi(s) & 222) : 0;
+  return s ? (std::atoi(s) & 94) : 0;
 }
 
 int env_variant() {
