@@ -214,48 +214,57 @@ __global__ void __launch_bounds__(LrCfg<R>::THREADS, 2)
     for (int a = 0; a < F; ++a)
 #pragma unroll
       for (int b = 0; b < F; ++b) e[a][b][0] = e[a][b][1] = 0.0;
+    // k-blocks (fm, h) ascending outermost: each A_X value is loaded once and
+    // every accumulator still receives its DMMAs in ascending m order
 #pragma unroll
-    for (int fn = 0; fn < F; ++fn)
+    for (int fm = 0; fm < F; ++fm)
 #pragma unroll
-      for (int fm = 0; fm < F; ++fm)
+      for (int h = 0; h < 2; ++h) {
+        const int src = g * 4 + 2 * h + (tq >> 1);
+        const int mcol = fm * 8 + 4 * h + tq;  // m
+        double a[F];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int src = g * 4 + 2 * h + (tq >> 1);
+        for (int fx = 0; fx < F; ++fx) {
+          const int x = fx * 8 + g;
+          a[fx] = (x < r && mcol < r) ? __ldg(ax + x * r + mcol) : 0.0;  // A_X[x][m]
+        }
+#pragma unroll
+        for (int fn = 0; fn < F; ++fn) {
           const double v0 = __shfl_sync(0xffffffffu, acc[fn][fm][0], src);
           const double v1 = __shfl_sync(0xffffffffu, acc[fn][fm][1], src);
           const double cb = (tq & 1) ? v1 : v0;  // B-operand C[m0 + tq][fn*8 + g]
-          const int mcol = fm * 8 + 4 * h + tq;  // m
 #pragma unroll
-          for (int fx = 0; fx < F; ++fx) {
-            const int x = fx * 8 + g;
-            const double a = (x < r && mcol < r) ? __ldg(ax + x * r + mcol) : 0.0;  // A_X[x][m]
-            dmma_8x8x4(e[fx][fn][0], e[fx][fn][1], a, cb);
-          }
+          for (int fx = 0; fx < F; ++fx) dmma_8x8x4(e[fx][fn][0], e[fx][fn][1], a[fx], cb);
         }
+      }
     // ---- G = E B_X:  o[fx][fy][c] = G[x = fx*8 + g][y = fy*8 + 2tq + c]
     double o[F][F][2];
 #pragma unroll
     for (int a = 0; a < F; ++a)
 #pragma unroll
       for (int b = 0; b < F; ++b) o[a][b][0] = o[a][b][1] = 0.0;
+    // k-blocks (fn, h) ascending outermost: each B_X value is loaded once
 #pragma unroll
-    for (int fx = 0; fx < F; ++fx)
+    for (int fn = 0; fn < F; ++fn)
 #pragma unroll
-      for (int fn = 0; fn < F; ++fn)
+      for (int h = 0; h < 2; ++h) {
+        const int src = g * 4 + 2 * h + (tq >> 1);
+        const int nrow = fn * 8 + 4 * h + tq;  // n
+        double b[F];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int src = g * 4 + 2 * h + (tq >> 1);
+        for (int fy = 0; fy < F; ++fy) {
+          const int y = fy * 8 + g;
+          b[fy] = (nrow < r && y < r) ? __ldg(bx + nrow * r + y) : 0.0;  // B_X[n][y]
+        }
+#pragma unroll
+        for (int fx = 0; fx < F; ++fx) {
           const double v0 = __shfl_sync(0xffffffffu, e[fx][fn][0], src);
           const double v1 = __shfl_sync(0xffffffffu, e[fx][fn][1], src);
           const double ea = (tq & 1) ? v1 : v0;  // A-operand E[fx*8 + g][n0 + tq]
-          const int nrow = fn * 8 + 4 * h + tq;  // n
 #pragma unroll
-          for (int fy = 0; fy < F; ++fy) {
-            const int y = fy * 8 + g;
-            const double b = (nrow < r && y < r) ? __ldg(bx + nrow * r + y) : 0.0;  // B_X[n][y]
-            dmma_8x8x4(o[fx][fy][0], o[fx][fy][1], ea, b);
-          }
+          for (int fy = 0; fy < F; ++fy) dmma_8x8x4(o[fx][fy][0], o[fx][fy][1], ea, b[fy]);
         }
+      }
     // ---- store G once (row-major r x r)
     double* gp = p.g + item * int64_t(r) * r;
     const bool vec = ((r & 1) == 0) && ((reinterpret_cast<uintptr_t>(gp) & 15) == 0);
