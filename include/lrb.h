@@ -76,6 +76,9 @@ int lrb_ctx_device(const lrb_ctx* ctx);
 int lrb_ctx_sm_count(const lrb_ctx* ctx);
 /* number of kernels this context has launched so far (GEMM + fill + flush) */
 uint64_t lrb_launch_count(const lrb_ctx* ctx);
+/* the kernel (variant id, lrb_variant_name) that served this context's last
+   strided GEMM, -1 before the first one */
+int lrb_last_variant(const lrb_ctx* ctx);
 
 /* ------------------------------------------------ memory / stream helpers */
 lrb_status lrb_malloc(lrb_ctx* ctx, size_t bytes, void** dptr);

@@ -58,6 +58,7 @@ SIGNATURES = {
     "lrb_ctx_device": (C.c_int, [vp]),
     "lrb_ctx_sm_count": (C.c_int, [vp]),
     "lrb_launch_count": (u64, [vp]),
+    "lrb_last_variant": (C.c_int, [vp]),
     "lrb_malloc": (C.c_int, [vp, C.c_size_t, P(vp)]),
     "lrb_free": (C.c_int, [vp, vp]),
     "lrb_host_alloc": (C.c_int, [vp, C.c_size_t, P(vp)]),

@@ -18,6 +18,7 @@
 
 #include "lrb_dispatch.cuh"
 #include "lrb_internal.h"
+#include "lrb_panel.h"
 
 // ===================================================================== errors
 namespace {
@@ -72,8 +73,17 @@ struct VariantMeta {
    VariantTraits<id>::Cfg<false, false, true>::NB, VariantTraits<id>::Cfg<false, false, true>::KB,      \
    VariantTraits<id>::Cfg<false, false, true>::STAGES, VariantTraits<id>::Cfg<false, false, true>::THREADS, \
    VariantTraits<id>::Cfg<false, false, true>::MINB, VariantTraits<id>::Cfg<false, false, true>::SMEM_BYTES},
-static const VariantMeta kVariants[LRB_NUM_VARIANTS] = {LRB_VARIANT_LIST(LRB_X)};
+// the row-panel kernel (lrb_panel.cu) follows the tile variants: id
+// LRB_NUM_VARIANTS, name "p256" (256-row units, 32-column chunks)
+constexpr int kPanelVariant = LRB_NUM_VARIANTS;
+constexpr int kNumKernels = LRB_NUM_VARIANTS + 1;
+static const VariantMeta kVariants[kNumKernels] = {
+    LRB_VARIANT_LIST(LRB_X){"p256", kPanelRows, kPanelCols, kPanelKMax, kPanelStages, panel_threads(), 1,
+                            panel_smem_bytes()}};
 #undef LRB_X
+// the panel kernel's TMA boxes: 128-row half panels (+4 pad) and 32-column
+// chunks (+4 pad), both 32 deep in k
+static const VariantMeta kPanelBoxes = {"p256", kPanelRows / 2, kPanelCols, kPanelKMax, 0, 0, 0, 0};
 
 #define LRB_X(id, ...) &launch_variant<id>,
 static const LaunchFn kLaunch[LRB_NUM_VARIANTS] = {LRB_VARIANT_LIST(LRB_X)};
@@ -232,10 +242,12 @@ int auto_variant(int64_t m, int64_t n, int64_t k_hint, int64_t batch, int sm_cou
 // debug-only kernel flags for probes (tools/probe_cfg2.py): bit 1 skips C
 // stores, bit 2 orders tiles j-fastest, bit 3 uses default-policy stores,
 // bit 4 stops the operand refills after the prologue (stale data), bit 6
-// keeps C on the register epilogue (no TMA store)
+// keeps C on the register epilogue (no TMA store), bit 5 / bit 7 load every
+// operand box evict-normal / evict-first, bit 8 makes the panel kernel's MMA
+// groups take turns on the tensor pipe (ping-pong)
 int debug_flags() {
   const char* s = std::getenv("LRB_DEBUG_FLAGS");
-  return s ? (std::atoi(s) & 94) : 0;
+  return s ? (std::atoi(s) & 510) : 0;
 }
 
 int env_variant() {
@@ -244,11 +256,28 @@ int env_variant() {
   return lrb_variant_from_name(s);
 }
 
-int choose_variant(const lrb_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t batch) {
+// the caller's forced kernel (context override, else LRB_VARIANT), or -1
+int forced_variant(const lrb_ctx* ctx) {
   if (ctx && ctx->variant_override >= 0) return ctx->variant_override;
-  int v = env_variant();
-  if (v >= 0) return v;
+  return env_variant();
+}
+
+// a tile variant for the general kernel (the panel kernel, when forced, falls
+// back to the automatic tile choice on paths it does not serve)
+int choose_variant(const lrb_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t batch) {
+  const int v = forced_variant(ctx);
+  if (v >= 0 && v != kPanelVariant) return v;
   return auto_variant(m, n, k, batch, ctx ? ctx->sm_count : 148);
+}
+
+// The row-panel kernel serves strided products whose column-major view has
+// op(A) = N and 1 <= k <= 32 (the U panel must fit shared memory). The
+// automatic choice takes it where 256-row units fill the rows and at least
+// one wave of units exists (cfg2 and the low-rank expansions).
+bool panel_serves(int a_t, int64_t k) { return !a_t && k >= 1 && k <= kPanelKMax; }
+bool panel_auto(int64_t m, int64_t n, int64_t batch, int sm_count) {
+  const int64_t units = (m + kPanelRows - 1) / kPanelRows * batch;
+  return m >= 192 && n >= 128 && units >= sm_count;
 }
 
 // ============================================================ normalisation
@@ -342,10 +371,56 @@ Gemm normalize(char order, char opA, char opB, int64_t m, int64_t n, int64_t k, 
   return g;
 }
 
+// Launch the row-panel kernel; false (nothing launched) when the operands are
+// not TMA-eligible.
+bool run_panel(lrb_ctx* ctx, const Gemm& g, int64_t batch, int beta_one, cudaStream_t stream,
+               lrb_status* status) {
+  StridedProblem p;
+  std::memset(&p, 0, sizeof(p));
+  if (loader_mode(ctx) != 1) return false;
+  if (!encode_pair(kPanelBoxes, 0, g.b_t, g.m, g.n, g.k, g.A, g.lda, g.sA, g.B, g.ldb, g.sB, batch,
+                   &p.tmA, &p.tmB, &p.a_batched, &p.b_batched))
+    return false;
+  p.A = g.A;
+  p.B = g.B;
+  p.C = g.C;
+  p.lda = g.lda;
+  p.ldb = g.ldb;
+  p.ldc = g.ldc;
+  p.sA = g.sA;
+  p.sB = g.sB;
+  p.sC = g.sC;
+  p.m = int(g.m);
+  p.n = int(g.n);
+  p.k = int(g.k);
+  p.num_tiles = (g.m + kPanelRows - 1) / kPanelRows * batch;  // units
+  const int flags = beta_one | debug_flags();
+  int64_t grid = 0;
+  cudaError_t e =
+      launch_panel(g.b_t, (flags & 256) ? 1 : 0, p, flags, ctx->sm_count, stream, &grid);
+  if (e != cudaSuccess) {
+    *status = cuda_fail(ctx, e, "lrb_panel_kernel launch");
+    return true;
+  }
+  if (grid > 0) ctx->launches.fetch_add(1, std::memory_order_relaxed);
+  *status = LRB_OK;
+  return true;
+}
+
 lrb_status run_strided(lrb_ctx* ctx, const Gemm& g, int64_t batch, int beta_one,
                        cudaStream_t stream, int* variant_used) {
   if (batch == 0 || g.m == 0 || g.n == 0) return LRB_OK;
   if (g.k == 0 && beta_one) return LRB_OK;  // C = C
+  const int forced = forced_variant(ctx);
+  if (panel_serves(g.a_t, g.k) &&
+      (forced == kPanelVariant || (forced < 0 && panel_auto(g.m, g.n, batch, ctx->sm_count)))) {
+    lrb_status st = LRB_OK;
+    if (run_panel(ctx, g, batch, beta_one, stream, &st)) {
+      if (st == LRB_OK) ctx->last_variant = kPanelVariant;
+      if (st == LRB_OK && variant_used) *variant_used = kPanelVariant;
+      return st;
+    }
+  }
   const int v = choose_variant(ctx, g.m, g.n, g.k, batch);
   const VariantMeta& vm = kVariants[v];
   const int64_t ti = (g.m + vm.mb - 1) / vm.mb, tj = (g.n + vm.nb - 1) / vm.nb;
@@ -389,6 +464,7 @@ lrb_status run_strided(lrb_ctx* ctx, const Gemm& g, int64_t batch, int beta_one,
                              ctx->device, ctx->sm_count, stream, &info);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "lrb_gemm_kernel launch");
   if (info.grid > 0) ctx->launches.fetch_add(1, std::memory_order_relaxed);
+  ctx->last_variant = v;
   if (variant_used) *variant_used = v;
   return LRB_OK;
 }
@@ -511,6 +587,7 @@ extern "C" const char* lrb_last_error(const lrb_ctx* ctx) {
 extern "C" int lrb_ctx_device(const lrb_ctx* ctx) { return ctx ? ctx->device : -1; }
 extern "C" int lrb_ctx_sm_count(const lrb_ctx* ctx) { return ctx ? ctx->sm_count : 0; }
 extern "C" uint64_t lrb_launch_count(const lrb_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
+extern "C" int lrb_last_variant(const lrb_ctx* ctx) { return ctx ? ctx->last_variant : -1; }
 
 // ===================================================== context workspace
 namespace lrb {
@@ -696,19 +773,19 @@ extern "C" lrb_status lrb_l2_flush(lrb_ctx* ctx, void* stream) {
 }
 
 // ============================================================ selector / planner
-extern "C" int lrb_variant_count(void) { return LRB_NUM_VARIANTS; }
+extern "C" int lrb_variant_count(void) { return kNumKernels; }
 extern "C" const char* lrb_variant_name(int v) {
-  return (v >= 0 && v < LRB_NUM_VARIANTS) ? kVariants[v].name : nullptr;
+  return (v >= 0 && v < kNumKernels) ? kVariants[v].name : nullptr;
 }
 extern "C" int lrb_variant_from_name(const char* name) {
   if (!name) return -1;
-  for (int v = 0; v < LRB_NUM_VARIANTS; ++v)
+  for (int v = 0; v < kNumKernels; ++v)
     if (std::strcmp(name, kVariants[v].name) == 0) return v;
   return -1;
 }
 extern "C" lrb_status lrb_set_variant_override(lrb_ctx* ctx, int variant) {
   if (!ctx) return fail(nullptr, LRB_ERR_ARG, "lrb_set_variant_override: null ctx");
-  if (variant < -1 || variant >= LRB_NUM_VARIANTS)
+  if (variant < -1 || variant >= kNumKernels)
     return fail(ctx, LRB_ERR_ARG, "lrb_set_variant_override: variant %d out of range", variant);
   ctx->variant_override = variant;
   return LRB_OK;
@@ -738,7 +815,13 @@ extern "C" lrb_status lrb_select(const lrb_ctx* ctx, char order, char opA, char 
   if (m < 0 || n < 0 || k < 0 || batch < 0)
     return fail(mctx, LRB_ERR_SHAPE, "lrb_select: negative dimension");
   const int64_t cm = row_major(order) ? n : m, cn = row_major(order) ? m : n;
-  const int v = choose_variant(ctx, cm, cn, k, batch);
+  const int a_t = trans(row_major(order) ? opB : opA) ? 1 : 0;
+  const int forced = forced_variant(ctx);
+  // (the panel kernel additionally needs TMA-eligible operands at run time)
+  const bool panel = panel_serves(a_t, k) &&
+                     (forced == kPanelVariant ||
+                      (forced < 0 && panel_auto(cm, cn, batch, ctx ? ctx->sm_count : 148)));
+  const int v = panel ? kPanelVariant : choose_variant(ctx, cm, cn, k, batch);
   const VariantMeta& vm = kVariants[v];
   std::memset(out, 0, sizeof(*out));
   out->variant = v;
@@ -751,7 +834,7 @@ extern "C" lrb_status lrb_select(const lrb_ctx* ctx, char order, char opA, char 
   const int64_t ti = cm ? (cm + vm.mb - 1) / vm.mb : 0, tj = cn ? (cn + vm.nb - 1) / vm.nb : 0;
   out->tiles = ti * tj * batch;
   const int64_t sms = ctx ? ctx->sm_count : 148;
-  out->grid = std::min<int64_t>(out->tiles, sms * vm.minb);
+  out->grid = std::min<int64_t>(panel ? ti * batch : out->tiles, sms * vm.minb);
   const double bytes = lrb_item_bytes(m, n, k, 0.0);
   out->intensity = bytes > 0 ? lrb_item_flops(m, n, k) / bytes : 0.0;
   out->fp64_bound = out->intensity >= kFp64PeakFlops / kHbmBytesPerS ? 1 : 0;

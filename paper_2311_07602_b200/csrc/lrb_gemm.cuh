@@ -81,7 +81,6 @@ struct GemmCfg {
                                    (STAGE_ELEMS % 128 == 0) && (NB <= 256);
   static_assert(WI % 8 == 0 && WJ % 8 == 0, "warp tile must be a multiple of the 8x8 fragment");
   static_assert(KB % 4 == 0, "k chunk must be a multiple of the DMMA k (4)");
-  static_assert(WARPS % 4 == 0, "warps per CTA must fill all four SM sub-partitions");
   static_assert(A_BOX_IN <= 256 && A_BOX_OUT <= 256 && B_BOX_IN <= 256 && B_BOX_OUT <= 256,
                 "TMA box dimensions are limited to 256");
 
@@ -283,8 +282,10 @@ __device__ __forceinline__ void issue_chunk(const Problem& prob, double* smem, u
       // k-columns (k-contiguous boxes) or the neighbouring tile's first rows —
       // which must still be in L2 when that chunk or tile is loaded (measured:
       // r = 8/16 sweeps 0.87-0.99 -> 0.95-1.04 of HBM)
-      const uint64_t pol_a = (v.n <= NB) ? policy_evict_normal() : policy_evict_last();
-      const uint64_t pol_b = (v.m <= MB) ? policy_evict_normal() : policy_evict_last();
+      uint64_t pol_a = (v.n <= NB) ? policy_evict_normal() : policy_evict_last();
+      uint64_t pol_b = (v.m <= MB) ? policy_evict_normal() : policy_evict_last();
+      if (flags & 32) pol_a = pol_b = policy_evict_normal();  // debug probes
+      if (flags & 128) pol_a = pol_b = policy_evict_first();
       mbar_arrive_expect_tx(&full[stage], uint32_t(Cfg::A_BOX + Cfg::B_BOX) * 8u);
       if (Cfg::A_T)
         tma_load_3d(As, v.tmA, k0, v.i0, v.za, &full[stage], pol_a);
@@ -434,6 +435,7 @@ __device__ __forceinline__ void stage_c_tile(double* cs, const double (&acc)[Cfg
 template <class Cfg, class Problem>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     lrb_gemm_kernel(const __grid_constant__ Problem prob, const int flags) {
+  static_assert(Cfg::WARPS % 4 == 0, "warps per CTA must fill all four SM sub-partitions");
   // flags bit 0: beta = 1 (accumulate into C); debug probes (LRB_DEBUG_FLAGS,
   // never set by the library itself): bit 1 skips the epilogue stores, bit 3
   // uses default-policy instead of streaming stores, bit 4 stops refilling the

@@ -17,6 +17,7 @@ struct lrb_ctx {
   int sm_count = 148;
   size_t l2_bytes = 0;
   int variant_override = -1;
+  int last_variant = -1;  // kernel of the last strided GEMM (lrb_last_variant)
   int loader_override = -1;  // -1 auto, 0 segment copies, 1 TMA tensor maps (when eligible)
   std::string err;
   std::atomic<uint64_t> launches{0};

@@ -363,6 +363,12 @@ class Context:
     def launch_count(self) -> int:
         return int(lib.lrb_launch_count(self._h))
 
+    @property
+    def last_variant(self) -> Optional[str]:
+        """name of the kernel that served the last strided GEMM on this context"""
+        v = int(lib.lrb_last_variant(self._h))
+        return None if v < 0 else lib.lrb_variant_name(v).decode()
+
     def mem_info(self):
         f, t = C.c_size_t(), C.c_size_t()
         _check(lib.lrb_mem_info(self._h, C.byref(f), C.byref(t)), self._h)
