@@ -508,7 +508,8 @@ def run_gpu_arm(args, w, world, rank, local, pg):
     tr = traffic_from_profiles(w.name)
     roof["traffic"] = tr.get("dram_bytes_per_launch") if isinstance(tr, dict) else None
     roof["algorithmic"] = w.item_bytes() * launch_items
-    roof["kernel"] = f"lrb_gemm_kernel<{sel['name']}>"
+    roof["kernel"] = ("lrb_panel_kernel<p256>" if sel["name"] == "p256" else
+                      f"lrb_gemm_kernel<{sel['name']}>")
     roof["kernel_ms"] = round(per_launch_ms, 4)
     roof["roofline_frac"] = round(
         (w.item_flops() * launch_items / (per_launch_ms * 1e-3)) /

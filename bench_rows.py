@@ -433,12 +433,17 @@ def run_expand_gpu(args, w, world, rank, local, pg, B):
         ctx.synchronize()
         step = lambda: BL.lowrank_expand_device(ctx, n, m, m, r, *bufs, out, stream=s)  # noqa
         fl, by = w.flops(), w.bytes()
-        kernel = "lrb_gemm_kernel x2 (UX, then (UX) Vt on q64)"
+        kernel = None  # named after a step: the kernel that served (UX) Vt
     ms_rank, launches, clocks = _timed(ctx, s, step, args.steps, args.warmup, pg, B,
                                        B.ClockSampler(local))
     ms_step = B.all_max(pg, ms_rank) / args.steps
     fl_all, by_all = B.all_sum(pg, fl), B.all_sum(pg, by)
     roof = _roof(fl, by, ms_rank / args.steps, hbm, fp64, fsrc, hsrc, w.name)
+    if kernel is None:
+        v = ctx.last_variant
+        kernel = ("lrb_gemm_kernel<q64> (UX), then " +
+                  ("lrb_panel_kernel<p256>" if v == "p256" else f"lrb_gemm_kernel<{v}>") +
+                  " ((UX) Vt)")
     roof["kernel"] = kernel
     roof["kernel_ms"] = round(ms_rank / max(1, launches), 4)
     e2e = None

@@ -243,11 +243,10 @@ int auto_variant(int64_t m, int64_t n, int64_t k_hint, int64_t batch, int sm_cou
 // stores, bit 2 orders tiles j-fastest, bit 3 uses default-policy stores,
 // bit 4 stops the operand refills after the prologue (stale data), bit 6
 // keeps C on the register epilogue (no TMA store), bit 5 / bit 7 load every
-// operand box evict-normal / evict-first, bit 8 makes the panel kernel's MMA
-// groups take turns on the tensor pipe (ping-pong)
+// operand box evict-normal / evict-first
 int debug_flags() {
   const char* s = std::getenv("LRB_DEBUG_FLAGS");
-  return s ? (std::atoi(s) & 510) : 0;
+  return s ? (std::atoi(s) & 254) : 0;
 }
 
 int env_variant() {
@@ -272,12 +271,14 @@ int choose_variant(const lrb_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t 
 
 // The row-panel kernel serves strided products whose column-major view has
 // op(A) = N and 1 <= k <= 32 (the U panel must fit shared memory). The
-// automatic choice takes it where 256-row units fill the rows and at least
-// one wave of units exists (cfg2 and the low-rank expansions).
+// automatic choice takes it where 256-row units fill the rows, at least one
+// wave of units exists, and k > 16: cfg2 0.79 -> 0.91 of FP64 peak, the
+// rank-32 expansion 0.73 -> 0.82. At k <= 16 the product is write-bound and
+// the tile kernel's TMA-store epilogue wins (rank-8 expansion 0.78 vs 0.74).
 bool panel_serves(int a_t, int64_t k) { return !a_t && k >= 1 && k <= kPanelKMax; }
-bool panel_auto(int64_t m, int64_t n, int64_t batch, int sm_count) {
+bool panel_auto(int64_t m, int64_t n, int64_t k, int64_t batch, int sm_count) {
   const int64_t units = (m + kPanelRows - 1) / kPanelRows * batch;
-  return m >= 192 && n >= 128 && units >= sm_count;
+  return m >= 192 && n >= 128 && k > 16 && units >= sm_count;
 }
 
 // ============================================================ normalisation
@@ -397,7 +398,7 @@ bool run_panel(lrb_ctx* ctx, const Gemm& g, int64_t batch, int beta_one, cudaStr
   const int flags = beta_one | debug_flags();
   int64_t grid = 0;
   cudaError_t e =
-      launch_panel(g.b_t, (flags & 256) ? 1 : 0, p, flags, ctx->sm_count, stream, &grid);
+      launch_panel(g.b_t, p, flags, ctx->sm_count, stream, &grid);
   if (e != cudaSuccess) {
     *status = cuda_fail(ctx, e, "lrb_panel_kernel launch");
     return true;
@@ -413,7 +414,7 @@ lrb_status run_strided(lrb_ctx* ctx, const Gemm& g, int64_t batch, int beta_one,
   if (g.k == 0 && beta_one) return LRB_OK;  // C = C
   const int forced = forced_variant(ctx);
   if (panel_serves(g.a_t, g.k) &&
-      (forced == kPanelVariant || (forced < 0 && panel_auto(g.m, g.n, batch, ctx->sm_count)))) {
+      (forced == kPanelVariant || (forced < 0 && panel_auto(g.m, g.n, g.k, batch, ctx->sm_count)))) {
     lrb_status st = LRB_OK;
     if (run_panel(ctx, g, batch, beta_one, stream, &st)) {
       if (st == LRB_OK) ctx->last_variant = kPanelVariant;
@@ -820,7 +821,7 @@ extern "C" lrb_status lrb_select(const lrb_ctx* ctx, char order, char opA, char 
   // (the panel kernel additionally needs TMA-eligible operands at run time)
   const bool panel = panel_serves(a_t, k) &&
                      (forced == kPanelVariant ||
-                      (forced < 0 && panel_auto(cm, cn, batch, ctx ? ctx->sm_count : 148)));
+                      (forced < 0 && panel_auto(cm, cn, k, batch, ctx ? ctx->sm_count : 148)));
   const int v = panel ? kPanelVariant : choose_variant(ctx, cm, cn, k, batch);
   const VariantMeta& vm = kVariants[v];
   std::memset(out, 0, sizeof(*out));

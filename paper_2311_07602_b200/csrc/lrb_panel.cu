@@ -20,13 +20,13 @@
 //     general kernel, so no warp ever blocks to issue.
 //   * The MMA warps form two groups of four. Group g takes the chunks of
 //     parity g: each warp owns a 64 x 32 slab of the chunk's 256 x 32 C tile
-//     (64 accumulators, 256 DMMAs per chunk at k = 32), and one group's MMAs
-//     overlap the other's epilogue. The groups run free by default. PINGPONG
-//     (debug bit 8) makes them take strict turns on the FP64 tensor pipe
-//     (two named barriers); one warp per SM sub-partition with 32 independent
-//     accumulators sustains 0.96 of the DMMA peak
-//     (tools/microbench/dmma_ilp.cu), but on cfg2 the strict turns measure
-//     0.88 of FP64 peak against 0.91 free-running.
+//     (64 accumulators, 256 DMMAs per chunk at k = 32), and the groups run
+//     free, so one group's MMAs cover the other's epilogue. Measured
+//     alternatives (cfg2, fraction of FP64 peak): strict turns on the tensor
+//     pipe through named barriers 0.88 (free: 0.91); splitting each slab into
+//     two row halves so one half's stores interleave with the other half's
+//     MMAs 0.79-0.81 (16 accumulators per phase, and the stores between
+//     k-steps break the fragment-load schedule).
 // Arithmetic is the general kernel's: DMMA 8x8x4 k-steps in ascending k and a
 // scalar fma() tail, so every C entry is the reference's in-order FMA chain.
 #include "lrb_gemm.cuh"
@@ -56,10 +56,6 @@ struct PanelCfg {
   static_assert(S % 2 == 0, "a slot must always feed the same group");
   static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
 };
-
-__device__ __forceinline__ void named_barrier_arrive(int id, int threads) {
-  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(threads) : "memory");
-}
 
 // Issue unit lu's U panel (both half boxes) into buffer lu & 1 (one lane).
 template <class P>
@@ -103,7 +99,7 @@ __device__ __forceinline__ void issue_chunk_v(const StridedProblem& prob, double
     tma_load_3d(vs, &prob.tmB, 0, c * P::COLS, zb, &v_full[s], pol);
 }
 
-template <bool B_T, bool PINGPONG>
+template <bool B_T>
 __global__ void __launch_bounds__(PanelCfg<B_T>::THREADS, 1)
     lrb_panel_kernel(const __grid_constant__ StridedProblem prob, const int flags) {
   using P = PanelCfg<B_T>;
@@ -156,8 +152,6 @@ __global__ void __launch_bounds__(PanelCfg<B_T>::THREADS, 1)
   const int half = slab >> 1;      // which 128-row half panel
   const int wi = slab & 1;         // 64-row warp tile inside the half
   const int g = lane >> 2, tq = lane & 3;
-  // ping-pong: group 0 holds the tensor pipe first (named barriers 2, 3)
-  if (PINGPONG && grp == 1 && q_total > 0) named_barrier_arrive(2, 2 * 128);
 
   int64_t q = 0;
   int64_t lu = 0;
@@ -200,7 +194,6 @@ __global__ void __launch_bounds__(PanelCfg<B_T>::THREADS, 1)
       }
 
       mbar_wait(&v_full[s], int(q / S) & 1);
-      if (PINGPONG) named_barrier_sync(2 + grp, 2 * 128);
       const double* Bs = V + s * P::V_ELEMS;
       if (k == P::KMAX) {
 #pragma unroll
@@ -224,7 +217,6 @@ __global__ void __launch_bounds__(PanelCfg<B_T>::THREADS, 1)
           }
         }
       }
-      if (PINGPONG && q + 1 < q_total) named_barrier_arrive(2 + (grp ^ 1), 2 * 128);
       // hand the V slot back; the group's last warp out refills it with
       // chunk q + S (same parity: this group's again). acq_rel orders the
       // four warps' reads of the slot before the async-proxy refill.
@@ -267,11 +259,11 @@ __global__ void __launch_bounds__(PanelCfg<B_T>::THREADS, 1)
   }
 }
 
-template <bool B_T, bool PINGPONG>
+template <bool B_T>
 cudaError_t launch_one(const StridedProblem& prob, int flags, int sm_count, cudaStream_t stream,
                        int64_t* grid_out) {
   using P = PanelCfg<B_T>;
-  auto kern = lrb_panel_kernel<B_T, PINGPONG>;
+  auto kern = lrb_panel_kernel<B_T>;
   static bool attr_set = false;  // per process; the attribute is per function
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -292,13 +284,10 @@ cudaError_t launch_one(const StridedProblem& prob, int flags, int sm_count, cuda
 size_t panel_smem_bytes() { return PanelCfg<true>::SMEM_BYTES; }
 int panel_threads() { return PanelCfg<true>::THREADS; }
 
-cudaError_t launch_panel(int b_t, int pingpong, const StridedProblem& prob, int flags,
-                         int sm_count, cudaStream_t stream, int64_t* grid) {
-  if (b_t)
-    return pingpong ? launch_one<true, true>(prob, flags, sm_count, stream, grid)
-                    : launch_one<true, false>(prob, flags, sm_count, stream, grid);
-  return pingpong ? launch_one<false, true>(prob, flags, sm_count, stream, grid)
-                  : launch_one<false, false>(prob, flags, sm_count, stream, grid);
+cudaError_t launch_panel(int b_t, const StridedProblem& prob, int flags, int sm_count,
+                         cudaStream_t stream, int64_t* grid) {
+  return b_t ? launch_one<true>(prob, flags, sm_count, stream, grid)
+             : launch_one<false>(prob, flags, sm_count, stream, grid);
 }
 
 }  // namespace lrb

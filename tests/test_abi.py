@@ -108,6 +108,9 @@ def test_selector_long_k_general_shapes_use_t64():
     assert P.select("C", "T", "T", 512, 512, 32, 4096)["name"] == "q64"
     # too few 256-row units for one wave, or too short: the tile kernel
     assert P.select("C", "N", "T", 512, 512, 32, 50)["name"] == "q64"
+    # write-bound short k: the tile kernel's TMA-store epilogue
+    assert P.select("C", "N", "T", 512, 512, 16, 4096)["name"] == "q64"
+    assert P.select("C", "N", "T", 512, 512, 17, 4096)["name"] == "p256"
     assert P.select("C", "N", "T", 128, 512, 32, 4096)["name"] != "p256"
     assert P.select("R", "N", "N", 64, 64, 1024, 20000)["name"] == "q64"
 
