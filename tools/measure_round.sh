@@ -45,7 +45,7 @@ log "reference arm rc=$?"
 
 log "full capture of the cfg2 kernel"
 if timeout 300 python tools/profile_one.py --config cfg2 --launches 2 > /dev/null 2>&1; then
-  timeout 1200 ncu --set full --import-source on --clock-control none -k regex:lrb_gemm_kernel \
+  timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"lrb_(gemm|panel)_kernel" \
     -c 1 -f -o $O/ncu_cfg2_$R python tools/profile_one.py --config cfg2 --launches 2 \
     > $O/ncu_cfg2_$R.log 2>&1
   log "ncu full rc=$?"
