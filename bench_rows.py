@@ -251,7 +251,7 @@ def run_blr_gpu(args, w, world, rank, local, pg, B):
     ms_step = B.all_max(pg, ms_rank) / args.steps
     fl_all, by_all = B.all_sum(pg, w.flops()), B.all_sum(pg, w.bytes())
     roof = _roof(w.flops(), w.bytes(), ms_rank / args.steps, hbm, fp64, fsrc, hsrc, w.name)
-    roof["kernel"] = "lrb_gemm_kernel x3 + blr_couple_kernel per matvec"
+    roof["kernel"] = "lrb_gemm_kernel x2 + blr_couple_kernel per matvec"
     roof["kernel_ms"] = round(ms_rank / max(1, launches), 4)
     e2e = None
     if args.e2e_steps > 0:

@@ -7,37 +7,40 @@
 // with rhs, y row-major n x nrhs. Per row tile i the reference computes
 //   y_i  = D_i rhs_i,   then for j != i ascending:
 //   y_i += U_ij (X_ij (Vt_ij rhs_j))
-// each product a naive in-order chain. On the device this is three launches of
-// the batched GEMM kernels and one small coupling kernel, every chain kept in
-// the reference's order:
-//   1. y_i = D_i rhs_i                       strided batch over i
-//   2. W_.j = [Vt_0j; Vt_1j; ...] rhs_j       strided batch over j (the tiles of
+// each product a naive in-order chain. On the device this is two launches of
+// the batched GEMM kernels around one small coupling kernel, on one stream,
+// every chain kept in the reference's order:
+//   1. W_.j = [Vt_0j; Vt_1j; ...] rhs_j       strided batch over j (the tiles of
 //                                            block column j stacked, one GEMM)
-//   3. Z_ij = X_ij W_ij                      one thread per Z entry (an r-long
-//                                            FMA chain; reads W in column order,
-//                                            writes Z stacked by row)
-//   4. y_i += [U_i0 | U_i1 | ...] [Z_i0; Z_i1; ...]   strided batch over i,
-//      K = (tiles-1) rank, beta 1: the concatenated K runs j-major then p,
-//      exactly the reference's sequential per-j accumulation into y_i.
-// The device layout (stacked Vt by column, concatenated U by row) is built
-// once at lrb_blr_create.
+//   2. Z_ij = X_ij W_ij                      register-blocked r-long FMA chains
+//                                            (reads W in column order, writes Z
+//                                            into row i's operand block), and
+//                                            rhs_i copied into the same block
+//   3. y_i = [D_i | U_i0 | U_i1 | ...] [rhs_i; Z_i0; Z_i1; ...]
+//      strided batch over i, K = block + (tiles-1) rank, beta 0: the
+//      concatenated K runs over D's columns, then j-major then p — exactly the
+//      reference's y_i = D_i rhs_i followed by its sequential per-j
+//      accumulation into y_i, as ONE chain per entry.
+// The device layout (stacked Vt by column, [D_i | U_i*] by row) is built once
+// at lrb_blr_create.
 #include <algorithm>
 #include <cstring>
 #include <vector>
 
+#include "lrb_device.cuh"
 #include "lrb_internal.h"
 
 struct lrb_blr {
   int device = 0;
   int64_t n = 0, block = 0, rank = 0, tiles = 0;
-  double* d_diag = nullptr;   // tiles x block^2, row-major tiles
+  int64_t pitch = 0;          // block + (tiles-1) rank: row pitch of d_dcat
+  double* d_dcat = nullptr;   // per row i: block x pitch, [D_i | U_i0 | U_i1 | ...]
   double* d_vtcol = nullptr;  // per column j: (tiles-1) rank x block (i != j ascending)
   double* d_x = nullptr;      // same (j, i) order: rank x rank each
-  double* d_ucat = nullptr;   // per row i: block x (tiles-1) rank, [U_i0 | U_i1 | ...]
   // per-nrhs workspace
   int64_t ws_nrhs = -1;
   double* d_w = nullptr;
-  double* d_z = nullptr;
+  double* d_rz = nullptr;     // per row i: pitch x nrhs, [rhs_i; Z_i0; Z_i1; ...]
   // reconstruct_dense: UX tiles in Vt's (j, i) order and the tile plan for
   // the last output buffer
   double* d_ux = nullptr;
@@ -66,8 +69,8 @@ void free_recon(lrb_ctx* ctx, lrb_blr* m) {
 
 void free_ws(lrb_ctx*, lrb_blr* m) {
   if (m->d_w) cudaFree(m->d_w);
-  if (m->d_z) cudaFree(m->d_z);
-  m->d_w = m->d_z = nullptr;
+  if (m->d_rz) cudaFree(m->d_rz);
+  m->d_w = m->d_rz = nullptr;
   m->ws_nrhs = -1;
 }
 
@@ -75,9 +78,8 @@ lrb_status ensure_ws(lrb_ctx* ctx, lrb_blr* m, int64_t nrhs) {
   if (m->ws_nrhs == nrhs) return LRB_OK;
   free_ws(ctx, m);
   const int64_t T = m->tiles, r = m->rank, items = T * (T - 1);
-  const size_t bytes = size_t(items * r * nrhs) * sizeof(double);
-  LRB_CUDA_TRY(ctx, cudaMalloc(&m->d_w, bytes));
-  LRB_CUDA_TRY(ctx, cudaMalloc(&m->d_z, bytes));
+  LRB_CUDA_TRY(ctx, cudaMalloc(&m->d_w, size_t(std::max<int64_t>(1, items * r * nrhs)) * sizeof(double)));
+  LRB_CUDA_TRY(ctx, cudaMalloc(&m->d_rz, size_t(T * m->pitch * nrhs) * sizeof(double)));
   m->ws_nrhs = nrhs;
   return LRB_OK;
 }
@@ -90,8 +92,10 @@ lrb_status ensure_ws(lrb_ctx* ctx, lrb_blr* m, int64_t nrhs) {
 template <int CP>
 __global__ void __launch_bounds__(256) blr_couple_kernel(const double* __restrict__ x,
                                                          const double* __restrict__ w,
-                                                         double* __restrict__ z, int tiles,
-                                                         int rank, int nrhs) {
+                                                         const double* __restrict__ rhs,
+                                                         double* __restrict__ rz, int tiles,
+                                                         int block, int rank, int nrhs) {
+  lrb::pdl_entry();
   // a thread owns a 4-row x CP-column block of one Z_q (CP = 2 when nrhs is
   // even): per step k it loads four X values and one W pair for 4*CP FMAs;
   // every entry is still one r-long chain over k ascending. 32-bit indices:
@@ -101,6 +105,14 @@ __global__ void __launch_bounds__(256) blr_couple_kernel(const double* __restric
   const int per_item = rg_n * cg_n, per = rank * nrhs;
   const int Q = tiles * (tiles - 1);
   const int total = Q * per_item;
+  const int64_t pitch = block + int64_t(tiles - 1) * rank;
+  // rhs_i into the first block rows of row i's operand block
+  const int64_t n_rhs = int64_t(tiles) * block * nrhs;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n_rhs;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / (int64_t(block) * nrhs), rem = e - i * block * nrhs;
+    rz[i * pitch * nrhs + rem] = __ldg(rhs + e);
+  }
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
     const int q = t / per_item, rem = t - q * per_item;
     const int rg = rem / cg_n, cg = rem - rg * cg_n;
@@ -135,7 +147,7 @@ __global__ void __launch_bounds__(256) blr_couple_kernel(const double* __restric
         for (int c = 0; c < CP; ++c) acc[a][c] = fma(xv, wv[c], acc[a][c]);
       }
     }
-    double* zq = z + (int64_t(i) * (tiles - 1) + jp) * per + c0;
+    double* zq = rz + (int64_t(i) * pitch + block + int64_t(jp) * rank) * nrhs + c0;
 #pragma unroll
     for (int a = 0; a < RP; ++a)
       if (p0 + a < rank) {
@@ -147,25 +159,26 @@ __global__ void __launch_bounds__(256) blr_couple_kernel(const double* __restric
 
 // reconstruct_dense step 1: UX_p = U_ij X_ij for every off-diagonal tile, p
 // in Vt's (column j, row i != j) order, U_ij read from the concatenated row
-// layout [U_i0 | U_i1 | ...]. One block per item (32-bit indices within it).
+// layout [D_i | U_i0 | U_i1 | ...]. One block per item (32-bit indices within it).
 // A thread owns a 4-row x CP-column block of UX (CP = 2 when rank is even):
 // per step q it loads four U values and one X pair for 4*CP FMAs. Every
 // entry is still one r-long FMA chain over q ascending.
 template <int CP>
-__global__ void __launch_bounds__(256) blr_ux_kernel(const double* __restrict__ ucat,
+__global__ void __launch_bounds__(256) blr_ux_kernel(const double* __restrict__ dcat,
                                                      const double* __restrict__ x,
                                                      double* __restrict__ ux, int tiles,
                                                      int block, int rank) {
+  lrb::pdl_entry();
   constexpr int RP = 4;
   const int Q = tiles * (tiles - 1);
-  const int64_t K = int64_t(tiles - 1) * rank;
+  const int64_t K = block + int64_t(tiles - 1) * rank;  // row pitch of [D_i | U_i*]
   const int row_groups = (block + RP - 1) / RP, col_groups = rank / CP;
   const int work = row_groups * col_groups;
   for (int p = blockIdx.x; p < Q; p += gridDim.x) {
     const int j = p / (tiles - 1), ip = p - j * (tiles - 1);
     const int i = ip < j ? ip : ip + 1;
     const int jp = j < i ? j : j - 1;
-    const double* ub = ucat + int64_t(i) * block * K + int64_t(jp) * rank;
+    const double* ub = dcat + int64_t(i) * block * K + block + int64_t(jp) * rank;
     const double* xb = x + int64_t(p) * rank * rank;
     double* out = ux + int64_t(p) * block * rank;
     for (int wkr = threadIdx.x; wkr < work; wkr += blockDim.x) {
@@ -208,13 +221,14 @@ __global__ void __launch_bounds__(256) blr_ux_kernel(const double* __restrict__ 
 
 // reconstruct_dense: the diagonal tiles into the n x n row-major output, one
 // block per tile row
-__global__ void __launch_bounds__(256) blr_diag_kernel(const double* __restrict__ diag,
+__global__ void __launch_bounds__(256) blr_diag_kernel(const double* __restrict__ dcat,
                                                        double* __restrict__ out, int tiles,
-                                                       int block) {
+                                                       int block, int64_t pitch) {
+  lrb::pdl_entry();
   const int64_t n = int64_t(tiles) * block;
   for (int g = blockIdx.x; g < tiles * block; g += gridDim.x) {
     const int t = g / block, row = g - t * block;
-    const double* src = diag + int64_t(g) * block;
+    const double* src = dcat + int64_t(g) * pitch;
     double* dst = out + (int64_t(t) * block + row) * n + int64_t(t) * block;
     for (int c = threadIdx.x; c < block; c += blockDim.x) dst[c] = __ldg(src + c);
   }
@@ -256,14 +270,26 @@ extern "C" lrb_status lrb_blr_create(lrb_ctx* ctx, int64_t n, int64_t block, int
     if (e == cudaSuccess) e = cudaMemcpy(*dst, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice);
     return e;
   };
-  cudaError_t e = cudaMalloc(&m->d_diag, size_t(T * b * b) * sizeof(double));
-  if (e == cudaSuccess)
-    e = cudaMemcpy(m->d_diag, diag, size_t(T * b * b) * sizeof(double), cudaMemcpyHostToDevice);
+  const int64_t P = b + (T - 1) * r;  // [D_i | U_i0 | U_i1 | ...] row pitch
+  m->pitch = P;
+  // reference off-diagonal order: row-major over (i, j != i) (blr.hpp:33-35)
+  auto off = [&](int64_t i, int64_t j) { return i * (T - 1) + (j < i ? j : j - 1); };
+  std::vector<double> dcat(size_t(T * b * P));
+  for (int64_t i = 0; i < T; ++i)
+    for (int64_t row = 0; row < b; ++row) {
+      std::memcpy(&dcat[size_t((i * b + row) * P)], diag + (i * b + row) * b,
+                  size_t(b) * sizeof(double));
+      for (int64_t j = 0; j < T; ++j) {
+        if (i == j) continue;
+        const int64_t jp = j < i ? j : j - 1;
+        const double* uij = u + off(i, j) * b * r;  // block x rank, row-major
+        std::memcpy(&dcat[size_t((i * b + row) * P + b + jp * r)], uij + row * r,
+                    size_t(r) * sizeof(double));
+      }
+    }
+  cudaError_t e = upload(&m->d_dcat, dcat);
   if (e == cudaSuccess && T > 1) {
-    // reference off-diagonal order: row-major over (i, j != i) (blr.hpp:33-35)
-    auto off = [&](int64_t i, int64_t j) { return i * (T - 1) + (j < i ? j : j - 1); };
-    std::vector<double> vtcol(size_t(items * r * b)), xs(size_t(items * r * r)),
-        ucat(size_t(T * b * (T - 1) * r));
+    std::vector<double> vtcol(size_t(items * r * b)), xs(size_t(items * r * r));
     int64_t q = 0;
     for (int64_t j = 0; j < T; ++j)
       for (int64_t i = 0; i < T; ++i) {
@@ -273,19 +299,8 @@ extern "C" lrb_status lrb_blr_create(lrb_ctx* ctx, int64_t n, int64_t block, int
         std::memcpy(&xs[size_t(q * r * r)], x + o * r * r, size_t(r * r) * sizeof(double));
         ++q;
       }
-    const int64_t K = (T - 1) * r;
-    for (int64_t i = 0; i < T; ++i)
-      for (int64_t j = 0; j < T; ++j) {
-        if (i == j) continue;
-        const int64_t jp = j < i ? j : j - 1;
-        const double* uij = u + off(i, j) * b * r;  // block x rank, row-major
-        for (int64_t row = 0; row < b; ++row)
-          std::memcpy(&ucat[size_t(i * b * K + row * K + jp * r)], uij + row * r,
-                      size_t(r) * sizeof(double));
-      }
     e = upload(&m->d_vtcol, vtcol);
     if (e == cudaSuccess) e = upload(&m->d_x, xs);
-    if (e == cudaSuccess) e = upload(&m->d_ucat, ucat);
   }
   if (e != cudaSuccess) {
     lrb_blr_destroy(ctx, m);
@@ -304,47 +319,35 @@ extern "C" lrb_status lrb_blr_matvec_device(lrb_ctx* ctx, lrb_blr* m, const doub
   lrb_status st = lrb::bind(ctx);
   if (st) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int64_t T = m->tiles, b = m->block, r = m->rank, K = (T - 1) * r;
-  if (T == 1)  // 1. y = D rhs only
-    return lrb::run_strided_rowmajor_beta(ctx, b, nrhs, b, m->d_diag, b, b * b, rhs, nrhs,
+  const int64_t T = m->tiles, b = m->block, r = m->rank, K = (T - 1) * r, P = m->pitch;
+  if (T == 1)  // y = D rhs only
+    return lrb::run_strided_rowmajor_beta(ctx, b, nrhs, b, m->d_dcat, P, b * P, rhs, nrhs,
                                           b * nrhs, y, nrhs, b * nrhs, T, 0, s);
   st = ensure_ws(ctx, m, nrhs);
   if (st) return st;
-  // steps 1 and 2 are independent: step 1 runs forked on an auxiliary stream
-  // so the two launches' ramps and tails overlap; joined before step 4
-  st = lrb::ensure_aux(ctx);
-  if (st) return st;
-  cudaStream_t aux = ctx->aux_stream[lrb_ctx::kAux - 1];
-  cudaEvent_t done = ctx->aux_done[lrb_ctx::kAux - 1];
-  LRB_CUDA_TRY(ctx, cudaEventRecord(ctx->fork_ev, s));
-  LRB_CUDA_TRY(ctx, cudaStreamWaitEvent(aux, ctx->fork_ev, 0));
-  // 1. y_i = D_i rhs_i
-  st = lrb::run_strided_rowmajor_beta(ctx, b, nrhs, b, m->d_diag, b, b * b, rhs, nrhs, b * nrhs,
-                                      y, nrhs, b * nrhs, T, 0, aux);
-  if (st) return st;
-  LRB_CUDA_TRY(ctx, cudaEventRecord(done, aux));
-  // 2. W_.j = [Vt_ij]_i rhs_j
+  // 1. W_.j = [Vt_ij]_i rhs_j
   st = lrb::run_strided_rowmajor_beta(ctx, K, nrhs, b, m->d_vtcol, b, K * b, rhs, nrhs, b * nrhs,
                                       m->d_w, nrhs, K * nrhs, T, 0, s);
   if (st) return st;
-  // 3. Z_ij = X_ij W_ij
+  // 2. Z_ij = X_ij W_ij into [rhs_i; Z_i*], and rhs_i copied there
   {
     const int cp = (nrhs % 2 == 0) ? 2 : 1;
-    const int64_t work = T * (T - 1) * ((r + 3) / 4) * (nrhs / cp);
+    const int64_t work = std::max(T * (T - 1) * ((r + 3) / 4) * (nrhs / cp), T * b * nrhs);
     const int64_t blocks = std::min<int64_t>((work + 255) / 256, int64_t(ctx->sm_count) * 16);
     if (cp == 2)
-      blr_couple_kernel<2><<<unsigned(blocks), 256, 0, s>>>(m->d_x, m->d_w, m->d_z, int(T),
-                                                            int(r), int(nrhs));
+      LRB_CUDA_TRY(ctx, lrb::launch_pdl(blr_couple_kernel<2>, dim3(unsigned(blocks)), dim3(256), 0,
+                                        s, m->d_x, m->d_w, rhs, m->d_rz, int(T), int(b), int(r),
+                                        int(nrhs)));
     else
-      blr_couple_kernel<1><<<unsigned(blocks), 256, 0, s>>>(m->d_x, m->d_w, m->d_z, int(T),
-                                                            int(r), int(nrhs));
-    LRB_CUDA_TRY(ctx, cudaGetLastError());
+      LRB_CUDA_TRY(ctx, lrb::launch_pdl(blr_couple_kernel<1>, dim3(unsigned(blocks)), dim3(256), 0,
+                                        s, m->d_x, m->d_w, rhs, m->d_rz, int(T), int(b), int(r),
+                                        int(nrhs)));
     ctx->launches.fetch_add(1, std::memory_order_relaxed);
   }
-  // 4. y_i += [U_ij]_j [Z_ij]_j (after step 1's y)
-  LRB_CUDA_TRY(ctx, cudaStreamWaitEvent(s, done, 0));
-  return lrb::run_strided_rowmajor_beta(ctx, b, nrhs, K, m->d_ucat, K, b * K, m->d_z, nrhs,
-                                        K * nrhs, y, nrhs, b * nrhs, T, 1, s);
+  // 3. y_i = [D_i | U_i*] [rhs_i; Z_i*]: one chain per entry over D's columns,
+  //    then the off-diagonal blocks j-major
+  return lrb::run_strided_rowmajor_beta(ctx, b, nrhs, P, m->d_dcat, P, b * P, m->d_rz, nrhs,
+                                        P * nrhs, y, nrhs, b * nrhs, T, 0, s);
 }
 
 extern "C" lrb_status lrb_blr_matvec(lrb_ctx* ctx, lrb_blr* m, const double* rhs, int64_t nrhs,
@@ -378,10 +381,9 @@ extern "C" lrb_status lrb_blr_destroy(lrb_ctx* ctx, lrb_blr* m) {
   if (ctx) cudaSetDevice(ctx->device);
   free_ws(ctx, m);
   free_recon(ctx, m);
-  if (m->d_diag) cudaFree(m->d_diag);
+  if (m->d_dcat) cudaFree(m->d_dcat);
   if (m->d_vtcol) cudaFree(m->d_vtcol);
   if (m->d_x) cudaFree(m->d_x);
-  if (m->d_ucat) cudaFree(m->d_ucat);
   delete m;
   return LRB_OK;
 }
@@ -417,8 +419,8 @@ extern "C" lrb_status lrb_blr_reconstruct_dense(lrb_ctx* ctx, lrb_blr* m, double
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   {
     const int64_t blocks = std::min<int64_t>(T * b, int64_t(ctx->sm_count) * 32);
-    blr_diag_kernel<<<unsigned(blocks), 256, 0, s>>>(m->d_diag, out, int(T), int(b));
-    LRB_CUDA_TRY(ctx, cudaGetLastError());
+    LRB_CUDA_TRY(ctx, lrb::launch_pdl(blr_diag_kernel, dim3(unsigned(blocks)), dim3(256), 0, s,
+                                      m->d_dcat, out, int(T), int(b), m->pitch));
     ctx->launches.fetch_add(1, std::memory_order_relaxed);
   }
   if (T == 1) return LRB_OK;
@@ -447,12 +449,11 @@ extern "C" lrb_status lrb_blr_reconstruct_dense(lrb_ctx* ctx, lrb_blr* m, double
   {
     const int64_t blocks = std::min<int64_t>(items, int64_t(ctx->sm_count) * 16);
     if (r % 2 == 0)
-      blr_ux_kernel<2><<<unsigned(blocks), 256, 0, s>>>(m->d_ucat, m->d_x, m->d_ux, int(T),
-                                                        int(b), int(r));
+      LRB_CUDA_TRY(ctx, lrb::launch_pdl(blr_ux_kernel<2>, dim3(unsigned(blocks)), dim3(256), 0, s,
+                                        m->d_dcat, m->d_x, m->d_ux, int(T), int(b), int(r)));
     else
-      blr_ux_kernel<1><<<unsigned(blocks), 256, 0, s>>>(m->d_ucat, m->d_x, m->d_ux, int(T),
-                                                        int(b), int(r));
-    LRB_CUDA_TRY(ctx, cudaGetLastError());
+      LRB_CUDA_TRY(ctx, lrb::launch_pdl(blr_ux_kernel<1>, dim3(unsigned(blocks)), dim3(256), 0, s,
+                                        m->d_dcat, m->d_x, m->d_ux, int(T), int(b), int(r)));
     ctx->launches.fetch_add(1, std::memory_order_relaxed);
   }
   return lrb_ptr_plan_execute(ctx, m->recon_plan, stream);

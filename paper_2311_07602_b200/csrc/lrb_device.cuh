@@ -4,9 +4,49 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
+#include <utility>
 
 namespace lrb {
+
+// ------------------------------------------- programmatic dependent launch
+// Every library kernel opens with pdl_entry(): it lets the next kernel on the
+// stream be scheduled as soon as all of this grid's CTAs have started, and
+// waits (before touching global memory) until the previous kernel has
+// completed and its writes are visible. Launched through launch_pdl, a
+// dependent grid's launch latency and CTA start-up overlap its predecessor's
+// tail; without the launch attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+
+// LRB_PDL=0 launches without the programmatic-serialization attribute
+// (measurement probe)
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* s = std::getenv("LRB_PDL");
+    return !(s && s[0] == '0');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

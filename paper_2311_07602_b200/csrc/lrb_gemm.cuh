@@ -436,6 +436,7 @@ template <class Cfg, class Problem>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     lrb_gemm_kernel(const __grid_constant__ Problem prob, const int flags) {
   static_assert(Cfg::WARPS % 4 == 0, "warps per CTA must fill all four SM sub-partitions");
+  pdl_entry();
   // flags bit 0: beta = 1 (accumulate into C); debug probes (LRB_DEBUG_FLAGS,
   // never set by the library itself): bit 1 skips the epilogue stores, bit 3
   // uses default-policy instead of streaming stores, bit 4 stops refilling the
@@ -657,8 +658,8 @@ cudaError_t launch_gemm(const Problem& prob, int beta_one, int device, int sm_co
     info->occupancy = occ;
   }
   if (grid <= 0) return cudaSuccess;
-  kern<<<static_cast<unsigned>(grid), Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(prob, beta_one);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(Cfg::THREADS), Cfg::SMEM_BYTES,
+                    stream, prob, beta_one);
 }
 
 }  // namespace lrb

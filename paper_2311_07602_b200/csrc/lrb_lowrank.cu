@@ -113,6 +113,7 @@ __global__ void __launch_bounds__(LrCfg<R>::THREADS, 2)
     lrb_lowrank_kernel(const __grid_constant__ LrProblem p) {
   using Cf = LrCfg<R>;
   constexpr int F = Cf::F, KB = Cf::KB, STAGES = Cf::STAGES;
+  pdl_entry();
   extern __shared__ __align__(1024) double smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(STAGES) * Cf::STAGE);
   IssueState* st = reinterpret_cast<IssueState*>(full + STAGES);
@@ -294,6 +295,7 @@ __global__ void lrb_lowrank_simple_kernel(const double* __restrict__ a_vt,
                                           const double* __restrict__ a_x,
                                           const double* __restrict__ b_x, double* __restrict__ g,
                                           int64_t batch, int block, int rank) {
+  pdl_entry();
   extern __shared__ double sm[];
   double* cs = sm;
   double* es = sm + size_t(rank) * rank;
@@ -361,8 +363,8 @@ cudaError_t launch_fast(const LrProblem& p, int device, int sm_count, cudaStream
   }
   const int64_t grid = std::min<int64_t>(p.groups, int64_t(sm_count) * occ);
   *grid_out = grid;
-  if (grid > 0) kern<<<unsigned(grid), Cf::THREADS, Cf::SMEM, s>>>(p);
-  return cudaGetLastError();
+  if (grid > 0) return launch_pdl(kern, dim3(unsigned(grid)), dim3(Cf::THREADS), Cf::SMEM, s, p);
+  return cudaSuccess;
 }
 
 }  // namespace
@@ -432,9 +434,8 @@ lrb_status run_lowrank(lrb_ctx* ctx, int64_t batch, int64_t block, int64_t rank,
     LRB_CUDA_TRY(ctx, cudaFuncSetAttribute(lrb_lowrank_simple_kernel,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const int64_t grid = std::min<int64_t>(batch, int64_t(ctx->sm_count) * 8);
-  lrb_lowrank_simple_kernel<<<unsigned(grid), 128, smem, s>>>(a_vt, b_u, a_x, b_x, g, batch,
-                                                             int(block), int(rank));
-  LRB_CUDA_TRY(ctx, cudaGetLastError());
+  LRB_CUDA_TRY(ctx, launch_pdl(lrb_lowrank_simple_kernel, dim3(unsigned(grid)), dim3(128), smem,
+                                s, a_vt, b_u, a_x, b_x, g, batch, int(block), int(rank)));
   ctx->launches.fetch_add(1, std::memory_order_relaxed);
   return LRB_OK;
 }

@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(PanelCfg<B_T>::THREADS, 1)
   constexpr int S = P::S, FI = W::FI, FJ = W::FJ;
   // flags bit 0: beta = 1; debug probe bit 1 skips the C stores
   const int beta_one = flags & 1;
+  pdl_entry();
   extern __shared__ __align__(1024) double smem[];
   double* const U = smem;                    // [2 buffers][2 halves][HALF]
   double* const V = smem + 2 * P::U_ELEMS;   // [S][V_ELEMS]
@@ -275,8 +276,8 @@ cudaError_t launch_one(const StridedProblem& prob, int flags, int sm_count, cuda
   if (prob.num_tiles < grid) grid = prob.num_tiles;
   if (grid_out) *grid_out = grid;
   if (grid <= 0) return cudaSuccess;
-  kern<<<static_cast<unsigned>(grid), P::THREADS, P::SMEM_BYTES, stream>>>(prob, flags);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(P::THREADS), P::SMEM_BYTES,
+                    stream, prob, flags);
 }
 
 }  // namespace

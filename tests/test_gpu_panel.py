@@ -114,3 +114,11 @@ def test_panel_is_the_automatic_choice_for_cfg2_shape(ctx):
     got = c.run_device(ctx)
     assert ctx.last_variant == "p256"
     c.check(got, items=[0, 1, 150, 299])
+
+
+@pytest.mark.parametrize("beta,m", [(1.0, 300), (0.0, 302)])
+def test_panel_short_k_forced(ctx, beta, m):
+    # k <= 16 is not the automatic choice (write-bound: the tile kernel's
+    # TMA-store epilogue wins) but the forced panel stays exact there
+    c = panel_case("C", "N", "T", m, 64, 8, 3, beta=beta, pad=(0, 0, 6), spad=(0, 0, 10), seed=7)
+    c.check(run_panel(ctx, c))
