@@ -89,6 +89,81 @@ lrb_status ensure_ws(lrb_ctx* ctx, lrb_blr* m, int64_t nrhs) {
 // thread owns one entry Z[p][c] = sum_k X[p][k] W[k][c] as an in-order FMA
 // chain from zero (the order DMMA and the FMA-chain oracle use). Bytes: X
 // r^2 + W r*nrhs read, Z r*nrhs written per item — a few MB in total.
+// Warp-per-item form for small items (r^2 + r*nrhs <= kCoupleSmem doubles):
+// the warp stages X_q and W_q in shared memory with all its loads in flight,
+// then computes Z_q as the same r-long chains (k ascending, from 0): on DMMA
+// 8x8x4 tiles when r and nrhs are multiples of 8, else one entry per lane.
+// The register-blocked kernel below (scalar chains straight from global
+// memory) and a scalar shared-memory form both measured 16-18 us per matvec
+// on the 16-RHS bench shape, bound by one load per FMA.
+constexpr int kCoupleSmem = 512;  // doubles per warp (8 warps: 32 KB static)
+template <bool MMA>
+__global__ void __launch_bounds__(256) blr_couple_warp_kernel(const double* __restrict__ x,
+                                                              const double* __restrict__ w,
+                                                              const double* __restrict__ rhs,
+                                                              double* __restrict__ rz, int tiles,
+                                                              int block, int rank, int nrhs) {
+  lrb::pdl_entry();
+  __shared__ double sm[8][kCoupleSmem];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int Q = tiles * (tiles - 1);
+  const int rr = rank * rank, per = rank * nrhs;
+  const int64_t pitch = block + int64_t(tiles - 1) * rank;
+  // rhs_i into the first block rows of row i's operand block: block i of
+  // the grid copies row tile i (contiguous b * nrhs doubles both sides)
+  const int64_t tile_elems = int64_t(block) * nrhs;
+  for (int i = blockIdx.x; i < tiles; i += gridDim.x) {
+    const double* src = rhs + int64_t(i) * tile_elems;
+    double* dst = rz + int64_t(i) * pitch * nrhs;
+    for (int64_t e = threadIdx.x; e < tile_elems; e += blockDim.x) dst[e] = __ldg(src + e);
+  }
+  double* xs = sm[warp];
+  double* ws = xs + rr;
+  for (int q = blockIdx.x * 8 + warp; q < Q; q += gridDim.x * 8) {
+    const double* xq = x + int64_t(q) * rr;
+    const double* wq = w + int64_t(q) * per;
+    // all of the item's loads in flight at once (a rolled loop would wait
+    // one DRAM round trip per 32 elements)
+    double v[kCoupleSmem / 32];
+#pragma unroll
+    for (int t = 0; t < kCoupleSmem / 32; ++t) {
+      const int e = lane + 32 * t;
+      v[t] = e < rr ? __ldg(xq + e) : (e - rr < per ? __ldg(wq + (e - rr)) : 0.0);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < kCoupleSmem / 32; ++t) {
+      const int e = lane + 32 * t;
+      if (e < rr + per) xs[e] = v[t];  // ws == xs + rr
+    }
+    __syncwarp();
+    const int j = q / (tiles - 1), ip = q - j * (tiles - 1);
+    const int i = ip < j ? ip : ip + 1;
+    const int jp = j < i ? j : j - 1;
+    double* zq = rz + (int64_t(i) * pitch + block + int64_t(jp) * rank) * nrhs;
+    if (MMA) {
+      // r and nrhs multiples of 8: each 8 x 8 tile of Z is a chain of r/4
+      // DMMA 8x8x4 steps in ascending k (an in-order FMA chain per entry,
+      // bitwise the scalar form); lane (g, t) holds Z[p0+g][c0+2t .. +1]
+      const int g = lane >> 2, t = lane & 3;
+      for (int p0 = 0; p0 < rank; p0 += 8)
+        for (int c0 = 0; c0 < nrhs; c0 += 8) {
+          double d0 = 0.0, d1 = 0.0;
+          for (int k0 = 0; k0 < rank; k0 += 4)
+            lrb::dmma_8x8x4(d0, d1, xs[(p0 + g) * rank + k0 + t], ws[(k0 + t) * nrhs + c0 + g]);
+          *reinterpret_cast<double2*>(zq + (p0 + g) * nrhs + c0 + 2 * t) = make_double2(d0, d1);
+        }
+    } else {
+      for (int e = lane; e < per; e += 32) {
+        const int p = e / nrhs, c = e - p * nrhs;
+        double acc = 0.0;
+        for (int k = 0; k < rank; ++k) acc = fma(xs[p * rank + k], ws[k * nrhs + c], acc);
+        zq[e] = acc;
+      }
+    }
+  }
+}
+
 template <int CP>
 __global__ void __launch_bounds__(256) blr_couple_kernel(const double* __restrict__ x,
                                                          const double* __restrict__ w,
@@ -330,7 +405,19 @@ extern "C" lrb_status lrb_blr_matvec_device(lrb_ctx* ctx, lrb_blr* m, const doub
                                       m->d_w, nrhs, K * nrhs, T, 0, s);
   if (st) return st;
   // 2. Z_ij = X_ij W_ij into [rhs_i; Z_i*], and rhs_i copied there
-  {
+  if (r * r + r * nrhs <= kCoupleSmem) {
+    const int64_t blocks = std::min<int64_t>((T * (T - 1) + 7) / 8, int64_t(ctx->sm_count) * 8);
+    // Z rows land 16-byte aligned when b and r are even (pitch, offsets)
+    if (r % 8 == 0 && nrhs % 8 == 0)
+      LRB_CUDA_TRY(ctx, lrb::launch_pdl(blr_couple_warp_kernel<true>, dim3(unsigned(blocks)),
+                                        dim3(256), 0, s, m->d_x, m->d_w, rhs, m->d_rz, int(T),
+                                        int(b), int(r), int(nrhs)));
+    else
+      LRB_CUDA_TRY(ctx, lrb::launch_pdl(blr_couple_warp_kernel<false>, dim3(unsigned(blocks)),
+                                        dim3(256), 0, s, m->d_x, m->d_w, rhs, m->d_rz, int(T),
+                                        int(b), int(r), int(nrhs)));
+    ctx->launches.fetch_add(1, std::memory_order_relaxed);
+  } else {
     const int cp = (nrhs % 2 == 0) ? 2 : 1;
     const int64_t work = std::max(T * (T - 1) * ((r + 3) / 4) * (nrhs / cp), T * b * nrhs);
     const int64_t blocks = std::min<int64_t>((work + 255) / 256, int64_t(ctx->sm_count) * 16);

@@ -55,7 +55,10 @@ def test_identity_like_maps_rhs_to_itself(ctx):
 
 @pytest.mark.parametrize("tiles,rank,nrhs,block", [(2, 4, 8, 32), (4, 4, 1, 24), (4, 8, 8, 24),
                                                    (16, 4, 1, 24), (16, 8, 8, 24), (5, 4, 6, 20),
-                                                   (3, 8, 11, 16), (1, 4, 3, 16), (8, 16, 16, 64)])
+                                                   (3, 8, 11, 16), (1, 4, 3, 16), (8, 16, 16, 64),
+                                                   # r^2 + r nrhs > 512: the register-blocked
+                                                   # coupling kernel instead of warp-per-item
+                                                   (3, 24, 8, 48), (2, 16, 24, 32)])
 def test_grids_match_reference(ctx, tiles, rank, nrhs, block):
     m = B.BlrMatrix.random(tiles * block, block, rank, 100 + tiles + rank + nrhs)
     rhs = _rhs(tiles * block, nrhs, 17 + nrhs)
