@@ -421,7 +421,7 @@ def run_expand_gpu(args, w, world, rank, local, pg, B):
         out = ctx.empty(w.n * w.n)
         step = lambda: mat.reconstruct_dense_device(ctx, out, stream=s)  # noqa: E731
         fl, by = w.flops(), w.bytes()
-        kernel = "blr_diag_kernel + blr_ux_kernel + lrb_gemm_kernel<q64> (ptr plan)"
+        kernel = "blr_diag_kernel + blr_ux_mma_kernel + lrb_gemm_kernel<q64, BlrTileProblem> (TMA-store epilogue)"
     else:
         m, r, n = w.m, w.rank, w.batch
         bufs = [ctx.empty(n * m * r), ctx.empty(n * r * r), ctx.empty(n * r * m)]

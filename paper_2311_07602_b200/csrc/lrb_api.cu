@@ -153,6 +153,23 @@ bool encode_c_map(CUtensorMap* map, double* C, int64_t m, int64_t n, int64_t ldc
   return r == CUDA_SUCCESS;
 }
 
+bool encode_tiles_c_map(CUtensorMap* map, double* out, int64_t n, int64_t b, int nb) {
+  auto fn = encode_fn();
+  if (!fn || n < 1 || b < 1 || n % b != 0) return false;
+  // 16-byte granules along x: b even, and every tile origin 16-byte aligned
+  if ((b & 1) != 0 || (reinterpret_cast<uintptr_t>(out) & 15) != 0) return false;
+  if (n * n * 8 >= (int64_t(1) << 40) || n > UINT32_MAX) return false;
+  const int64_t T = n / b;
+  cuuint64_t dims[4] = {cuuint64_t(b), cuuint64_t(b), cuuint64_t(T), cuuint64_t(T)};
+  cuuint64_t strides[3] = {cuuint64_t(n * 8), cuuint64_t(b * 8), cuuint64_t(b * n * 8)};
+  cuuint32_t box[4] = {16, cuuint32_t(nb), 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, out, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // loader choice: ctx override, else LRB_LOADER=segment|tma, else automatic
 int loader_mode(const lrb_ctx* ctx) {
   if (ctx && ctx->loader_override >= 0) return ctx->loader_override;

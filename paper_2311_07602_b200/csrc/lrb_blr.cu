@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "lrb_device.cuh"
+#include "lrb_dispatch.cuh"
 #include "lrb_internal.h"
 
 struct lrb_blr {
@@ -294,6 +295,53 @@ __global__ void __launch_bounds__(256) blr_ux_kernel(const double* __restrict__ 
   }
 }
 
+// reconstruct_dense step 1 on DMMA (r % 8 == 0, b % 8 == 0, r <= 32): one
+// block per item; X_ij staged in shared memory; warp w takes 8-row groups of
+// UX and runs each 8 x 8 tile as r/4 DMMA 8x8x4 steps in ascending q (the
+// same in-order chains as the scalar kernel above, which measured 66 us on
+// the 16384 / 512 / 16 reconstruction at 1.3 TB/s). Each U value is loaded
+// once per item, straight from the [D_i | U_i*] row panel.
+__global__ void __launch_bounds__(256) blr_ux_mma_kernel(const double* __restrict__ dcat,
+                                                         const double* __restrict__ x,
+                                                         double* __restrict__ ux, int tiles,
+                                                         int block, int rank) {
+  lrb::pdl_entry();
+  __shared__ double xs[32 * 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int Q = tiles * (tiles - 1);
+  const int64_t K = block + int64_t(tiles - 1) * rank;  // row pitch of [D_i | U_i*]
+  const int ct_n = rank / 8;
+  for (int p = blockIdx.x; p < Q; p += gridDim.x) {
+    const int j = p / (tiles - 1), ip = p - j * (tiles - 1);
+    const int i = ip < j ? ip : ip + 1;
+    const int jp = j < i ? j : j - 1;
+    const double* ub = dcat + int64_t(i) * block * K + block + int64_t(jp) * rank;
+    double* out = ux + int64_t(p) * block * rank;
+    __syncthreads();  // the previous item's X is no longer read
+    for (int e = threadIdx.x; e < rank * rank; e += blockDim.x)
+      xs[e] = __ldg(x + int64_t(p) * rank * rank + e);
+    __syncthreads();
+    for (int p0 = warp * 8; p0 < block; p0 += 64) {
+      double d[4][2];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) d[c][0] = d[c][1] = 0.0;
+      const double* urow = ub + int64_t(p0 + g) * K + t;
+      for (int k0 = 0; k0 < rank; k0 += 4) {
+        const double a = __ldg(urow + k0);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (c < ct_n) lrb::dmma_8x8x4(d[c][0], d[c][1], a, xs[(k0 + t) * rank + 8 * c + g]);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (c < ct_n)
+          *reinterpret_cast<double2*>(out + (p0 + g) * rank + 8 * c + 2 * t) =
+              make_double2(d[c][0], d[c][1]);
+    }
+  }
+}
+
 // reconstruct_dense: the diagonal tiles into the n x n row-major output, one
 // block per tile row
 __global__ void __launch_bounds__(256) blr_diag_kernel(const double* __restrict__ dcat,
@@ -477,8 +525,11 @@ extern "C" lrb_status lrb_blr_destroy(lrb_ctx* ctx, lrb_blr* m) {
 
 // BlrMatrix::reconstruct_dense (blr.hpp:62-86) on the device: diagonal tiles
 // copied; off-diagonal tiles (U X) Vt in the reference's order — UX by
-// blr_ux_kernel, then the b x b tiles by a pointer-array plan of the batched
-// GEMM (K = rank, q64 tiles) writing straight into the n x n output.
+// blr_ux_kernel, then the b x b tiles by one launch of the batched GEMM kernel
+// (q64 tiles, K = rank) over a BlrTileProblem that writes straight into the
+// n x n output, through the TMA-store epilogue when rank <= 16 (the
+// write-bound case) and the output is TMA-aligned. Operands that TMA cannot
+// address (odd rank or block) take a pointer-array plan instead.
 extern "C" lrb_status lrb_blr_reconstruct_dense(lrb_ctx* ctx, lrb_blr* m, double* out,
                                                 int on_device, void* stream) {
   static const char* fn = "lrb_blr_reconstruct_dense";
@@ -513,7 +564,16 @@ extern "C" lrb_status lrb_blr_reconstruct_dense(lrb_ctx* ctx, lrb_blr* m, double
   if (T == 1) return LRB_OK;
   const int64_t items = T * (T - 1);
   if (!m->d_ux) LRB_CUDA_TRY(ctx, cudaMalloc(&m->d_ux, size_t(items * b * r) * sizeof(double)));
-  if (m->recon_out != out) {
+  using TileCfg = lrb::VariantTraits<LRB_V_Q64>::Cfg<false, false, true>;
+  lrb::BlrTileProblem tp;
+  std::memset(&tp, 0, sizeof(tp));
+  const bool tiles_ok =
+      items <= INT32_MAX &&
+      lrb::encode_operand(&tp.tmA, m->d_vtcol, b, r, b, r * b, items, TileCfg::A_BOX_IN,
+                          TileCfg::A_BOX_OUT) &&
+      lrb::encode_operand(&tp.tmB, m->d_ux, r, b, r, b * r, items, TileCfg::B_BOX_IN,
+                          TileCfg::B_BOX_OUT);
+  if (!tiles_ok && m->recon_out != out) {
     if (m->recon_plan) lrb_ptr_plan_destroy(ctx, m->recon_plan);
     m->recon_plan = nullptr;
     m->recon_out = nullptr;
@@ -535,7 +595,10 @@ extern "C" lrb_status lrb_blr_reconstruct_dense(lrb_ctx* ctx, lrb_blr* m, double
   }
   {
     const int64_t blocks = std::min<int64_t>(items, int64_t(ctx->sm_count) * 16);
-    if (r % 2 == 0)
+    if (r % 8 == 0 && r <= 32 && b % 8 == 0)
+      LRB_CUDA_TRY(ctx, lrb::launch_pdl(blr_ux_mma_kernel, dim3(unsigned(blocks)), dim3(256), 0, s,
+                                        m->d_dcat, m->d_x, m->d_ux, int(T), int(b), int(r)));
+    else if (r % 2 == 0)
       LRB_CUDA_TRY(ctx, lrb::launch_pdl(blr_ux_kernel<2>, dim3(unsigned(blocks)), dim3(256), 0, s,
                                         m->d_dcat, m->d_x, m->d_ux, int(T), int(b), int(r)));
     else
@@ -543,5 +606,23 @@ extern "C" lrb_status lrb_blr_reconstruct_dense(lrb_ctx* ctx, lrb_blr* m, double
                                         m->d_dcat, m->d_x, m->d_ux, int(T), int(b), int(r)));
     ctx->launches.fetch_add(1, std::memory_order_relaxed);
   }
-  return lrb_ptr_plan_execute(ctx, m->recon_plan, stream);
+  if (!tiles_ok) return lrb_ptr_plan_execute(ctx, m->recon_plan, stream);
+  tp.A = m->d_vtcol;
+  tp.B = m->d_ux;
+  tp.C = out;
+  tp.n = n;
+  tp.b = int(b);
+  tp.r = int(r);
+  tp.tiles = int(T);
+  tp.tiles_i = int((b + TileCfg::MB - 1) / TileCfg::MB);
+  tp.tiles_per_item = tp.tiles_i * int((b + TileCfg::NB - 1) / TileCfg::NB);
+  tp.num_tiles = items * tp.tiles_per_item;
+  tp.c_tma = (r <= 16 && !(lrb::debug_flags() & 64) &&
+              lrb::encode_tiles_c_map(&tp.tmC, out, n, b, TileCfg::NB))
+                 ? 1
+                 : 0;
+  lrb::LaunchInfo info{0, 0};
+  LRB_CUDA_TRY(ctx, lrb::launch_gemm<TileCfg>(tp, 0, ctx->device, ctx->sm_count, s, &info));
+  if (info.grid > 0) ctx->launches.fetch_add(1, std::memory_order_relaxed);
+  return LRB_OK;
 }

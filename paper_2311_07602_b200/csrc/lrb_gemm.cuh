@@ -127,6 +127,7 @@ struct TileView {
   const void* tmB;
   const void* tmC;  // C map for the TMA-store epilogue (strided problems)
   int za, zb, zc;   // batch coordinate inside the maps
+  int zc2;          // 4-D C maps (BlrTileProblem): the tile-row coordinate
 };
 
 // Fixed-stride batch: item i at base + i * stride (the reference's
@@ -147,6 +148,11 @@ struct StridedProblem {
   int64_t num_tiles;
 
   __device__ __forceinline__ bool tma_store() const { return c_tma != 0; }
+  // TMA-store one staged 16-row box of C at tile rows (x, y) of item v
+  __device__ __forceinline__ void store_box(const TileView& v, const double* src, int x,
+                                            int y) const {
+    tma_store_3d(v.tmC, src, x, y, v.zc);
+  }
 
   template <int MB, int NB>
   __device__ __forceinline__ TileView tile(int64_t t) const {
@@ -185,6 +191,7 @@ struct StridedProblem {
     v.za = a_batched ? static_cast<int>(item) : 0;
     v.zb = b_batched ? static_cast<int>(item) : 0;
     v.zc = static_cast<int>(item);
+    v.zc2 = 0;
     return v;
   }
   __device__ __forceinline__ int tile_k(int64_t) const { return k; }
@@ -209,6 +216,7 @@ struct PtrProblem {
   int64_t num_tiles;
 
   __device__ __forceinline__ bool tma_store() const { return false; }
+  __device__ __forceinline__ void store_box(const TileView&, const double*, int, int) const {}
 
   template <int MB, int NB>
   __device__ __forceinline__ TileView tile(int64_t t) const {
@@ -233,9 +241,66 @@ struct PtrProblem {
     v.za = 0;
     v.zb = 0;
     v.zc = 0;
+    v.zc2 = 0;
     return v;
   }
   __device__ __forceinline__ int tile_k(int64_t t) const { return items[tiles[t] >> 32].k; }
+};
+
+// The off-diagonal tiles of a BLR matrix's dense reconstruction (reference
+// blr.hpp:62-86): item q in the Vt-stacking order (column j, row i != j), C_q
+// the b x b tile (i, j) of the n x n row-major output. In the column-major view
+// C_q^T = Vt_q^T UX_q^T: A = Vt_q (b x r col-major, ld b), B = UX_q (r x b,
+// ld r), both strided by q (3-D maps); C lives at out + i b n + j b with ld n.
+// C leaves through a 4-D map (x, y, tile column j, tile row i) so the
+// TMA-store epilogue covers every tile with one descriptor.
+struct BlrTileProblem {
+  CUtensorMap tmA;
+  CUtensorMap tmB;
+  CUtensorMap tmC;
+  const double* A;  // Vt tiles, stacked by column
+  const double* B;  // UX tiles, same order
+  double* C;        // the n x n output
+  int64_t n;
+  int b, r, tiles;
+  int tiles_i, tiles_per_item;
+  int c_tma;
+  int64_t num_tiles;
+
+  __device__ __forceinline__ bool tma_store() const { return c_tma != 0; }
+  __device__ __forceinline__ void store_box(const TileView& v, const double* src, int x,
+                                            int y) const {
+    tma_store_4d(v.tmC, src, x, y, v.zc, v.zc2);
+  }
+  template <int MB, int NB>
+  __device__ __forceinline__ TileView tile(int64_t t) const {
+    const uint32_t tt = static_cast<uint32_t>(t), tpi = static_cast<uint32_t>(tiles_per_item);
+    const uint32_t q = tt / tpi;
+    const int rr = static_cast<int>(tt - q * tpi);
+    const int j = int(q) / (tiles - 1), ip = int(q) - j * (tiles - 1);
+    const int i = ip < j ? ip : ip + 1;
+    TileView v;
+    v.A = A + int64_t(q) * b * r;
+    v.B = B + int64_t(q) * r * b;
+    v.C = C + int64_t(i) * b * n + int64_t(j) * b;
+    v.lda = b;
+    v.ldb = r;
+    v.ldc = n;
+    v.m = b;
+    v.n = b;
+    v.k = r;
+    v.i0 = (rr % tiles_i) * MB;
+    v.j0 = (rr / tiles_i) * NB;
+    v.tmA = &tmA;
+    v.tmB = &tmB;
+    v.tmC = &tmC;
+    v.za = int(q);
+    v.zb = int(q);
+    v.zc = j;
+    v.zc2 = i;
+    return v;
+  }
+  __device__ __forceinline__ int tile_k(int64_t) const { return r; }
 };
 
 // next chunk to issue, shared by the CTA's warps
@@ -556,7 +621,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
 #pragma unroll 1
               for (int q = 0; q < MB / 16; ++q)
                 if (v.i0 + 16 * q < v.m)
-                  tma_store_3d(v.tmC, cs + q * 16 * NB, v.i0 + 16 * q, v.j0, v.zc);
+                  prob.store_box(v, cs + q * 16 * NB, v.i0 + 16 * q, v.j0);
             }
             bulk_commit_group();
             bulk_wait_group_read0();

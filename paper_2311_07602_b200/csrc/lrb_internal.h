@@ -1,6 +1,7 @@
 // lrb_internal.h — context object and helpers shared by the C-ABI units.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -99,6 +100,14 @@ class HostPipe {
   std::vector<Pending> pend_[lrb_ctx::kLanes];
 };
 bool host_pinned(const void* p);
+int debug_flags();  // LRB_DEBUG_FLAGS probe bits (lrb_api.cu)
+// tensor maps (lrb_api.cu): a (rows, cols, z) column-major operand with box
+// (box_in, box_out, 1); the 4-D reconstruction output map (x, y, j, i) of an
+// n x n row-major matrix of b x b tiles, box 16 x nb, 128-byte swizzle.
+// False when TMA's alignment rules are not met.
+bool encode_operand(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld,
+                    int64_t stride, int64_t zdim, int box_in, int box_out);
+bool encode_tiles_c_map(CUtensorMap* map, double* out, int64_t n, int64_t b, int nb);
 void par_memcpy(void* dst, const void* src, size_t bytes);
 // stream-ordered allocation from the context pool (blocks stay mapped)
 inline cudaError_t pool_alloc(lrb_ctx* ctx, void** p, size_t bytes, cudaStream_t s) {

@@ -54,7 +54,7 @@ def test_expand_padded_output_leaves_gaps(ctx):
 
 
 @pytest.mark.parametrize("n,block,rank", [(96, 32, 6), (64, 16, 4), (256, 64, 16), (48, 48, 8),
-                                          (120, 24, 5), (1024, 128, 8)])
+                                          (120, 24, 5), (1024, 128, 8), (256, 32, 24), (512, 64, 32)])
 def test_reconstruct_dense_matches_reference(ctx, n, block, rank):
     m = B.BlrMatrix.random(n, block, rank, n + rank)
     full = m.reconstruct_dense(ctx=ctx)
