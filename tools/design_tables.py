@@ -43,7 +43,7 @@ def sweep_table(traffic):
                  f"**{c['roofline_frac']:.2f}** (single cold launch; bench, graph of 50 steps: 0.77) | "
                  f"{dram('cfg1'):.2f} |")
     c = by["cfg2"]
-    lines.append(f"| cfg2 | 512×512×32 × 4096 (NT) | q64 | {c['ms']:.3f} | {c['gflops']:.0f} | 7.11 | fp64 | "
+    lines.append(f"| cfg2 | 512×512×32 × 4096 (NT) | {c['variant']} | {c['ms']:.3f} | {c['gflops']:.0f} | 7.11 | fp64 | "
                  f"**{c['roofline_frac']:.2f}** | {dram('cfg2'):.2f} |")
     for b in W.CFG3_B:
         rs = [by[f"cfg3_b{b}_r{r}"] for r in W.CFG3_R]
