@@ -415,7 +415,7 @@ bool run_panel(lrb_ctx* ctx, const Gemm& g, int64_t batch, int beta_one, cudaStr
   const int flags = beta_one | debug_flags();
   int64_t grid = 0;
   cudaError_t e =
-      launch_panel(g.b_t, p, flags, ctx->sm_count, stream, &grid);
+      launch_panel(g.b_t, p, flags, ctx->device, ctx->sm_count, stream, &grid);
   if (e != cudaSuccess) {
     *status = cuda_fail(ctx, e, "lrb_panel_kernel launch");
     return true;

@@ -261,16 +261,18 @@ __global__ void __launch_bounds__(PanelCfg<B_T>::THREADS, 1)
 }
 
 template <bool B_T>
-cudaError_t launch_one(const StridedProblem& prob, int flags, int sm_count, cudaStream_t stream,
-                       int64_t* grid_out) {
+cudaError_t launch_one(const StridedProblem& prob, int flags, int device, int sm_count,
+                       cudaStream_t stream, int64_t* grid_out) {
   using P = PanelCfg<B_T>;
   auto kern = lrb_panel_kernel<B_T>;
-  static bool attr_set = false;  // per process; the attribute is per function
-  if (!attr_set) {
+  // the shared-memory opt-in is per function and device (set once each)
+  static bool attr_set[64] = {false};
+  const bool cached = device >= 0 && device < 64 && attr_set[device];
+  if (!cached) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(P::SMEM_BYTES));
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    if (device >= 0 && device < 64) attr_set[device] = true;
   }
   int64_t grid = sm_count;
   if (prob.num_tiles < grid) grid = prob.num_tiles;
@@ -285,10 +287,10 @@ cudaError_t launch_one(const StridedProblem& prob, int flags, int sm_count, cuda
 size_t panel_smem_bytes() { return PanelCfg<true>::SMEM_BYTES; }
 int panel_threads() { return PanelCfg<true>::THREADS; }
 
-cudaError_t launch_panel(int b_t, const StridedProblem& prob, int flags, int sm_count,
-                         cudaStream_t stream, int64_t* grid) {
-  return b_t ? launch_one<true>(prob, flags, sm_count, stream, grid)
-             : launch_one<false>(prob, flags, sm_count, stream, grid);
+cudaError_t launch_panel(int b_t, const StridedProblem& prob, int flags, int device,
+                         int sm_count, cudaStream_t stream, int64_t* grid) {
+  return b_t ? launch_one<true>(prob, flags, device, sm_count, stream, grid)
+             : launch_one<false>(prob, flags, device, sm_count, stream, grid);
 }
 
 }  // namespace lrb

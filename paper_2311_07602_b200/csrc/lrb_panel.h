@@ -20,7 +20,7 @@ size_t panel_smem_bytes();
 int panel_threads();
 // prob: the operand maps encoded with boxes (128 + 4) x 32 (A) and
 // (32 + 4) x 32 (B); num_tiles = units = ceil(m / 256) * batch.
-cudaError_t launch_panel(int b_t, const StridedProblem& prob, int flags, int sm_count,
-                         cudaStream_t stream, int64_t* grid);
+cudaError_t launch_panel(int b_t, const StridedProblem& prob, int flags, int device,
+                         int sm_count, cudaStream_t stream, int64_t* grid);
 
 }  // namespace lrb
