@@ -110,13 +110,28 @@ __global__ void __launch_bounds__(256) blr_couple_warp_kernel(const double* __re
   const int Q = tiles * (tiles - 1);
   const int rr = rank * rank, per = rank * nrhs;
   const int64_t pitch = block + int64_t(tiles - 1) * rank;
-  // rhs_i into the first block rows of row i's operand block: block i of
-  // the grid copies row tile i (contiguous b * nrhs doubles both sides)
-  const int64_t tile_elems = int64_t(block) * nrhs;
-  for (int i = blockIdx.x; i < tiles; i += gridDim.x) {
-    const double* src = rhs + int64_t(i) * tile_elems;
-    double* dst = rz + int64_t(i) * pitch * nrhs;
-    for (int64_t e = threadIdx.x; e < tile_elems; e += blockDim.x) dst[e] = __ldg(src + e);
+  // rhs_i into the first block rows of row i's operand block (contiguous
+  // b * nrhs doubles both sides), spread over the whole grid, four
+  // independent loads per thread in flight
+  {
+    const int64_t tile_elems = int64_t(block) * nrhs, total = int64_t(tiles) * tile_elems;
+    const int64_t step = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t e0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e0 < total; e0 += 4 * step) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t e = e0 + u * step;
+        v[u] = e < total ? __ldg(rhs + e) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t e = e0 + u * step;
+        if (e < total) {
+          const int64_t i = e / tile_elems;
+          rz[e + i * (pitch - block) * nrhs] = v[u];
+        }
+      }
+    }
   }
   double* xs = sm[warp];
   double* ws = xs + rr;
