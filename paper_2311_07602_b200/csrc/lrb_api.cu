@@ -260,10 +260,11 @@ int auto_variant(int64_t m, int64_t n, int64_t k_hint, int64_t batch, int sm_cou
 // stores, bit 2 orders tiles j-fastest, bit 3 uses default-policy stores,
 // bit 4 stops the operand refills after the prologue (stale data), bit 6
 // keeps C on the register epilogue (no TMA store), bit 5 / bit 7 load every
-// operand box evict-normal / evict-first
+// operand box evict-normal / evict-first, bit 8 runs the BLR matvec's row
+// step through the strided path instead of the two-source BlrRowProblem
 int debug_flags() {
   const char* s = std::getenv("LRB_DEBUG_FLAGS");
-  return s ? (std::atoi(s) & 254) : 0;
+  return s ? (std::atoi(s) & 510) : 0;
 }
 
 int env_variant() {

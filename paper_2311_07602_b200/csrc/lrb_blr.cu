@@ -112,8 +112,9 @@ __global__ void __launch_bounds__(256) blr_couple_warp_kernel(const double* __re
   const int64_t pitch = block + int64_t(tiles - 1) * rank;
   // rhs_i into the first block rows of row i's operand block (contiguous
   // b * nrhs doubles both sides), spread over the whole grid, four
-  // independent loads per thread in flight
-  {
+  // independent loads per thread in flight; skipped (rhs null) when the row
+  // step reads rhs directly (BlrRowProblem)
+  if (rhs) {
     const int64_t tile_elems = int64_t(block) * nrhs, total = int64_t(tiles) * tile_elems;
     const int64_t step = int64_t(gridDim.x) * blockDim.x;
     for (int64_t e0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e0 < total; e0 += 4 * step) {
@@ -199,7 +200,7 @@ __global__ void __launch_bounds__(256) blr_couple_kernel(const double* __restric
   const int64_t pitch = block + int64_t(tiles - 1) * rank;
   // rhs_i into the first block rows of row i's operand block
   const int64_t n_rhs = int64_t(tiles) * block * nrhs;
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n_rhs;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; rhs && e < n_rhs;
        e += int64_t(gridDim.x) * blockDim.x) {
     const int64_t i = e / (int64_t(block) * nrhs), rem = e - i * block * nrhs;
     rz[i * pitch * nrhs + rem] = __ldg(rhs + e);
@@ -467,18 +468,36 @@ extern "C" lrb_status lrb_blr_matvec_device(lrb_ctx* ctx, lrb_blr* m, const doub
   st = lrb::run_strided_rowmajor_beta(ctx, K, nrhs, b, m->d_vtcol, b, K * b, rhs, nrhs, b * nrhs,
                                       m->d_w, nrhs, K * nrhs, T, 0, s);
   if (st) return st;
-  // 2. Z_ij = X_ij W_ij into [rhs_i; Z_i*], and rhs_i copied there
+  // 3 (prepared first): the row step as a BlrRowProblem when its operands
+  // are TMA-addressable and b is a multiple of the 64-deep chunks: it reads
+  // rhs itself and starts its D_i rhs_i part while step 2 still runs
+  lrb::BlrRowProblem rp;
+  std::memset(&rp, 0, sizeof(rp));
+  using RowCfg8 = lrb::VariantTraits<LRB_V_M8K64>::Cfg<false, false, true>;
+  using RowCfg16 = lrb::VariantTraits<LRB_V_M16K64>::Cfg<false, false, true>;
+  const int mb = nrhs <= 8 ? RowCfg8::MB : RowCfg16::MB;
+  const bool row_ok =
+      nrhs <= 16 && b % RowCfg16::KB == 0 && !(lrb::debug_flags() & 256) &&
+      lrb::encode_operand(&rp.tmA, rhs, nrhs, b, nrhs, b * nrhs, T, mb + lrb::kPad,
+                          RowCfg16::KB) &&
+      lrb::encode_operand(&rp.tmA2, m->d_rz + b * nrhs, nrhs, K, nrhs, P * nrhs, T,
+                          mb + lrb::kPad, RowCfg16::KB) &&
+      lrb::encode_operand(&rp.tmB, m->d_dcat, P, b, P, b * P, T, RowCfg16::KB + lrb::kPad,
+                          RowCfg16::NB);
+  const double* copy_src = row_ok ? nullptr : rhs;
+  // 2. Z_ij = X_ij W_ij into [rhs_i; Z_i*] (and rhs_i copied there for the
+  //    strided fallback of step 3)
   if (r * r + r * nrhs <= kCoupleSmem) {
     const int64_t blocks = std::min<int64_t>((T * (T - 1) + 7) / 8, int64_t(ctx->sm_count) * 8);
     // Z rows land 16-byte aligned when b and r are even (pitch, offsets)
     if (r % 8 == 0 && nrhs % 8 == 0)
       LRB_CUDA_TRY(ctx, lrb::launch_pdl(blr_couple_warp_kernel<true>, dim3(unsigned(blocks)),
-                                        dim3(256), 0, s, m->d_x, m->d_w, rhs, m->d_rz, int(T),
-                                        int(b), int(r), int(nrhs)));
+                                        dim3(256), 0, s, m->d_x, m->d_w, copy_src, m->d_rz,
+                                        int(T), int(b), int(r), int(nrhs)));
     else
       LRB_CUDA_TRY(ctx, lrb::launch_pdl(blr_couple_warp_kernel<false>, dim3(unsigned(blocks)),
-                                        dim3(256), 0, s, m->d_x, m->d_w, rhs, m->d_rz, int(T),
-                                        int(b), int(r), int(nrhs)));
+                                        dim3(256), 0, s, m->d_x, m->d_w, copy_src, m->d_rz,
+                                        int(T), int(b), int(r), int(nrhs)));
     ctx->launches.fetch_add(1, std::memory_order_relaxed);
   } else {
     const int cp = (nrhs % 2 == 0) ? 2 : 1;
@@ -486,16 +505,33 @@ extern "C" lrb_status lrb_blr_matvec_device(lrb_ctx* ctx, lrb_blr* m, const doub
     const int64_t blocks = std::min<int64_t>((work + 255) / 256, int64_t(ctx->sm_count) * 16);
     if (cp == 2)
       LRB_CUDA_TRY(ctx, lrb::launch_pdl(blr_couple_kernel<2>, dim3(unsigned(blocks)), dim3(256), 0,
-                                        s, m->d_x, m->d_w, rhs, m->d_rz, int(T), int(b), int(r),
-                                        int(nrhs)));
+                                        s, m->d_x, m->d_w, copy_src, m->d_rz, int(T), int(b),
+                                        int(r), int(nrhs)));
     else
       LRB_CUDA_TRY(ctx, lrb::launch_pdl(blr_couple_kernel<1>, dim3(unsigned(blocks)), dim3(256), 0,
-                                        s, m->d_x, m->d_w, rhs, m->d_rz, int(T), int(b), int(r),
-                                        int(nrhs)));
+                                        s, m->d_x, m->d_w, copy_src, m->d_rz, int(T), int(b),
+                                        int(r), int(nrhs)));
     ctx->launches.fetch_add(1, std::memory_order_relaxed);
   }
   // 3. y_i = [D_i | U_i*] [rhs_i; Z_i*]: one chain per entry over D's columns,
   //    then the off-diagonal blocks j-major
+  if (row_ok) {
+    rp.C = y;
+    rp.m = int(nrhs);
+    rp.n = int(b);
+    rp.k = int(P);
+    rp.kb = int(b);
+    rp.tiles_i = 1;
+    rp.tiles_per_item = int((b + RowCfg16::NB - 1) / RowCfg16::NB);
+    rp.num_tiles = T * rp.tiles_per_item;
+    lrb::LaunchInfo info{0, 0};
+    if (nrhs <= 8)
+      LRB_CUDA_TRY(ctx, lrb::launch_gemm<RowCfg8>(rp, 0, ctx->device, ctx->sm_count, s, &info));
+    else
+      LRB_CUDA_TRY(ctx, lrb::launch_gemm<RowCfg16>(rp, 0, ctx->device, ctx->sm_count, s, &info));
+    if (info.grid > 0) ctx->launches.fetch_add(1, std::memory_order_relaxed);
+    return LRB_OK;
+  }
   return lrb::run_strided_rowmajor_beta(ctx, b, nrhs, P, m->d_dcat, P, b * P, m->d_rz, nrhs,
                                         P * nrhs, y, nrhs, b * nrhs, T, 0, s);
 }

@@ -21,6 +21,12 @@ __device__ __forceinline__ void pdl_entry() {
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
 }
+// the two halves, for kernels that start on independent data and wait only
+// before their first dependent read (BlrRowProblem)
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
 // LRB_PDL=0 launches without the programmatic-serialization attribute
 // (measurement probe)

@@ -147,6 +147,12 @@ struct StridedProblem {
   int c_tma;                 // tmC is valid: beta = 0, k >= 1, C TMA-aligned
   int64_t num_tiles;
 
+  static constexpr bool kDeferWait = false;
+  // the A map and k coordinate of chunk k0 (two-source problems switch maps)
+  __device__ __forceinline__ const void* a_src(const TileView& v, int k0, int* kc) const {
+    *kc = k0;
+    return v.tmA;
+  }
   __device__ __forceinline__ bool tma_store() const { return c_tma != 0; }
   // TMA-store one staged 16-row box of C at tile rows (x, y) of item v
   __device__ __forceinline__ void store_box(const TileView& v, const double* src, int x,
@@ -215,6 +221,11 @@ struct PtrProblem {
   const CUtensorMap* maps;  // 2 per item (A, B); null on the segment path
   int64_t num_tiles;
 
+  static constexpr bool kDeferWait = false;
+  __device__ __forceinline__ const void* a_src(const TileView& v, int k0, int* kc) const {
+    *kc = k0;
+    return v.tmA;
+  }
   __device__ __forceinline__ bool tma_store() const { return false; }
   __device__ __forceinline__ void store_box(const TileView&, const double*, int, int) const {}
 
@@ -267,6 +278,11 @@ struct BlrTileProblem {
   int c_tma;
   int64_t num_tiles;
 
+  static constexpr bool kDeferWait = false;
+  __device__ __forceinline__ const void* a_src(const TileView& v, int k0, int* kc) const {
+    *kc = k0;
+    return v.tmA;
+  }
   __device__ __forceinline__ bool tma_store() const { return c_tma != 0; }
   __device__ __forceinline__ void store_box(const TileView& v, const double* src, int x,
                                             int y) const {
@@ -301,6 +317,63 @@ struct BlrTileProblem {
     return v;
   }
   __device__ __forceinline__ int tile_k(int64_t) const { return r; }
+};
+
+// The BLR matvec's row step y_i = [D_i | U_i*] [rhs_i; Z_i*] (lrb_blr.cu) in
+// the column-major view y_i^T = [rhs_i^T | Z_i^T] [D_i | U_i*]^T: m = nrhs,
+// n = b, k = b + (T-1) r. The A operand has two sources split at k = kb (= b,
+// a multiple of the chunk depth): rhs_i (an input) for k < kb, and Z_i (the
+// coupling kernel's output) beyond. The kernel therefore starts on the D_i
+// rhs_i part while the coupling kernel still runs, and the issuing lane
+// executes griddepcontrol.wait before the first chunk that reads Z.
+struct BlrRowProblem {
+  CUtensorMap tmA;   // rhs: (nrhs, b, T), item stride b nrhs
+  CUtensorMap tmA2;  // Z: (nrhs, K, T), item stride pitch nrhs (rows b.. of rz)
+  CUtensorMap tmB;   // [D_i | U_i*]: (pitch, b, T) column-major view
+  double* C;         // y: nrhs x b per item (column-major view), ld nrhs
+  int m, n, k, kb;
+  int tiles_i, tiles_per_item;
+  int64_t num_tiles;
+
+  static constexpr bool kDeferWait = true;
+  __device__ __forceinline__ const void* a_src(const TileView&, int k0, int* kc) const {
+    if (k0 < kb) {
+      *kc = k0;
+      return &tmA;
+    }
+    pdl_wait();
+    *kc = k0 - kb;
+    return &tmA2;
+  }
+  __device__ __forceinline__ bool tma_store() const { return false; }
+  __device__ __forceinline__ void store_box(const TileView&, const double*, int, int) const {}
+  template <int MB, int NB>
+  __device__ __forceinline__ TileView tile(int64_t t) const {
+    const uint32_t tt = static_cast<uint32_t>(t), tpi = static_cast<uint32_t>(tiles_per_item);
+    const uint32_t item = tt / tpi;
+    const int rr = static_cast<int>(tt - item * tpi);
+    TileView v;
+    v.A = nullptr;  // TMA only
+    v.B = nullptr;
+    v.C = C + int64_t(item) * m * n;
+    v.lda = m;
+    v.ldb = k;
+    v.ldc = m;
+    v.m = m;
+    v.n = n;
+    v.k = k;
+    v.i0 = (rr % tiles_i) * MB;
+    v.j0 = (rr / tiles_i) * NB;
+    v.tmA = &tmA;
+    v.tmB = &tmB;
+    v.tmC = nullptr;
+    v.za = int(item);
+    v.zb = int(item);
+    v.zc = int(item);
+    v.zc2 = 0;
+    return v;
+  }
+  __device__ __forceinline__ int tile_k(int64_t) const { return k; }
 };
 
 // next chunk to issue, shared by the CTA's warps
@@ -352,10 +425,12 @@ __device__ __forceinline__ void issue_chunk(const Problem& prob, double* smem, u
       if (flags & 32) pol_a = pol_b = policy_evict_normal();  // debug probes
       if (flags & 128) pol_a = pol_b = policy_evict_first();
       mbar_arrive_expect_tx(&full[stage], uint32_t(Cfg::A_BOX + Cfg::B_BOX) * 8u);
+      int ka;
+      const void* map_a = prob.a_src(v, k0, &ka);
       if (Cfg::A_T)
-        tma_load_3d(As, v.tmA, k0, v.i0, v.za, &full[stage], pol_a);
+        tma_load_3d(As, map_a, ka, v.i0, v.za, &full[stage], pol_a);
       else
-        tma_load_3d(As, v.tmA, v.i0, k0, v.za, &full[stage], pol_a);
+        tma_load_3d(As, map_a, v.i0, ka, v.za, &full[stage], pol_a);
       if (Cfg::B_T)
         tma_load_3d(Bs, v.tmB, v.j0, k0, v.zb, &full[stage], pol_b);
       else
@@ -501,7 +576,10 @@ template <class Cfg, class Problem>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     lrb_gemm_kernel(const __grid_constant__ Problem prob, const int flags) {
   static_assert(Cfg::WARPS % 4 == 0, "warps per CTA must fill all four SM sub-partitions");
-  pdl_entry();
+  if constexpr (Problem::kDeferWait)
+    pdl_trigger();  // the problem waits before its first dependent load
+  else
+    pdl_entry();
   // flags bit 0: beta = 1 (accumulate into C); debug probes (LRB_DEBUG_FLAGS,
   // never set by the library itself): bit 1 skips the epilogue stores, bit 3
   // uses default-policy instead of streaming stores, bit 4 stops refilling the

@@ -58,7 +58,11 @@ def test_identity_like_maps_rhs_to_itself(ctx):
                                                    (3, 8, 11, 16), (1, 4, 3, 16), (8, 16, 16, 64),
                                                    # r^2 + r nrhs > 512: the register-blocked
                                                    # coupling kernel instead of warp-per-item
-                                                   (3, 24, 8, 48), (2, 16, 24, 32)])
+                                                   (3, 24, 8, 48), (2, 16, 24, 32),
+                                                   # b a multiple of 64, even nrhs <= 16: the
+                                                   # row step reads rhs itself (BlrRowProblem)
+                                                   (4, 8, 8, 64), (3, 16, 2, 128), (5, 8, 4, 64),
+                                                   (6, 16, 16, 128)])
 def test_grids_match_reference(ctx, tiles, rank, nrhs, block):
     m = B.BlrMatrix.random(tiles * block, block, rank, 100 + tiles + rank + nrhs)
     rhs = _rhs(tiles * block, nrhs, 17 + nrhs)
@@ -98,3 +102,33 @@ def test_constraints():
     m = B.BlrMatrix.random(64, 16, 4, 1)
     with pytest.raises(ShapeError, match="rhs has"):
         B.blr_matvec(m, DenseBlock(32, 2))
+
+
+@pytest.mark.parametrize("tiles,rank,nrhs,block", [(4, 8, 8, 64), (3, 8, 6, 20)])
+def test_device_matvec_in_a_graph_replayed(ctx, tiles, rank, nrhs, block):
+    # the three launches under stream capture (programmatic-dependent edges,
+    # the row step's deferred wait), replayed back to back: every replay
+    # bitwise equal to the eager device result and the FMA-chain oracle
+    from paper_2311_07602_b200.lrbatch import _check as check, lib
+
+    m = B.BlrMatrix.random(tiles * block, block, rank, 61 + tiles)
+    rhs = _rhs(tiles * block, nrhs, 5)
+    h = m.device_handle(ctx)
+    s = ctx.stream()
+    d_rhs = ctx.to_device(rhs.data)
+    y_eager, y_graph = ctx.empty(rhs.data.size), ctx.empty(rhs.data.size)
+    check(lib.lrb_blr_matvec_device(ctx._h, h, d_rhs.ptr, nrhs, y_eager.ptr, s.handle), ctx._h)
+    s.synchronize()
+    with ctx.capture(s) as cap:
+        check(lib.lrb_blr_matvec_device(ctx._h, h, d_rhs.ptr, nrhs, y_graph.ptr, s.handle),
+              ctx._h)
+    assert cap.graph.launches == 3
+    want = y_eager.download(rhs.data.size)
+    _check(m, rhs, DenseBlock(rhs.rows, rhs.cols, want))
+    for _ in range(5):
+        y_graph.fill_bytes(0)
+        ctx.synchronize()
+        cap.graph.launch(s)
+        cap.graph.launch(s)
+        s.synchronize()
+        assert np.array_equal(y_graph.download(rhs.data.size), want)
