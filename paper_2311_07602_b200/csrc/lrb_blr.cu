@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(256) blr_couple_warp_kernel(const double* __re
                                                               const double* __restrict__ rhs,
                                                               double* __restrict__ rz, int tiles,
                                                               int block, int rank, int nrhs) {
-  lrb::pdl_entry();
+  lrb::pdl_entry_ordered();  // the row step reads rhs before its own wait
   __shared__ double sm[8][kCoupleSmem];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Q = tiles * (tiles - 1);
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(256) blr_couple_kernel(const double* __restric
                                                          const double* __restrict__ rhs,
                                                          double* __restrict__ rz, int tiles,
                                                          int block, int rank, int nrhs) {
-  lrb::pdl_entry();
+  lrb::pdl_entry_ordered();  // the row step reads rhs before its own wait
   // a thread owns a 4-row x CP-column block of one Z_q (CP = 2 when nrhs is
   // even): per step k it loads four X values and one W pair for 4*CP FMAs;
   // every entry is still one r-long chain over k ascending. 32-bit indices:

@@ -27,6 +27,14 @@ __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// wait first, then let dependents launch: for the predecessor of a kernel
+// that reads some inputs before its own wait (BlrRowProblem reads rhs early).
+// Its dependents then start only after this grid's predecessor completed, so
+// data written two launches back (rhs, by the caller's kernel) is final.
+__device__ __forceinline__ void pdl_entry_ordered() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
 
 // LRB_PDL=0 launches without the programmatic-serialization attribute
 // (measurement probe)
