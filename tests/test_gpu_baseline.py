@@ -91,6 +91,30 @@ def test_cfg2_low_rank_expansion_sampled(ctx):
     _check_items(w, Cd, _sample(w.batch))
 
 
+def test_cfg2_every_item_panel_equals_tile_kernel(ctx):
+    # full size, every item: the row-panel kernel (p256, the automatic choice)
+    # and the tile kernel (q64) are independent implementations of the same
+    # in-order FMA chain, so all 4096 C_i must agree bitwise; sampled items
+    # are checked against the oracle above
+    w = W.get("cfg2")
+    A, B, Cd = _device_batch(ctx, w)
+    _run(ctx, w, A, B, Cd, w.batch)
+    assert ctx.last_variant == "p256"
+    C2 = ctx.empty(w.sC * w.batch)
+    ctx.set_variant_override("q64")
+    try:
+        _run(ctx, w, A, B, C2, w.batch)
+        assert ctx.last_variant == "q64"
+    finally:
+        ctx.set_variant_override(None)
+    per = 256
+    for it0 in range(0, w.batch, per):
+        cnt = min(per, w.batch - it0)
+        a = Cd.download(w.sC * cnt, offset_bytes=8 * w.sC * it0)
+        b = C2.download(w.sC * cnt, offset_bytes=8 * w.sC * it0)
+        assert np.array_equal(a, b), f"items {it0}..{it0 + cnt - 1}: p256 != q64"
+
+
 @pytest.mark.parametrize("b", W.CFG3_B)
 @pytest.mark.parametrize("r", W.CFG3_R)
 def test_cfg3_sweep_sampled(ctx, b, r):
