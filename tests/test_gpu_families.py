@@ -15,3 +15,11 @@ def test_every_kernel_family_once():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sanitize_cases.py")],
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("0 failures"), r.stdout + r.stderr
+
+
+def test_every_kernel_family_without_pdl():
+    # the same calls launched without programmatic dependent launch
+    env = dict(os.environ, LRB_PDL="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sanitize_cases.py")],
+                       capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0 and r.stdout.strip().endswith("0 failures"), r.stdout + r.stderr

@@ -54,6 +54,22 @@ def main():
                 check(f"gemm {v} {loader} beta={beta}", np.array_equal(dC.download(), want))
     ctx.set_variant_override(None)
     ctx.set_loader(None)
+    # the row-panel kernel (short k, U V^T): k = 32 and a k-tail, beta 0 and 1
+    for kp, beta in ((32, 0.0), (13, 1.0)):
+        mp, np_, bp = 300, 70, 3
+        Up = rng.uniform(-1, 1, mp * kp * bp)
+        Vp = rng.uniform(-1, 1, np_ * kp * bp)
+        Cp = rng.uniform(-1, 1, mp * np_ * bp)
+        dC = ctx.to_device(Cp)
+        ctx.set_variant_override("p256")
+        ctx.dgemm_strided_batched("C", "N", "T", mp, np_, kp, beta, ctx.to_device(Up), mp, mp * kp,
+                                  ctx.to_device(Vp), np_, np_ * kp, dC, mp, mp * np_, bp)
+        ran = ctx.last_variant
+        ctx.set_variant_override(None)
+        want = Cp.copy()
+        O.dgemm_strided("C", "N", "T", mp, np_, kp, beta, Up, mp, mp * kp, Vp, np_, np_ * kp, want,
+                        mp, mp * np_, bp)
+        check(f"panel k={kp} beta={beta}", ran == "p256" and np.array_equal(dC.download(), want))
     # pointer-array plan (variable sizes)
     ms, ns, ks = [64, 33, 130], [16, 40, 8], [64, 77, 130]
     As = [rng.uniform(-1, 1, a * c) for a, c in zip(ms, ks)]
@@ -83,6 +99,18 @@ def main():
     check("blr matvec", np.array_equal(y.data, O.blr_matvec(96, 32, 6, d, u, x, vt, rhs.data, 3)))
     full = mat.reconstruct_dense(ctx=ctx)
     check("blr reconstruct", np.array_equal(full.data, O.blr_reconstruct(96, 32, 6, d, u, x, vt)))
+    mat.invalidate()
+    # BLR with b a multiple of 64 and even nrhs: the two-source row step and
+    # the 4-D TMA-store reconstruction
+    mat = B.BlrMatrix.random(192, 64, 8, 4)
+    rhs = DenseBlock(192, 8, rng.uniform(-1, 1, 192 * 8))
+    y = B.blr_matvec(mat, rhs, ctx=ctx)
+    d, u, x, vt = mat.packed_arrays()
+    check("blr matvec (row problem)",
+          np.array_equal(y.data, O.blr_matvec(192, 64, 8, d, u, x, vt, rhs.data, 8)))
+    full = mat.reconstruct_dense(ctx=ctx)
+    check("blr reconstruct (tile problem)",
+          np.array_equal(full.data, O.blr_reconstruct(192, 64, 8, d, u, x, vt)))
     mat.invalidate()
     # low-rank expansion
     u2, x2, v2 = (rng.uniform(-1, 1, s) for s in (2 * 40 * 6, 2 * 36, 2 * 6 * 30))
