@@ -206,9 +206,12 @@ constexpr double kHbmBytesPerS = 6553.6e9;
 // sizes per shape class were chosen from the per-variant sweep in
 // profiles/sweep_variants_r01.jsonl.
 int auto_variant(int64_t m, int64_t n, int64_t k_hint, int64_t batch, int sm_count) {
+  // 64 x 64 tiles: the producer-warp form (q64p) unless k <= 16, where q64's
+  // TMA-store epilogue serves the write-bound products
+  const int q64 = k_hint > 16 ? LRB_V_Q64P : LRB_V_Q64;
   // small square-ish outputs (the r x r products of the low-rank product's
   // three-GEMM path): one 64 x 64 tile covers them with the least padding
-  if (m <= 64 && n <= 64 && m > 32 && n > 32) return LRB_V_Q64;
+  if (m <= 64 && n <= 64 && m > 32 && n > 32) return q64;
   if (n <= 64 && n <= m) {
     // small batches of skinny products (cfg1: 256 items of 256 x 16) would
     // fill fewer than two waves of 128-row tiles: 32-row tiles at five CTAs
@@ -246,10 +249,10 @@ int auto_variant(int64_t m, int64_t n, int64_t k_hint, int64_t batch, int sm_cou
   auto padded = [&](int64_t mb, int64_t nb) {
     return double((m + mb - 1) / mb * mb) * double((n + nb - 1) / nb * nb);
   };
-  int best = (k_hint >= 128 && m >= 128 && n >= 64) ? LRB_V_T64 : LRB_V_Q64;
+  int best = (k_hint >= 128 && m >= 128 && n >= 64) ? LRB_V_T64 : q64;
   double best_area = best == LRB_V_T64 ? padded(128, 64) : padded(64, 64);
   if (padded(64, 64) < best_area) {
-    best = LRB_V_Q64;
+    best = q64;
     best_area = padded(64, 64);
   }
   if (padded(96, 96) < best_area) best = LRB_V_S96;

@@ -3,6 +3,8 @@
 // lrb_gemm_v*.cu so the 9 x 4 x 2 kernels compile in parallel units).
 #pragma once
 
+#include <type_traits>
+
 #include "lrb_gemm.cuh"
 #include "lrb_variants.h"
 
@@ -11,11 +13,31 @@ namespace lrb {
 template <int ID>
 struct VariantTraits;
 
+// Variants whose TMA instantiations run a producer warp (ProdCfg): the
+// 4-warp tile shapes, where the fifth warp still leaves >= 128 registers per
+// thread. Measured against the all-computing-warps form on one box
+// (DESIGN.md 4.1): r = 32 class 0.79-0.83 -> 0.90-0.94 of FP64 peak, r = 16
+// rows 0.97-1.05 -> 1.05-1.09 of HBM, row-major short-wide rows +2-14%, the
+// BLR matvec +7-13%. The 8-warp shapes (n48, n56, n64, n64s4, sq, m64) were
+// neutral to -2.4%, s96 -8% and q64 with its TMA-store epilogue -9%: those
+// keep the release-counter form.
+template <int ID>
+struct VariantProd {
+  static constexpr bool value =
+      ID == LRB_V_N8 || ID == LRB_V_N16 || ID == LRB_V_N24 || ID == LRB_V_N32 ||
+      ID == LRB_V_N40 || ID == LRB_V_M8 || ID == LRB_V_M16 || ID == LRB_V_M32 ||
+      ID == LRB_V_N16T || ID == LRB_V_N16H || ID == LRB_V_M8T || ID == LRB_V_M16T ||
+      ID == LRB_V_T64 || ID == LRB_V_M16K64 || ID == LRB_V_M8K64 || ID == LRB_V_Q64P;
+};
+
 #define LRB_X(id, nm, WARPS_I, WARPS_J, WI, WJ, KB, ST, MINB)                        \
   template <>                                                                        \
   struct VariantTraits<id> {                                                         \
     template <bool AT, bool BT, bool TMA>                                            \
-    using Cfg = GemmCfg<WARPS_I, WARPS_J, WI, WJ, KB, ST, MINB, AT, BT, TMA>;        \
+    using Base = GemmCfg<WARPS_I, WARPS_J, WI, WJ, KB, ST, MINB, AT, BT, TMA>;       \
+    template <bool AT, bool BT, bool TMA>                                            \
+    using Cfg = std::conditional_t<VariantProd<id>::value && TMA,                    \
+                                   ProdCfg<Base<AT, BT, TMA>>, Base<AT, BT, TMA>>;   \
     static constexpr const char* name = #nm;                                         \
   };
 LRB_VARIANT_LIST(LRB_X)

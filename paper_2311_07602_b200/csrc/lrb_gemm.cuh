@@ -58,7 +58,10 @@ struct GemmCfg {
   static constexpr int MB = WARPS_I * WI, NB = WARPS_J * WJ;
   static constexpr int FI = WI / 8, FJ = WJ / 8;
   static constexpr int WARPS = WARPS_I * WARPS_J;
-  static constexpr int THREADS = WARPS * 32;
+  static constexpr int THREADS = WARPS * 32;  // the computing warps
+  // producer-warp form (ProdCfg): 0 here, all warps compute and refill
+  static constexpr int PROD_WARPS = 0;
+  static constexpr int LAUNCH_THREADS = THREADS;
   // operand pitches (doubles)
   static constexpr int PMA = MB + kPad;  // A K-rows  (op(A)=N): As[kk][i]
   static constexpr int PKA = KB + kPad;  // A K-contig (op(A)=T): As[i][kk]
@@ -113,6 +116,20 @@ struct GemmCfg {
   __device__ __forceinline__ static int b_off(int kk, int j) {
     return B_T ? kk * PNB + j : j * PKB + kk;
   }
+};
+
+// Producer-warp form of a TMA configuration: one extra warp issues every
+// refill behind per-slot empty mbarriers, so the computing warps only wait on
+// full / arrive on empty per chunk (no release counter, tile decode or TMA
+// issue on their path). With the TMA-store epilogue, warp 0 hands the slot
+// back for all computing warps once the TMA engine has read the staged C.
+template <class Base>
+struct ProdCfg : Base {
+  static constexpr int PROD_WARPS = 1;
+  static constexpr int LAUNCH_THREADS = Base::THREADS + 32;
+  // + the empty barriers (8-byte aligned after the release counters)
+  static constexpr size_t SMEM_BYTES = Base::SMEM_BYTES + size_t(Base::STAGES) * 8 + 8;
+  static_assert(Base::TMA, "the producer warp issues tensor-map loads only");
 };
 
 // ---------------------------------------------------------------- problems
@@ -391,6 +408,36 @@ __device__ __forceinline__ int64_t skip_empty_tiles(const Problem& prob, int64_t
 }
 
 // Issue the chunk described by *st into `stage` (whole warp), then advance *st.
+// Issue the TMA loads of chunk (v, k0) into `stage` (one lane).
+template <class Cfg, class Problem>
+__device__ __forceinline__ void issue_tma(const Problem& prob, const TileView& v, int k0,
+                                          double* As, double* Bs, uint64_t* full, int stage,
+                                          int flags) {
+  constexpr int MB = Cfg::MB, NB = Cfg::NB;
+  // An operand is streamed once when one column (A) / row (B) tile covers
+  // C, else reused by the neighbouring tiles (evict-last). Single-use
+  // streams still load evict-normal, not evict-first: every box reads
+  // kPad elements past the tile for its pitch — the next chunk's first
+  // k-columns (k-contiguous boxes) or the neighbouring tile's first rows —
+  // which must still be in L2 when that chunk or tile is loaded (measured:
+  // r = 8/16 sweeps 0.87-0.99 -> 0.95-1.04 of HBM)
+  uint64_t pol_a = (v.n <= NB) ? policy_evict_normal() : policy_evict_last();
+  uint64_t pol_b = (v.m <= MB) ? policy_evict_normal() : policy_evict_last();
+  if (flags & 32) pol_a = pol_b = policy_evict_normal();  // debug probes
+  if (flags & 128) pol_a = pol_b = policy_evict_first();
+  mbar_arrive_expect_tx(&full[stage], uint32_t(Cfg::A_BOX + Cfg::B_BOX) * 8u);
+  int ka;
+  const void* map_a = prob.a_src(v, k0, &ka);
+  if (Cfg::A_T)
+    tma_load_3d(As, map_a, ka, v.i0, v.za, &full[stage], pol_a);
+  else
+    tma_load_3d(As, map_a, v.i0, ka, v.za, &full[stage], pol_a);
+  if (Cfg::B_T)
+    tma_load_3d(Bs, v.tmB, v.j0, k0, v.zb, &full[stage], pol_b);
+  else
+    tma_load_3d(Bs, v.tmB, k0, v.j0, v.zb, &full[stage], pol_b);
+}
+
 template <class Cfg, class Problem>
 __device__ __forceinline__ void issue_chunk(const Problem& prob, double* smem, uint64_t* full,
                                             IssueState* st, int stage, int lane, int flags) {
@@ -412,30 +459,7 @@ __device__ __forceinline__ void issue_chunk(const Problem& prob, double* smem, u
   // order this CTA's generic-proxy reads of the slot before the async-proxy refill
   fence_proxy_async_smem();
   if constexpr (Cfg::TMA) {
-    if (lane == 0) {
-      // An operand is streamed once when one column (A) / row (B) tile covers
-      // C, else reused by the neighbouring tiles (evict-last). Single-use
-      // streams still load evict-normal, not evict-first: every box reads
-      // kPad elements past the tile for its pitch — the next chunk's first
-      // k-columns (k-contiguous boxes) or the neighbouring tile's first rows —
-      // which must still be in L2 when that chunk or tile is loaded (measured:
-      // r = 8/16 sweeps 0.87-0.99 -> 0.95-1.04 of HBM)
-      uint64_t pol_a = (v.n <= NB) ? policy_evict_normal() : policy_evict_last();
-      uint64_t pol_b = (v.m <= MB) ? policy_evict_normal() : policy_evict_last();
-      if (flags & 32) pol_a = pol_b = policy_evict_normal();  // debug probes
-      if (flags & 128) pol_a = pol_b = policy_evict_first();
-      mbar_arrive_expect_tx(&full[stage], uint32_t(Cfg::A_BOX + Cfg::B_BOX) * 8u);
-      int ka;
-      const void* map_a = prob.a_src(v, k0, &ka);
-      if (Cfg::A_T)
-        tma_load_3d(As, map_a, ka, v.i0, v.za, &full[stage], pol_a);
-      else
-        tma_load_3d(As, map_a, v.i0, ka, v.za, &full[stage], pol_a);
-      if (Cfg::B_T)
-        tma_load_3d(Bs, v.tmB, v.j0, k0, v.zb, &full[stage], pol_b);
-      else
-        tma_load_3d(Bs, v.tmB, k0, v.j0, v.zb, &full[stage], pol_b);
-    }
+    if (lane == 0) issue_tma<Cfg>(prob, v, k0, As, Bs, full, stage, flags);
   } else {
     const int ivalid = min(MB, v.m - v.i0);
     const int jvalid = min(NB, v.n - v.j0);
@@ -573,7 +597,7 @@ __device__ __forceinline__ void stage_c_tile(double* cs, const double (&acc)[Cfg
 }
 
 template <class Cfg, class Problem>
-__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
+__global__ void __launch_bounds__(Cfg::LAUNCH_THREADS, Cfg::MINB)
     lrb_gemm_kernel(const __grid_constant__ Problem prob, const int flags) {
   static_assert(Cfg::WARPS % 4 == 0, "warps per CTA must fill all four SM sub-partitions");
   if constexpr (Problem::kDeferWait)
@@ -596,6 +620,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(STAGES) * Cfg::STAGE_ELEMS);
   IssueState* st = reinterpret_cast<IssueState*>(full + STAGES);
   int* released = reinterpret_cast<int*>(st + 1);
+  // producer form: per-slot empty barriers after the release counters
+  uint64_t* empty = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(released + STAGES) + 7) & ~uintptr_t(7));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -605,15 +632,49 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       released[s] = 0;
+      if constexpr (Cfg::PROD_WARPS > 0) mbar_init(&empty[s], Cfg::WARPS);
     }
     st->t = skip_empty_tiles(prob, int64_t(blockIdx.x));
     st->k0 = 0;
     fence_mbar_init();
   }
   __syncthreads();
-  if (warp == 0) {
+  if constexpr (Cfg::PROD_WARPS > 0) {
+    if (warp == Cfg::WARPS) {
+      // the producer: the CTA's (tile, k-chunk) sequence in order, each
+      // chunk into slot q % STAGES once the computing warps have released it
+      if (lane == 0) {
+        int64_t t = skip_empty_tiles(prob, int64_t(blockIdx.x));
+        int k0 = 0;
+        int stage = 0;
+        uint32_t phase = 0;
+        int64_t q = 0;
 #pragma unroll 1
-    for (int s = 0; s < STAGES; ++s) issue_chunk<Cfg>(prob, smem, full, st, s, lane, flags);
+        while (t < prob.num_tiles) {
+          const TileView v = prob.template tile<MB, NB>(t);
+          if (q >= STAGES) mbar_wait(&empty[stage], phase ^ 1);
+          fence_proxy_async_smem();
+          double* As = smem + size_t(stage) * Cfg::STAGE_ELEMS;
+          issue_tma<Cfg>(prob, v, k0, As, As + Cfg::A_ELEMS, full, stage, flags);
+          k0 += KB;
+          if (k0 >= v.k) {
+            k0 = 0;
+            t = skip_empty_tiles(prob, t + gridDim.x);
+          }
+          ++q;
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      return;
+    }
+  } else {
+    if (warp == 0) {
+#pragma unroll 1
+      for (int s = 0; s < STAGES; ++s) issue_chunk<Cfg>(prob, smem, full, st, s, lane, flags);
+    }
   }
 
   const int wi = warp % Cfg::WARPS_I;
@@ -705,8 +766,16 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB)
             bulk_wait_group_read0();
           }
           __syncwarp();
-          if (!(flags & 16)) issue_chunk<Cfg>(prob, smem, full, st, stage, lane, flags);
+          if constexpr (Cfg::PROD_WARPS > 0) {
+            if (lane == 0) mbar_arrive_cnt(&empty[stage], Cfg::WARPS);
+          } else if (!(flags & 16)) {
+            issue_chunk<Cfg>(prob, smem, full, st, stage, lane, flags);
+          }
         }
+      } else if constexpr (Cfg::PROD_WARPS > 0) {
+        // hand the slot back to the producer
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
       } else {
         // release the slot; the last warp out refills it with the next chunk
         __syncwarp();
@@ -789,7 +858,8 @@ cudaError_t launch_gemm(const Problem& prob, int beta_one, int device, int sm_co
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(Cfg::SMEM_BYTES));
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::THREADS, Cfg::SMEM_BYTES);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::LAUNCH_THREADS,
+                                                      Cfg::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;
     if (device >= 0 && device < 64) occ_cache[device] = occ;
@@ -801,7 +871,7 @@ cudaError_t launch_gemm(const Problem& prob, int beta_one, int device, int sm_co
     info->occupancy = occ;
   }
   if (grid <= 0) return cudaSuccess;
-  return launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(Cfg::THREADS), Cfg::SMEM_BYTES,
+  return launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(Cfg::LAUNCH_THREADS), Cfg::SMEM_BYTES,
                     stream, prob, beta_one);
 }
 

@@ -36,6 +36,11 @@
 //         128 (the paper's rank-96 low-rank products: 0.48 -> 0.93).
 //   n24, n40, n48, n56 : intermediate widths so a variable-rank batch
 //         (cfg4, r_i in 8..64) wastes less than one 8-column fragment.
+//   q64p : q64 with a producer warp (lrb_dispatch.cuh VariantProd), for
+//         general shapes with k > 16; q64 itself keeps the TMA-store
+//         epilogue's synchronous slot hand-back for the write-bound k <= 16.
+// The 4-warp variants run a producer warp on their TMA path (VariantProd):
+// the computing warps then only wait on full / arrive on empty per chunk.
 #pragma once
 
 //            id  name  WARPS_I WARPS_J WI  WJ  KB  STAGES MINB
@@ -62,9 +67,10 @@
   X(19, t64, 2, 2, 64, 32, 32, 2, 2)   \
   X(20, s96, 2, 2, 48, 48, 32, 2, 2)   \
   X(21, m16k64, 1, 4, 16, 16, 64, 2, 2) \
-  X(22, m8k64, 1, 4, 8, 16, 64, 2, 2)
+  X(22, m8k64, 1, 4, 8, 16, 64, 2, 2)  \
+  X(23, q64p, 2, 2, 32, 32, 32, 2, 3)
 
-#define LRB_NUM_VARIANTS 23
+#define LRB_NUM_VARIANTS 24
 
 enum {
   LRB_V_N8 = 0,
@@ -89,5 +95,6 @@ enum {
   LRB_V_T64 = 19,
   LRB_V_S96 = 20,
   LRB_V_M16K64 = 21,
-  LRB_V_M8K64 = 22
+  LRB_V_M8K64 = 22,
+  LRB_V_Q64P = 23
 };

@@ -67,7 +67,7 @@ def test_no_device_here_fails_loudly():
 
 # ----------------------------------------------------------------- selector
 @pytest.mark.parametrize("m,n,k,want", [
-    (256, 16, 256, "n16"), (512, 512, 32, "p256"), (512, 512, 48, "q64"), (512, 32, 512, "n32"), (1024, 8, 1024, "n8"),
+    (256, 16, 256, "n16"), (512, 512, 32, "p256"), (512, 512, 48, "q64p"), (512, 512, 16, "q64"), (512, 32, 512, "n32"), (1024, 8, 1024, "n8"),
     (2048, 64, 2048, "n64"), (512, 24, 512, "n24"), (512, 40, 512, "n40"), (512, 48, 512, "n48"),
     (512, 56, 512, "n56"), (16, 512, 512, "m16k64"), (16, 512, 32, "m16"), (8, 300, 7, "m8"),
     (8, 300, 300, "m8k64"), (64, 200, 64, "m64"),
@@ -100,19 +100,20 @@ def test_selector_row_major_long_k_uses_k64_tiles():
 def test_selector_long_k_general_shapes_use_t64():
     # 128 x 64 tiles with 64 x 32 warp tiles once k >= 128 (the low-rank
     # product's r = 128 GEMMs); short-k U V^T (cfg2) takes the row-panel
-    # kernel, and stays on q64 where the panel does not serve (k > 32, op(A) = T)
+    # kernel, and q64p (q64 with a producer warp) where the panel does not
+    # serve (k > 32, op(A) = T)
     assert P.select("R", "N", "N", 128, 128, 1024, 20000)["name"] == "t64"
     assert P.select("R", "N", "N", 128, 128, 128, 20000)["name"] == "t64"
     assert P.select("C", "N", "T", 512, 512, 32, 4096)["name"] == "p256"
-    assert P.select("C", "N", "T", 512, 512, 33, 4096)["name"] == "q64"
-    assert P.select("C", "T", "T", 512, 512, 32, 4096)["name"] == "q64"
+    assert P.select("C", "N", "T", 512, 512, 33, 4096)["name"] == "q64p"
+    assert P.select("C", "T", "T", 512, 512, 32, 4096)["name"] == "q64p"
     # too few 256-row units for one wave, or too short: the tile kernel
-    assert P.select("C", "N", "T", 512, 512, 32, 50)["name"] == "q64"
+    assert P.select("C", "N", "T", 512, 512, 32, 50)["name"] == "q64p"
     # write-bound short k: the tile kernel's TMA-store epilogue
     assert P.select("C", "N", "T", 512, 512, 16, 4096)["name"] == "q64"
     assert P.select("C", "N", "T", 512, 512, 17, 4096)["name"] == "p256"
     assert P.select("C", "N", "T", 128, 512, 32, 4096)["name"] != "p256"
-    assert P.select("R", "N", "N", 64, 64, 1024, 20000)["name"] == "q64"
+    assert P.select("R", "N", "N", 64, 64, 1024, 20000)["name"] == "q64p"
 
 
 def test_selector_rank96_uses_s96():
@@ -120,7 +121,7 @@ def test_selector_rank96_uses_s96():
     assert P.select("R", "N", "N", 96, 96, 1024, 20000)["name"] == "s96"
     assert P.select("R", "N", "N", 96, 96, 96, 20000)["name"] == "s96"
     assert P.select("C", "N", "N", 80, 80, 64, 1000)["name"] == "s96"
-    assert P.select("C", "N", "T", 512, 512, 48, 4096)["name"] == "q64"
+    assert P.select("C", "N", "T", 512, 512, 48, 4096)["name"] == "q64p"
 
 
 def test_selector_row_major_swaps_roles():
