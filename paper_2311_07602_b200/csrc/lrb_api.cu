@@ -205,7 +205,8 @@ constexpr double kHbmBytesPerS = 6553.6e9;
 // Automatic choice on the column-major view (m x n output, inner k); tile
 // sizes per shape class were chosen from the per-variant sweep in
 // profiles/sweep_variants_r01.jsonl.
-int auto_variant(int64_t m, int64_t n, int64_t k_hint, int64_t batch, int sm_count) {
+int auto_variant(int64_t m, int64_t n, int64_t k_hint, int64_t batch, int sm_count,
+                 bool pointer_array = false) {
   // 64 x 64 tiles: the producer-warp form (q64p) unless k <= 16, where q64's
   // TMA-store epilogue serves the write-bound products
   const int q64 = k_hint > 16 ? LRB_V_Q64P : LRB_V_Q64;
@@ -225,7 +226,11 @@ int auto_variant(int64_t m, int64_t n, int64_t k_hint, int64_t batch, int sm_cou
     if (n <= 40) return LRB_V_N40;
     if (n <= 48) return LRB_V_N48;
     if (n <= 56) return LRB_V_N56;
-    return LRB_V_N64;
+    // r = 57..64: t64's 64 x 32 warp tiles with a producer warp beat n64's
+    // eight 32 x 32 warps once k >= 256 on strided batches (cfg3 r = 64:
+    // +1.2-2.3%, equal at b = 128); inside cfg4's concurrent pointer-array
+    // buckets n64 stays 1.7% ahead
+    return (k_hint >= 256 && !pointer_array) ? LRB_V_T64 : LRB_V_N64;
   }
   if (m <= 64 && m < n) {
     // short-wide C with a long inner dimension (the reference's row-major
@@ -284,10 +289,11 @@ int forced_variant(const lrb_ctx* ctx) {
 
 // a tile variant for the general kernel (the panel kernel, when forced, falls
 // back to the automatic tile choice on paths it does not serve)
-int choose_variant(const lrb_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t batch) {
+int choose_variant(const lrb_ctx* ctx, int64_t m, int64_t n, int64_t k, int64_t batch,
+                   bool pointer_array = false) {
   const int v = forced_variant(ctx);
   if (v >= 0 && v != kPanelVariant) return v;
-  return auto_variant(m, n, k, batch, ctx ? ctx->sm_count : 148);
+  return auto_variant(m, n, k, batch, ctx ? ctx->sm_count : 148, pointer_array);
 }
 
 // The row-panel kernel serves strided products whose column-major view has
@@ -971,7 +977,7 @@ extern "C" lrb_status lrb_ptr_plan_create(lrb_ctx* ctx, char order, char opA, ch
     d.k = int32_t(g.k);
     d.pad = 0;
     if (g.m == 0 || g.n == 0 || (g.k == 0 && beta == 1.0)) continue;
-    const int v = choose_variant(ctx, g.m, g.n, g.k, batch);
+    const int v = choose_variant(ctx, g.m, g.n, g.k, batch, true);
     const int64_t ti = (g.m + kVariants[v].mb - 1) / kVariants[v].mb;
     const int64_t tj = (g.n + kVariants[v].nb - 1) / kVariants[v].nb;
     if (ti > 0xFFFF || tj > 0xFFFF)

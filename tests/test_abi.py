@@ -68,7 +68,7 @@ def test_no_device_here_fails_loudly():
 # ----------------------------------------------------------------- selector
 @pytest.mark.parametrize("m,n,k,want", [
     (256, 16, 256, "n16"), (512, 512, 32, "p256"), (512, 512, 48, "q64p"), (512, 512, 16, "q64"), (512, 32, 512, "n32"), (1024, 8, 1024, "n8"),
-    (2048, 64, 2048, "n64"), (512, 24, 512, "n24"), (512, 40, 512, "n40"), (512, 48, 512, "n48"),
+    (2048, 64, 2048, "t64"), (128, 64, 128, "n64"), (512, 24, 512, "n24"), (512, 40, 512, "n40"), (512, 48, 512, "n48"),
     (512, 56, 512, "n56"), (16, 512, 512, "m16k64"), (16, 512, 32, "m16"), (8, 300, 7, "m8"),
     (8, 300, 300, "m8k64"), (64, 200, 64, "m64"),
 ])
