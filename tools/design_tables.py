@@ -73,8 +73,10 @@ def sweep_table(traffic):
                  f"{c['gflops']:.0f} | 8.18 | fp64 | **{c['roofline_frac']:.2f}** | {dram('cfg4'):.2f} |")
     w5 = W.get("cfg5")
     tr5 = traffic["cfg5"]["dram_bytes_per_launch"] / (w5.item_bytes() * 16384)
-    lines.append(f"| cfg5 | 512×32×512 × 16384 per launch | n32 | (bench) | 30300 | 7.11 | fp64 | **0.82** | "
-                 f"{tr5:.2f} |")
+    b5 = json.load(open(os.path.join(P, "bench_cfg5_r01.json")))
+    lines.append(f"| cfg5 | 512×32×512 × 131072 (1 GPU: 2 chunks per step) | {b5['config']['kernel_variant']} "
+                 f"| {b5['ms_per_step']:.2f} (bench) | {b5['value']:.0f} | 7.11 | fp64 | "
+                 f"**{b5['roofline']['frac']:.2f}** | {tr5:.2f} |")
     rr = jl("sweep_r01_rowmajor.jsonl")
     lines.append(
         "| cfg3r (reference row-major) | "
