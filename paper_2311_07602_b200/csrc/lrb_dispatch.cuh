@@ -18,14 +18,16 @@ struct VariantTraits;
 // thread. Measured against the all-computing-warps form on one box
 // (DESIGN.md 4.1): r = 32 class 0.79-0.83 -> 0.90-0.94 of FP64 peak, r = 16
 // rows 0.97-1.05 -> 1.05-1.09 of HBM, row-major short-wide rows +2-14%, the
-// BLR matvec +7-13%. The 8-warp shapes (n48, n56, n64, n64s4, sq, m64) were
-// neutral to -2.4%, s96 -8% and q64 with its TMA-store epilogue -9%: those
-// keep the release-counter form.
+// BLR matvec +7-13%; n48 / n56 as four 32 x 48 / 32 x 56 warps with the
+// producer beat their former 8-warp shapes by 2.6% / 4-4.5%. The 8-warp
+// shapes (n64, n64s4, sq, m64) were neutral to -2.4%, s96 -8% and q64 with
+// its TMA-store epilogue -9%: those keep the release-counter form.
 template <int ID>
 struct VariantProd {
   static constexpr bool value =
       ID == LRB_V_N8 || ID == LRB_V_N16 || ID == LRB_V_N24 || ID == LRB_V_N32 ||
-      ID == LRB_V_N40 || ID == LRB_V_M8 || ID == LRB_V_M16 || ID == LRB_V_M32 ||
+      ID == LRB_V_N40 || ID == LRB_V_N48 || ID == LRB_V_N56 || ID == LRB_V_M8 ||
+      ID == LRB_V_M16 || ID == LRB_V_M32 ||
       ID == LRB_V_N16T || ID == LRB_V_N16H || ID == LRB_V_M8T || ID == LRB_V_M16T ||
       ID == LRB_V_T64 || ID == LRB_V_M16K64 || ID == LRB_V_M8K64 || ID == LRB_V_Q64P;
 };

@@ -35,7 +35,8 @@
 //         sides are (multiples of) 96, where 64- and 128-wide tiles pad 96 to
 //         128 (the paper's rank-96 low-rank products: 0.48 -> 0.93).
 //   n24, n40, n48, n56 : intermediate widths so a variable-rank batch
-//         (cfg4, r_i in 8..64) wastes less than one 8-column fragment.
+//         (cfg4, r_i in 8..64) wastes less than one 8-column fragment; all
+//         four warps 32 rows tall (n48 / n56: 32 x 48 / 32 x 56 warp tiles).
 //   q64p : q64 with a producer warp (lrb_dispatch.cuh VariantProd), for
 //         general shapes with k > 16; q64 itself keeps the TMA-store
 //         epilogue's synchronous slot hand-back for the write-bound k <= 16.
@@ -56,8 +57,8 @@
   X(8, m64, 2, 4, 32, 32, 32, 2, 2)  \
   X(9, n24, 4, 1, 32, 24, 32, 2, 2)  \
   X(10, n40, 4, 1, 32, 40, 32, 2, 2) \
-  X(11, n48, 4, 2, 32, 24, 32, 2, 2) \
-  X(12, n56, 8, 1, 16, 56, 32, 2, 2) \
+  X(11, n48, 4, 1, 32, 48, 32, 2, 2) \
+  X(12, n56, 4, 1, 32, 56, 32, 2, 2) \
   X(13, q64, 2, 2, 32, 32, 32, 2, 3) \
   X(14, n64s4, 4, 2, 32, 32, 16, 4, 2) \
   X(15, n16t, 4, 1, 8, 16, 32, 2, 5)   \
