@@ -13,11 +13,14 @@
 //     across units. V streams in 32-column chunks through an 8-slot ring. The
 //     operands therefore leave DRAM about once, whatever the C stream does
 //     to L2.
-//   * Eight warps, all computing (2 per SM sub-partition, so each may hold
-//     255 registers; a ninth producer warp would cap them at 168 and spill).
-//     Operands arrive by TMA on full mbarriers; the last warp to release a
-//     V slot (or a U buffer) issues its refill from one lane, as in the
-//     general kernel, so no warp ever blocks to issue.
+//   * Eight MMA warps (two warpgroups, 2 warps per SM sub-partition) and a
+//     third warpgroup whose first warp issues every TMA load (U panels, V
+//     chunks) behind full / empty mbarriers. setmaxnreg moves the producer
+//     warpgroup's registers to the MMA warpgroups (40 / 232 per thread): a
+//     plain ninth warp caps everyone at 168 and the 64 x 32 slabs spill
+//     (cfg2 0.56). Against the self-refilling eight-warp form (the last warp
+//     to release a V slot or U buffer issues its refill, kept behind
+//     LRB_PANEL_PROD=0): cfg2 0.911 -> 0.918, store-free probe 0.948 -> 0.959.
 //   * The MMA warps form two groups of four. Group g takes the chunks of
 //     parity g: each warp owns a 64 x 32 slab of the chunk's 256 x 32 C tile
 //     (64 accumulators, 256 DMMAs per chunk at k = 32), and the groups run
@@ -36,7 +39,7 @@ namespace lrb {
 
 namespace {
 
-template <bool B_T>
+template <bool B_T, bool PROD = false>
 struct PanelCfg {
   // one MMA warp's view: a 128-row half panel (pitch 132) times a 32-column
   // chunk, warp tile 64 x 32 (GemmCfg supplies the fragment maps and offsets)
@@ -49,9 +52,12 @@ struct PanelCfg {
   static constexpr int U_ELEMS = 2 * HALF;
   static constexpr int V_ELEMS = W::B_ELEMS;
   static constexpr int MMA_WARPS = 8;
-  static constexpr int THREADS = MMA_WARPS * 32;
-  static constexpr size_t SMEM_BYTES =
-      (size_t(2) * U_ELEMS + size_t(S) * V_ELEMS) * 8 + size_t(2 + S) * 8 + size_t(2 + S) * 4;
+  // PROD: a third warpgroup whose first warp issues every TMA load;
+  // setmaxnreg moves its registers to the two MMA warpgroups
+  static constexpr int THREADS = MMA_WARPS * 32 + (PROD ? 128 : 0);
+  static constexpr int MMA_REGS = 232, PROD_REGS = 40;
+  static constexpr size_t SMEM_BYTES = (size_t(2) * U_ELEMS + size_t(S) * V_ELEMS) * 8 +
+                                       size_t(2 + S) * 8 * (PROD ? 2 : 1) + size_t(2 + S) * 4 + 8;
   static_assert(W::MB * 2 == ROWS, "two half panels per unit");
   static_assert(S % 2 == 0, "a slot must always feed the same group");
   static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
@@ -99,10 +105,10 @@ __device__ __forceinline__ void issue_chunk_v(const StridedProblem& prob, double
     tma_load_3d(vs, &prob.tmB, 0, c * P::COLS, zb, &v_full[s], pol);
 }
 
-template <bool B_T>
-__global__ void __launch_bounds__(PanelCfg<B_T>::THREADS, 1)
+template <bool B_T, bool PROD>
+__global__ void __launch_bounds__(PanelCfg<B_T, PROD>::THREADS, 1)
     lrb_panel_kernel(const __grid_constant__ StridedProblem prob, const int flags) {
-  using P = PanelCfg<B_T>;
+  using P = PanelCfg<B_T, PROD>;
   using W = typename P::W;
   constexpr int S = P::S, FI = W::FI, FJ = W::FJ;
   // flags bit 0: beta = 1; debug probe bit 1 skips the C stores
@@ -116,6 +122,10 @@ __global__ void __launch_bounds__(PanelCfg<B_T>::THREADS, 1)
   uint64_t* const v_full = bars + 2;         // [S]
   int* const u_rel = reinterpret_cast<int*>(bars + 2 + S);  // [2] warps past the unit
   int* const v_rel = u_rel + 2;                              // [S] warps past the chunk
+  // producer form: empty barriers after the counters (8-byte aligned)
+  uint64_t* const u_empty = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(v_rel + S) + 7) & ~uintptr_t(7));
+  uint64_t* const v_empty = u_empty + 2;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -132,20 +142,46 @@ __global__ void __launch_bounds__(PanelCfg<B_T>::THREADS, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&u_full[b], 1);
       u_rel[b] = 0;
+      if (PROD) mbar_init(&u_empty[b], P::MMA_WARPS);
     }
 #pragma unroll 1
     for (int s = 0; s < S; ++s) {
       mbar_init(&v_full[s], 1);
       v_rel[s] = 0;
+      if (PROD) mbar_init(&v_empty[s], P::MMA_WARPS / 2);
     }
     fence_mbar_init();
-    // prologue: the first two U panels and the first S chunks
-    for (int64_t lu = 0; lu < 2 && lu < my_units; ++lu)
-      issue_panel<P>(prob, U, u_full, lu, units_per_item);
-    for (int64_t q = 0; q < S && q < q_total; ++q)
-      issue_chunk_v<P, B_T>(prob, V, v_full, q, chunks, units_per_item);
+    if (!PROD) {
+      // prologue: the first two U panels and the first S chunks
+      for (int64_t lu = 0; lu < 2 && lu < my_units; ++lu)
+        issue_panel<P>(prob, U, u_full, lu, units_per_item);
+      for (int64_t q = 0; q < S && q < q_total; ++q)
+        issue_chunk_v<P, B_T>(prob, V, v_full, q, chunks, units_per_item);
+    }
   }
   __syncthreads();
+  if constexpr (PROD) {
+    if (warp >= P::MMA_WARPS) {
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(P::PROD_REGS));
+      // producer: U panels and V chunks in consumption order behind the
+      // empty barriers
+      if (warp == P::MMA_WARPS && lane == 0) {
+        int64_t q = 0;
+#pragma unroll 1
+        for (int64_t lu = 0; lu < my_units; ++lu) {
+          if (lu >= 2) mbar_wait(&u_empty[lu & 1], int((lu >> 1) - 1) & 1);
+          issue_panel<P>(prob, U, u_full, lu, units_per_item);
+#pragma unroll 1
+          for (int c = 0; c < chunks; ++c, ++q) {
+            if (q >= S) mbar_wait(&v_empty[q % S], int(q / S - 1) & 1);
+            issue_chunk_v<P, B_T>(prob, V, v_full, q, chunks, units_per_item);
+          }
+        }
+      }
+      return;
+    }
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(P::MMA_REGS));
+  }
 
   // -------------------------------------------------------------- MMA warps
   const int grp = warp >> 2;       // chunk parity this warp's group takes
@@ -222,7 +258,9 @@ __global__ void __launch_bounds__(PanelCfg<B_T>::THREADS, 1)
       // chunk q + S (same parity: this group's again). acq_rel orders the
       // four warps' reads of the slot before the async-proxy refill.
       __syncwarp();
-      if (lane == 0 && atom_add_acq_rel_cta(&v_rel[s], 1) == P::MMA_WARPS / 2 - 1) {
+      if (PROD) {
+        if (lane == 0) mbar_arrive(&v_empty[s]);
+      } else if (lane == 0 && atom_add_acq_rel_cta(&v_rel[s], 1) == P::MMA_WARPS / 2 - 1) {
         v_rel[s] = 0;
         if (q + S < q_total) issue_chunk_v<P, B_T>(prob, V, v_full, q + S, chunks, units_per_item);
       }
@@ -253,18 +291,20 @@ __global__ void __launch_bounds__(PanelCfg<B_T>::THREADS, 1)
     // the unit's U buffer is refilled (unit lu + 2) once all eight warps are
     // past it
     __syncwarp();
-    if (lane == 0 && atom_add_acq_rel_cta(&u_rel[b], 1) == P::MMA_WARPS - 1) {
+    if (PROD) {
+      if (lane == 0) mbar_arrive(&u_empty[b]);
+    } else if (lane == 0 && atom_add_acq_rel_cta(&u_rel[b], 1) == P::MMA_WARPS - 1) {
       u_rel[b] = 0;
       if (lu + 2 < my_units) issue_panel<P>(prob, U, u_full, lu + 2, units_per_item);
     }
   }
 }
 
-template <bool B_T>
+template <bool B_T, bool PROD>
 cudaError_t launch_one(const StridedProblem& prob, int flags, int device, int sm_count,
                        cudaStream_t stream, int64_t* grid_out) {
-  using P = PanelCfg<B_T>;
-  auto kern = lrb_panel_kernel<B_T>;
+  using P = PanelCfg<B_T, PROD>;
+  auto kern = lrb_panel_kernel<B_T, PROD>;
   // the shared-memory opt-in is per function and device (set once each)
   static bool attr_set[64] = {false};
   const bool cached = device >= 0 && device < 64 && attr_set[device];
@@ -284,13 +324,22 @@ cudaError_t launch_one(const StridedProblem& prob, int flags, int device, int sm
 
 }  // namespace
 
-size_t panel_smem_bytes() { return PanelCfg<true>::SMEM_BYTES; }
-int panel_threads() { return PanelCfg<true>::THREADS; }
+size_t panel_smem_bytes() { return PanelCfg<true, true>::SMEM_BYTES; }
+int panel_threads() { return PanelCfg<true, true>::THREADS; }
 
 cudaError_t launch_panel(int b_t, const StridedProblem& prob, int flags, int device,
                          int sm_count, cudaStream_t stream, int64_t* grid) {
-  return b_t ? launch_one<true>(prob, flags, device, sm_count, stream, grid)
-             : launch_one<false>(prob, flags, device, sm_count, stream, grid);
+  // the producer-warpgroup form by default; LRB_PANEL_PROD=0 (probe) runs
+  // the self-refilling eight-warp form
+  static const bool prod = [] {
+    const char* e = std::getenv("LRB_PANEL_PROD");
+    return !(e && e[0] == '0');
+  }();
+  if (prod)
+    return b_t ? launch_one<true, true>(prob, flags, device, sm_count, stream, grid)
+               : launch_one<false, true>(prob, flags, device, sm_count, stream, grid);
+  return b_t ? launch_one<true, false>(prob, flags, device, sm_count, stream, grid)
+             : launch_one<false, false>(prob, flags, device, sm_count, stream, grid);
 }
 
 }  // namespace lrb
