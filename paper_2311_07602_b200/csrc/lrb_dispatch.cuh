@@ -32,14 +32,23 @@ struct VariantProd {
       ID == LRB_V_T64 || ID == LRB_V_M16K64 || ID == LRB_V_M8K64 || ID == LRB_V_Q64P;
 };
 
+// variants that run a producer warpgroup with setmaxnreg (ProdWgCfg): s96,
+// whose 48 x 48 warp tiles need ~200 registers per thread
+template <int ID>
+struct VariantProdWg {
+  static constexpr bool value = ID == LRB_V_S96;
+};
+
 #define LRB_X(id, nm, WARPS_I, WARPS_J, WI, WJ, KB, ST, MINB)                        \
   template <>                                                                        \
   struct VariantTraits<id> {                                                         \
     template <bool AT, bool BT, bool TMA>                                            \
     using Base = GemmCfg<WARPS_I, WARPS_J, WI, WJ, KB, ST, MINB, AT, BT, TMA>;       \
     template <bool AT, bool BT, bool TMA>                                            \
-    using Cfg = std::conditional_t<VariantProd<id>::value && TMA,                    \
-                                   ProdCfg<Base<AT, BT, TMA>>, Base<AT, BT, TMA>>;   \
+    using Cfg = std::conditional_t<                                                  \
+        VariantProdWg<id>::value && TMA, ProdWgCfg<Base<AT, BT, TMA>, 40, 216>,      \
+        std::conditional_t<VariantProd<id>::value && TMA, ProdCfg<Base<AT, BT, TMA>>, \
+                           Base<AT, BT, TMA>>>;                                      \
     static constexpr const char* name = #nm;                                         \
   };
 LRB_VARIANT_LIST(LRB_X)

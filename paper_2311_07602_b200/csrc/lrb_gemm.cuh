@@ -62,6 +62,7 @@ struct GemmCfg {
   // producer-warp form (ProdCfg): 0 here, all warps compute and refill
   static constexpr int PROD_WARPS = 0;
   static constexpr int LAUNCH_THREADS = THREADS;
+  static constexpr int PROD_REGS = 0, MMA_REGS = 0;
   // operand pitches (doubles)
   static constexpr int PMA = MB + kPad;  // A K-rows  (op(A)=N): As[kk][i]
   static constexpr int PKA = KB + kPad;  // A K-contig (op(A)=T): As[i][kk]
@@ -127,9 +128,23 @@ template <class Base>
 struct ProdCfg : Base {
   static constexpr int PROD_WARPS = 1;
   static constexpr int LAUNCH_THREADS = Base::THREADS + 32;
+  static constexpr int PROD_REGS = 0, MMA_REGS = 0;  // no register hand-over
   // + the empty barriers (8-byte aligned after the release counters)
   static constexpr size_t SMEM_BYTES = Base::SMEM_BYTES + size_t(Base::STAGES) * 8 + 8;
   static_assert(Base::TMA, "the producer warp issues tensor-map loads only");
+};
+
+// Warpgroup-producer form for one computing warpgroup (4 warps) whose tiles
+// need more registers than a plain fifth warp leaves (s96's 48 x 48 warp
+// tiles): a whole producer warpgroup (one active warp) hands its registers
+// to the computing warpgroup with setmaxnreg. Two CTAs per SM: 2 x 256
+// threads at launch, then 128 x PR + 128 x MR = 32768 per CTA.
+template <class Base, int PR, int MR>
+struct ProdWgCfg : ProdCfg<Base> {
+  static_assert(Base::WARPS == 4, "one computing warpgroup");
+  static constexpr int PROD_WARPS = 4;
+  static constexpr int LAUNCH_THREADS = Base::THREADS + 128;
+  static constexpr int PROD_REGS = PR, MMA_REGS = MR;
 };
 
 // ---------------------------------------------------------------- problems
@@ -640,10 +655,14 @@ __global__ void __launch_bounds__(Cfg::LAUNCH_THREADS, Cfg::MINB)
   }
   __syncthreads();
   if constexpr (Cfg::PROD_WARPS > 0) {
-    if (warp == Cfg::WARPS) {
+    if (warp >= Cfg::WARPS) {
+      // warpgroup form: hand the producer warpgroup's registers to the
+      // computing warpgroup
+      if constexpr (Cfg::PROD_REGS > 0)
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(Cfg::PROD_REGS));
       // the producer: the CTA's (tile, k-chunk) sequence in order, each
       // chunk into slot q % STAGES once the computing warps have released it
-      if (lane == 0) {
+      if (warp == Cfg::WARPS && lane == 0) {
         int64_t t = skip_empty_tiles(prob, int64_t(blockIdx.x));
         int k0 = 0;
         int stage = 0;
@@ -670,6 +689,8 @@ __global__ void __launch_bounds__(Cfg::LAUNCH_THREADS, Cfg::MINB)
       }
       return;
     }
+    if constexpr (Cfg::MMA_REGS > 0)
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(Cfg::MMA_REGS));
   } else {
     if (warp == 0) {
 #pragma unroll 1
