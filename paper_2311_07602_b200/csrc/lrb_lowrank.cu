@@ -42,7 +42,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn();
 template <int R>
 struct LrCfg {
   static constexpr int G = 4;  // items per CTA, one warp each
-  static constexpr int THREADS = 32 * G;
+  // r = 8: a fifth warp issues the refills behind empty barriers (the item
+  // warps' 4-stage ring turns over fastest there): 0.95-0.98 -> 1.00-1.02 of
+  // HBM. r = 16 measured within +-1% either way, and r = 32 needs 255
+  // registers: both keep the last-warp-out refill
+  static constexpr bool PROD = R <= 8;
+  static constexpr int THREADS = 32 * G + (PROD ? 32 : 0);
   static constexpr int KB = (R >= 32) ? 16 : 32;
   static constexpr int STAGES = (R <= 8) ? 4 : 2;
   static constexpr int F = R / 8;
@@ -54,7 +59,8 @@ struct LrCfg {
   static constexpr int BU_ELEMS = round_up_c(BU * G, 16);
   static constexpr int STAGE = AV_ELEMS + BU_ELEMS;
   static constexpr size_t SMEM =
-      size_t(STAGES) * STAGE * 8 + size_t(STAGES) * 8 + size_t(STAGES) * 4 + 32;
+      size_t(STAGES) * STAGE * 8 + size_t(STAGES) * 8 + size_t(STAGES) * 4 + 32 +
+      (PROD ? size_t(STAGES) * 8 + 8 : 0);
 };
 
 struct LrProblem {
@@ -118,6 +124,8 @@ __global__ void __launch_bounds__(LrCfg<R>::THREADS, 2)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(STAGES) * Cf::STAGE);
   IssueState* st = reinterpret_cast<IssueState*>(full + STAGES);
   int* released = reinterpret_cast<int*>(st + 1);
+  uint64_t* empty = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(released + STAGES) + 7) & ~uintptr_t(7));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
   const int r = p.rank;
@@ -126,14 +134,36 @@ __global__ void __launch_bounds__(LrCfg<R>::THREADS, 2)
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       released[s] = 0;
+      if (Cf::PROD) mbar_init(&empty[s], Cf::G);
     }
     st->t = blockIdx.x;
     st->k0 = 0;
     fence_mbar_init();
   }
   __syncthreads();
-  if (warp == 0)
-    for (int s = 0; s < STAGES; ++s) lr_issue<Cf>(p, smem, full, st, s, lane);
+  if constexpr (Cf::PROD) {
+    if (warp == Cf::G) {
+      // producer: every (group, k-chunk) of the CTA in order, each into its
+      // slot once the four item warps have released it
+      int q = 0;
+#pragma unroll 1
+      for (;; ++q) {
+        const int s = q % STAGES;
+        if (q >= STAGES) {
+          if (lane == 0) mbar_wait(&empty[s], ((q / STAGES) - 1) & 1);
+          __syncwarp();
+        }
+        long long t_ll = 0;
+        if (lane == 0) t_ll = st->t;
+        if (__shfl_sync(0xffffffffu, t_ll, 0) >= p.groups) break;
+        lr_issue<Cf>(p, smem, full, st, s, lane);
+      }
+      return;
+    }
+  } else {
+    if (warp == 0)
+      for (int s = 0; s < STAGES; ++s) lr_issue<Cf>(p, smem, full, st, s, lane);
+  }
 
   int stage = 0;
   uint32_t phase = 0;
@@ -191,13 +221,17 @@ __global__ void __launch_bounds__(LrCfg<R>::THREADS, 2)
         }
       }
       __syncwarp();
-      int last = 0;
-      if (lane == 0) {
-        last = (atom_add_acq_rel_cta(&released[stage], 1) == Cf::G - 1);
-        if (last) released[stage] = 0;
+      if constexpr (Cf::PROD) {
+        if (lane == 0) mbar_arrive(&empty[stage]);
+      } else {
+        int last = 0;
+        if (lane == 0) {
+          last = (atom_add_acq_rel_cta(&released[stage], 1) == Cf::G - 1);
+          if (last) released[stage] = 0;
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) lr_issue<Cf>(p, smem, full, st, stage, lane);
       }
-      last = __shfl_sync(0xffffffffu, last, 0);
-      if (last) lr_issue<Cf>(p, smem, full, st, stage, lane);
       if (++stage == STAGES) {
         stage = 0;
         phase ^= 1;
