@@ -18,7 +18,8 @@
 //         low-rank expansion U * V^T, blr.hpp:75-78): more independent CTAs
 //         overlap one CTA's epilogue and operand wait with the others' MMAs.
 //   n64s4 : KB = 16 alternative kept for the selector sweep.
-//   n16t : 32-row tiles at five CTAs per SM for small skinny batches (cfg1).
+//   n16t : 32-row tiles at seven CTAs per SM for small skinny batches (cfg1;
+//         seven with the producer warp: 2048 tiles in 1.98 waves).
 //   n16h : 64-row tiles, sweep candidate.
 //   m8t, m16t : 32-column tiles at five CTAs per SM, the m* shapes of small
 //         batches (the BLR matvec's per-row launches: 64 items of 8 x 512).
@@ -61,7 +62,7 @@
   X(12, n56, 4, 1, 32, 56, 32, 2, 2) \
   X(13, q64, 2, 2, 32, 32, 32, 2, 3) \
   X(14, n64s4, 4, 2, 32, 32, 16, 4, 2) \
-  X(15, n16t, 4, 1, 8, 16, 32, 2, 5)   \
+  X(15, n16t, 4, 1, 8, 16, 32, 2, 7)   \
   X(16, n16h, 4, 1, 16, 16, 32, 2, 4)  \
   X(17, m8t, 1, 4, 8, 8, 32, 2, 5)     \
   X(18, m16t, 1, 4, 16, 8, 32, 2, 5)   \
