@@ -207,9 +207,10 @@ constexpr double kHbmBytesPerS = 6553.6e9;
 // profiles/sweep_variants_r01.jsonl.
 int auto_variant(int64_t m, int64_t n, int64_t k_hint, int64_t batch, int sm_count,
                  bool pointer_array = false) {
-  // 64 x 64 tiles: the producer-warp form (q64p) unless k <= 16, where q64's
-  // TMA-store epilogue serves the write-bound products
-  const int q64 = k_hint > 16 ? LRB_V_Q64P : LRB_V_Q64;
+  // 64 x 64 tiles: the producer-warp form (q64p; q64q with a 3-stage ring
+  // once k >= 256) unless k <= 16, where q64's TMA-store epilogue serves the
+  // write-bound products
+  const int q64 = k_hint >= 256 ? LRB_V_Q64Q : (k_hint > 16 ? LRB_V_Q64P : LRB_V_Q64);
   // small square-ish outputs (the r x r products of the low-rank product's
   // three-GEMM path): one 64 x 64 tile covers them with the least padding
   if (m <= 64 && n <= 64 && m > 32 && n > 32) return q64;

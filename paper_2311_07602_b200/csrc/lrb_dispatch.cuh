@@ -29,7 +29,8 @@ struct VariantProd {
       ID == LRB_V_N40 || ID == LRB_V_N48 || ID == LRB_V_N56 || ID == LRB_V_M8 ||
       ID == LRB_V_M16 || ID == LRB_V_M32 ||
       ID == LRB_V_N16T || ID == LRB_V_N16H || ID == LRB_V_M8T || ID == LRB_V_M16T ||
-      ID == LRB_V_T64 || ID == LRB_V_M16K64 || ID == LRB_V_M8K64 || ID == LRB_V_Q64P;
+      ID == LRB_V_T64 || ID == LRB_V_M16K64 || ID == LRB_V_M8K64 || ID == LRB_V_Q64P ||
+      ID == LRB_V_Q64Q;
 };
 
 // variants that run a producer warpgroup with setmaxnreg (ProdWgCfg): s96,

@@ -41,6 +41,8 @@
 //   q64p : q64 with a producer warp (lrb_dispatch.cuh VariantProd), for
 //         general shapes with k > 16; q64 itself keeps the TMA-store
 //         epilogue's synchronous slot hand-back for the write-bound k <= 16.
+//   q64q : q64p with a 3-stage ring at two CTAs per SM, for k >= 256 (the
+//         low-rank r = 64 product's 64 x 64 x b GEMM: +5-6%).
 // The 4-warp variants run a producer warp on their TMA path (VariantProd):
 // the computing warps then only wait on full / arrive on empty per chunk.
 #pragma once
@@ -70,9 +72,10 @@
   X(20, s96, 2, 2, 48, 48, 32, 2, 2)   \
   X(21, m16k64, 1, 4, 16, 16, 64, 2, 2) \
   X(22, m8k64, 1, 4, 8, 16, 64, 2, 2)  \
-  X(23, q64p, 2, 2, 32, 32, 32, 2, 3)
+  X(23, q64p, 2, 2, 32, 32, 32, 2, 3) \
+  X(24, q64q, 2, 2, 32, 32, 32, 3, 2)
 
-#define LRB_NUM_VARIANTS 24
+#define LRB_NUM_VARIANTS 25
 
 enum {
   LRB_V_N8 = 0,
@@ -98,5 +101,6 @@ enum {
   LRB_V_S96 = 20,
   LRB_V_M16K64 = 21,
   LRB_V_M8K64 = 22,
-  LRB_V_Q64P = 23
+  LRB_V_Q64P = 23,
+  LRB_V_Q64Q = 24
 };

@@ -113,7 +113,8 @@ def test_selector_long_k_general_shapes_use_t64():
     assert P.select("C", "N", "T", 512, 512, 16, 4096)["name"] == "q64"
     assert P.select("C", "N", "T", 512, 512, 17, 4096)["name"] == "p256"
     assert P.select("C", "N", "T", 128, 512, 32, 4096)["name"] != "p256"
-    assert P.select("R", "N", "N", 64, 64, 1024, 20000)["name"] == "q64p"
+    assert P.select("R", "N", "N", 64, 64, 1024, 20000)["name"] == "q64q"
+    assert P.select("R", "N", "N", 64, 64, 128, 20000)["name"] == "q64p"
 
 
 def test_selector_rank96_uses_s96():
