@@ -267,7 +267,8 @@ int auto_variant(int64_t m, int64_t n, int64_t k_hint, int64_t batch, int sm_cou
 
 // debug-only kernel flags for probes (tools/probe_cfg2.py): bit 1 skips C
 // stores, bit 2 orders tiles j-fastest, bit 3 uses default-policy stores,
-// bit 4 stops the operand refills after the prologue (stale data), bit 6
+// bit 4 stops the operand refills after the prologue (stale data; release-
+// counter form only), bit 6
 // keeps C on the register epilogue (no TMA store), bit 5 / bit 7 load every
 // operand box evict-normal / evict-first, bit 8 runs the BLR matvec's row
 // step through the strided path instead of the two-source BlrRowProblem
