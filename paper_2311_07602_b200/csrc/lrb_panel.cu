@@ -21,6 +21,10 @@
 //     (cfg2 0.56). Against the self-refilling eight-warp form (the last warp
 //     to release a V slot or U buffer issues its refill, kept behind
 //     LRB_PANEL_PROD=0): cfg2 0.911 -> 0.918, store-free probe 0.948 -> 0.959.
+//   * The producer form also splits the last round of units: its rem units
+//     are cut into column ranges over rem * split CTAs, so the wave tail
+//     costs 1 / split of a unit (cfg2: 55 rounds + 52 units, split in 2;
+//     0.918 -> 0.924).
 //   * The MMA warps form two groups of four. Group g takes the chunks of
 //     parity g: each warp owns a 64 x 32 slab of the chunk's 256 x 32 C tile
 //     (64 accumulators, 256 DMMAs per chunk at k = 32), and the groups run
@@ -39,6 +43,10 @@ namespace lrb {
 
 namespace {
 
+// producer form: registers per thread after setmaxnreg (MMA warpgroups,
+// producer warpgroup): 2 x 128 x 232 + 128 x 40 = 64.5K of the SM's 64K
+constexpr int kPanelMmaRegs = 232, kPanelProdRegs = 40;
+
 template <bool B_T, bool PROD = false>
 struct PanelCfg {
   // one MMA warp's view: a 128-row half panel (pitch 132) times a 32-column
@@ -55,7 +63,6 @@ struct PanelCfg {
   // PROD: a third warpgroup whose first warp issues every TMA load;
   // setmaxnreg moves its registers to the two MMA warpgroups
   static constexpr int THREADS = MMA_WARPS * 32 + (PROD ? 128 : 0);
-  static constexpr int MMA_REGS = 232, PROD_REGS = 40;
   static constexpr size_t SMEM_BYTES = (size_t(2) * U_ELEMS + size_t(S) * V_ELEMS) * 8 +
                                        size_t(2 + S) * 8 * (PROD ? 2 : 1) + size_t(2 + S) * 4 + 8;
   static_assert(W::MB * 2 == ROWS, "two half panels per unit");
@@ -80,6 +87,40 @@ __device__ __forceinline__ void issue_panel(const StridedProblem& prob, double* 
   mbar_arrive_expect_tx(&u_full[b], uint32_t(2 * W::A_BOX) * 8u);
   tma_load_3d(ub, &prob.tmA, i0, 0, za, &u_full[b], pol);
   tma_load_3d(ub + P::HALF, &prob.tmA, i0 + W::MB, 0, za, &u_full[b], pol);
+}
+
+// Producer form: unit u's U panel into buffer b, and chunk c of unit u into
+// slot s (one lane)
+template <class P>
+__device__ __forceinline__ void issue_panel_u(const StridedProblem& prob, double* U,
+                                              uint64_t* u_full, int b, int64_t u,
+                                              int units_per_item) {
+  using W = typename P::W;
+  const int64_t item = u / units_per_item;
+  const int i0 = int(u - item * units_per_item) * P::ROWS;
+  const int za = prob.a_batched ? int(item) : 0;
+  double* ub = U + b * P::U_ELEMS;
+  const uint64_t pol = policy_evict_normal();
+  fence_proxy_async_smem();
+  mbar_arrive_expect_tx(&u_full[b], uint32_t(2 * W::A_BOX) * 8u);
+  tma_load_3d(ub, &prob.tmA, i0, 0, za, &u_full[b], pol);
+  tma_load_3d(ub + P::HALF, &prob.tmA, i0 + W::MB, 0, za, &u_full[b], pol);
+}
+template <class P, bool B_T>
+__device__ __forceinline__ void issue_chunk_u(const StridedProblem& prob, double* V,
+                                              uint64_t* v_full, int s, int64_t u, int c,
+                                              int units_per_item) {
+  using W = typename P::W;
+  const int64_t item = u / units_per_item;
+  const int zb = prob.b_batched ? int(item) : 0;
+  double* vs = V + s * P::V_ELEMS;
+  const uint64_t pol = units_per_item > 1 ? policy_evict_last() : policy_evict_normal();
+  fence_proxy_async_smem();
+  mbar_arrive_expect_tx(&v_full[s], uint32_t(W::B_BOX) * 8u);
+  if (B_T)
+    tma_load_3d(vs, &prob.tmB, c * P::COLS, 0, zb, &v_full[s], pol);
+  else
+    tma_load_3d(vs, &prob.tmB, 0, c * P::COLS, zb, &v_full[s], pol);
 }
 
 // Issue chunk q (the CTA's q-th 32-column V chunk) into slot q % S (one lane).
@@ -136,6 +177,25 @@ __global__ void __launch_bounds__(PanelCfg<B_T, PROD>::THREADS, 1)
   const int64_t my_units =
       blockIdx.x < num_units ? (num_units - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t q_total = my_units * chunks;
+  // Producer form: when the last round of units would leave most CTAs idle,
+  // its rem units are split into column ranges over rem * split CTAs (cfg2:
+  // 8192 units on 148 CTAs = 55 rounds + 52 units, split in 2)
+  int64_t n_full = my_units, part_unit = -1;
+  int part_lo = 0, part_hi = 0;
+  if (PROD) {
+    const int64_t G = gridDim.x, rounds = num_units / G, rem = num_units - rounds * G;
+    const int64_t split = rem > 0 ? min(int64_t(chunks), G / rem) : 1;
+    if (split >= 2) {
+      n_full = rounds;
+      if (blockIdx.x < rem * split) {
+        const int64_t pu = blockIdx.x / split, part = blockIdx.x - pu * split;
+        part_unit = rounds * G + pu;
+        part_lo = int(part * chunks / split);
+        part_hi = int((part + 1) * chunks / split);
+      }
+    }
+  }
+  const int64_t n_items = n_full + (part_unit >= 0 ? 1 : 0);
 
   if (threadIdx.x == 0) {
 #pragma unroll
@@ -162,25 +222,28 @@ __global__ void __launch_bounds__(PanelCfg<B_T, PROD>::THREADS, 1)
   __syncthreads();
   if constexpr (PROD) {
     if (warp >= P::MMA_WARPS) {
-      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(P::PROD_REGS));
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kPanelProdRegs));
       // producer: U panels and V chunks in consumption order behind the
       // empty barriers
       if (warp == P::MMA_WARPS && lane == 0) {
         int64_t q = 0;
 #pragma unroll 1
-        for (int64_t lu = 0; lu < my_units; ++lu) {
+        for (int64_t lu = 0; lu < n_items; ++lu) {
+          const bool full = lu < n_full;
+          const int64_t u = full ? blockIdx.x + lu * gridDim.x : part_unit;
           if (lu >= 2) mbar_wait(&u_empty[lu & 1], int((lu >> 1) - 1) & 1);
-          issue_panel<P>(prob, U, u_full, lu, units_per_item);
+          issue_panel_u<P>(prob, U, u_full, int(lu & 1), u, units_per_item);
+          const int hi = full ? chunks : part_hi;
 #pragma unroll 1
-          for (int c = 0; c < chunks; ++c, ++q) {
+          for (int c = full ? 0 : part_lo; c < hi; ++c, ++q) {
             if (q >= S) mbar_wait(&v_empty[q % S], int(q / S - 1) & 1);
-            issue_chunk_v<P, B_T>(prob, V, v_full, q, chunks, units_per_item);
+            issue_chunk_u<P, B_T>(prob, V, v_full, int(q % S), u, c, units_per_item);
           }
         }
       }
       return;
     }
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(P::MMA_REGS));
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kPanelMmaRegs));
   }
 
   // -------------------------------------------------------------- MMA warps
@@ -191,17 +254,19 @@ __global__ void __launch_bounds__(PanelCfg<B_T, PROD>::THREADS, 1)
   const int g = lane >> 2, tq = lane & 3;
 
   int64_t q = 0;
-  int64_t lu = 0;
 #pragma unroll 1
-  for (int64_t u = blockIdx.x; u < num_units; u += gridDim.x, ++lu) {
+  for (int64_t lu = 0; lu < n_items; ++lu) {
+    const bool full_unit = lu < n_full;
+    const int64_t u = full_unit ? blockIdx.x + lu * gridDim.x : part_unit;
     const int64_t item = u / units_per_item;
     const int i0 = int(u - item * units_per_item) * P::ROWS + half * W::MB;  // this half's row 0
     double* const Cb = prob.C + item * prob.sC;
     const int b = int(lu & 1);
     mbar_wait(&u_full[b], int(lu >> 1) & 1);
     const double* As = U + b * P::U_ELEMS + half * P::HALF;
+    const int c_hi = full_unit ? chunks : part_hi;
 #pragma unroll 1
-    for (int c = 0; c < chunks; ++c, ++q) {
+    for (int c = full_unit ? 0 : part_lo; c < c_hi; ++c, ++q) {
       if (int(q & 1) != grp) continue;
       const int s = int(q % S);
       const int j0 = c * P::COLS;
