@@ -1,14 +1,28 @@
 #!/usr/bin/env python3
 """Benchmark: batched FP64 GEMM (BASELINE.json metric) on 1..N B200s.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl lrb|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl lrb|reference]
+    python bench.py --gpus N --plan-only      # the shard plan only (no GPU)
 
-A step is one pass of the hot path over the rank's batch, inputs resident in
-HBM (generated on device, untimed). Default workload: BASELINE configs[1]
-(cfg2, low-rank expansion U V^T, 4096 items of 512x32 * (512x32)^T), the
-config the metric is quoted on. Under torchrun each rank owns one GPU and a
-contiguous item range; there is no data-path collective (items are
-independent): only a barrier and a max-over-ranks of the device time.
+A step is one pass of the hot path over the rank's items, inputs resident in
+HBM (generated on device, untimed). Default workload: BASELINE configs[3]
+(cfg4, 8192 variable-size pointer-array products A_i(b_i x b_i) B_i(b_i x r_i)),
+the largest BASELINE config that fits one GPU (cfg5, the metric's 1/2/4/8-GPU
+batch, is 288 GiB).
+
+One process per GPU. Under torchrun the ranks come from RANK / LOCAL_RANK /
+WORLD_SIZE; without torchrun, ``--gpus N`` (N > 1) launches the N ranks itself
+(and fails when fewer than N GPUs are visible). Items are independent, so the
+ranks exchange nothing on the data path: each takes its range from the shard
+planner (lrb_shard_plan; cfg4 cut at equal cumulative per-item roofline time,
+cfg5 split evenly, the others one BASELINE batch per GPU) and generates its
+own items on device from global item indices. The only collectives are a
+barrier and gathers of host scalars over gloo.
+
+Timing: W untimed warm-up steps, then K steps, each one CUDA-graph replay
+bracketed by CUDA events on the launching stream; a barrier and a device
+synchronize on both sides of the timed region. The step time is the median
+over the K steps of the slowest rank's step (min / mean / max reported too).
 
 Prints ONE JSON line (rank 0).
 """
@@ -17,6 +31,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -28,6 +43,7 @@ sys.path.insert(0, ROOT)
 
 HBM_PEAK_FALLBACK = 6553.6  # GB/s
 FP64_PEAK_MEASURED = 36.9   # TFLOP/s, tools/microbench/fp64_peaks.cu on this pool (DMMA == DFMA)
+DEFAULT_CONFIG = "cfg4"
 
 
 # ------------------------------------------------------------------ helpers
@@ -52,65 +68,159 @@ def load_peaks():
     return hbm, src, fp64, fsrc
 
 
+def cpu_identity() -> dict:
+    """the host the CPU baseline ran on: model string, physical cores and
+    logical CPUs (the reference's acceptance header records the same,
+    proj/tests/acceptance.cpp:70-93)"""
+    model, cores, sockets = None, set(), set()
+    phys = core = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if ":" not in line:
+                    if phys is not None or core is not None:
+                        cores.add((phys, core))
+                    phys = core = None
+                    continue
+                k, v = [x.strip() for x in line.split(":", 1)]
+                if k == "model name" and model is None:
+                    model = v
+                elif k == "physical id":
+                    phys = v
+                    sockets.add(v)
+                elif k == "core id":
+                    core = v
+        if phys is not None or core is not None:
+            cores.add((phys, core))
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except Exception:
+        usable = os.cpu_count() or 1
+    return {"cpu_model": model, "physical_cores": len(cores) or None,
+            "sockets": len(sockets) or None, "logical_cpus": os.cpu_count(),
+            "usable_cpus": usable}
+
+
+def mapped_repo_libs():
+    """shared objects of this repo mapped into the current process"""
+    out = set()
+    try:
+        with open("/proc/self/maps") as f:
+            for line in f:
+                p = line.split()[-1] if line.strip() else ""
+                if p.endswith(".so") and p.startswith(ROOT):
+                    out.add(os.path.relpath(p, ROOT))
+    except OSError:
+        pass
+    return sorted(out)
+
+
+def _nvml_index(local: int):
+    """NVML handle selector for CUDA device `local` (CUDA_VISIBLE_DEVICES aware)"""
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        ids = [x.strip() for x in vis.split(",") if x.strip()]
+        if local < len(ids):
+            return ids[local]
+    return str(local)
+
+
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region"""
+    """SM clock and clock-event (throttle) reasons sampled every few ms
+    during the timed region, through NVML (nvidia-smi as a fallback)"""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, gpu_index: int):
+    def __init__(self, gpu_index: int, period_s: float = 0.004):
         self.gpu = gpu_index
+        self.period = period_s
+        self.sm, self.reasons, self.max_mhz = [], set(), None
+        self.stop_ev = threading.Event()
+        self.thread = None
         self.proc = None
         self.lines = []
-        self.thread = None
 
     def start(self):
         try:
+            import pynvml as N
+
+            N.nvmlInit()
+            sel = _nvml_index(self.gpu)
+            h = (N.nvmlDeviceGetHandleByUUID(sel) if sel.startswith(("GPU-", "MIG-"))
+                 else N.nvmlDeviceGetHandleByIndex(int(sel)))
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            get_reasons = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                N.nvmlDeviceGetCurrentClocksThrottleReasons
+
+            def loop():
+                while not self.stop_ev.is_set():
+                    try:
+                        self.sm.append(float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)))
+                        r = int(get_reasons(h))
+                        for bit, name in self.REASONS.items():
+                            if r & bit:
+                                self.reasons.add(name)
+                    except Exception:
+                        pass
+                    self.stop_ev.wait(self.period)
+
+            self.thread = threading.Thread(target=loop, daemon=True)
+            self.thread.start()
+            self.kind = "nvml"
+            return
+        except Exception:
+            pass
+        self.kind = "nvidia-smi"
+        fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                  "clocks_event_reasons.hw_thermal_slowdown,"
+                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                ["nvidia-smi", f"--id={_nvml_index(self.gpu)}", f"--query-gpu={fields}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread = threading.Thread(
+                target=lambda: [self.lines.append(l.strip()) for l in self.proc.stdout],
+                daemon=True)
             self.thread.start()
         except Exception:
             self.proc = None
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def stop(self):
-        if self.proc is None:
-            return None
-        time.sleep(0.05)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
+        self.stop_ev.set()
+        if self.proc is not None:
+            time.sleep(0.03)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for ln in self.lines:
+                parts = [p.strip() for p in ln.split(",")]
+                if len(parts) < 6:
+                    continue
+                try:
+                    self.sm.append(float(parts[0]))
+                    self.max_mhz = float(parts[1])
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[2:6]):
+                    if v.lower().startswith("active"):
+                        self.reasons.add(nm)
         if self.thread:
             self.thread.join(timeout=2)
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx = float(parts[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        if not sm:
+        if not self.sm:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.max_mhz,
+                "sm_mhz_min": min(self.sm), "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "source": getattr(self, "kind", None)}
 
 
+# ---------------------------------------------------------------- processes
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -120,8 +230,8 @@ def dist_setup():
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        # the only collectives are a barrier and a max of per-rank device time:
-        # gloo on host scalars keeps torch off the GPU entirely
+        # the only collectives are barriers and gathers of host scalars: gloo
+        # keeps torch off the GPU entirely
         dist.init_process_group("gloo", rank=rank, world_size=world)
         pg = dist
     return world, rank, local, pg
@@ -152,34 +262,123 @@ def all_sum(pg, x: float) -> float:
     return float(t.item())
 
 
-# ----------------------------------------------------------- workload slice
-def rank_items(w, world, rank):
-    """(first global item, count) of this rank. cfg5 is the whole-box batch
-    split across ranks (strong scaling); the others keep the BASELINE batch per
-    GPU and index items globally (weak scaling)."""
-    from paper_2311_07602_b200 import shard_plan
+def all_gather(pg, obj):
+    if pg is None:
+        return [obj]
+    out = [None] * pg.get_world_size()
+    pg.all_gather_object(out, obj)
+    return out
 
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def visible_gpus() -> int:
+    from paper_2311_07602_b200 import device_count
+
+    return device_count()
+
+
+def spawn_ranks(n: int) -> int:
+    """run this script as n ranks (one process per GPU), wait for all; the
+    first failing rank's exit code is returned and the others are stopped"""
+    port = _free_port()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:],
+                                      env=env))
+    rc = 0
+    while procs:
+        for p in list(procs):
+            code = p.poll()
+            if code is None:
+                continue
+            procs.remove(p)
+            if code != 0 and rc == 0:
+                rc = code
+                for q in procs:
+                    q.terminate()
+        time.sleep(0.05)
+    return rc
+
+
+# ----------------------------------------------------------- workload slice
+def item_roofline_s(w, i, hbm_gbs=None, fp64_tf=None):
+    """per-item roofline time max(flops / P_fp64, bytes / BW_hbm)"""
+    if hbm_gbs is None:
+        hbm_gbs, _, fp64_tf, _ = load_peaks()
+    return max(w.item_flops(i) / (fp64_tf * 1e12), w.item_bytes(i) / (hbm_gbs * 1e9))
+
+
+def shard_ranges(w, world):
+    """[(first global item, count)] per rank and the scaling mode.
+
+    cfg4 (variable sizes): one batch split at equal cumulative per-item
+    roofline time (lrb_shard_plan with costs); cfg5: the
+    whole-box batch split evenly (the reference's contiguous fan-out,
+    bench.hpp:69-75); every other config keeps one BASELINE batch per GPU
+    (weak scaling) indexed globally."""
+    from paper_2311_07602_b200 import shard_plan, workloads as W
+
+    if isinstance(w, W.Variable):
+        hbm, _, fp64, _ = load_peaks()
+        cost = [item_roofline_s(w, i, hbm, fp64) for i in range(w.batch)]
+        b = shard_plan(w.batch, world, cost)
+        return [(b[r], b[r + 1] - b[r]) for r in range(world)], "strong"
     if w.name == "cfg5":
         b = shard_plan(w.batch, world)
-        return b[rank], b[rank + 1] - b[rank], "strong"
-    return rank * w.batch, w.batch, "weak"
+        return [(b[r], b[r + 1] - b[r]) for r in range(world)], "strong"
+    return [(r * w.batch, w.batch) for r in range(world)], "weak"
 
 
-def traffic_from_profiles(config_name: str):
-    """dram bytes per launch of the top kernel from the committed ncu summary"""
+def scaling_of(w) -> str:
+    """the scaling mode shard_ranges applies (host-only, no library call)"""
+    from paper_2311_07602_b200 import workloads as W
+
+    return "strong" if isinstance(w, W.Variable) or getattr(w, "name", "") == "cfg5" else "weak"
+
+
+def rank_items(w, world, rank):
+    """(first global item, count, scaling) of this rank"""
+    spans, scaling = shard_ranges(w, world)
+    return spans[rank][0], spans[rank][1], scaling
+
+
+def traffic_from_profiles(config_name: str, items=None):
+    """DRAM read+write bytes of one launch of the config's kernel(s) from the
+    committed ncu summary (profiles/traffic.json). Entries record the items
+    they were captured on; a launch over a different item count is scaled
+    linearly and says so."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get(config_name)
     except Exception:
         return None
+    e = d.get(config_name)
+    if not isinstance(e, dict):
+        return None
+    e = dict(e)
+    cap = e.get("items")
+    if items is not None and cap and int(cap) != int(items):
+        e["dram_bytes_per_launch"] = e["dram_bytes_per_launch"] * float(items) / float(cap)
+        e["scaled_from_items"] = cap
+    elif items is not None and not cap:
+        return None  # capture size unknown: do not pair bytes of another launch size
+    return e
 
 
 # ------------------------------------------------------------- CPU baseline
 def cpu_sample_run(w, items, threads):
     """time the reference binary (oracle/_ref, else the C restatement) on a
-    bounded sample of the workload's items; returns (seconds, flops, kind)"""
+    bounded sample of the workload's items; returns (seconds, flops, bytes, kind)"""
     import numpy as np
 
     import oracle as O
@@ -241,12 +440,25 @@ def pick_sample(w, threads, target_s):
     return items
 
 
+def cpu_baseline(w, threads, target_s, what=None):
+    items = pick_sample(w, threads, target_s)
+    dt, fl, _, kind = cpu_sample_run(w, items, threads)
+    d = {"value": round(fl / dt / 1e9, 3), "unit": "GFLOP/s", "cores": threads, "kind": kind,
+         "sample": f"{len(items)} of {w.batch} items of {w.name} ({dt:.1f} s), per-item rate; "
+                   f"std::thread contiguous split like naive_multiply_batch"}
+    d.update(cpu_identity())
+    return d
+
+
 def run_reference_arm(args, w, world, rank):
     if rank != 0:
         return  # rank 0 alone runs the CPU reference
-    threads = os.cpu_count() or 1
-    items = pick_sample(w, threads, args.ref_seconds)
-    for _ in range(max(0, args.warmup_ref)):
+    ident = cpu_identity()
+    threads = ident["usable_cpus"] or 1
+    # each step a bounded sample, sized so the W + K steps end within minutes
+    per_step_s = min(args.ref_seconds, 150.0 / max(1, args.steps + args.warmup))
+    items = pick_sample(w, threads, per_step_s)
+    for _ in range(max(0, args.warmup)):
         cpu_sample_run(w, items, threads)
     times, fl, by, kind = [], 0.0, 0.0, "reference"
     for _ in range(args.steps):
@@ -257,24 +469,100 @@ def run_reference_arm(args, w, world, rank):
     sample = (f"{len(items)} of {w.batch} items of {w.name} per step "
               f"(items {items[0]}..{items[-1]}), std::thread contiguous split like "
               f"naive_multiply_batch; value extrapolates per-item rate to the workload")
+    libs = mapped_repo_libs()
+    if any("liblrb.so" in p for p in libs):
+        raise RuntimeError(f"reference arm mapped the product library: {libs}")
+    cb = {"value": round(gflops, 3), "unit": "GFLOP/s", "cores": threads, "kind": kind,
+          "sample": sample}
+    cb.update(ident)
     line = {
         "metric": "batched FP64 GFLOP/s", "value": round(gflops, 3), "unit": "GFLOP/s",
         "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": round(t * 1e3, 3), "higher_is_better": True,
+        "scaling": scaling_of(w),
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (counter RNG, uniform[-1,1))",
         "config": dict(w.describe(), sample_items=len(items)),
+        "step_ms": {"median": round(t * 1e3, 3), "min": round(min(times) * 1e3, 3),
+                    "max": round(max(times) * 1e3, 3)},
         "hbm_gbs": None,
-        "cpu_baseline": {"value": round(gflops, 3), "unit": "GFLOP/s", "cores": threads,
-                         "kind": kind, "sample": sample},
+        "cpu_baseline": cb,
         "e2e": {"value": round(gflops, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
+        "native_libs": libs,
     }
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ timing
+def timed_steps(ctx, stream, step, steps, warmup, pg, local, graphs=1):
+    """W warm-up steps, then K timed steps. The step is captured as `graphs`
+    CUDA graphs (consecutive captures of `step`, e.g. over rotating buffers)
+    replayed in turn, each replay bracketed by events on `stream`. Returns
+    (total ms, [per-step ms], launches, clocks)."""
+    for _ in range(warmup):
+        step()
+    stream.synchronize()
+    caps = []
+    for _ in range(max(1, graphs)):
+        with ctx.capture(stream) as cap:
+            step()
+        caps.append(cap.graph)
+    evs = [ctx.event() for _ in range(steps + 1)]
+    sampler = ClockSampler(local)
+    sampler.start()
+    barrier(pg)
+    stream.synchronize()
+    launches0 = ctx.launch_count
+    evs[0].record(stream)
+    for i in range(steps):
+        caps[i % len(caps)].launch(stream)
+        evs[i + 1].record(stream)
+    stream.synchronize()
+    barrier(pg)
+    clocks = sampler.stop()
+    per = [evs[i].elapsed_ms(evs[i + 1]) for i in range(steps)]
+    return evs[0].elapsed_ms(evs[-1]), per, ctx.launch_count - launches0, clocks
+
+
+def job_step_stats(pg, per_rank_steps, ms_total):
+    """per step: the slowest rank's time; reported median / mean / min / max,
+    plus each rank's total and median (the per-GPU spread)"""
+    mine = {"steps": per_rank_steps, "total": ms_total}
+    allr = all_gather(pg, mine)
+    K = len(per_rank_steps)
+    job = [max(r["steps"][i] for r in allr) for i in range(K)]
+    med = statistics.median(job)
+    ranks = [{"rank": i, "ms_total": round(r["total"], 4),
+              "ms_median": round(statistics.median(r["steps"]), 4)} for i, r in enumerate(allr)]
+    meds = [r["ms_median"] for r in ranks]
+    stats = {"median": round(med, 4), "mean": round(statistics.mean(job), 4),
+             "min": round(min(job), 4), "max": round(max(job), 4),
+             "per_rank": ranks,
+             "rank_spread": round((max(meds) - min(meds)) / max(meds), 4) if meds and max(meds) else 0.0}
+    return med, stats
+
+
+def roofline(flops, bytes_, ms, hbm_peak, fp64_peak, hbm_src, fp64_src):
+    intensity = flops / bytes_
+    fp64_bound = intensity * hbm_peak * 1e9 >= fp64_peak * 1e12
+    if fp64_bound:
+        ach = flops / (ms * 1e-3) / 1e12
+        r = {"bound": "tensor", "achieved": round(ach, 3), "peak": fp64_peak, "unit": "TFLOP/s",
+             "frac": round(ach / fp64_peak, 4),
+             "peak_source": fp64_src + " (FP64 DMMA; MEASURED_PEAKS.json has no FP64 figure)"}
+    else:
+        ach = bytes_ / (ms * 1e-3) / 1e9
+        r = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
+             "frac": round(ach / hbm_peak, 4), "peak_source": hbm_src}
+    r["roofline_frac"] = round(flops / (ms * 1e-3) /
+                               min(fp64_peak * 1e12, intensity * hbm_peak * 1e9), 4)
+    r["algorithmic"] = bytes_
+    return r
+
+
 # ------------------------------------------------------------------ GPU arm
-def alloc_inputs(ctx, w, first, count, shard=None):
+def alloc_inputs(ctx, w, first, count):
     from paper_2311_07602_b200 import workloads as W
 
     A = ctx.empty(w.sA * count)
@@ -292,99 +580,133 @@ def gemm(ctx, w, A, B, Cd, count, stream=None):
 
 
 class VariableSlice:
-    """cfg4 on one rank: arenas with 256-B aligned bases, a pointer-array plan"""
+    """cfg4 items [first, first + count) on one rank: three arenas with
+    256-B aligned item bases, generated on device from global item indices,
+    and the pointer-array plan over them"""
 
-    def __init__(self, ctx, w, items):
+    def __init__(self, ctx, w, first, count):
         from paper_2311_07602_b200 import workloads as W
 
-        self.items = items
-        offs, (na, nb, nc) = W.variable_layout(w, items)
+        self.items = list(range(first, first + count))
+        self.offs, (na, nb, nc) = W.variable_layout(w, self.items)
+        self.sizes = (na, nb, nc)
         self.arena = [ctx.malloc(na), ctx.malloc(nb), ctx.malloc(nc)]
-        pa = [self.arena[0].ptr + o[0] for o in offs]
-        pb = [self.arena[1].ptr + o[1] for o in offs]
-        pc = [self.arena[2].ptr + o[2] for o in offs]
-        bs = [w.bs[i] for i in items]
-        rs = [w.rs[i] for i in items]
-        # fill item by item with GLOBAL indices: contiguous runs keep it one call
-        ctx.fill_uniform_ptr(pa, bs, bs, bs, w.seed, W.ROLE_A, items[0])
-        ctx.fill_uniform_ptr(pb, bs, rs, bs, w.seed, W.ROLE_B, items[0])
-        self.plan = ctx.ptr_plan("C", "N", "N", bs, rs, bs, pa, bs, pb, bs, pc, bs, 0.0)
+        self.pa = [self.arena[0].ptr + o[0] for o in self.offs]
+        self.pb = [self.arena[1].ptr + o[1] for o in self.offs]
+        self.pc = [self.arena[2].ptr + o[2] for o in self.offs]
+        self.bs = [w.bs[i] for i in self.items]
+        self.rs = [w.rs[i] for i in self.items]
+        ctx.fill_uniform_ptr(self.pa, self.bs, self.bs, self.bs, w.seed, W.ROLE_A, first)
+        ctx.fill_uniform_ptr(self.pb, self.bs, self.rs, self.bs, w.seed, W.ROLE_B, first)
+        self.plan = ctx.ptr_plan("C", "N", "N", self.bs, self.rs, self.bs, self.pa, self.bs,
+                                 self.pb, self.bs, self.pc, self.bs, 0.0)
         ctx.synchronize()
 
 
-def run_gpu_arm_variable(args, w, world, rank, local, pg):
-    from paper_2311_07602_b200 import Context, shard_plan
+def host_mem_available() -> int:
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 16 << 30
+
+
+def run_e2e_variable(args, ctx, w, vs, pg):
+    """cfg4 through lrb_dgemm_ptr_batched_host: every item's A_i, B_i, C_i in
+    pinned HOST arenas (the same 256-B aligned layout), H2D + kernels + D2H of
+    the results inside the timed region"""
+    na, nb, nc = vs.sizes
+    budget = int(0.4 * host_mem_available())
+    n = len(vs.items)
+    if na + nb + nc > budget:  # the largest item prefix that fits the host
+        acc = 0
+        for i, o in enumerate(vs.offs):
+            if o[0] + o[1] + o[2] > budget:
+                n = i
+                break
+        na, nb, nc = vs.offs[n][0], vs.offs[n][1], vs.offs[n][2]
+    hA, hB, hC = ctx.pinned(na // 8), ctx.pinned(nb // 8), ctx.pinned(nc // 8)
+    from paper_2311_07602_b200.lrbatch import _check, lib
+
+    _check(lib.lrb_memcpy_d2h(ctx._h, hA.ptr, vs.arena[0].ptr, na), ctx._h)
+    _check(lib.lrb_memcpy_d2h(ctx._h, hB.ptr, vs.arena[1].ptr, nb), ctx._h)
+    offs = vs.offs[:n]
+    pa = [hA.ptr + o[0] for o in offs]
+    pb = [hB.ptr + o[1] for o in offs]
+    pc = [hC.ptr + o[2] for o in offs]
+    bs, rs = vs.bs[:n], vs.rs[:n]
+
+    def once():
+        ctx.dgemm_ptr_batched_host("C", "N", "N", bs, rs, bs, pa, bs, pb, bs, pc, bs, 0.0)
+
+    once()
+    barrier(pg)
+    times = []
+    for _ in range(args.e2e_steps):
+        t0 = time.perf_counter()
+        once()
+        times.append(time.perf_counter() - t0)
+    dt = all_max(pg, statistics.median(times))
+    ids = vs.items[:n]
+    fl_all = all_sum(pg, w.flops(ids))
+    h2d = sum(8 * (b * b + b * r) for b, r in zip(bs, rs))
+    d2h = sum(8 * b * r for b, r in zip(bs, rs))
+    return {"value": round(fl_all / dt / 1e9, 2), "unit": "GFLOP/s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "items_per_rank": n, "ms_per_step": round(dt * 1e3, 2),
+            "path": "lrb_dgemm_ptr_batched_host (pinned host blocks; coalesced runs, "
+                    "3-stream chunked H2D / pointer-array kernels / D2H)"}
+
+
+def run_gpu_arm_variable(args, w, world, rank, local, pg, spans, scaling):
+    from paper_2311_07602_b200 import Context
 
     hbm_peak, hbm_src, fp64_peak, fp64_src = load_peaks()
     ctx = Context(local)
     stream = ctx.stream()
-    # weak scaling: every rank runs the full 8192-item cfg4 batch with its own
-    # global item range (items rank*batch ..), drawn from the same seed stream
-    base = rank * w.batch
-    import copy
-
-    wr = copy.copy(w)
-    if base:
-        wr = type(w)(w.name, w.batch * (rank + 1), w.seed)
-    items = list(range(base, base + w.batch))
-    vs = VariableSlice(ctx, wr, items)
-    for _ in range(args.warmup):
-        vs.plan.execute(stream)
-    stream.synchronize()
-    sampler = ClockSampler(local)
-    sampler.start()
-    barrier(pg)
-    launches0 = ctx.launch_count
-    t0, t1 = ctx.event(), ctx.event()
-    t0.record(stream)
-    for _ in range(args.steps):
-        vs.plan.execute(stream)
-    t1.record(stream)
-    stream.synchronize()
-    barrier(pg)
-    clocks = sampler.stop()
-    launches = ctx.launch_count - launches0
-    ms_rank = t0.elapsed_ms(t1)
-    ms_step = all_max(pg, ms_rank) / args.steps
-    fl = wr.flops(items)
-    by = wr.bytes(items)
+    first, count = spans[rank]
+    vs = VariableSlice(ctx, w, first, count)
+    ms_rank, per, launches, clocks = timed_steps(ctx, stream, lambda: vs.plan.execute(stream),
+                                                 args.steps, args.warmup, pg, local)
+    ms_step, stats = job_step_stats(pg, per, ms_rank)
+    fl = w.flops(vs.items)
+    by = w.bytes(vs.items)
     fl_all = all_sum(pg, fl)
     by_all = all_sum(pg, by)
     gflops = fl_all / (ms_step * 1e-3) / 1e9
-    intensity = fl / by
-    roof_t = min(fp64_peak * 1e12, intensity * hbm_peak * 1e9)
-    achieved = fl / (ms_rank / args.steps * 1e-3)
-    roof = {"bound": "tensor" if intensity * hbm_peak * 1e9 >= fp64_peak * 1e12 else "hbm",
-            "achieved": round(achieved / 1e12, 3), "peak": fp64_peak, "unit": "TFLOP/s",
-            "frac": round(achieved / (fp64_peak * 1e12), 4),
-            "roofline_frac": round(achieved / roof_t, 4), "traffic": None,
-            "algorithmic": by, "kernel": "lrb_gemm_kernel<n8|n16|n32|n64> (ptr)",
-            "kernel_ms": round(ms_rank / max(1, launches), 4),
-            "peak_source": fp64_src}
-    tr = traffic_from_profiles(w.name)
-    if isinstance(tr, dict):
-        roof["traffic"] = tr.get("dram_bytes_per_launch")
+    my_med = statistics.median(per)
+    roof = roofline(fl, by, my_med, hbm_peak, fp64_peak, hbm_src, fp64_src)
+    # the per-item roofline: sum over items of max(flops/P, bytes/BW)
+    t_item = sum(item_roofline_s(w, i, hbm_peak, fp64_peak) for i in vs.items)
+    roof["per_item_roofline_frac"] = round(t_item / (my_med * 1e-3), 4)
+    roof["kernel"] = "lrb_gemm_kernel (pointer-array plan, %d launches)" % vs.plan.launches
+    roof["kernel_ms"] = round(my_med, 4)
+    tr = traffic_from_profiles(w.name, count)
+    roof["traffic"] = tr.get("dram_bytes_per_launch") if isinstance(tr, dict) else None
+    e2e = run_e2e_variable(args, ctx, w, vs, pg) if args.e2e_steps > 0 else None
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        sample = pick_sample(w, threads, args.ref_seconds)
-        dt, sfl, _, kind = cpu_sample_run(w, sample, threads)
-        cpu = {"value": round(sfl / dt / 1e9, 3), "unit": "GFLOP/s", "cores": threads,
-               "kind": kind, "sample": f"{len(sample)} of {w.batch} cfg4 items ({dt:.1f} s)"}
+        cpu = cpu_baseline(w, cpu_identity()["usable_cpus"] or 1, args.ref_seconds)
     if rank == 0:
         cfg = dict(w.describe())
         cfg.update({"parallelism": f"shard{world} (independent items, no collective)",
+                    "shards": [list(s) for s in spans],
+                    "shard_rule": "equal cumulative per-item roofline time (lrb_shard_plan)",
                     "launches_per_step": vs.plan.launches,
+                    "timed_launch": "one CUDA graph per step",
                     "l2": "inputs larger than L2 (no flush)"})
         line = {
             "metric": "batched FP64 GFLOP/s", "value": round(gflops, 2), "unit": "GFLOP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (device counter RNG, uniform[-1,1), BASELINE seeds)",
             "config": cfg, "hbm_gbs": round(by_all / (ms_step * 1e-3) / 1e9, 1),
-            "roofline": roof, "cpu_baseline": cpu, "e2e": None, "clocks": clocks,
-            "gpu_launches": int(launches),
+            "step_ms": stats, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "clocks": clocks, "gpu_launches": int(launches),
         }
         print(json.dumps(line), flush=True)
     ctx.close()
@@ -393,13 +715,14 @@ def run_gpu_arm_variable(args, w, world, rank, local, pg):
 def run_gpu_arm(args, w, world, rank, local, pg):
     from paper_2311_07602_b200 import Context, select, workloads as W
 
+    spans, scaling = shard_ranges(w, world)
     if isinstance(w, W.Variable):
-        return run_gpu_arm_variable(args, w, world, rank, local, pg)
+        return run_gpu_arm_variable(args, w, world, rank, local, pg, spans, scaling)
 
     hbm_peak, hbm_src, fp64_peak, fp64_src = load_peaks()
     ctx = Context(local)
     stream = ctx.stream()
-    first, count, scaling = rank_items(w, world, rank)
+    first, count = spans[rank]
 
     # ---- device-resident inputs (chunked if the slice exceeds HBM)
     free, _ = ctx.mem_info()
@@ -419,122 +742,79 @@ def run_gpu_arm(args, w, world, rank, local, pg):
     A, B, Cd = bufs[0]
     rot = [0]
 
-    def step():
-        """one pass over this rank's items; returns device ms of the GEMM launches"""
-        if resident:
+    if resident:
+        def step():
             a, b, c = bufs[rot[0] % copies]
             rot[0] += 1
             gemm(ctx, w, a, b, c, count, stream)
-            return None
-        # chunked (cfg5 below 4 GPUs): regenerate each chunk (untimed), time GEMMs
-        total = 0.0
-        for c in range(nchunks):
-            c0 = c * chunk
-            cn = min(chunk, count - c0)
-            ctx.fill_uniform(A, w.a_rows, w.a_cols, w.lda, w.sA, cn, w.seed, W.ROLE_A, first + c0,
-                             stream)
-            ctx.fill_uniform(B, w.b_rows, w.b_cols, w.ldb, w.sB, cn, w.seed, W.ROLE_B, first + c0,
-                             stream)
-            e0.record(stream)
-            gemm(ctx, w, A, B, Cd, cn, stream)
-            e1.record(stream)
-            stream.synchronize()
-            total += e0.elapsed_ms(e1)
-        return total
 
-    e0, e1 = ctx.event(), ctx.event()
-    for _ in range(args.warmup):
-        step()
-    stream.synchronize()
-
-    # resident batches: the K timed steps are captured once as a CUDA graph
-    # (lrb_graph_*) and replayed with one host call, so short steps (cfg1,
-    # ~35 us) are not separated by host enqueue gaps
-    graph = None
-    if resident and not args.no_graph:
-        with ctx.capture(stream) as cap:
-            for _ in range(args.steps):
-                step()
-        graph = cap.graph
-
-    # ---- timed region
-    sampler = ClockSampler(local)
-    sampler.start()
-    barrier(pg)
-    stream.synchronize()
-    launches0 = ctx.launch_count
-    t_start, t_end = ctx.event(), ctx.event()
-    chunk_ms = 0.0
-    t_start.record(stream)
-    if graph is not None:
-        graph.launch(stream)
+        ms_rank, per, launches, clocks = timed_steps(ctx, stream, step, args.steps, args.warmup,
+                                                     pg, local, graphs=copies)
     else:
-        for _ in range(args.steps):
-            r = step()
-            if r is not None:
-                chunk_ms += r
-    t_end.record(stream)
-    stream.synchronize()
-    barrier(pg)
-    clocks = sampler.stop()
-    launches = ctx.launch_count - launches0
-    ms_rank = t_start.elapsed_ms(t_end) if resident else chunk_ms
-    if not resident:  # only GEMM launches count (fills between chunks are setup)
-        launches = args.steps * nchunks
-    ms_total = all_max(pg, ms_rank)
-    ms_step = ms_total / args.steps
+        # chunked (cfg5 below 4 GPUs): each chunk regenerated untimed; a step's
+        # time is the sum of its chunks' GEMM launches (events around each)
+        e0, e1 = ctx.event(), ctx.event()
+
+        def chunked_step():
+            total = 0.0
+            for c in range(nchunks):
+                c0 = c * chunk
+                cn = min(chunk, count - c0)
+                ctx.fill_uniform(A, w.a_rows, w.a_cols, w.lda, w.sA, cn, w.seed, W.ROLE_A,
+                                 first + c0, stream)
+                ctx.fill_uniform(B, w.b_rows, w.b_cols, w.ldb, w.sB, cn, w.seed, W.ROLE_B,
+                                 first + c0, stream)
+                e0.record(stream)
+                gemm(ctx, w, A, B, Cd, cn, stream)
+                e1.record(stream)
+                stream.synchronize()
+                total += e0.elapsed_ms(e1)
+            return total
+
+        for _ in range(args.warmup):
+            chunked_step()
+        sampler = ClockSampler(local)
+        sampler.start()
+        barrier(pg)
+        per = [chunked_step() for _ in range(args.steps)]
+        barrier(pg)
+        clocks = sampler.stop()
+        ms_rank = sum(per)
+        launches = args.steps * nchunks  # only GEMM launches count
+    ms_step, stats = job_step_stats(pg, per, ms_rank)
     items_all = all_sum(pg, float(count))
     flops_all = w.item_flops() * items_all
     bytes_all = w.item_bytes() * items_all
     gflops = flops_all / (ms_step * 1e-3) / 1e9
     gbs = bytes_all / (ms_step * 1e-3) / 1e9
 
-    # ---- dominant kernel roofline (this rank, per launch)
-    per_launch_ms = ms_rank / max(1, launches)
-    # average items per launch (chunks may be unequal; algorithmic units per launch)
+    # ---- dominant kernel roofline (this rank, per launch, median step)
+    launches_per_step = max(1, launches // max(1, args.steps))
+    per_launch_ms = statistics.median(per) / launches_per_step
     launch_items = count / nchunks
     sel = select(w.order, w.opA, w.opB, w.m, w.n, w.k, chunk, ctx)
-    intensity = w.item_flops() / w.item_bytes()
-    fp64_bound = intensity >= (fp64_peak * 1e12) / (hbm_peak * 1e9)
-    if fp64_bound:
-        achieved = w.item_flops() * launch_items / (per_launch_ms * 1e-3) / 1e12
-        roof = {"bound": "tensor", "achieved": round(achieved, 3), "peak": fp64_peak,
-                "unit": "TFLOP/s", "frac": round(achieved / fp64_peak, 4),
-                "peak_source": fp64_src + " (FP64 DMMA; MEASURED_PEAKS.json has no FP64 figure)"}
-    else:
-        achieved = w.item_bytes() * launch_items / (per_launch_ms * 1e-3) / 1e9
-        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(achieved / hbm_peak, 4), "peak_source": hbm_src}
-    tr = traffic_from_profiles(w.name)
+    roof = roofline(w.item_flops() * launch_items, w.item_bytes() * launch_items, per_launch_ms,
+                    hbm_peak, fp64_peak, hbm_src, fp64_src)
+    tr = traffic_from_profiles(w.name, int(round(launch_items)))
     roof["traffic"] = tr.get("dram_bytes_per_launch") if isinstance(tr, dict) else None
-    roof["algorithmic"] = w.item_bytes() * launch_items
     roof["kernel"] = ("lrb_panel_kernel<p256>" if sel["name"] == "p256" else
                       f"lrb_gemm_kernel<{sel['name']}>")
     roof["kernel_ms"] = round(per_launch_ms, 4)
-    roof["roofline_frac"] = round(
-        (w.item_flops() * launch_items / (per_launch_ms * 1e-3)) /
-        min(fp64_peak * 1e12, intensity * hbm_peak * 1e9), 4)
+    roof["items_per_launch"] = launch_items
 
     # ---- e2e through the host-buffer C-ABI (pinned host memory, copies timed)
     del A, B, Cd, bufs
     e2e = run_e2e(args, ctx, w, first, count, pg) if args.e2e_steps > 0 else None
 
-    # ---- CPU baseline on rank 0 at N = 1
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        items = pick_sample(w, threads, args.ref_seconds)
-        dt, fl, _, kind = cpu_sample_run(w, items, threads)
-        cpu = {"value": round(fl / dt / 1e9, 3), "unit": "GFLOP/s", "cores": threads,
-               "kind": kind,
-               "sample": f"{len(items)} of {w.batch} items of {w.name} ({dt:.1f} s), per-item "
-                         f"rate; std::thread contiguous split like naive_multiply_batch"}
+        cpu = cpu_baseline(w, cpu_identity()["usable_cpus"] or 1, args.ref_seconds)
 
     if rank == 0:
         cfg = dict(w.describe())
         cfg.update({"items_per_rank": count, "global_items": int(items_all),
-                    "timed_launch": "CUDA graph of the K steps" if graph is not None
-                    else "eager launches",
+                    "shards": [list(s) for s in spans],
+                    "timed_launch": "one CUDA graph per step" if resident else "eager launches",
                     "parallelism": f"shard{world} (independent items, no collective)",
                     "kernel_variant": sel["name"],
                     "l2": (f"{copies} rotating copies of inputs+outputs "
@@ -547,8 +827,8 @@ def run_gpu_arm(args, w, world, rank, local, pg):
             "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (device counter RNG, uniform[-1,1), BASELINE seeds)",
-            "config": cfg, "hbm_gbs": round(gbs, 1), "roofline": roof, "cpu_baseline": cpu,
-            "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches),
+            "config": cfg, "hbm_gbs": round(gbs, 1), "step_ms": stats, "roofline": roof,
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches),
         }
         print(json.dumps(line), flush=True)
     ctx.close()
@@ -557,10 +837,11 @@ def run_gpu_arm(args, w, world, rank, local, pg):
 def run_e2e(args, ctx, w, first, count, pg):
     """same metric through lrb_dgemm_strided_batched_host: pinned host inputs,
     H2D + kernels + D2H of the result inside the timed region"""
-    # whole batch when it fits in 16 GiB of pinned host memory (cfg5's 288 GiB
+    # whole batch when it fits the host's pinned-memory budget (cfg5's 288 GiB
     # does not: its e2e runs on the largest prefix that does)
     per_item = 8 * (w.sA + w.sB + w.sC)
-    n = min(count, args.e2e_items) if args.e2e_items else min(count, (16 << 30) // per_item)
+    budget = min(16 << 30, int(0.4 * host_mem_available()))
+    n = min(count, args.e2e_items) if args.e2e_items else min(count, max(1, budget // per_item))
     A, B, _ = alloc_inputs(ctx, w, first, n)
     hA, hB, hC = ctx.pinned(w.sA * n), ctx.pinned(w.sB * n), ctx.pinned(w.sC * n)
     from paper_2311_07602_b200.lrbatch import _check, lib  # noqa
@@ -576,11 +857,12 @@ def run_e2e(args, ctx, w, first, count, pg):
 
     once()
     barrier(pg)
-    t0 = time.perf_counter()
+    times = []
     for _ in range(args.e2e_steps):
+        t0 = time.perf_counter()
         once()
-    dt = (time.perf_counter() - t0) / args.e2e_steps
-    dt = all_max(pg, dt)
+        times.append(time.perf_counter() - t0)
+    dt = all_max(pg, statistics.median(times))
     items_all = all_sum(pg, float(n))
     return {"value": round(w.item_flops() * items_all / dt / 1e9, 2), "unit": "GFLOP/s",
             "h2d_bytes_per_step": int(8 * (w.sA + w.sB) * n),
@@ -589,54 +871,110 @@ def run_e2e(args, ctx, w, first, count, pg):
             "path": "lrb_dgemm_strided_batched_host (3-stream chunked H2D/kernel/D2H)"}
 
 
+def run_plan_only(args, w, world, rank, pg):
+    """each rank reports the item range the planner gives it; rank 0 prints
+    the gathered plan (no GPU work)"""
+    spans, scaling = shard_ranges(w, world)
+    first, count = spans[rank]
+    mine = {"rank": rank, "begin": first, "end": first + count, "items": count,
+            "pid": os.getpid()}
+    from paper_2311_07602_b200 import workloads as W
+
+    if isinstance(w, W.Variable):
+        hbm, _, fp64, _ = load_peaks()
+        mine["roofline_s"] = sum(item_roofline_s(w, i, hbm, fp64)
+                                 for i in range(first, first + count))
+    allr = all_gather(pg, mine)
+    if rank == 0:
+        print(json.dumps({"plan_only": True, "n_gpus": world, "config": w.describe(),
+                          "scaling": scaling, "ranks": allr}), flush=True)
+
+
+def run_reference(args, w, world, rank):
+    """the reference arm: the reference's own CPU implementation of the
+    workload, rank 0 only; nothing from the product package is loaded"""
+    if rank != 0:
+        return
+    from paper_2311_07602_b200 import workloads as W
+    import bench_rows as R
+
+    bench_mod = sys.modules[__name__]
+    if isinstance(w, W.LowRank):
+        R.run_lowrank_reference(args, w, world, rank, bench_mod)
+    elif isinstance(w, W.Blr):
+        R.run_blr_reference(args, w, world, rank, bench_mod)
+    elif isinstance(w, (W.LrExpand, W.BlrDense)):
+        R.run_expand_reference(args, w, world, rank, bench_mod)
+    else:
+        run_reference_arm(args, w, world, rank)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default=DEFAULT_CONFIG)
     ap.add_argument("--impl", default="lrb", choices=["lrb", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-items", type=int, default=0, help="0 = the rank's whole batch")
     ap.add_argument("--ref-seconds", type=float, default=4.0,
                     help="CPU work per reference-arm step / cpu_baseline sample")
-    ap.add_argument("--warmup-ref", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-graph", action="store_true",
-                    help="launch the timed steps one by one instead of as a CUDA graph")
+    ap.add_argument("--plan-only", action="store_true",
+                    help="print each rank's item range from the shard planner and exit")
     args = ap.parse_args()
-    if args.warmup < 3 and args.impl == "lrb":
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if args.warmup < 3 and args.impl == "lrb" and not args.plan_only:
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
 
     from paper_2311_07602_b200 import workloads as W
 
     w = W.get(args.config)
-    world, rank, local, pg = dist_setup()
-    import bench_rows as R
+    launched = "WORLD_SIZE" in os.environ
+    if launched and int(os.environ["WORLD_SIZE"]) != args.gpus and args.gpus != 1:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}",
+              file=sys.stderr)
+        sys.exit(2)
+    if not launched and args.gpus > 1:
+        if args.impl == "reference":
+            # rank 0 alone runs the CPU reference: no other process is needed
+            run_reference(args, w, args.gpus, 0)
+            return
+        if not args.plan_only:
+            have = visible_gpus()
+            if have < args.gpus:
+                print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}",
+                      file=sys.stderr)
+                sys.exit(2)
+        sys.exit(spawn_ranks(args.gpus))
 
-    bench_mod = sys.modules[__name__]
-    if isinstance(w, W.LowRank):
-        if args.impl == "reference":
-            R.run_lowrank_reference(args, w, world, rank, bench_mod)
-        else:
-            R.run_lowrank_gpu(args, w, world, rank, local, pg, bench_mod)
-    elif isinstance(w, W.Blr):
-        if args.impl == "reference":
-            R.run_blr_reference(args, w, world, rank, bench_mod)
-        else:
-            R.run_blr_gpu(args, w, world, rank, local, pg, bench_mod)
-    elif isinstance(w, (W.LrExpand, W.BlrDense)):
-        if args.impl == "reference":
-            R.run_expand_reference(args, w, world, rank, bench_mod)
-        else:
-            R.run_expand_gpu(args, w, world, rank, local, pg, bench_mod)
-    elif args.impl == "reference":
-        run_reference_arm(args, w, world, rank)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, w, world, rank)  # ranks > 0 exit without work
+        return
+    world, rank, local, pg = dist_setup()
+    if args.plan_only:
+        run_plan_only(args, w, world, rank, pg)
     else:
-        run_gpu_arm(args, w, world, rank, local, pg)
+        import bench_rows as R
+
+        bench_mod = sys.modules[__name__]
+        if isinstance(w, W.LowRank):
+            R.run_lowrank_gpu(args, w, world, rank, local, pg, bench_mod)
+        elif isinstance(w, W.Blr):
+            R.run_blr_gpu(args, w, world, rank, local, pg, bench_mod)
+        elif isinstance(w, (W.LrExpand, W.BlrDense)):
+            R.run_expand_gpu(args, w, world, rank, local, pg, bench_mod)
+        else:
+            run_gpu_arm(args, w, world, rank, local, pg)
     if pg is not None:
         pg.destroy_process_group()
 
 
 if __name__ == "__main__":
+    if __package__ is None and os.path.basename(sys.argv[0]) == "bench.py":
+        sys.modules.setdefault("bench", sys.modules[__name__])
     main()

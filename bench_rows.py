@@ -46,26 +46,12 @@ def _roof(fl, by, ms, hbm, fp64, fsrc, hsrc, name=None):
     return r
 
 
-def _timed(ctx, stream, step, steps, warmup, pg, B, clock_sampler):
-    for _ in range(warmup):
-        step()
-    stream.synchronize()
-    with ctx.capture(stream) as cap:
-        for _ in range(steps):
-            step()
-    graph = cap.graph
-    sampler = clock_sampler
-    sampler.start()
-    B.barrier(pg)
-    launches0 = ctx.launch_count
-    e0, e1 = ctx.event(), ctx.event()
-    e0.record(stream)
-    graph.launch(stream)
-    e1.record(stream)
-    stream.synchronize()
-    B.barrier(pg)
-    clocks = sampler.stop()
-    return e0.elapsed_ms(e1), ctx.launch_count - launches0, clocks
+def _timed(ctx, stream, step, steps, warmup, pg, B, local):
+    """bench.timed_steps: one CUDA graph per step, events between replays;
+    returns (median step ms of this rank, launches, clocks, job step stats)"""
+    total, per, launches, clocks = B.timed_steps(ctx, stream, step, steps, warmup, pg, local)
+    med, stats = B.job_step_stats(pg, per, total)
+    return statistics.median(per), med, launches, clocks, stats
 
 
 # ------------------------------------------------------------ low-rank product
@@ -94,13 +80,12 @@ def run_lowrank_gpu(args, w, world, rank, local, pg, B):
     ctx.fill_uniform(bufs[3], r, r, r, r * r, n, w.seed, 3, first)
     ctx.synchronize()
     step = lambda: L.lowrank_multiply_device(ctx, n, blk, r, *bufs, stream=s)  # noqa: E731
-    ms_rank, launches, clocks = _timed(ctx, s, step, args.steps, args.warmup, pg, B,
-                                       B.ClockSampler(local))
-    ms_step = B.all_max(pg, ms_rank) / args.steps
+    ms_med, ms_step, launches, clocks, stats = _timed(ctx, s, step, args.steps, args.warmup, pg,
+                                                      B, local)
     fl_all, by_all = B.all_sum(pg, w.flops()), B.all_sum(pg, w.bytes())
-    roof = _roof(w.flops(), w.bytes(), ms_rank / args.steps, hbm, fp64, fsrc, hsrc, w.name)
+    roof = _roof(w.flops(), w.bytes(), ms_med, hbm, fp64, fsrc, hsrc, w.name)
     roof["kernel"] = "lrb_lowrank_kernel<R>" if r <= 32 else "lrb_gemm_kernel x3"
-    roof["kernel_ms"] = round(ms_rank / max(1, launches), 4)
+    roof["kernel_ms"] = round(ms_med * args.steps / max(1, launches), 4)
     e2e = None
     if args.e2e_steps > 0:
         hb = lowrank_inputs_host(w, n)
@@ -130,7 +115,7 @@ def run_lowrank_gpu(args, w, world, rank, local, pg, B):
     if rank == 0:
         cfg = dict(w.describe())
         cfg.update({"parallelism": f"shard{world} (independent items, no collective)",
-                    "timed_launch": "CUDA graph of the K steps",
+                    "timed_launch": "one CUDA graph per step",
                     "l2": "inputs larger than L2 (no flush)" if w.bytes() > 3 * 132644864
                           else "inputs within 3x L2"})
         print(json.dumps({
@@ -140,7 +125,8 @@ def run_lowrank_gpu(args, w, world, rank, local, pg, B):
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (device counter RNG, uniform[-1,1))", "config": cfg,
             "hbm_gbs": round(by_all / (ms_step * 1e-3) / 1e9, 1), "roofline": roof,
-            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches)}),
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "step_ms": stats,
+            "gpu_launches": int(launches)}),
             flush=True)
     ctx.close()
 
@@ -246,13 +232,12 @@ def run_blr_gpu(args, w, world, rank, local, pg, B):
     d_rhs, d_y = ctx.to_device(rhs.data), ctx.empty(w.n * w.nrhs)
     step = lambda: _check(lib.lrb_blr_matvec_device(ctx._h, h, d_rhs.ptr, w.nrhs, d_y.ptr,  # noqa
                                                      s.handle), ctx._h)
-    ms_rank, launches, clocks = _timed(ctx, s, step, args.steps, args.warmup, pg, B,
-                                       B.ClockSampler(local))
-    ms_step = B.all_max(pg, ms_rank) / args.steps
+    ms_med, ms_step, launches, clocks, stats = _timed(ctx, s, step, args.steps, args.warmup, pg,
+                                                      B, local)
     fl_all, by_all = B.all_sum(pg, w.flops()), B.all_sum(pg, w.bytes())
-    roof = _roof(w.flops(), w.bytes(), ms_rank / args.steps, hbm, fp64, fsrc, hsrc, w.name)
+    roof = _roof(w.flops(), w.bytes(), ms_med, hbm, fp64, fsrc, hsrc, w.name)
     roof["kernel"] = "lrb_gemm_kernel x2 + blr_couple_kernel per matvec"
-    roof["kernel_ms"] = round(ms_rank / max(1, launches), 4)
+    roof["kernel_ms"] = round(ms_med * args.steps / max(1, launches), 4)
     e2e = None
     if args.e2e_steps > 0:
         y = np.zeros(w.n * w.nrhs)
@@ -277,7 +262,7 @@ def run_blr_gpu(args, w, world, rank, local, pg, B):
     if rank == 0:
         cfg = dict(w.describe())
         cfg.update({"parallelism": f"replicas{world} (one matvec per GPU, no collective)",
-                    "timed_launch": "CUDA graph of the K steps"})
+                    "timed_launch": "one CUDA graph per step"})
         print(json.dumps({
             "metric": "batched FP64 GFLOP/s", "value": round(fl_all / (ms_step * 1e-3) / 1e9, 2),
             "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -285,7 +270,8 @@ def run_blr_gpu(args, w, world, rank, local, pg, B):
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (counter RNG, uniform[-1,1))", "config": cfg,
             "hbm_gbs": round(by_all / (ms_step * 1e-3) / 1e9, 1), "roofline": roof,
-            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches)}),
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "step_ms": stats,
+            "gpu_launches": int(launches)}),
             flush=True)
     ctx.close()
 
@@ -434,18 +420,17 @@ def run_expand_gpu(args, w, world, rank, local, pg, B):
         step = lambda: BL.lowrank_expand_device(ctx, n, m, m, r, *bufs, out, stream=s)  # noqa
         fl, by = w.flops(), w.bytes()
         kernel = None  # named after a step: the kernel that served (UX) Vt
-    ms_rank, launches, clocks = _timed(ctx, s, step, args.steps, args.warmup, pg, B,
-                                       B.ClockSampler(local))
-    ms_step = B.all_max(pg, ms_rank) / args.steps
+    ms_med, ms_step, launches, clocks, stats = _timed(ctx, s, step, args.steps, args.warmup, pg,
+                                                      B, local)
     fl_all, by_all = B.all_sum(pg, fl), B.all_sum(pg, by)
-    roof = _roof(fl, by, ms_rank / args.steps, hbm, fp64, fsrc, hsrc, w.name)
+    roof = _roof(fl, by, ms_med, hbm, fp64, fsrc, hsrc, w.name)
     if kernel is None:
         v = ctx.last_variant
         kernel = ("lrb_gemm_kernel<q64> (UX), then " +
                   ("lrb_panel_kernel<p256>" if v == "p256" else f"lrb_gemm_kernel<{v}>") +
                   " ((UX) Vt)")
     roof["kernel"] = kernel
-    roof["kernel_ms"] = round(ms_rank / max(1, launches), 4)
+    roof["kernel_ms"] = round(ms_med * args.steps / max(1, launches), 4)
     e2e = None
     if args.e2e_steps > 0:
         from paper_2311_07602_b200.lrbatch import _check, lib
@@ -497,7 +482,7 @@ def run_expand_gpu(args, w, world, rank, local, pg, B):
     if rank == 0:
         cfg = dict(w.describe())
         cfg.update({"parallelism": (f"replicas{world}" if dense else f"shard{world}")
-                    + " (no collective)", "timed_launch": "CUDA graph of the K steps",
+                    + " (no collective)", "timed_launch": "one CUDA graph per step",
                     "l2": "output larger than L2 (no flush)"})
         print(json.dumps({
             "metric": "batched FP64 GFLOP/s", "value": round(fl_all / (ms_step * 1e-3) / 1e9, 2),
@@ -506,7 +491,8 @@ def run_expand_gpu(args, w, world, rank, local, pg, B):
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (counter RNG, uniform[-1,1))", "config": cfg,
             "hbm_gbs": round(by_all / (ms_step * 1e-3) / 1e9, 1), "roofline": roof,
-            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches)}),
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "step_ms": stats,
+            "gpu_launches": int(launches)}),
             flush=True)
     ctx.close()
 

@@ -168,6 +168,23 @@ lrb_status lrb_dgemm_strided_batched_host(lrb_ctx* ctx, char order, char opA, ch
                                           const double* B, int64_t ldb, int64_t strideB,
                                           double* C, int64_t ldc, int64_t strideC,
                                           int64_t batch);
+/*
+ * Pointer-array batch on HOST buffers (the reference's own mode: per-tile
+ * gemm_naive_raw calls over separately allocated blocks, blr.hpp:141-175;
+ * the per-item fan-out of naive_multiply_batch, bench.hpp:55-77). Same
+ * descriptor arrays as lrb_dgemm_ptr_batched, but A[i], B[i], C[i] are host
+ * pointers. Items are cut into chunks; within a chunk, operands that lie back
+ * to back in host memory move as one copy (input runs may span up to 4 KiB of
+ * allocation padding), and each chunk's H2D copy, pointer-array kernels and
+ * D2H copy are pipelined over three streams. Pinned memory (lrb_host_alloc)
+ * gets full PCIe rate; pageable memory goes through pinned staging.
+ * Synchronous.
+ */
+lrb_status lrb_dgemm_ptr_batched_host(lrb_ctx* ctx, char order, char opA, char opB, int64_t batch,
+                                      const int64_t* m, const int64_t* n, const int64_t* k,
+                                      const double* const* A, const int64_t* lda,
+                                      const double* const* B, const int64_t* ldb,
+                                      double* const* C, const int64_t* ldc, double beta);
 
 /* ------------------------------------------- the paper's low-rank product */
 /*

@@ -1,7 +1,10 @@
 """ctypes binding of the C-ABI in include/lrb.h (liblrb.so, built in-tree).
 
 The shared library is the product: there is no Python or CPU fallback. If the
-in-tree ``liblrb.so`` is missing, importing this module raises.
+in-tree ``liblrb.so`` is missing, importing this module raises. The library is
+mapped into the process on the first call through ``lib`` (not at import), so
+processes that only use the host-side workload definitions (bench.py's CPU
+reference arm) never load it.
 """
 from __future__ import annotations
 
@@ -102,6 +105,11 @@ SIGNATURES = {
         [vp, C.c_char, C.c_char, C.c_char, i64, i64, i64, dbl, vp, i64, i64, vp, i64, i64, vp, i64,
          i64, i64],
     ),
+    "lrb_dgemm_ptr_batched_host": (
+        C.c_int,
+        [vp, C.c_char, C.c_char, C.c_char, i64, P(i64), P(i64), P(i64), P(vp), P(i64), P(vp),
+         P(i64), P(vp), P(i64), dbl],
+    ),
     "lrb_lowrank_multiply": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, vp]),
     "lrb_lowrank_multiply_host": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp]),
     "lrb_lowrank_expand": (C.c_int, [vp, i64, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64,
@@ -150,4 +158,22 @@ def _load() -> C.CDLL:
     return lib
 
 
-lib = _load()
+class _LazyLib:
+    """``liblrb.so`` bound on first use (every attribute is a C-ABI symbol)"""
+
+    _cdll = None
+
+    def __getattr__(self, name):
+        if _LazyLib._cdll is None:
+            _LazyLib._cdll = _load()
+        return getattr(_LazyLib._cdll, name)
+
+    @staticmethod
+    def loaded() -> bool:
+        return _LazyLib._cdll is not None
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `make lib` (or "
+                      "__graft_entry__.build()); there is no CPU fallback")
+lib = _LazyLib()

@@ -1225,6 +1225,196 @@ extern "C" lrb_status lrb_dgemm_strided_batched_host(lrb_ctx* ctx, char order, c
   return pipe.finish();
 }
 
+// ------------------------------------------------ pointer array, host buffers
+namespace {
+// One contiguous host range moved with a single cudaMemcpyAsync. Consecutive
+// items whose operands lie back to back are merged (input runs may span
+// allocation padding), so a packed arena of 8192 blocks costs a few large
+// copies instead of one per block.
+struct HostRun {
+  const char* host;
+  size_t bytes;
+  size_t dev_off;  // offset inside the role's staging region
+  bool upload;     // C runs: uploaded too (beta = 1, or column gaps)
+};
+// The runs of one operand role inside a chunk. A run's device offset keeps
+// its host address's residue mod 256, so every item keeps its alignment (and
+// its TMA eligibility) on the device.
+struct RoleRuns {
+  std::vector<HostRun> runs;
+  size_t cursor = 0;
+  const char* start = nullptr;
+  const char* end = nullptr;
+  size_t off = 0;
+  bool upload = false;
+  void close() {
+    if (start) runs.push_back({start, size_t(end - start), off, upload});
+    start = end = nullptr;
+    upload = false;
+  }
+  // device offset (inside the role region) of an operand at host p
+  size_t place(const void* p, size_t bytes, size_t max_gap, bool up) {
+    const char* s = static_cast<const char*>(p);
+    if (!(start && s >= end && size_t(s - end) <= max_gap)) {
+      close();
+      start = s;
+      off = (cursor + 255) / 256 * 256 + (reinterpret_cast<uintptr_t>(s) & 255);
+    }
+    end = s + bytes;
+    upload = upload || up;
+    cursor = off + size_t(end - start);
+    return off + size_t(s - start);
+  }
+};
+}  // namespace
+
+extern "C" lrb_status lrb_dgemm_ptr_batched_host(lrb_ctx* ctx, char order, char opA, char opB,
+                                                 int64_t batch, const int64_t* m, const int64_t* n,
+                                                 const int64_t* k, const double* const* A,
+                                                 const int64_t* lda, const double* const* B,
+                                                 const int64_t* ldb, double* const* C,
+                                                 const int64_t* ldc, double beta) {
+  static const char* fn = "lrb_dgemm_ptr_batched_host";
+  if (!ctx) return fail(nullptr, LRB_ERR_ARG, "%s: null ctx", fn);
+  if (batch < 0) return fail(ctx, LRB_ERR_SHAPE, "%s: batch must be >= 0", fn);
+  if (batch == 0) return LRB_OK;
+  if (!m || !n || !k || !A || !B || !C || !lda || !ldb || !ldc)
+    return fail(ctx, LRB_ERR_ARG, "%s: a descriptor array is null", fn);
+  lrb_status st = bind(ctx);
+  if (st) return st;
+  const int beta_one = beta == 1.0;
+  // per-item footprints (elements) in the caller's order; C is uploaded when
+  // it is read (beta = 1) or has gaps between columns the kernel leaves alone
+  struct Foot {
+    int64_t a, b, c;
+    bool up_c;
+  };
+  std::vector<Foot> foot(static_cast<size_t>(batch));
+  double total_bytes = 0;
+  for (int64_t i = 0; i < batch; ++i) {
+    char where[64];
+    std::snprintf(where, sizeof(where), "%s: item %lld", fn, (long long)i);
+    st = validate(ctx, where, order, opA, opB, m[i], n[i], k[i], beta, A[i], lda[i], 0, B[i],
+                  ldb[i], 0, C[i], ldc[i], 0, 1);
+    if (st) return st;
+    Foot& f = foot[size_t(i)];
+    const bool work = m[i] > 0 && n[i] > 0 && !(k[i] == 0 && beta_one);
+    f.a = work && k[i] > 0 ? footprint(order, stored_a(opA, m[i], k[i]), lda[i]) : 0;
+    f.b = work && k[i] > 0 ? footprint(order, stored_b(opB, k[i], n[i]), ldb[i]) : 0;
+    f.c = work ? footprint(order, Stored{m[i], n[i]}, ldc[i]) : 0;
+    f.up_c = work && (beta_one || f.c != m[i] * n[i]);
+    total_bytes += 8.0 * double(f.a + f.b + f.c);
+  }
+  // chunks of consecutive items, ~1/8 of the batch each, within [64 MiB, 2 GiB]
+  const size_t target =
+      size_t(std::min(2.0 * (1 << 30), std::max(64.0 * (1 << 20), total_bytes / 8)));
+  constexpr size_t kMaxGap = 4096;
+  struct Chunk {
+    int64_t lo, hi;
+    RoleRuns ra, rb, rc;
+    std::vector<size_t> oa, ob, oc;  // per-item offsets inside the role regions
+    size_t base_b = 0, base_c = 0, bytes = 0;
+    std::vector<const double*> dA, dB;
+    std::vector<double*> dC;
+  };
+  std::vector<Chunk> chunks;
+  for (int64_t lo = 0; lo < batch;) {
+    chunks.emplace_back();
+    Chunk& ch = chunks.back();
+    ch.lo = lo;
+    int64_t i = lo;
+    for (; i < batch; ++i) {
+      const Foot& f = foot[size_t(i)];
+      const size_t now = ch.ra.cursor + ch.rb.cursor + ch.rc.cursor;
+      if (i > lo && now + 8 * size_t(f.a + f.b + f.c) > target) break;
+      ch.oa.push_back(f.a ? ch.ra.place(A[i], 8 * size_t(f.a), kMaxGap, true) : 0);
+      ch.ob.push_back(f.b ? ch.rb.place(B[i], 8 * size_t(f.b), kMaxGap, true) : 0);
+      ch.oc.push_back(f.c ? ch.rc.place(C[i], 8 * size_t(f.c), 0, f.up_c) : 0);
+    }
+    ch.ra.close();
+    ch.rb.close();
+    ch.rc.close();
+    ch.hi = i;
+    ch.base_b = (ch.ra.cursor + 255) / 256 * 256;
+    ch.base_c = ch.base_b + (ch.rb.cursor + 255) / 256 * 256;
+    ch.bytes = ch.base_c + (ch.rc.cursor + 255) / 256 * 256;
+    lo = i;
+  }
+  size_t lane_need = 0;
+  for (const Chunk& ch : chunks) lane_need = std::max(lane_need, ch.bytes);
+  const int lanes = int(std::min<size_t>(lrb_ctx::kLanes, chunks.size()));
+  for (int l = 0; l < lanes; ++l) {
+    if (ctx->lane_bytes[l] < lane_need) {
+      LRB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->lane_stream[l]));
+      if (ctx->lane_buf[l]) cudaFree(ctx->lane_buf[l]);
+      ctx->lane_buf[l] = nullptr;
+      ctx->lane_bytes[l] = 0;
+      LRB_CUDA_TRY(ctx, cudaMalloc(&ctx->lane_buf[l], lane_need));
+      ctx->lane_bytes[l] = lane_need;
+    }
+  }
+  // every chunk's plan is built before the pipeline starts (plan creation
+  // allocates and uploads its descriptors synchronously)
+  std::vector<lrb_ptr_plan*> plans(chunks.size(), nullptr);
+  auto destroy_plans = [&] {
+    for (lrb_ptr_plan* p : plans) lrb_ptr_plan_destroy(ctx, p);
+  };
+  size_t in_max = 0, out_max = 0;
+  bool page_in = false, page_out = false;
+  for (size_t c = 0; c < chunks.size(); ++c) {
+    Chunk& ch = chunks[c];
+    char* base = reinterpret_cast<char*>(ctx->lane_buf[c % size_t(lanes)]);
+    const int64_t cnt = ch.hi - ch.lo;
+    for (int64_t j = 0; j < cnt; ++j) {
+      ch.dA.push_back(reinterpret_cast<const double*>(base + ch.oa[size_t(j)]));
+      ch.dB.push_back(reinterpret_cast<const double*>(base + ch.base_b + ch.ob[size_t(j)]));
+      ch.dC.push_back(reinterpret_cast<double*>(base + ch.base_c + ch.oc[size_t(j)]));
+    }
+    st = lrb_ptr_plan_create(ctx, order, opA, opB, cnt, m + ch.lo, n + ch.lo, k + ch.lo,
+                             ch.dA.data(), lda + ch.lo, ch.dB.data(), ldb + ch.lo, ch.dC.data(),
+                             ldc + ch.lo, beta, &plans[c]);
+    if (st) {
+      destroy_plans();
+      return st;
+    }
+    size_t in_b = 0, out_b = 0;
+    for (const RoleRuns* rr : {&ch.ra, &ch.rb, &ch.rc})
+      for (const HostRun& r : rr->runs) {
+        if (!r.upload) continue;
+        in_b += (r.bytes + 255) / 256 * 256;
+        page_in = page_in || !host_pinned(r.host);
+      }
+    for (const HostRun& r : ch.rc.runs) {
+      out_b += (r.bytes + 255) / 256 * 256;
+      page_out = page_out || !host_pinned(r.host);
+    }
+    in_max = std::max(in_max, in_b);
+    out_max = std::max(out_max, out_b);
+  }
+  HostPipe pipe(ctx, lanes);
+  st = pipe.prepare(page_in ? in_max : 0, page_out ? out_max : 0);
+  for (size_t c = 0; !st && c < chunks.size(); ++c) {
+    const Chunk& ch = chunks[c];
+    const int l = int(c % size_t(lanes));
+    char* base = reinterpret_cast<char*>(ctx->lane_buf[l]);
+    const size_t region[3] = {0, ch.base_b, ch.base_c};
+    const RoleRuns* roles[3] = {&ch.ra, &ch.rb, &ch.rc};
+    if ((st = pipe.begin(l))) break;
+    for (int q = 0; q < 3 && !st; ++q)
+      for (const HostRun& r : roles[q]->runs)
+        if (r.upload && (st = pipe.h2d(l, base + region[q] + r.dev_off, r.host, r.bytes))) break;
+    if (st || (st = pipe.inputs_done(l))) break;
+    if ((st = lrb_ptr_plan_execute(ctx, plans[c], ctx->lane_stream[l]))) break;
+    for (const HostRun& r : ch.rc.runs)
+      if ((st = pipe.d2h(l, const_cast<char*>(r.host), base + ch.base_c + r.dev_off, r.bytes)))
+        break;
+    if (st || (st = pipe.outputs_done(l))) break;
+  }
+  const lrb_status st2 = pipe.finish();
+  destroy_plans();
+  return st ? st : st2;
+}
+
 extern "C" lrb_status lrb_gemm_naive_raw(lrb_ctx* ctx, const double* a, const double* b, double* c,
                                          size_t m, size_t k, size_t n, int accumulate,
                                          uint64_t* flops) {

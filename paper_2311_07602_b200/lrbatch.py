@@ -464,6 +464,23 @@ class Context:
                                          stream.handle if stream else None), self._h)
         del ma, na, ka, la, lb, lc
 
+    def dgemm_ptr_batched_host(self, order, opA, opB, m, n, k, A, lda, B, ldb, Cs, ldc,
+                               beta) -> None:
+        """pointer-array batch over HOST blocks (raw addresses or numpy arrays);
+        synchronous, copies pipelined with the kernels"""
+        batch = len(m)
+        ma, mp = _i64arr(m, batch, "m")
+        na, np_ = _i64arr(n, batch, "n")
+        ka, kp = _i64arr(k, batch, "k")
+        la, lp = _i64arr(lda, batch, "lda")
+        lb, lbp = _i64arr(ldb, batch, "ldb")
+        lc, lcp = _i64arr(ldc, batch, "ldc")
+        pa, pb, pc = _ptrarr(A, batch, "A"), _ptrarr(B, batch, "B"), _ptrarr(Cs, batch, "C")
+        _check(lib.lrb_dgemm_ptr_batched_host(self._h, _b(order), _b(opA), _b(opB), batch, mp,
+                                              np_, kp, pa, lp, pb, lbp, pc, lcp, float(beta)),
+               self._h)
+        del ma, na, ka, la, lb, lc
+
     # -- synthetic inputs (include/lrb_rng.h)
     def fill_uniform(self, buf, rows, cols, ld, stride, batch, seed, role, item_offset=0,
                      stream: Optional[Stream] = None) -> None:

@@ -11,11 +11,8 @@ Per-item accounting (beta = 0): flops 2mnk, algorithmic bytes 8(mk+kn+mn).
 """
 from __future__ import annotations
 
-import ctypes as C
 from dataclasses import dataclass, field
 from typing import List, Optional
-
-from . import _lib
 
 ROLE_A, ROLE_B, ROLE_C, ROLE_SHAPE_B, ROLE_SHAPE_R = 0, 1, 2, 3, 4
 GIB = 1 << 30
