@@ -682,7 +682,13 @@ def run_gpu_arm_variable(args, w, world, rank, local, pg, spans, scaling):
     # the per-item roofline: sum over items of max(flops/P, bytes/BW)
     t_item = sum(item_roofline_s(w, i, hbm_peak, fp64_peak) for i in vs.items)
     roof["per_item_roofline_frac"] = round(t_item / (my_med * 1e-3), 4)
-    roof["kernel"] = "lrb_gemm_kernel (pointer-array plan, %d launches)" % vs.plan.launches
+    # DMMA works on 8-column fragments: r_i pads to a multiple of 8 on the
+    # tensor pipe; the padded figure is the pipe's own utilisation
+    fl_pad = sum(2.0 * w.bs[i] * w.bs[i] * ((w.rs[i] + 7) // 8 * 8) for i in vs.items)
+    roof["padded_dmma_frac"] = round(fl_pad / (my_med * 1e-3) / (fp64_peak * 1e12), 4)
+    roof["kernel"] = ("lrb_varn_kernel (single-launch pointer-array kernel)"
+                      if vs.plan.launches == 1 else
+                      "lrb_gemm_kernel (pointer-array plan, %d launches)" % vs.plan.launches)
     roof["kernel_ms"] = round(my_med, 4)
     tr = traffic_from_profiles(w.name, count)
     roof["traffic"] = tr.get("dram_bytes_per_launch") if isinstance(tr, dict) else None

@@ -19,6 +19,7 @@
 #include "lrb_dispatch.cuh"
 #include "lrb_internal.h"
 #include "lrb_panel.h"
+#include "lrb_varn.h"
 
 // ===================================================================== errors
 namespace {
@@ -929,13 +930,109 @@ struct lrb_ptr_plan {
   ItemDesc* d_items = nullptr;
   uint64_t* d_tiles = nullptr;
   CUtensorMap* d_maps = nullptr;  // 2 per item on the TMA path
+  unsigned long long* d_ticket = nullptr;  // the single-launch kernel's tile tickets
+  int varn_flags = 0;                      // its kernel flags (scalar-column threshold)
   struct Group {
-    int variant;
+    int variant;  // a tile variant, or kVarnGroup: the single-launch kernel
     int64_t offset, count;
     int tma;
   };
   std::vector<Group> groups;
 };
+
+namespace lrb {
+constexpr int kVarnGroup = -2;
+
+// The single-launch variable-size kernel (lrb_varn.cu) serves every item it
+// can (TMA-eligible operands, k > 0) unless a tile variant is forced or
+// LRB_PTR_BUCKETS=1 asks for the per-variant buckets (A/B probe).
+bool varn_enabled(const lrb_ctx* ctx) {
+  if (forced_variant(ctx) >= 0) return false;
+  const char* s = std::getenv("LRB_PTR_BUCKETS");
+  return !(s && s[0] == '1');
+}
+
+// Columns past the last full 8-column fragment: up to `rem_max` of them run
+// as scalar DFMA chains, more as one zero-padded fragment. LRB_VARN_REM_MAX
+// (0..7) overrides the default.
+int varn_rem_max() {
+  const char* s = std::getenv("LRB_VARN_REM_MAX");
+  if (s && *s) return std::max(0, std::min(7, std::atoi(s)));
+  return kVarnRemMax;
+}
+int varn_rem_flags() { return (varn_rem_max() + 1) << 8; }
+
+// per-item tensor maps for the single-launch kernel's boxes
+bool encode_varn_pair(int a_t, int b_t, const ItemDesc& d, CUtensorMap* mA, CUtensorMap* mB) {
+  if (d.k <= 0) return false;
+  const bool okA = a_t ? encode_operand(mA, d.A, d.k, d.m, d.lda, 0, 1, kVarnKB + kPad, kVarnMB)
+                       : encode_operand(mA, d.A, d.m, d.k, d.lda, 0, 1, kVarnMB + kPad, kVarnKB);
+  if (!okA) return false;
+  return b_t ? encode_operand(mB, d.B, d.n, d.k, d.ldb, 0, 1, kVarnNB + kPad, kVarnKB)
+             : encode_operand(mB, d.B, d.k, d.n, d.ldb, 0, 1, kVarnKB + kPad, varn_box_cols(d.n));
+}
+
+// Claim order of the single-launch kernel's tiles. Each tile's time is
+// estimated at the roofline (its useful flops at the FP64 peak vs its bytes
+// at the HBM rate); FP64-bound and HBM-bound tiles go into two lists sorted
+// longest first (an item's tiles stay adjacent, so its B panel is reused from
+// L2), merged in proportion to their total time: the two CTAs of an SM then
+// tend to hold one tile of each kind, and the last tickets are the shortest.
+void varn_order(const std::vector<ItemDesc>& items, const std::vector<int64_t>& ids,
+                std::vector<uint64_t>* out) {
+  struct T {
+    uint64_t e;
+    double t;
+  };
+  std::vector<T> fp, mem;
+  double tot_fp = 0, tot_mem = 0;
+  for (int64_t id : ids) {
+    const ItemDesc& d = items[size_t(id)];
+    const int64_t ti = (d.m + kVarnMB - 1) / kVarnMB, tj = (d.n + kVarnNB - 1) / kVarnNB;
+    for (int64_t b = 0; b < tj; ++b)
+      for (int64_t a = 0; a < ti; ++a) {
+        const double rows = double(std::min<int64_t>(kVarnMB, d.m - a * kVarnMB));
+        const double cols = double(std::min<int64_t>(kVarnNB, d.n - b * kVarnNB));
+        const double fl = 2.0 * rows * cols * d.k;
+        const double by = 8.0 * (rows * d.k + rows * cols + (a == 0 ? cols * d.k : 0.0));
+        const double tf = fl / kFp64PeakFlops, tm = by / kHbmBytesPerS;
+        const T t{(uint64_t(id) << 32) | (uint64_t(a) << 16) | uint64_t(b), std::max(tf, tm)};
+        if (tf >= tm) {
+          fp.push_back(t);
+          tot_fp += t.t;
+        } else {
+          mem.push_back(t);
+          tot_mem += t.t;
+        }
+      }
+  }
+  auto by_time = [](const T& x, const T& y) { return x.t > y.t; };
+  // probe orders (LRB_VARN_ORDER): 1 = one list, longest first; 2 = item order
+  const char* env = std::getenv("LRB_VARN_ORDER");
+  const int mode = env ? std::atoi(env) : 0;
+  if (mode == 1 || mode == 2) {
+    fp.insert(fp.end(), mem.begin(), mem.end());
+    if (mode == 1) std::stable_sort(fp.begin(), fp.end(), by_time);
+    for (const T& t : fp) out->push_back(t.e);
+    return;
+  }
+  std::stable_sort(fp.begin(), fp.end(), by_time);
+  std::stable_sort(mem.begin(), mem.end(), by_time);
+  size_t i = 0, j = 0;
+  double used_fp = 0, used_mem = 0;
+  while (i < fp.size() || j < mem.size()) {
+    const bool take_fp = j >= mem.size() ||
+                         (i < fp.size() && used_fp * tot_mem <= used_mem * tot_fp);
+    if (take_fp) {
+      out->push_back(fp[i].e);
+      used_fp += fp[i++].t;
+    } else {
+      out->push_back(mem[j].e);
+      used_mem += mem[j++].t;
+    }
+  }
+}
+}  // namespace lrb
 
 extern "C" lrb_status lrb_ptr_plan_create(lrb_ctx* ctx, char order, char opA, char opB,
                                           int64_t batch, const int64_t* m, const int64_t* n,
@@ -1003,6 +1100,29 @@ extern "C" lrb_status lrb_ptr_plan_create(lrb_ctx* ctx, char order, char opA, ch
   const bool want_tma = loader_mode(ctx) == 1;
   if (want_tma && batch > 0) maps.resize(2 * size_t(batch));
   std::vector<uint64_t> tiles;
+  // the single-launch kernel takes every item whose operands its tensor maps
+  // can address; the rest stay in their variant buckets
+  if (want_tma && batch > 0 && varn_enabled(ctx)) {
+    std::vector<int64_t> varn_ids;
+    for (int v = 0; v < LRB_NUM_VARIANTS; ++v) {
+      auto& ids = per_variant[size_t(v)];
+      std::vector<int64_t> keep;
+      for (int64_t id : ids) {
+        const ItemDesc& d = items[size_t(id)];
+        if (encode_varn_pair(a_t, b_t, d, &maps[2 * size_t(id)], &maps[2 * size_t(id) + 1]))
+          varn_ids.push_back(id);
+        else
+          keep.push_back(id);
+      }
+      ids.swap(keep);
+    }
+    if (!varn_ids.empty()) {
+      plan->varn_flags = varn_rem_flags();
+      std::sort(varn_ids.begin(), varn_ids.end());
+      varn_order(items, varn_ids, &tiles);
+      plan->groups.push_back({kVarnGroup, 0, int64_t(tiles.size()), 1});
+    }
+  }
   for (int v = 0; v < LRB_NUM_VARIANTS; ++v) {
     auto& ids = per_variant[size_t(v)];
     if (ids.empty()) continue;
@@ -1052,6 +1172,14 @@ extern "C" lrb_status lrb_ptr_plan_create(lrb_ctx* ctx, char order, char opA, ch
       return cuda_fail(ctx, e, "lrb_ptr_plan_create: tensor map upload");
     }
   }
+  if (!plan->groups.empty() && plan->groups[0].variant == kVarnGroup) {
+    e = cudaMalloc(&plan->d_ticket, 2 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(plan->d_ticket, 0, 2 * sizeof(unsigned long long));
+    if (e != cudaSuccess) {
+      lrb_ptr_plan_destroy(ctx, plan);
+      return cuda_fail(ctx, e, "lrb_ptr_plan_create: ticket counter");
+    }
+  }
   if (!tiles.empty()) {
     e = cudaMalloc(&plan->d_tiles, sizeof(uint64_t) * tiles.size());
     if (e == cudaSuccess)
@@ -1087,10 +1215,21 @@ extern "C" lrb_status lrb_ptr_plan_execute(lrb_ctx* ctx, const lrb_ptr_plan* pla
   }
   for (int gi = 0; gi < ngroups; ++gi) {
     const auto& grp = plan->groups[size_t(gi)];
+    cudaStream_t s = fork ? ctx->aux_stream[gi % lrb_ctx::kAux] : user;
+    if (grp.variant == kVarnGroup) {
+      VarnProblem vp{plan->d_items, plan->d_tiles + grp.offset, plan->d_maps, grp.count,
+                     plan->d_ticket};
+      int64_t grid = 0;
+      cudaError_t e = launch_varn(plan->a_t, plan->b_t, vp,
+                                  plan->beta_one | plan->varn_flags | (debug_flags() & 6),
+                                  ctx->device, ctx->sm_count, s, &grid);
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "lrb_varn_kernel launch");
+      if (grid > 0) ctx->launches.fetch_add(1, std::memory_order_relaxed);
+      continue;
+    }
     PtrProblem p{plan->d_items, plan->d_tiles + grp.offset, grp.tma ? plan->d_maps : nullptr,
                  grp.count};
     LaunchInfo info{0, 0};
-    cudaStream_t s = fork ? ctx->aux_stream[gi % lrb_ctx::kAux] : user;
     cudaError_t e = kLaunch[grp.variant](plan->a_t, plan->b_t, grp.tma, nullptr, &p,
                                          plan->beta_one, ctx->device, ctx->sm_count, s, &info);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "lrb_gemm_kernel (ptr) launch");
@@ -1115,6 +1254,7 @@ extern "C" lrb_status lrb_ptr_plan_destroy(lrb_ctx* ctx, lrb_ptr_plan* plan) {
   if (plan->d_items) cudaFree(plan->d_items);
   if (plan->d_tiles) cudaFree(plan->d_tiles);
   if (plan->d_maps) cudaFree(plan->d_maps);
+  if (plan->d_ticket) cudaFree(plan->d_ticket);
   delete plan;
   return LRB_OK;
 }

@@ -1,0 +1,75 @@
+#!/usr/bin/env python3
+"""A/B probe of the cfg4 pointer-array paths on one box: the single-launch
+kernel under its tile orders and with the scalar remainder columns padded
+away, against the per-variant buckets.
+
+    python tools/probe_varn.py [--reps 10] [--items N]
+prints one JSON line per setting (median ms per execute, fraction of FP64 peak)
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+from paper_2311_07602_b200 import Context, workloads as W  # noqa: E402
+
+SETTINGS = [
+    ("varn interleaved", {}),
+    ("varn longest-first", {"LRB_VARN_ORDER": "1"}),
+    ("varn item order", {"LRB_VARN_ORDER": "2"}),
+    ("varn padded (no scalar columns)", {"LRB_DEBUG_FLAGS": "4"}),
+    ("varn scalar rem<=1", {"LRB_VARN_REM_MAX": "1"}),
+    ("varn scalar rem<=2", {"LRB_VARN_REM_MAX": "2"}),
+    ("varn scalar rem<=3", {"LRB_VARN_REM_MAX": "3"}),
+    ("varn scalar rem<=4", {"LRB_VARN_REM_MAX": "4"}),
+    ("varn scalar rem<=5", {"LRB_VARN_REM_MAX": "5"}),
+    ("varn no stores", {"LRB_DEBUG_FLAGS": "2"}),
+    ("buckets", {"LRB_PTR_BUCKETS": "1"}),
+]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--items", type=int, default=0)
+    ap.add_argument("--only", default="")
+    args = ap.parse_args()
+    ctx = Context(0)
+    w = W.get("cfg4")
+    n = args.items or w.batch
+    vs = bench.VariableSlice(ctx, w, 0, n)
+    fl = w.flops(vs.items)
+    s = ctx.stream()
+    for name, env in SETTINGS:
+        if args.only and args.only not in name:
+            continue
+        for k in ("LRB_VARN_ORDER", "LRB_DEBUG_FLAGS", "LRB_PTR_BUCKETS", "LRB_VARN_REM_MAX"):
+            os.environ.pop(k, None)
+        os.environ.update(env)
+        plan = ctx.ptr_plan("C", "N", "N", vs.bs, vs.rs, vs.bs, vs.pa, vs.bs, vs.pb, vs.bs,
+                            vs.pc, vs.bs, 0.0)
+        for _ in range(3):
+            plan.execute(s)
+        s.synchronize()
+        ts = []
+        for _ in range(args.reps):
+            e0, e1 = ctx.event(), ctx.event()
+            e0.record(s)
+            plan.execute(s)
+            e1.record(s)
+            s.synchronize()
+            ts.append(e0.elapsed_ms(e1))
+        ms = statistics.median(ts)
+        print(json.dumps({"setting": name, "env": env, "items": n, "launches": plan.launches,
+                          "ms": round(ms, 4), "tflops": round(fl / ms / 1e9, 2),
+                          "frac": round(fl / ms / 1e9 / 36.9, 4)}), flush=True)
+        plan.destroy()
+
+
+if __name__ == "__main__":
+    main()
