@@ -147,6 +147,28 @@ lrb_status lrb_dgemm_ptr_batched(lrb_ctx* ctx, char order, char opA, char opB, i
                                  double* const* C, const int64_t* ldc, double beta,
                                  void* stream);
 
+/*
+ * Pointer-array batch whose descriptor arrays (m, n, k, A, lda, B, ldb, C,
+ * ldc, each of length `batch`) live in DEVICE memory, e.g. built by the
+ * caller's own kernels (SURVEY §8(b)'s lrb_dgemm_ptr_batched). No host round
+ * trip: descriptor checks, tensor-map construction (tensormap.replace), cost
+ * ordering and tile prefix sums run as small kernels on `stream`, followed by
+ * the single-launch variable-size kernel and a generic kernel for items TMA
+ * cannot address. Asynchronous and capturable in lrb_graph_*. Items with
+ * invalid descriptors (negative extents, too-small leading dimensions, null
+ * operands, more than 65535 x 64 rows or columns) are skipped; when `info`
+ * (a DEVICE int64_t[2]) is non-null it receives {number of skipped items,
+ * first skipped index or -1}. Replaces: per-item gemm_naive_raw over blocks a
+ * GPU-resident BLR caller enumerates (blr.hpp:141-175).
+ */
+lrb_status lrb_dgemm_ptr_batched_device(lrb_ctx* ctx, char order, char opA, char opB,
+                                        int64_t batch, const int64_t* m, const int64_t* n,
+                                        const int64_t* k, const double* const* A,
+                                        const int64_t* lda, const double* const* B,
+                                        const int64_t* ldb, double* const* C,
+                                        const int64_t* ldc, double beta, int64_t* info,
+                                        void* stream);
+
 /* ------------------------------------------------ host-buffer entry points */
 /*
  * Drop-in for lrbatch::gemm_naive_raw (dense.hpp:43-45): row-major HOST

@@ -105,6 +105,10 @@ SIGNATURES = {
         [vp, C.c_char, C.c_char, C.c_char, i64, i64, i64, dbl, vp, i64, i64, vp, i64, i64, vp, i64,
          i64, i64],
     ),
+    "lrb_dgemm_ptr_batched_device": (
+        C.c_int,
+        [vp, C.c_char, C.c_char, C.c_char, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, dbl, vp, vp],
+    ),
     "lrb_dgemm_ptr_batched_host": (
         C.c_int,
         [vp, C.c_char, C.c_char, C.c_char, i64, P(i64), P(i64), P(i64), P(vp), P(i64), P(vp),

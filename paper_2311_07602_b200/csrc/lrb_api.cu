@@ -1221,7 +1221,7 @@ extern "C" lrb_status lrb_ptr_plan_execute(lrb_ctx* ctx, const lrb_ptr_plan* pla
                      plan->d_ticket};
       int64_t grid = 0;
       cudaError_t e = launch_varn(plan->a_t, plan->b_t, vp,
-                                  plan->beta_one | plan->varn_flags | (debug_flags() & 6),
+                                  plan->beta_one | plan->varn_flags | (debug_flags() & 14),
                                   ctx->device, ctx->sm_count, s, &grid);
       if (e != cudaSuccess) return cuda_fail(ctx, e, "lrb_varn_kernel launch");
       if (grid > 0) ctx->launches.fetch_add(1, std::memory_order_relaxed);

@@ -1,0 +1,522 @@
+// lrb_ptr_device.cu — pointer-array batches whose descriptors live in DEVICE
+// memory (lrb_dgemm_ptr_batched_device): a GPU-resident caller that builds
+// its block list on the device (the BLR per-tile products over separately
+// allocated blocks, reference blr.hpp:141-175; per item the reference's
+// gemm_naive_raw, dense.hpp:43-56) hands the arrays over without a host
+// round trip. Everything is stream-ordered and graph-capturable:
+//
+//   1. classify (one thread per item): read and check the descriptors, write
+//      the item's column-major view, and for TMA-addressable items build its
+//      two tensor maps in place (copies of host-encoded templates patched with
+//      tensormap.replace: address, extents, strides, the B box width), then
+//      bin it by estimated cost (power-of-two classes);
+//   2. scatter: items into claim order, costliest class first (the
+//      single-launch kernel's tail then holds the short tiles); the rest
+//      (misaligned operands, k = 0) into the generic list;
+//   3. a three-pass exclusive scan of tiles per ordered item (both lists);
+//   4. lrb_varn_kernel in device mode (tickets -> tiles through the prefix),
+//      and lrb_ptr_generic_kernel for the generic list.
+// Invalid descriptors (negative extents, leading dimensions too small) are
+// skipped and counted into the caller's optional device `info` pair.
+#include <algorithm>
+#include <cstring>
+
+#include "lrb_gemm.cuh"
+#include "lrb_internal.h"
+#include "lrb_varn.h"
+
+namespace lrb {
+
+bool encode_operand(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld,
+                    int64_t stride, int64_t zdim, int box_in, int box_out);
+
+namespace {
+
+constexpr int kClasses = 48;
+constexpr unsigned kSkip = 0xFFFFFFFFu, kGeneric = 0xFFFFFFFEu;
+constexpr int kGenTile = 64;  // generic kernel: 64 x 64 C tiles
+
+struct DevDesc {
+  const int64_t *m, *n, *k, *lda, *ldb, *ldc;
+  const double* const* A;
+  const double* const* B;
+  double* const* C;
+  int64_t batch;
+  int row_major, opA_t, opB_t, beta_one;
+};
+
+struct DevWs {
+  ItemDesc* items;          // [batch] column-major views
+  CUtensorMap* maps;        // [2 batch]
+  unsigned* cls;            // [batch] cost class, kSkip or kGeneric
+  uint32_t* order;          // [batch] single-launch items, claim order
+  uint32_t* order_g;        // [batch] generic items
+  int64_t* prefix;          // [batch + 1]
+  int64_t* prefix_g;        // [batch + 1]
+  int64_t* bsum;            // [2 * nblocks] scan block sums
+  unsigned* counters;       // [kClasses] histogram, [kClasses] cursors, n_varn, n_gen, n_gen_cursor
+  int64_t* totals;          // [2]
+  unsigned long long* tickets;  // [4]: single-launch pair, generic pair
+  long long* info;          // [2] invalid count, first invalid (-1)
+};
+
+__device__ __forceinline__ void tmr_address(CUtensorMap* m, const void* p) {
+  asm volatile("tensormap.replace.tile.global_address.global.b1024.b64 [%0], %1;\n" ::"l"(m),
+               "l"(p)
+               : "memory");
+}
+template <int ORD>
+__device__ __forceinline__ void tmr_dim(CUtensorMap* m, unsigned v) {
+  asm volatile("tensormap.replace.tile.global_dim.global.b1024.b32 [%0], %1, %2;\n" ::"l"(m),
+               "n"(ORD), "r"(v)
+               : "memory");
+}
+template <int ORD>
+__device__ __forceinline__ void tmr_stride(CUtensorMap* m, unsigned long long v) {
+  asm volatile("tensormap.replace.tile.global_stride.global.b1024.b64 [%0], %1, %2;\n" ::"l"(m),
+               "n"(ORD), "l"(v)
+               : "memory");
+}
+template <int ORD>
+__device__ __forceinline__ void tmr_box(CUtensorMap* m, unsigned v) {
+  asm volatile("tensormap.replace.tile.box_dim.global.b1024.b32 [%0], %1, %2;\n" ::"l"(m),
+               "n"(ORD), "r"(v)
+               : "memory");
+}
+
+// a (rows, cols, 1) column-major operand map from its template
+__device__ void build_map(CUtensorMap* dst, const CUtensorMap& tmpl, const double* base,
+                          int64_t rows, int64_t cols, int64_t ld, int box_out) {
+  const uint4* s = reinterpret_cast<const uint4*>(&tmpl);
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) d[i] = s[i];
+  tmr_address(dst, base);
+  tmr_dim<0>(dst, unsigned(rows));
+  tmr_dim<1>(dst, unsigned(cols));
+  tmr_dim<2>(dst, 1u);
+  tmr_stride<0>(dst, (unsigned long long)(ld * 8));
+  tmr_stride<1>(dst, (unsigned long long)(((ld * cols + 1) / 2 * 2) * 8));
+  if (box_out > 0) tmr_box<1>(dst, unsigned(box_out));
+}
+
+__device__ __forceinline__ bool tma_ok(const double* p, int64_t ld, int64_t rows, int64_t cols) {
+  return (reinterpret_cast<uintptr_t>(p) & 15) == 0 && (ld & 1) == 0 && ld * 8 < (int64_t(1) << 40) &&
+         rows <= 0x7FFFFFFF && cols <= 0x7FFFFFFF;
+}
+
+__device__ __forceinline__ int cost_class(double c) {
+  int e = 0;
+  frexp(c, &e);
+  return max(0, min(kClasses - 1, e));
+}
+
+__global__ void ptrdev_classify(const DevDesc a, const DevWs w, const __grid_constant__ CUtensorMap tA,
+                                const __grid_constant__ CUtensorMap tB, const int a_t,
+                                const int b_t) {
+  pdl_entry();
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= a.batch) return;
+  const int64_t m = a.m[i], n = a.n[i], k = a.k[i];
+  const int64_t lda = a.lda[i], ldb = a.ldb[i], ldc = a.ldc[i];
+  // stored shapes in the caller's order
+  const int64_t ar = a.opA_t ? k : m, ac = a.opA_t ? m : k;
+  const int64_t br = a.opB_t ? n : k, bc = a.opB_t ? k : n;
+  auto min_ld = [&](int64_t r, int64_t c) { return max(int64_t(1), a.row_major ? c : r); };
+  const bool bad = m < 0 || n < 0 || k < 0 || m > 0x7FFFFFFF || n > 0x7FFFFFFF ||
+                   k > 0x7FFFFFFF || lda < min_ld(ar, ac) || ldb < min_ld(br, bc) ||
+                   ldc < min_ld(m, n) || max(m, n) > int64_t(0xFFFF) * kGenTile ||
+                   (m > 0 && n > 0 && (!a.C[i] || (k > 0 && (!a.A[i] || !a.B[i]))));
+  if (bad) {
+    w.cls[i] = kSkip;
+    atomicAdd(reinterpret_cast<unsigned long long*>(&w.info[0]), 1ull);
+    atomicMin(&w.info[1], static_cast<long long>(i));
+    return;
+  }
+  // the column-major view (row-major C = op(A) op(B) <=> C^T = op(B)^T op(A)^T)
+  ItemDesc d;
+  if (!a.row_major) {
+    d.A = a.A[i], d.B = a.B[i], d.lda = lda, d.ldb = ldb;
+    d.m = int32_t(m), d.n = int32_t(n);
+  } else {
+    d.A = a.B[i], d.B = a.A[i], d.lda = ldb, d.ldb = lda;
+    d.m = int32_t(n), d.n = int32_t(m);
+  }
+  d.C = a.C[i];
+  d.ldc = ldc;
+  d.k = int32_t(k);
+  d.pad = 0;
+  w.items[i] = d;
+  if (d.m == 0 || d.n == 0 || (k == 0 && a.beta_one)) {
+    w.cls[i] = kSkip;
+    return;
+  }
+  const int64_t sar = a_t ? k : d.m, sac = a_t ? d.m : k;  // stored A in the view
+  const int64_t sbr = b_t ? d.n : k, sbc = b_t ? k : d.n;
+  if (k > 0 && tma_ok(d.A, d.lda, sar, sac) && tma_ok(d.B, d.ldb, sbr, sbc)) {
+    build_map(&w.maps[2 * i], tA, d.A, sar, sac, d.lda, 0);
+    build_map(&w.maps[2 * i + 1], tB, d.B, sbr, sbc, d.ldb, b_t ? 0 : varn_box_cols(d.n));
+    asm volatile("fence.proxy.tensormap::generic.release.gpu;\n" ::: "memory");
+    const double tiles = double((d.m + kVarnMB - 1) / kVarnMB) * double((d.n + kVarnNB - 1) / kVarnNB);
+    const int c = cost_class(tiles * double(k) * double(min(d.n, kVarnNB)));
+    w.cls[i] = unsigned(c);
+    atomicAdd(&w.counters[c], 1u);
+  } else {
+    w.cls[i] = kGeneric;
+    atomicAdd(&w.counters[2 * kClasses + 1], 1u);
+  }
+}
+
+__global__ void ptrdev_scatter(const DevDesc a, const DevWs w) {
+  pdl_entry();
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= a.batch) return;
+  const unsigned c = w.cls[i];
+  if (c == kSkip) return;
+  if (c == kGeneric) {
+    const unsigned pos = atomicAdd(&w.counters[2 * kClasses + 2], 1u);
+    w.order_g[pos] = uint32_t(i);
+    return;
+  }
+  unsigned base = 0;  // costliest class first
+  for (int q = kClasses - 1; q > int(c); --q) base += w.counters[q];
+  const unsigned pos = base + atomicAdd(&w.counters[kClasses + c], 1u);
+  w.order[pos] = uint32_t(i);
+}
+
+__device__ __forceinline__ int64_t item_tiles(const ItemDesc& d, int list) {
+  if (list == 0) return int64_t((d.m + kVarnMB - 1) / kVarnMB) * ((d.n + kVarnNB - 1) / kVarnNB);
+  return int64_t((d.m + kGenTile - 1) / kGenTile) * ((d.n + kGenTile - 1) / kGenTile);
+}
+
+__device__ __forceinline__ unsigned list_count(const DevWs& w, int list) {
+  if (list == 1) return w.counters[2 * kClasses + 1];
+  unsigned n = 0;
+  for (int q = 0; q < kClasses; ++q) n += w.counters[q];
+  return n;
+}
+
+// block-local exclusive scan of 1024 values (blockIdx.y = list)
+__device__ int64_t block_scan_excl(int64_t v, int64_t* total) {
+  __shared__ int64_t warp_sum[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sum[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int64_t s = lane < int(blockDim.x >> 5) ? warp_sum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    warp_sum[lane] = s;  // inclusive over warps
+  }
+  __syncthreads();
+  const int64_t before = wid ? warp_sum[wid - 1] : 0;
+  *total = warp_sum[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return before + x - v;
+}
+
+// pass 1: per-block exclusive scans of tiles per ordered item + block sums
+__global__ void ptrdev_scan1(const DevWs w) {
+  pdl_entry();
+  const int list = blockIdx.y;
+  const unsigned cnt = list_count(w, list);
+  const uint32_t* ord = list ? w.order_g : w.order;
+  int64_t* pre = list ? w.prefix_g : w.prefix;
+  const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  int64_t v = 0;
+  if (p < cnt) v = item_tiles(w.items[ord[p]], list);
+  int64_t tot;
+  const int64_t ex = block_scan_excl(v, &tot);
+  if (p < cnt) pre[p] = ex;
+  if (threadIdx.x == 0) w.bsum[int64_t(list) * gridDim.x + blockIdx.x] = tot;
+}
+
+// pass 2 (one block per list): exclusive scan of the block sums, totals
+__global__ void ptrdev_scan2(const DevWs w, const int nblocks) {
+  pdl_entry();
+  const int list = blockIdx.x;
+  int64_t* bs = w.bsum + int64_t(list) * nblocks;
+  int64_t run = 0;
+  for (int base = 0; base < nblocks; base += blockDim.x) {
+    const int j = base + threadIdx.x;
+    const int64_t v = j < nblocks ? bs[j] : 0;
+    int64_t tot;
+    const int64_t ex = block_scan_excl(v, &tot);
+    if (j < nblocks) bs[j] = run + ex;
+    run += tot;
+  }
+  if (threadIdx.x == 0) {
+    w.totals[list] = run;
+    const unsigned cnt = list_count(w, list);
+    (list ? w.prefix_g : w.prefix)[cnt] = run;
+    if (list == 0) w.counters[2 * kClasses] = cnt;
+  }
+}
+
+// pass 3: add the block offsets
+__global__ void ptrdev_scan3(const DevWs w) {
+  pdl_entry();
+  const int list = blockIdx.y;
+  const unsigned cnt = list_count(w, list);
+  const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p < cnt) (list ? w.prefix_g : w.prefix)[p] += w.bsum[int64_t(list) * gridDim.x + blockIdx.x];
+}
+
+// The generic path: items whose operands TMA cannot address (odd leading
+// dimensions, unaligned bases) or with k = 0. A persistent grid claims 64 x 64
+// C tiles by ticket; 256 threads stage 16-deep k slices of A and B in shared
+// memory with plain loads and each thread keeps a 4 x 4 block of C, every
+// entry one in-order FMA chain over k.
+__global__ void __launch_bounds__(256) lrb_ptr_generic_kernel(const DevWs w, const int a_t,
+                                                              const int b_t, const int beta_one) {
+  pdl_entry();
+  constexpr int T = kGenTile, KS = 16;
+  __shared__ double As[KS][T + 1];  // op(A)(i, kk) at As[kk][i]
+  __shared__ double Bs[KS][T + 1];  // op(B)(kk, j) at Bs[kk][j]
+  __shared__ long long s_entry;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // rows 4 tx.., cols 4 ty..
+  const int64_t limit = w.totals[1];
+  const int64_t count = w.counters[2 * kClasses + 1];
+  int64_t cursor = 0;
+#pragma unroll 1
+  while (true) {
+    if (threadIdx.x == 0) {
+      const long long t = static_cast<long long>(atomicAdd(&w.tickets[2], 1ull));
+      long long e = -1;
+      if (t < limit) {
+        const int64_t p = prefix_search(w.prefix_g, count, t, &cursor);
+        const uint32_t it = w.order_g[p];
+        const ItemDesc d = w.items[it];
+        const int64_t local = t - w.prefix_g[p];
+        const int64_t ti = (d.m + T - 1) / T;
+        e = (static_cast<long long>(it) << 32) | ((local % ti) << 16) | (local / ti);
+      }
+      s_entry = e;
+    }
+    __syncthreads();
+    const long long e = s_entry;
+    __syncthreads();
+    if (e < 0) break;
+    const ItemDesc d = w.items[uint32_t(e >> 32)];
+    const int i0 = int((e >> 16) & 0xFFFF) * T, j0 = int(e & 0xFFFF) * T;
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int i = i0 + 4 * tx + a, j = j0 + 4 * ty + b;
+        acc[a][b] = (beta_one && i < d.m && j < d.n) ? d.C[int64_t(j) * d.ldc + i] : 0.0;
+      }
+#pragma unroll 1
+    for (int k0 = 0; k0 < d.k; k0 += KS) {
+      for (int q = threadIdx.x; q < KS * T; q += blockDim.x) {
+        const int kk = q / T, o = q % T;
+        const int kg = k0 + kk;
+        const int i = i0 + o, j = j0 + o;
+        double av = 0.0, bv = 0.0;
+        if (kg < d.k && i < d.m) av = a_t ? d.A[int64_t(i) * d.lda + kg] : d.A[int64_t(kg) * d.lda + i];
+        if (kg < d.k && j < d.n) bv = b_t ? d.B[int64_t(kg) * d.ldb + j] : d.B[int64_t(j) * d.ldb + kg];
+        As[kk][o] = av;
+        Bs[kk][o] = bv;
+      }
+      __syncthreads();
+      const int kv = min(KS, d.k - k0);
+#pragma unroll 4
+      for (int kk = 0; kk < kv; ++kk) {
+        double av[4], bv[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) av[a] = As[kk][4 * tx + a];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) bv[b] = Bs[kk][4 * ty + b];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int i = i0 + 4 * tx + a, j = j0 + 4 * ty + b;
+        if (i < d.m && j < d.n) d.C[int64_t(j) * d.ldc + i] = acc[a][b];
+      }
+  }
+  // last CTA out resets the generic tickets
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long done = atomicAdd(&w.tickets[3], 1ull);
+    if (done == gridDim.x - 1) {
+      w.tickets[2] = 0;
+      w.tickets[3] = 0;
+      __threadfence();
+    }
+  }
+}
+
+__global__ void ptrdev_info_out(const DevWs w, long long* out) {
+  pdl_entry();
+  if (threadIdx.x == 0) {
+    out[0] = w.info[0];
+    out[1] = w.info[1] == 0x7FFFFFFFFFFFFFFFLL ? -1 : w.info[1];
+  }
+}
+
+__global__ void ptrdev_init(const DevWs w) {
+  pdl_entry();
+  const int t = threadIdx.x;
+  if (t < 2 * kClasses + 3) w.counters[t] = 0;
+  if (t < 4) w.tickets[t] = 0;
+  if (t == 0) {
+    w.info[0] = 0;
+    w.info[1] = 0x7FFFFFFFFFFFFFFFLL;
+  }
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+}  // namespace lrb
+
+using namespace lrb;
+
+extern "C" lrb_status lrb_dgemm_ptr_batched_device(lrb_ctx* ctx, char order, char opA, char opB,
+                                                   int64_t batch, const int64_t* m,
+                                                   const int64_t* n, const int64_t* k,
+                                                   const double* const* A, const int64_t* lda,
+                                                   const double* const* B, const int64_t* ldb,
+                                                   double* const* C, const int64_t* ldc,
+                                                   double beta, int64_t* info, void* stream) {
+  static const char* fn = "lrb_dgemm_ptr_batched_device";
+  if (!ctx) return fail(nullptr, LRB_ERR_ARG, "%s: null ctx", fn);
+  const bool rm = order == 'R' || order == 'r';
+  if (!(rm || order == 'C' || order == 'c'))
+    return fail(ctx, LRB_ERR_ARG, "%s: order must be 'C' or 'R', got '%c'", fn, order);
+  auto is_op = [](char o) { return o == 'N' || o == 'n' || o == 'T' || o == 't'; };
+  if (!is_op(opA)) return fail(ctx, LRB_ERR_ARG, "%s: opA must be 'N' or 'T', got '%c'", fn, opA);
+  if (!is_op(opB)) return fail(ctx, LRB_ERR_ARG, "%s: opB must be 'N' or 'T', got '%c'", fn, opB);
+  if (!(beta == 0.0 || beta == 1.0))
+    return fail(ctx, LRB_ERR_UNSUPPORTED,
+                "%s: beta must be 0 or 1 (the reference 'accumulate' flag), got %g", fn, beta);
+  if (batch < 0) return fail(ctx, LRB_ERR_SHAPE, "%s: batch must be >= 0", fn);
+  if (batch >= (int64_t(1) << 31)) return fail(ctx, LRB_ERR_UNSUPPORTED, "%s: batch >= 2^31", fn);
+  if (batch > 0 && (!m || !n || !k || !A || !B || !C || !lda || !ldb || !ldc))
+    return fail(ctx, LRB_ERR_ARG, "%s: a descriptor array is null", fn);
+  lrb_status st = bind(ctx);
+  if (st) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (batch == 0) {
+    if (info) {
+      const int64_t z[2] = {0, -1};
+      LRB_CUDA_TRY(ctx, cudaMemcpyAsync(info, z, sizeof(z), cudaMemcpyHostToDevice, s));
+    }
+    return LRB_OK;
+  }
+  const bool tA = opA == 'T' || opA == 't', tB = opB == 'T' || opB == 't';
+  // op flags of the column-major view
+  const int a_t = rm ? (tB ? 1 : 0) : (tA ? 1 : 0);
+  const int b_t = rm ? (tA ? 1 : 0) : (tB ? 1 : 0);
+
+  // workspace: a stream-ordered allocation per call (graph-owned under capture)
+  const int64_t nblocks = (batch + 1023) / 1024;
+  const size_t nb = size_t(batch);
+  size_t off = 0;
+  auto take = [&](size_t bytes, size_t al) {
+    off = align_up(off, al);
+    const size_t at = off;
+    off += bytes;
+    return at;
+  };
+  const size_t o_items = take(sizeof(ItemDesc) * nb, 128);
+  const size_t o_maps = take(sizeof(CUtensorMap) * 2 * nb, 128);
+  const size_t o_cls = take(4 * nb, 16);
+  const size_t o_order = take(4 * nb, 16);
+  const size_t o_order_g = take(4 * nb, 16);
+  const size_t o_prefix = take(8 * (nb + 1), 16);
+  const size_t o_prefix_g = take(8 * (nb + 1), 16);
+  const size_t o_bsum = take(8 * 2 * size_t(nblocks), 16);
+  const size_t o_cnt = take(4 * (2 * kClasses + 3), 16);
+  const size_t o_tot = take(8 * 2, 16);
+  const size_t o_tick = take(8 * 4, 16);
+  const size_t o_info = take(8 * 2, 16);
+  void* base = nullptr;
+  LRB_CUDA_TRY(ctx, pool_alloc(ctx, &base, off, s));
+  char* b = static_cast<char*>(base);
+  DevWs w;
+  w.items = reinterpret_cast<ItemDesc*>(b + o_items);
+  w.maps = reinterpret_cast<CUtensorMap*>(b + o_maps);
+  w.cls = reinterpret_cast<unsigned*>(b + o_cls);
+  w.order = reinterpret_cast<uint32_t*>(b + o_order);
+  w.order_g = reinterpret_cast<uint32_t*>(b + o_order_g);
+  w.prefix = reinterpret_cast<int64_t*>(b + o_prefix);
+  w.prefix_g = reinterpret_cast<int64_t*>(b + o_prefix_g);
+  w.bsum = reinterpret_cast<int64_t*>(b + o_bsum);
+  w.counters = reinterpret_cast<unsigned*>(b + o_cnt);
+  w.totals = reinterpret_cast<int64_t*>(b + o_tot);
+  w.tickets = reinterpret_cast<unsigned long long*>(b + o_tick);
+  w.info = reinterpret_cast<long long*>(b + o_info);
+
+  // tensor-map templates: the single-launch kernel's boxes, any valid 16-byte
+  // aligned placeholder geometry (address, extents, strides and the B box
+  // width are patched per item on the device)
+  CUtensorMap tmA, tmB;
+  std::memset(&tmA, 0, sizeof(tmA));
+  std::memset(&tmB, 0, sizeof(tmB));
+  const double* ph = reinterpret_cast<const double*>(b + o_items);
+  bool ok = a_t ? encode_operand(&tmA, ph, 64, 256, 64, 0, 1, kVarnKB + kPad, kVarnMB)
+                : encode_operand(&tmA, ph, 256, 64, 256, 0, 1, kVarnMB + kPad, kVarnKB);
+  ok = ok && (b_t ? encode_operand(&tmB, ph, 128, 64, 128, 0, 1, kVarnNB + kPad, kVarnKB)
+                  : encode_operand(&tmB, ph, 64, 128, 64, 0, 1, kVarnKB + kPad, kVarnNB));
+  if (!ok) {
+    cudaFreeAsync(base, s);
+    return fail(ctx, LRB_ERR_UNSUPPORTED, "%s: tensor-map templates unavailable", fn);
+  }
+  DevDesc a{m, n, k, lda, ldb, ldc, A, B, C, batch, rm ? 1 : 0, tA ? 1 : 0, tB ? 1 : 0,
+            beta == 1.0 ? 1 : 0};
+  const unsigned g1 = unsigned((batch + 255) / 256);
+  cudaError_t e = launch_pdl(ptrdev_init, dim3(1), dim3(128), 0, s, w);
+  if (e == cudaSuccess) e = launch_pdl(ptrdev_classify, dim3(g1), dim3(256), 0, s, a, w, tmA, tmB, a_t, b_t);
+  if (e == cudaSuccess) e = launch_pdl(ptrdev_scatter, dim3(g1), dim3(256), 0, s, a, w);
+  if (e == cudaSuccess)
+    e = launch_pdl(ptrdev_scan1, dim3(unsigned(nblocks), 2), dim3(1024), 0, s, w);
+  if (e == cudaSuccess) e = launch_pdl(ptrdev_scan2, dim3(2), dim3(1024), 0, s, w, int(nblocks));
+  if (e == cudaSuccess)
+    e = launch_pdl(ptrdev_scan3, dim3(unsigned(nblocks), 2), dim3(1024), 0, s, w);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(base, s);
+    return cuda_fail(ctx, e, "lrb_dgemm_ptr_batched_device: plan kernels");
+  }
+  ctx->launches.fetch_add(6, std::memory_order_relaxed);
+  // the single-launch list's item count (the histogram sum) is published by
+  // ptrdev_scan2 at counters[2 kClasses]
+  VarnProblem vp{w.items, nullptr, w.maps, 0, w.tickets, w.prefix, w.order,
+                 w.counters + 2 * kClasses, w.totals};
+  int64_t grid = 0;
+  e = launch_varn(a_t, b_t, vp, (beta == 1.0 ? 1 : 0) | (debug_flags() & 30), ctx->device,
+                  ctx->sm_count, s, &grid);
+  if (e == cudaSuccess && grid > 0) ctx->launches.fetch_add(1, std::memory_order_relaxed);
+  if (e == cudaSuccess) {
+    e = launch_pdl(lrb_ptr_generic_kernel, dim3(unsigned(2 * ctx->sm_count)), dim3(256), 0, s, w,
+                   a_t, b_t, beta == 1.0 ? 1 : 0);
+    if (e == cudaSuccess) ctx->launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  if (e == cudaSuccess && info) {
+    e = launch_pdl(ptrdev_info_out, dim3(1), dim3(32), 0, s, w, reinterpret_cast<long long*>(info));
+    if (e == cudaSuccess) ctx->launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  cudaError_t e2 = cudaFreeAsync(base, s);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "lrb_dgemm_ptr_batched_device: launch");
+  if (e2 != cudaSuccess) return cuda_fail(ctx, e2, "lrb_dgemm_ptr_batched_device: free");
+  return LRB_OK;
+}

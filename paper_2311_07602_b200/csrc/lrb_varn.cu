@@ -75,7 +75,7 @@ struct VarnLayout {
   // + a producer warpgroup (one active lane) that hands its registers to the
   // computing warpgroup (setmaxnreg): 64 x 32 accumulators need ~200
   static constexpr int THREADS = WARPS * 32 + 128;
-  static constexpr int PROD_REGS = 40, MMA_REGS = 216;
+  static constexpr int PROD_REGS = 48, MMA_REGS = 208;
   // stages, full + empty barriers, the slot -> tile ticket table
   static constexpr size_t SMEM_BYTES =
       size_t(STAGES) * STAGE_ELEMS * 8 + size_t(STAGES) * 8 * 2 + size_t(STAGES) * 8;
@@ -86,7 +86,7 @@ struct VarnLayout {
   }
 };
 
-// 64-byte descriptor load, bypassing L1 allocation
+// 64-byte descriptor load
 __device__ __forceinline__ ItemDesc load_desc(const ItemDesc* p) { return *p; }
 
 // Four k steps (k .. k+3) of the scalar columns 8F .. 8F+rem-1 for this
@@ -297,31 +297,69 @@ __global__ void __launch_bounds__(VarnLayout<AT, BT>::THREADS, 2)
       int stage = 0;
       uint32_t phase = 0;
       int64_t q = 0;
+      // host-built tile list, or (device-built plans) the tile prefix over
+      // the ordered items, searched forward from this CTA's last position
+      const bool dev = prob.tiles == nullptr;
+      const long long limit = dev ? static_cast<long long>(*prob.total) : prob.num_tiles;
+      const int64_t count = dev ? int64_t(*prob.count) : 0;
+      int64_t cursor = 0;
+      // claim a ticket and decode it into (entry, m, n, k); entry -1 = done
+      struct Claim {
+        long long e;
+        int m, n, k;
+      };
+      auto claim = [&]() -> Claim {
+        const long long t = static_cast<long long>(atomicAdd(prob.next, 1ull));
+        if (t >= limit) return Claim{-1, 0, 0, 0};
+        uint64_t e;
+        if (!dev) {
+          e = prob.tiles[t];
+          const ItemDesc* d = prob.items + uint32_t(e >> 32);
+          return Claim{static_cast<long long>(e), d->m, d->n, d->k};
+        }
+        const int64_t p = prefix_search(prob.prefix, count, t, &cursor);
+        const uint32_t it = prob.order[p];
+        const ItemDesc* d = prob.items + it;
+        const int m = d->m, n = d->n, k = d->k;
+        const int64_t local = t - prob.prefix[p];
+        const int64_t tiles_i = (m + L::MB - 1) / L::MB;
+        e = (uint64_t(it) << 32) | (uint64_t(local % tiles_i) << 16) | uint64_t(local / tiles_i);
+        return Claim{static_cast<long long>(e), m, n, k};
+      };
+      Claim cur = claim();
 #pragma unroll 1
       while (true) {
-        const long long t = static_cast<long long>(atomicAdd(prob.next, 1ull));
         if (q >= L::STAGES) mbar_wait(&empty[stage], phase ^ 1);
-        if (t >= prob.num_tiles) {
+        if (cur.e < 0) {
           slot_tile[stage] = -1;  // end of the sequence
           mbar_arrive(&full[stage]);
           break;
         }
-        const uint64_t e = prob.tiles[t];
+        const uint64_t e = static_cast<uint64_t>(cur.e);
         const uint32_t item = uint32_t(e >> 32);
-        const ItemDesc d = load_desc(prob.items + item);
         const int i0 = int((e >> 16) & 0xFFFF) * L::MB;
         const int j0 = int(e & 0xFFFF) * L::NBMAX;
         const void* mA = &prob.maps[2 * size_t(item)];
         const void* mB = &prob.maps[2 * size_t(item) + 1];
+        if (dev && !(flags & 16)) {  // (bit 4: probe without the fences)
+          // maps written by the planning kernels (tensormap.replace): order
+          // those generic-proxy writes before the TMA reads them
+          fence_tensormap_acquire(mA);
+          fence_tensormap_acquire(mB);
+        }
         // A is single-use unless other column tiles re-read it; B is re-read
         // by every row tile of the item
-        const uint64_t pol_a = d.n <= L::NBMAX ? policy_evict_normal() : policy_evict_last();
-        const uint64_t pol_b = d.m <= L::MB ? policy_evict_normal() : policy_evict_last();
-        const uint32_t bytes = L::chunk_bytes(d.n);
+        const uint64_t pol_a = cur.n <= L::NBMAX ? policy_evict_normal() : policy_evict_last();
+        const uint64_t pol_b = cur.m <= L::MB ? policy_evict_normal() : policy_evict_last();
+        const uint32_t bytes = L::chunk_bytes(cur.n);
+        const int kk = cur.k;
+        // (flags bit 3, a probe: claim the next tile only after this one)
+        const bool ahead = !(flags & 8);
+        Claim nxt{-1, 0, 0, 0};
 #pragma unroll 1
-        for (int k0 = 0; k0 < d.k; k0 += L::KB) {
+        for (int k0 = 0; k0 < kk; k0 += L::KB) {
           if (k0 > 0 && q >= L::STAGES) mbar_wait(&empty[stage], phase ^ 1);
-          slot_tile[stage] = t;
+          slot_tile[stage] = static_cast<long long>(e);
           fence_proxy_async_smem();
           double* As = smem + size_t(stage) * L::STAGE_ELEMS;
           double* Bs = As + L::A_ELEMS;
@@ -339,7 +377,11 @@ __global__ void __launch_bounds__(VarnLayout<AT, BT>::THREADS, 2)
             stage = 0;
             phase ^= 1;
           }
+          // the next tile is claimed and decoded while this one's first
+          // chunks are in flight, so its descriptor loads stay off the ring
+          if (ahead && k0 == 0) nxt = claim();
         }
+        cur = ahead ? nxt : claim();
       }
       // every claim of this CTA is over: the last CTA out resets the tickets
       // for the next launch (which waits for this grid before its first claim)
@@ -360,9 +402,9 @@ __global__ void __launch_bounds__(VarnLayout<AT, BT>::THREADS, 2)
 #pragma unroll 1
   while (true) {
     mbar_wait(&full[stage], phase);
-    const long long t = slot_tile[stage];
-    if (t < 0) break;
-    const uint64_t e = prob.tiles[t];
+    const long long te = slot_tile[stage];
+    if (te < 0) break;
+    const uint64_t e = static_cast<uint64_t>(te);
     const ItemDesc d = load_desc(prob.items + uint32_t(e >> 32));
     const int i0 = int((e >> 16) & 0xFFFF) * L::MB;
     const int j0 = int(e & 0xFFFF) * L::NBMAX;
@@ -404,7 +446,8 @@ cudaError_t launch_varn_t(const VarnProblem& p, int flags, int device, int sm_co
     if (device >= 0 && device < 64) occ_cache[device] = occ;
   }
   int64_t grid = int64_t(sm_count) * occ;
-  if (p.num_tiles < grid) grid = p.num_tiles;
+  // (device-built plans: the tile count is known only on the device)
+  if (p.tiles && p.num_tiles < grid) grid = p.num_tiles;
   if (grid_out) *grid_out = grid;
   if (grid <= 0) return cudaSuccess;
   return launch_pdl(kern, dim3(unsigned(grid)), dim3(L::THREADS), L::SMEM_BYTES, stream, p, flags);

@@ -30,11 +30,48 @@ __host__ __device__ __forceinline__ int varn_box_cols(int n) {
 
 struct VarnProblem {
   const ItemDesc* items;
-  const uint64_t* tiles;       // (item << 32) | (ti << 16) | tj, in claim order
+  const uint64_t* tiles;       // (item << 32) | (ti << 16) | tj, in claim order; or null:
   const CUtensorMap* maps;     // 2 per item (A, B), 3-D with z extent 1
-  int64_t num_tiles;
+  int64_t num_tiles;           // (host-built tile list)
   unsigned long long* next;    // [0] ticket counter, [1] finished CTAs (self-resetting)
+  // device-built plans (tiles == null): tickets index the tiles of the
+  // ordered items through their exclusive tile prefix
+  const int64_t* prefix;       // [count + 1]
+  const uint32_t* order;       // [count] item ids, claim order
+  const unsigned int* count;   // number of ordered items
+  const int64_t* total;        // prefix[count]
 };
+
+// Position p of ticket t in an exclusive prefix (prefix[p] <= t <
+// prefix[p + 1], p < count). Tickets a CTA takes only grow, so the search
+// runs forward from its previous position (*cursor): exponential, then binary.
+__device__ __forceinline__ int64_t prefix_search(const int64_t* prefix, int64_t count, int64_t t,
+                                                 int64_t* cursor) {
+  int64_t p = *cursor;
+  if (p >= count || prefix[p] > t) p = 0;
+  int64_t step = 1, hi = p + 1;
+  while (hi < count && prefix[hi] <= t) {
+    p = hi;
+    step *= 2;
+    hi = p + step;
+  }
+  if (hi > count) hi = count;
+  while (hi - p > 1) {
+    const int64_t mid = (p + hi) / 2;
+    if (prefix[mid] <= t)
+      p = mid;
+    else
+      hi = mid;
+  }
+  *cursor = p;
+  return p;
+}
+
+// order generic-proxy writes of a tensor map in global memory (another
+// kernel's tensormap.replace, or a copy) before TMA reads through it
+__device__ __forceinline__ void fence_tensormap_acquire(const void* map) {
+  asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;\n" ::"l"(map) : "memory");
+}
 
 // a_t / b_t: op flags of the column-major view; flags bit 0: beta = 1
 cudaError_t launch_varn(int a_t, int b_t, const VarnProblem& p, int flags, int device,

@@ -382,7 +382,10 @@ class Context:
         return DeviceBuffer(self, int(count) * 8)
 
     def to_device(self, host: np.ndarray) -> DeviceBuffer:
-        host = np.ascontiguousarray(host, dtype=np.float64)
+        """float64 copy on the device; integer arrays (descriptor arrays for
+        lrb_dgemm_ptr_batched_device) keep their dtype"""
+        host = np.asarray(host)
+        host = np.ascontiguousarray(host, dtype=None if host.dtype.kind in "iu" else np.float64)
         return DeviceBuffer(self, host.nbytes).upload(host)
 
     def pinned(self, count: int) -> PinnedBuffer:
@@ -463,6 +466,16 @@ class Context:
                                          pa, lp, pb, lbp, pc, lcp, float(beta),
                                          stream.handle if stream else None), self._h)
         del ma, na, ka, la, lb, lc
+
+    def dgemm_ptr_batched_device(self, order, opA, opB, batch, m, n, k, A, lda, B, ldb, Cs, ldc,
+                                 beta, info=None, stream: Optional[Stream] = None) -> None:
+        """pointer-array batch whose descriptor arrays are DEVICE addresses
+        (int64 m/n/k/ld arrays, pointer arrays as int64 device addresses);
+        asynchronous on `stream`; `info` an optional device int64[2]"""
+        _check(lib.lrb_dgemm_ptr_batched_device(
+            self._h, _b(order), _b(opA), _b(opB), int(batch), _ptr(m), _ptr(n), _ptr(k), _ptr(A),
+            _ptr(lda), _ptr(B), _ptr(ldb), _ptr(Cs), _ptr(ldc), float(beta), _ptr(info),
+            stream.handle if stream else None), self._h)
 
     def dgemm_ptr_batched_host(self, order, opA, opB, m, n, k, A, lda, B, ldb, Cs, ldc,
                                beta) -> None:

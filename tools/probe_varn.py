@@ -20,6 +20,9 @@ from paper_2311_07602_b200 import Context, workloads as W  # noqa: E402
 
 SETTINGS = [
     ("varn interleaved", {}),
+    ("varn claim-late", {"LRB_DEBUG_FLAGS": "8"}),
+    ("varn interleaved again", {}),
+    ("varn claim-late again", {"LRB_DEBUG_FLAGS": "8"}),
     ("varn longest-first", {"LRB_VARN_ORDER": "1"}),
     ("varn item order", {"LRB_VARN_ORDER": "2"}),
     ("varn padded (no scalar columns)", {"LRB_DEBUG_FLAGS": "4"}),
@@ -45,6 +48,38 @@ def main():
     vs = bench.VariableSlice(ctx, w, 0, n)
     fl = w.flops(vs.items)
     s = ctx.stream()
+    for dev_env in ({}, {"LRB_DEBUG_FLAGS": "16"}, {}, {"LRB_DEBUG_FLAGS": "16"}):
+        if args.only and "device" not in args.only:
+            break
+        os.environ.pop("LRB_DEBUG_FLAGS", None)
+        os.environ.update(dev_env)
+        import numpy as np
+
+        d = {kk: ctx.to_device(np.asarray(v, dtype=np.int64)) for kk, v in
+             dict(m=vs.bs, n=vs.rs, k=vs.bs, lda=vs.bs, ldb=vs.bs, ldc=vs.bs, A=vs.pa, B=vs.pb,
+                  C=vs.pc).items()}
+
+        def dev_call():
+            ctx.dgemm_ptr_batched_device("C", "N", "N", n, d["m"], d["n"], d["k"], d["A"],
+                                         d["lda"], d["B"], d["ldb"], d["C"], d["ldc"], 0.0,
+                                         None, s)
+
+        for _ in range(3):
+            dev_call()
+        s.synchronize()
+        ts = []
+        for _ in range(args.reps):
+            e0, e1 = ctx.event(), ctx.event()
+            e0.record(s)
+            dev_call()
+            e1.record(s)
+            s.synchronize()
+            ts.append(e0.elapsed_ms(e1))
+        ms = statistics.median(ts)
+        print(json.dumps({"setting": "device descriptors (lrb_dgemm_ptr_batched_device)",
+                          "env": dev_env,
+                          "items": n, "ms": round(ms, 4), "tflops": round(fl / ms / 1e9, 2),
+                          "frac": round(fl / ms / 1e9 / 36.9, 4)}), flush=True)
     for name, env in SETTINGS:
         if args.only and args.only not in name:
             continue
