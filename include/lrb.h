@@ -272,10 +272,12 @@ lrb_status lrb_batch_file_save(lrb_ctx* ctx, const char* path, int64_t batch, in
  * row-major (u block x rank, x rank x rank, vt rank x block).
  * lrb_blr_matvec: y = M rhs (blr_matvec, blr.hpp:141-175) for row-major
  * n x nrhs HOST buffers; the _device form takes device buffers and is
- * asynchronous. Three batched GEMM launches and one coupling kernel (the
- * first two forked onto an auxiliary stream and joined), every chain in the
- * reference's order (y_i = D_i rhs_i, then += U_ij X_ij Vt_ij rhs_j for j
- * ascending).
+ * asynchronous. Two batched GEMM launches around one coupling kernel, on the
+ * caller's stream, every chain in the reference's order (y_i = D_i rhs_i,
+ * then += U_ij X_ij Vt_ij rhs_j for j ascending). The matrix owns a
+ * grow-only matvec workspace: eager calls on different streams are ordered
+ * through an event, and buffers a captured graph references stay alive
+ * until lrb_blr_destroy.
  */
 typedef struct lrb_blr lrb_blr;
 lrb_status lrb_blr_create(lrb_ctx* ctx, int64_t n, int64_t block, int64_t rank, const double* diag,

@@ -606,6 +606,10 @@ extern "C" lrb_status lrb_destroy(lrb_ctx* ctx) {
     cudaEventDestroy(ctx->ws_ev);
   }
   if (ctx->ws) cudaFree(ctx->ws);
+  if (!ctx->ws_retired.empty()) {
+    cudaDeviceSynchronize();
+    for (void* p : ctx->ws_retired) cudaFree(p);
+  }
   if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
   if (ctx->flush_buf) cudaFree(ctx->flush_buf);
   delete ctx;
@@ -639,8 +643,9 @@ lrb_status acquire_workspace(lrb_ctx* ctx, size_t bytes, cudaStream_t s, void** 
     return LRB_OK;
   }
   if (bytes > ctx->ws_bytes) {
-    if (ctx->ws_pending) LRB_CUDA_TRY(ctx, cudaEventSynchronize(ctx->ws_ev));
-    if (ctx->ws) cudaFree(ctx->ws);
+    // grow-only; the outgrown buffer is retired, not freed (a captured graph
+    // may still reference it), and the new one starts with no pending user
+    if (ctx->ws) ctx->ws_retired.push_back(ctx->ws);
     ctx->ws = nullptr;
     ctx->ws_bytes = 0;
     ctx->ws_pending = false;
@@ -1610,7 +1615,15 @@ extern "C" lrb_status lrb_graph_launch(lrb_ctx* ctx, const lrb_graph* g, void* s
   if (!g) return fail(ctx, LRB_ERR_ARG, "lrb_graph_launch: null graph");
   lrb_status st = bind(ctx);
   if (st) return st;
-  LRB_CUDA_TRY(ctx, cudaGraphLaunch(g->exec, static_cast<cudaStream_t>(stream)));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // a replay may use the context workspace (captured multi-launch products):
+  // order it after the last eager user and make it the last user
+  if (ctx->ws_pending) LRB_CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ws_ev, 0));
+  LRB_CUDA_TRY(ctx, cudaGraphLaunch(g->exec, s));
+  if (ctx->ws_ev) {
+    LRB_CUDA_TRY(ctx, cudaEventRecord(ctx->ws_ev, s));
+    ctx->ws_pending = true;
+  }
   ctx->launches.fetch_add(g->launches, std::memory_order_relaxed);
   return LRB_OK;
 }

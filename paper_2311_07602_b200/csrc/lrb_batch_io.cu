@@ -160,6 +160,13 @@ extern "C" lrb_status lrb_batch_file_save(lrb_ctx* ctx, const char* path, int64_
     cudaGetLastError();
     return fail(ctx, LRB_ERR_CAPACITY, "lrb_batch_file_save: pinned staging");
   }
+  // the role buffers may still be written by work on non-blocking streams
+  // (e.g. lrb_fill_uniform on a context stream), which the legacy-stream
+  // copies below would not wait for: let all device work finish first
+  if (ok && device_ptrs && cudaDeviceSynchronize() != cudaSuccess) {
+    cudaFreeHost(stage);
+    return lrb::cuda_fail(ctx, cudaGetLastError(), "lrb_batch_file_save: device sync");
+  }
   for (int r = 0; r < 4 && ok; ++r) {
     if (!device_ptrs) {
       ok = std::fwrite(src[r], 8, size_t(n[r]), out.f) == size_t(n[r]);

@@ -38,10 +38,18 @@ struct lrb_blr {
   double* d_dcat = nullptr;   // per row i: block x pitch, [D_i | U_i0 | U_i1 | ...]
   double* d_vtcol = nullptr;  // per column j: (tiles-1) rank x block (i != j ascending)
   double* d_x = nullptr;      // same (j, i) order: rank x rank each
-  // per-nrhs workspace
-  int64_t ws_nrhs = -1;
+  // matvec workspace, grow-only (laid out for the call's nrhs inside the
+  // capacity). A buffer that is outgrown is retired, not freed: a captured
+  // graph may still reference it; retired buffers and plans are released by
+  // lrb_blr_destroy. ws_ev orders the matrix's eager matvecs on different
+  // streams (they share d_w / d_rz).
+  size_t w_cap = 0, rz_cap = 0;  // doubles
   double* d_w = nullptr;
   double* d_rz = nullptr;     // per row i: pitch x nrhs, [rhs_i; Z_i0; Z_i1; ...]
+  cudaEvent_t ws_ev = nullptr;
+  bool ws_pending = false;
+  std::vector<void*> retired;
+  std::vector<lrb_ptr_plan*> retired_plans;
   // reconstruct_dense: UX tiles in Vt's (j, i) order and the tile plan for
   // the last output buffer
   double* d_ux = nullptr;
@@ -60,29 +68,45 @@ using lrb::fail;
 
 namespace {
 
-void free_recon(lrb_ctx* ctx, lrb_blr* m) {
+// everything the matrix owns, after the device is idle (lrb_blr_destroy)
+void free_all(lrb_ctx* ctx, lrb_blr* m) {
+  cudaDeviceSynchronize();
   if (m->recon_plan) lrb_ptr_plan_destroy(ctx, m->recon_plan);
+  for (lrb_ptr_plan* p : m->retired_plans) lrb_ptr_plan_destroy(ctx, p);
+  for (void* p : m->retired) cudaFree(p);
   if (m->d_ux) cudaFree(m->d_ux);
-  m->recon_plan = nullptr;
-  m->recon_out = nullptr;
-  m->d_ux = nullptr;
-}
-
-void free_ws(lrb_ctx*, lrb_blr* m) {
   if (m->d_w) cudaFree(m->d_w);
   if (m->d_rz) cudaFree(m->d_rz);
-  m->d_w = m->d_rz = nullptr;
-  m->ws_nrhs = -1;
+  if (m->ws_ev) cudaEventDestroy(m->ws_ev);
+  m->retired.clear();
+  m->retired_plans.clear();
+  m->recon_plan = nullptr;
+  m->d_ux = m->d_w = m->d_rz = nullptr;
+  m->ws_ev = nullptr;
+}
+
+// grow-only: a capacity that is outgrown retires the old buffer
+lrb_status grow(lrb_ctx* ctx, lrb_blr* m, double** buf, size_t* cap, size_t need) {
+  if (*cap >= need && *buf) return LRB_OK;
+  if (*buf) m->retired.push_back(*buf);
+  *buf = nullptr;
+  *cap = 0;
+  // a plain allocation even while a graph is being captured on this thread
+  // (relaxed mode): the graph then references it like any caller buffer
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  cudaError_t e = cudaMalloc(buf, need * sizeof(double));
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  if (e != cudaSuccess) return lrb::cuda_fail(ctx, e, "lrb_blr workspace");
+  *cap = need;
+  return LRB_OK;
 }
 
 lrb_status ensure_ws(lrb_ctx* ctx, lrb_blr* m, int64_t nrhs) {
-  if (m->ws_nrhs == nrhs) return LRB_OK;
-  free_ws(ctx, m);
   const int64_t T = m->tiles, r = m->rank, items = T * (T - 1);
-  LRB_CUDA_TRY(ctx, cudaMalloc(&m->d_w, size_t(std::max<int64_t>(1, items * r * nrhs)) * sizeof(double)));
-  LRB_CUDA_TRY(ctx, cudaMalloc(&m->d_rz, size_t(T * m->pitch * nrhs) * sizeof(double)));
-  m->ws_nrhs = nrhs;
-  return LRB_OK;
+  lrb_status st = grow(ctx, m, &m->d_w, &m->w_cap, size_t(std::max<int64_t>(1, items * r * nrhs)));
+  if (st) return st;
+  return grow(ctx, m, &m->d_rz, &m->rz_cap, size_t(T * m->pitch * nrhs));
 }
 
 // Step 3: Z_ij = X_ij W_ij for every off-diagonal tile. Item q runs in W's
@@ -449,6 +473,11 @@ extern "C" lrb_status lrb_blr_create(lrb_ctx* ctx, int64_t n, int64_t block, int
   return LRB_OK;
 }
 
+namespace {
+lrb_status matvec_steps(lrb_ctx* ctx, lrb_blr* m, const double* rhs, int64_t nrhs, double* y,
+                        cudaStream_t s);
+}
+
 extern "C" lrb_status lrb_blr_matvec_device(lrb_ctx* ctx, lrb_blr* m, const double* rhs,
                                             int64_t nrhs, double* y, void* stream) {
   static const char* fn = "lrb_blr_matvec";
@@ -458,12 +487,33 @@ extern "C" lrb_status lrb_blr_matvec_device(lrb_ctx* ctx, lrb_blr* m, const doub
   lrb_status st = lrb::bind(ctx);
   if (st) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int64_t T = m->tiles, b = m->block, r = m->rank, K = (T - 1) * r, P = m->pitch;
+  const int64_t T = m->tiles, b = m->block, P = m->pitch;
   if (T == 1)  // y = D rhs only
     return lrb::run_strided_rowmajor_beta(ctx, b, nrhs, b, m->d_dcat, P, b * P, rhs, nrhs,
                                           b * nrhs, y, nrhs, b * nrhs, T, 0, s);
   st = ensure_ws(ctx, m, nrhs);
   if (st) return st;
+  // eager calls on different streams share the workspace: wait for the last
+  // user (captured calls are ordered by the graph's own stream)
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  LRB_CUDA_TRY(ctx, cudaStreamIsCapturing(s, &cap));
+  const bool eager = cap == cudaStreamCaptureStatusNone;
+  if (eager && m->ws_pending) LRB_CUDA_TRY(ctx, cudaStreamWaitEvent(s, m->ws_ev, 0));
+  st = matvec_steps(ctx, m, rhs, nrhs, y, s);
+  if (st) return st;
+  if (eager) {
+    if (!m->ws_ev) LRB_CUDA_TRY(ctx, cudaEventCreateWithFlags(&m->ws_ev, cudaEventDisableTiming));
+    LRB_CUDA_TRY(ctx, cudaEventRecord(m->ws_ev, s));
+    m->ws_pending = true;
+  }
+  return LRB_OK;
+}
+
+namespace {
+lrb_status matvec_steps(lrb_ctx* ctx, lrb_blr* m, const double* rhs, int64_t nrhs, double* y,
+                        cudaStream_t s) {
+  lrb_status st = LRB_OK;
+  const int64_t T = m->tiles, b = m->block, r = m->rank, K = (T - 1) * r, P = m->pitch;
   // 1. W_.j = [Vt_ij]_i rhs_j
   st = lrb::run_strided_rowmajor_beta(ctx, K, nrhs, b, m->d_vtcol, b, K * b, rhs, nrhs, b * nrhs,
                                       m->d_w, nrhs, K * nrhs, T, 0, s);
@@ -535,6 +585,7 @@ extern "C" lrb_status lrb_blr_matvec_device(lrb_ctx* ctx, lrb_blr* m, const doub
   return lrb::run_strided_rowmajor_beta(ctx, b, nrhs, P, m->d_dcat, P, b * P, m->d_rz, nrhs,
                                         P * nrhs, y, nrhs, b * nrhs, T, 0, s);
 }
+}  // namespace
 
 extern "C" lrb_status lrb_blr_matvec(lrb_ctx* ctx, lrb_blr* m, const double* rhs, int64_t nrhs,
                                      double* y) {
@@ -565,8 +616,7 @@ extern "C" lrb_status lrb_blr_matvec(lrb_ctx* ctx, lrb_blr* m, const double* rhs
 extern "C" lrb_status lrb_blr_destroy(lrb_ctx* ctx, lrb_blr* m) {
   if (!m) return LRB_OK;
   if (ctx) cudaSetDevice(ctx->device);
-  free_ws(ctx, m);
-  free_recon(ctx, m);
+  free_all(ctx, m);
   if (m->d_dcat) cudaFree(m->d_dcat);
   if (m->d_vtcol) cudaFree(m->d_vtcol);
   if (m->d_x) cudaFree(m->d_x);
@@ -614,7 +664,11 @@ extern "C" lrb_status lrb_blr_reconstruct_dense(lrb_ctx* ctx, lrb_blr* m, double
   }
   if (T == 1) return LRB_OK;
   const int64_t items = T * (T - 1);
-  if (!m->d_ux) LRB_CUDA_TRY(ctx, cudaMalloc(&m->d_ux, size_t(items * b * r) * sizeof(double)));
+  if (!m->d_ux) {
+    size_t ux_cap = 0;
+    st = grow(ctx, m, &m->d_ux, &ux_cap, size_t(items * b * r));
+    if (st) return st;
+  }
   using TileCfg = lrb::VariantTraits<LRB_V_Q64>::Cfg<false, false, true>;
   lrb::BlrTileProblem tp;
   std::memset(&tp, 0, sizeof(tp));
@@ -625,7 +679,8 @@ extern "C" lrb_status lrb_blr_reconstruct_dense(lrb_ctx* ctx, lrb_blr* m, double
       lrb::encode_operand(&tp.tmB, m->d_ux, r, b, r, b * r, items, TileCfg::B_BOX_IN,
                           TileCfg::B_BOX_OUT);
   if (!tiles_ok && m->recon_out != out) {
-    if (m->recon_plan) lrb_ptr_plan_destroy(ctx, m->recon_plan);
+    // a captured graph may still execute the previous plan: retire it
+    if (m->recon_plan) m->retired_plans.push_back(m->recon_plan);
     m->recon_plan = nullptr;
     m->recon_out = nullptr;
     std::vector<int64_t> mm(items, b), nn(items, b), kk(items, r), la(items, r), lb(items, b),

@@ -52,6 +52,9 @@ struct lrb_ctx {
   size_t ws_bytes = 0;
   cudaEvent_t ws_ev = nullptr;
   bool ws_pending = false;
+  // outgrown workspaces: a captured graph may still reference them, so they
+  // are released only by lrb_destroy (after the device is idle)
+  std::vector<void*> ws_retired;
   // L2 flush buffer
   void* flush_buf = nullptr;
   size_t flush_bytes = 0;

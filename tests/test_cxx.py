@@ -42,3 +42,30 @@ def test_cxx_random_inputs_equal_the_reference(tmp_path):
                    capture_output=True, text=True)
     r = subprocess.run([exe], capture_output=True, text=True, timeout=60)
     assert r.returncode == 0 and "0 mismatches" in r.stdout, r.stdout + r.stderr
+
+
+DROPIN = os.path.join(ROOT, "tests", "cxx", "test_dropin.cpp")
+
+
+def _build_dropin(out):
+    # the reference's include path swapped for the repo's: include/lrbatch/*.hpp
+    cmd = ["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"), "-I",
+           os.path.join(ROOT, "tests", "cxx"), DROPIN, "-o", out, "-L", LIBDIR, "-llrb",
+           f"-Wl,-rpath,{LIBDIR}"]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+
+
+def test_dropin_reference_call_sites_compile(tmp_path):
+    """test_core.cpp:13-88 and lrbatch_main.cpp:79-102 as written, in
+    namespace lrbatch, against include/lrbatch/*.hpp"""
+    _build_dropin(str(tmp_path / "d"))
+    assert os.path.exists(tmp_path / "d")
+
+
+@pytest.mark.gpu
+def test_dropin_reference_call_sites_run(tmp_path):
+    exe = str(tmp_path / "d")
+    _build_dropin(exe)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failures" in r.stdout and "FAIL" not in r.stdout, r.stdout

@@ -132,3 +132,35 @@ def test_device_matvec_in_a_graph_replayed(ctx, tiles, rank, nrhs, block):
         cap.graph.launch(s)
         s.synchronize()
         assert np.array_equal(y_graph.download(rhs.data.size), want)
+
+
+def test_graph_survives_workspace_growth_and_other_streams(ctx):
+    # a matvec captured with one nrhs, then eager calls with a
+    # larger nrhs (the workspace grows: the old buffers are retired, not
+    # freed) and on a second stream; every replay of the graph still equals
+    # the eager result
+    from paper_2311_07602_b200.lrbatch import _check as check, lib
+
+    tiles, block, rank = 4, 64, 8
+    m = B.BlrMatrix.random(tiles * block, block, rank, 77)
+    h = m.device_handle(ctx)
+    s1, s2 = ctx.stream(), ctx.stream()
+    small, big = _rhs(tiles * block, 4, 1), _rhs(tiles * block, 16, 2)
+    d_small, d_big = ctx.to_device(small.data), ctx.to_device(big.data)
+    y_eager, y_graph = ctx.empty(small.data.size), ctx.empty(small.data.size)
+    y_big1, y_big2 = ctx.empty(big.data.size), ctx.empty(big.data.size)
+    check(lib.lrb_blr_matvec_device(ctx._h, h, d_small.ptr, 4, y_eager.ptr, s1.handle), ctx._h)
+    s1.synchronize()
+    with ctx.capture(s1) as cap:
+        check(lib.lrb_blr_matvec_device(ctx._h, h, d_small.ptr, 4, y_graph.ptr, s1.handle),
+              ctx._h)
+    want = y_eager.download(small.data.size)
+    # grow the workspace, then alternate streams (ordered by the matrix's event)
+    check(lib.lrb_blr_matvec_device(ctx._h, h, d_big.ptr, 16, y_big1.ptr, s1.handle), ctx._h)
+    check(lib.lrb_blr_matvec_device(ctx._h, h, d_big.ptr, 16, y_big2.ptr, s2.handle), ctx._h)
+    for _ in range(3):
+        cap.graph.launch(s1)
+    ctx.synchronize()
+    assert np.array_equal(y_graph.download(small.data.size), want)
+    _check(m, big, DenseBlock(big.rows, big.cols, y_big1.download(big.data.size)))
+    assert np.array_equal(y_big1.download(big.data.size), y_big2.download(big.data.size))

@@ -148,3 +148,33 @@ def test_negative_control():
     if O.ref_available():
         err, wi, we = O.ref_compare_to_reference(6, 32, 4, *args, g)
         assert err > 1e-12 and wi == 3 and we == 5
+
+
+def test_graph_survives_context_workspace_growth():
+    # the r > 32 path captured while the context workspace fits;
+    # an eager product that needs more grows it (the old buffer is retired,
+    # not freed): the graph's replays stay correct
+    from paper_2311_07602_b200 import Context
+
+    c = Context(0)
+    try:
+        blk, r = 256, 64
+        small = L.LowRankBatch.random(3, blk, r, 5151)
+        big = L.LowRankBatch.random(40, blk, r, 5152)
+        ds = [c.to_device(x) for x in (small.a_vt_batch, small.b_u_batch, small.a_x_batch,
+                                       small.b_x_batch)]
+        db = [c.to_device(x) for x in (big.a_vt_batch, big.b_u_batch, big.a_x_batch,
+                                       big.b_x_batch)]
+        gs, gg, gb = c.empty(3 * r * r), c.empty(3 * r * r), c.empty(40 * r * r)
+        s = c.stream()
+        L.lowrank_multiply_device(c, 3, blk, r, *ds, gs, stream=s)
+        with c.capture(s) as cap:
+            L.lowrank_multiply_device(c, 3, blk, r, *ds, gg, stream=s)
+        L.lowrank_multiply_device(c, 40, blk, r, *db, gb, stream=s)  # grows the workspace
+        for _ in range(3):
+            cap.graph.launch(s)
+        s.synchronize()
+        assert np.array_equal(gg.download(), gs.download())
+        _check(big, gb.download())
+    finally:
+        c.close()
