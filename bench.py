@@ -788,6 +788,7 @@ def run_gpu_arm(args, w, world, rank, local, pg):
         ms_rank = sum(per)
         launches = args.steps * nchunks  # only GEMM launches count
     ms_step, stats = job_step_stats(pg, per, ms_rank)
+    cold = cold_single_call(ctx, stream, w, bufs[0], count, args.steps) if copies > 1 else None
     items_all = all_sum(pg, float(count))
     flops_all = w.item_flops() * items_all
     bytes_all = w.item_bytes() * items_all
@@ -827,17 +828,43 @@ def run_gpu_arm(args, w, world, rank, local, pg):
                            f"({per_item * count * copies / 2**20:.0f} MiB) > 3x L2"
                            if copies > 1 else "inputs larger than L2 (no flush)"),
                     "chunks_per_step": nchunks})
+        if cold is not None:
+            by = w.item_bytes() * count
+            for k in ("evict", "flush"):
+                cold[f"{k}_hbm_frac"] = round(by / (cold[f"{k}_ms"] * 1e-3) / 1e9 / hbm_peak, 4)
         line = {
             "metric": "batched FP64 GFLOP/s", "value": round(gflops, 2), "unit": "GFLOP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (device counter RNG, uniform[-1,1), BASELINE seeds)",
-            "config": cfg, "hbm_gbs": round(gbs, 1), "step_ms": stats, "roofline": roof,
+            "config": cfg, "hbm_gbs": round(gbs, 1), "step_ms": stats, "cold_call": cold,
+            "roofline": roof,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches),
         }
         print(json.dumps(line), flush=True)
     ctx.close()
+
+
+def cold_single_call(ctx, stream, w, buf, count, reps):
+    """one launch at a time (outside the timed steps) with the working set
+    out of L2: after a clean eviction (lrb_l2_evict: L2 refilled with clean
+    lines) and after a memset flush (lrb_l2_flush: L2 full of dirty lines the
+    kernel's reads must write back first); median ms of `reps` each"""
+    A, B, Cd = buf
+    e0, e1 = ctx.event(), ctx.event()
+    out = {}
+    for mode in ("evict", "flush"):
+        ts = []
+        for _ in range(max(3, reps)):
+            (ctx.l2_evict if mode == "evict" else ctx.l2_flush)(stream)
+            e0.record(stream)
+            gemm(ctx, w, A, B, Cd, count, stream)
+            e1.record(stream)
+            stream.synchronize()
+            ts.append(e0.elapsed_ms(e1))
+        out[f"{mode}_ms"] = round(statistics.median(ts), 5)
+    return out
 
 
 def run_e2e(args, ctx, w, first, count, pg):

@@ -102,6 +102,10 @@ lrb_status lrb_event_record(lrb_ctx* ctx, void* ev, void* stream);
 lrb_status lrb_event_elapsed_ms(lrb_ctx* ctx, void* ev_start, void* ev_end, float* ms);
 /* write a buffer larger than L2 on `stream` (timing hygiene between reps) */
 lrb_status lrb_l2_flush(lrb_ctx* ctx, void* stream);
+/* read a clean buffer of twice the L2 size on `stream`: the next kernel
+   starts with none of its data in L2 and no dirty lines to write back
+   (a cold call without lrb_l2_flush's write-back tail) */
+lrb_status lrb_l2_evict(lrb_ctx* ctx, void* stream);
 
 /* ------------------------------------------------------------- hot path */
 /*

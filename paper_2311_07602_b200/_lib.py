@@ -79,6 +79,7 @@ SIGNATURES = {
     "lrb_event_record": (C.c_int, [vp, vp, vp]),
     "lrb_event_elapsed_ms": (C.c_int, [vp, vp, vp, P(C.c_float)]),
     "lrb_l2_flush": (C.c_int, [vp, vp]),
+    "lrb_l2_evict": (C.c_int, [vp, vp]),
     "lrb_dgemm_strided_batched": (
         C.c_int,
         [vp, C.c_char, C.c_char, C.c_char, i64, i64, i64, dbl, vp, i64, i64, vp, i64, i64, vp, i64,

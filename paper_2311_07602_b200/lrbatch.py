@@ -408,6 +408,10 @@ class Context:
     def l2_flush(self, stream: Optional[Stream] = None) -> None:
         _check(lib.lrb_l2_flush(self._h, stream.handle if stream else None), self._h)
 
+    def l2_evict(self, stream: Optional[Stream] = None) -> None:
+        """clean eviction (reads 2x L2): a cold start without dirty write-backs"""
+        _check(lib.lrb_l2_evict(self._h, stream.handle if stream else None), self._h)
+
     def set_variant_override(self, name: Optional[str]) -> None:
         v = -1 if name is None else variant_from_name(name)
         if name is not None and v < 0:

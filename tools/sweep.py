@@ -30,7 +30,7 @@ def time_launches(ctx, stream, launch, reps, flush):
     out = []
     for _ in range(reps):
         if flush:
-            ctx.l2_flush(stream)
+            ctx.l2_evict(stream)  # clean eviction (no dirty write-backs in the timed launch)
         e0.record(stream)
         launch()
         e1.record(stream)
