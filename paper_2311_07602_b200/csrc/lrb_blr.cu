@@ -48,6 +48,9 @@ struct lrb_blr {
   double* d_rz = nullptr;     // per row i: pitch x nrhs, [rhs_i; Z_i0; Z_i1; ...]
   cudaEvent_t ws_ev = nullptr;
   bool ws_pending = false;
+  // the fused matvec's self-resetting sync words: [T] ready counts, then two
+  // 64-bit ticket words (allocated and zeroed at create)
+  unsigned* d_sync = nullptr;
   std::vector<void*> retired;
   std::vector<lrb_ptr_plan*> retired_plans;
   // reconstruct_dense: UX tiles in Vt's (j, i) order and the tile plan for
@@ -58,6 +61,10 @@ struct lrb_blr {
 };
 
 namespace lrb {
+bool launch_blr_fused(lrb_ctx* ctx, const double* rhs, int64_t nrhs, double* y, int64_t T,
+                      int64_t b, int64_t r, int64_t P, const double* vtcol, const double* x,
+                      const double* dcat, double* rz, unsigned* ready,
+                      unsigned long long* next, cudaStream_t s, lrb_status* st);
 lrb_status run_strided_rowmajor_beta(lrb_ctx* ctx, int64_t m, int64_t n, int64_t k,
                                      const double* A, int64_t lda, int64_t sA, const double* B,
                                      int64_t ldb, int64_t sB, double* C, int64_t ldc, int64_t sC,
@@ -78,6 +85,8 @@ void free_all(lrb_ctx* ctx, lrb_blr* m) {
   if (m->d_w) cudaFree(m->d_w);
   if (m->d_rz) cudaFree(m->d_rz);
   if (m->ws_ev) cudaEventDestroy(m->ws_ev);
+  if (m->d_sync) cudaFree(m->d_sync);
+  m->d_sync = nullptr;
   m->retired.clear();
   m->retired_plans.clear();
   m->recon_plan = nullptr;
@@ -452,6 +461,11 @@ extern "C" lrb_status lrb_blr_create(lrb_ctx* ctx, int64_t n, int64_t block, int
     }
   cudaError_t e = upload(&m->d_dcat, dcat);
   if (e == cudaSuccess && T > 1) {
+    const size_t sync_bytes = (size_t(T) * 4 + 15) / 16 * 16 + 16;
+    e = cudaMalloc(&m->d_sync, sync_bytes);
+    if (e == cudaSuccess) e = cudaMemset(m->d_sync, 0, sync_bytes);
+  }
+  if (e == cudaSuccess && T > 1) {
     std::vector<double> vtcol(size_t(items * r * b)), xs(size_t(items * r * r));
     int64_t q = 0;
     for (int64_t j = 0; j < T; ++j)
@@ -514,6 +528,17 @@ lrb_status matvec_steps(lrb_ctx* ctx, lrb_blr* m, const double* rhs, int64_t nrh
                         cudaStream_t s) {
   lrb_status st = LRB_OK;
   const int64_t T = m->tiles, b = m->block, r = m->rank, K = (T - 1) * r, P = m->pitch;
+  // one persistent launch when the shape allows it (lrb_blr_fused.cu);
+  // LRB_BLR_FUSED=0 or debug bit 9 keeps the three-launch form below
+  const char* fe = std::getenv("LRB_BLR_FUSED");
+  if (!(fe && fe[0] == '0') && !(lrb::debug_flags() & 512) && m->d_sync) {
+    unsigned* ready = m->d_sync;
+    auto* next = reinterpret_cast<unsigned long long*>(
+        reinterpret_cast<char*>(m->d_sync) + (size_t(T) * 4 + 15) / 16 * 16);
+    if (lrb::launch_blr_fused(ctx, rhs, nrhs, y, T, b, r, P, m->d_vtcol, m->d_x, m->d_dcat,
+                              m->d_rz, ready, next, s, &st))
+      return st;
+  }
   // 1. W_.j = [Vt_ij]_i rhs_j
   st = lrb::run_strided_rowmajor_beta(ctx, K, nrhs, b, m->d_vtcol, b, K * b, rhs, nrhs, b * nrhs,
                                       m->d_w, nrhs, K * nrhs, T, 0, s);

@@ -1,0 +1,382 @@
+// lrb_blr_fused.cu — the BLR multi-RHS matvec (reference blr_matvec,
+// proj/include/lrbatch/blr.hpp:141-175) as ONE persistent launch.
+//
+// The three-launch form (lrb_blr.cu: W GEMM, coupling kernel, row GEMM) pays
+// two launch ramps and two wave tails on a ~0.1 ms problem, and its row step
+// is a single partial wave (T x b/64 tiles on 2 x 148 slots). Here every tile
+// of both GEMMs comes from one ticket sequence on one persistent grid:
+//   * W tiles (column j, 64 rows of the stacked [Vt_ij]_i): W^T = rhs_j^T Vt_j^T
+//     on DMMA, then — with the tile still in shared memory — the coupling
+//     Z_ij = X_ij W_ij of its 64 / r items as r-long FMA chains, Z written
+//     into row i's operand block and row i's ready count bumped (release).
+//     W itself is never stored.
+//   * row tiles (row i, 64 columns of y_i): y_i^T = [rhs_i; Z_i*]^T [D_i|U_i*]^T
+//     over K' = b + (T-1) r in ascending k; the producer streams the D_i part
+//     straight from rhs and, before the first Z chunk, waits until all T-1
+//     items of row i have landed (acquire), then fences the async proxy.
+// W tickets precede row tickets, so a waiting row tile only ever waits on
+// tiles already claimed by running CTAs: progress is guaranteed. Every entry
+// keeps the reference's chain order (W and Z chains over their k ascending;
+// y_i's chain over D's columns, then j-major, p), so results are bitwise the
+// three-launch path and the FMA-chain oracle. Tickets and ready counts reset
+// themselves at the end of the launch (last CTA out), so graph replays need
+// no memset.
+#include <cstdint>
+#include <cstring>
+
+#include "lrb_gemm.cuh"
+#include "lrb_internal.h"
+
+namespace lrb {
+
+struct BlrFusedProblem {
+  CUtensorMap tmRhs;   // rhs: (nrhs, b, T), item stride b nrhs      box (MB+4, KB)
+  CUtensorMap tmVt;    // stacked Vt per column: (b, K, T)          box (KB+4, NB)
+  CUtensorMap tmZ;     // Z part of rz: (nrhs, K, T), stride P nrhs box (MB+4, KB)
+  CUtensorMap tmDcat;  // [D_i | U_i*] rows: (P, b, T)              box (KB+4, NB)
+  const double* x;     // X_ij in (j, i) order, r x r row-major
+  double* rz;          // per row i: P x nrhs, Z_ij at rows b + jp r
+  double* y;           // n x nrhs row-major
+  int T, b, r, nrhs, K, P;
+  int tw, tr;          // 64-row blocks per W column, 64-column blocks per row
+  long long nw, total;  // W tiles, all tiles
+  unsigned* ready;     // [T] Z items landed per row
+  unsigned long long* next;  // [0] tickets, [1] finished CTAs
+  int flags;           // debug probe bits (LRB_DEBUG_FLAGS)
+};
+
+namespace {
+
+using FCfg = GemmCfg<1, 4, 16, 16, 64, 2, 2, false, false, true>;  // the m16k64 tile
+constexpr int kFStages = 2;
+constexpr int kFWarps = 4;
+constexpr int kFThreads = kFWarps * 32 + 32;  // + the producer warp
+constexpr int kScratch = FCfg::MB * FCfg::NB;  // the W^T tile (nrhs x 64)
+constexpr int kMaxRank = 16;                   // X tiles of one W tile: 64 / r items of r x r
+constexpr int kXs = FCfg::NB * kMaxRank;
+constexpr size_t kFSmem = size_t(kFStages) * FCfg::STAGE_ELEMS * 8 + size_t(kScratch) * 8 +
+                          size_t(kXs) * 8 + size_t(kFStages) * 8 * 3 + 16;
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kFThreads, 2)
+    blr_fused_kernel(const __grid_constant__ BlrFusedProblem p) {
+  pdl_entry();
+  constexpr int KB = FCfg::KB, NB = FCfg::NB, MB = FCfg::MB;
+  extern __shared__ __align__(1024) double smem[];
+  double* scratch = smem + size_t(kFStages) * FCfg::STAGE_ELEMS;
+  double* xs = scratch + kScratch;  // the W tile's X_ij (bulk copy by the producer)
+  uint64_t* full = reinterpret_cast<uint64_t*>(xs + kXs);
+  uint64_t* empty = full + kFStages;
+  volatile long long* slot = reinterpret_cast<volatile long long*>(empty + kFStages);
+  // X staging: xfull (producer's bulk copy landed), xfree (the computing
+  // warps are done with the previous W tile's X)
+  uint64_t* xfull = reinterpret_cast<uint64_t*>(const_cast<long long*>(slot + kFStages));
+  uint64_t* xfree = xfull + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kFStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kFWarps);
+    }
+    mbar_init(xfull, 1);
+    mbar_init(xfree, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kFWarps) {  // the producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      long long q = 0;
+      long long nwt = 0;  // W tiles issued (X staging parity)
+      const uint32_t bytes = uint32_t(FCfg::A_BOX + FCfg::B_BOX) * 8u;
+      const uint64_t pol_stream = policy_evict_normal(), pol_keep = policy_evict_last();
+      long long t = static_cast<long long>(atomicAdd(p.next, 1ull));
+      // (bit 3: probe, claim the next tile while this one's first chunk is in
+      // flight; measured slower: a CTA busy on a long row tile then holds a
+      // ticket other CTAs could start)
+      const bool ahead = (p.flags & 8) != 0;
+#pragma unroll 1
+      while (true) {
+        if (q >= kFStages) mbar_wait(&empty[stage], phase ^ 1);
+        if (t >= p.total) {
+          slot[stage] = -1;
+          mbar_arrive(&full[stage]);
+          break;
+        }
+        const bool wtile = t < p.nw;
+        const long long u = wtile ? t : t - p.nw;
+        const int z = int(wtile ? u / p.tw : u / p.tr);  // column j / row i
+        const int n0 = int(wtile ? u % p.tw : u % p.tr) * NB;
+        const int kend = wtile ? p.b : p.P;
+        bool waited = false;
+        long long t_next = -1;
+#pragma unroll 1
+        for (int k0 = 0; k0 < kend; k0 += KB) {
+          if (k0 > 0 && q >= kFStages) mbar_wait(&empty[stage], phase ^ 1);
+          const void* mapA = &p.tmRhs;
+          int ka = k0;
+          if (!wtile && k0 >= p.b) {
+            if (!waited) {  // Z_i* lands from the W tiles' coupling
+              while (!(p.flags & 32) && ld_acquire_u32(&p.ready[z]) < unsigned(p.T - 1))
+                __nanosleep(64);  // (bit 5: probe, no wait: wrong results)
+              fence_proxy_async_global();
+              waited = true;
+            }
+            mapA = &p.tmZ;
+            ka = k0 - p.b;
+          }
+          slot[stage] = t;
+          fence_proxy_async_smem();
+          double* As = smem + size_t(stage) * FCfg::STAGE_ELEMS;
+          double* Bs = As + FCfg::A_ELEMS;
+          mbar_arrive_expect_tx(&full[stage], bytes);
+          tma_load_3d(As, mapA, 0, ka, z, &full[stage], pol_keep);
+          if (wtile)
+            tma_load_3d(Bs, &p.tmVt, k0, n0, z, &full[stage], pol_stream);
+          else
+            tma_load_3d(Bs, &p.tmDcat, k0, n0, z, &full[stage], pol_stream);
+          ++q;
+          if (++stage == kFStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+          if (k0 == 0 && ahead) t_next = static_cast<long long>(atomicAdd(p.next, 1ull));
+        }
+        if (wtile) {
+          // the tile's X_ij (items ip0 .. of column j are consecutive in
+          // (j, i) order: one contiguous bulk copy), issued after the tile's
+          // chunks: by now the computing warps have finished the previous W
+          // tile's coupling and released xs
+          if (nwt > 0) mbar_wait(xfree, uint32_t((nwt - 1) & 1));
+          const int items = min(NB, p.K - n0) / p.r;
+          const uint32_t xb = uint32_t(items) * p.r * p.r * 8u;
+          mbar_arrive_expect_tx(xfull, xb);
+          bulk_g2s(xs, p.x + (int64_t(z) * (p.T - 1) + n0 / p.r) * p.r * p.r, xb, xfull,
+                   pol_stream);
+          ++nwt;
+        }
+        t = ahead ? t_next : static_cast<long long>(atomicAdd(p.next, 1ull));
+      }
+      // the last CTA out resets the tickets and ready counts
+      __threadfence();
+      const unsigned long long done = atomicAdd(p.next + 1, 1ull);
+      if (done == gridDim.x - 1) {
+        for (int i = 0; i < p.T; ++i) p.ready[i] = 0;
+        p.next[0] = 0;
+        p.next[1] = 0;
+        __threadfence();
+      }
+    }
+    return;
+  }
+
+  const int wi = 0, wj = warp, g = lane >> 2, tq = lane & 3;
+  int stage = 0;
+  uint32_t phase = 0;
+  long long nwc = 0;  // W tiles consumed (X staging parity)
+#pragma unroll 1
+  while (true) {
+    mbar_wait(&full[stage], phase);
+    const long long t = slot[stage];
+    if (t < 0) break;
+    const bool wtile = t < p.nw;
+    const long long u = wtile ? t : t - p.nw;
+    const int z = int(wtile ? u / p.tw : u / p.tr);
+    const int n0 = int(wtile ? u % p.tw : u % p.tr) * NB;
+    const int chunks = ((wtile ? p.b : p.P) + KB - 1) / KB;
+    double acc[FCfg::FJ][FCfg::FI][2];
+#pragma unroll
+    for (int fj = 0; fj < FCfg::FJ; ++fj)
+#pragma unroll
+      for (int fi = 0; fi < FCfg::FI; ++fi) acc[fj][fi][0] = acc[fj][fi][1] = 0.0;
+#pragma unroll 1
+    for (int c = 0; c < chunks; ++c) {
+      if (c > 0) mbar_wait(&full[stage], phase);
+      const double* As = smem + size_t(stage) * FCfg::STAGE_ELEMS;
+      const double* Bs = As + FCfg::A_ELEMS;
+      // a partial last chunk is zero-filled by TMA: +0 terms leave the chains exact
+#pragma unroll
+      for (int kq = 0; kq < KB / 4; ++kq) mma_kstep<FCfg>(acc, As, Bs, wi, wj, g, kq * 4 + tq);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == kFStages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    if (!wtile) {
+      // y_i rows n0.. : C^T(c, j) -> y[(i b + n0 + j) nrhs + c]
+      const int i = z;
+#pragma unroll
+      for (int fj = 0; fj < FCfg::FJ; ++fj) {
+        const int j = n0 + FCfg::load_col(wj, fj, g);
+        if (j >= p.b) continue;
+        double* yr = p.y + (int64_t(i) * p.b + j) * p.nrhs;
+        const int c0 = FCfg::acc_row(wi, 0, 0, tq);  // rows c0 .. c0 + 3
+        const double v[4] = {acc[fj][0][0], acc[fj][1][0], acc[fj][0][1], acc[fj][1][1]};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (c0 + e < p.nrhs) yr[c0 + e] = v[e];
+      }
+      continue;
+    }
+    // W tile: W^T (nrhs x 64) into the scratch as W rows (col-major C^T:
+    // scratch[j * MB + c] = W(n0 + j, c)), then the coupling of its items
+    named_barrier_sync(1, kFWarps * 32);  // the previous tile's coupling is done
+#pragma unroll
+    for (int fj = 0; fj < FCfg::FJ; ++fj) {
+      const int j = FCfg::load_col(wj, fj, g);
+      const int c0 = FCfg::acc_row(wi, 0, 0, tq);
+      scratch[j * MB + c0 + 0] = acc[fj][0][0];
+      scratch[j * MB + c0 + 1] = acc[fj][1][0];
+      scratch[j * MB + c0 + 2] = acc[fj][0][1];
+      scratch[j * MB + c0 + 3] = acc[fj][1][1];
+    }
+    named_barrier_sync(1, kFWarps * 32);
+    const int jcol = z, r = p.r, nrhs = p.nrhs;
+    const int items = min(NB, p.K - n0) / r;
+    const int ip0 = n0 / r;
+    const int per = r * nrhs, total = items * per;
+    mbar_wait(xfull, uint32_t(nwc & 1));  // this tile's X_ij landed
+    ++nwc;
+    if (!(p.flags & 16) && r % 8 == 0 && nrhs % 8 == 0) {
+      // Z_ij = X_ij W_ij on DMMA: item it on warp it % 4, 8x8 output blocks,
+      // k ascending in steps of 4 (each entry one in-order FMA chain)
+      for (int it = warp; it < items; it += kFWarps) {
+        const int ip = ip0 + it;
+        const int i = ip < jcol ? ip : ip + 1;
+        const int jp = jcol < i ? jcol : jcol - 1;
+        double* zrow = p.rz + (int64_t(i) * p.P + p.b + int64_t(jp) * r) * nrhs;
+        for (int p0 = 0; p0 < r; p0 += 8)
+          for (int c0 = 0; c0 < nrhs; c0 += 8) {
+            double d0 = 0.0, d1 = 0.0;
+            for (int k0 = 0; k0 < r; k0 += 4) {
+              const double a = xs[(it * r + p0 + g) * r + k0 + tq];
+              const double bv = scratch[(it * r + k0 + tq) * MB + c0 + g];
+              dmma_8x8x4(d0, d1, a, bv);
+            }
+            *reinterpret_cast<double2*>(zrow + int64_t(p0 + g) * nrhs + c0 + 2 * tq) =
+                make_double2(d0, d1);
+          }
+      }
+    } else {
+      // scalar: every thread keeps up to 8 independent Z chains (k
+      // ascending), X from xs and W from the scratch, both in shared memory
+      constexpr int U = (FCfg::NB * FCfg::MB) / (kFWarps * 32);
+      int xo[U], wo[U];
+      double zacc[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int e = threadIdx.x + q * kFWarps * 32;
+        const int it = e / per, rem = e - it * per;
+        const int pr = rem / nrhs, cc = rem - pr * nrhs;
+        xo[q] = (it * r + pr) * r;
+        wo[q] = (it * r) * MB + cc;
+        zacc[q] = 0.0;
+      }
+#pragma unroll 1
+      for (int k = 0; k < ((p.flags & 16) ? 0 : r); ++k) {  // (bit 4: probe, no coupling)
+#pragma unroll
+        for (int q = 0; q < U; ++q)
+          if (threadIdx.x + q * kFWarps * 32 < total)
+            zacc[q] = fma(xs[xo[q] + k], scratch[wo[q] + k * MB], zacc[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int e = threadIdx.x + q * kFWarps * 32;
+        if (e >= total) continue;
+        const int it = e / per, rem = e - it * per;
+        const int pr = rem / nrhs, cc = rem - pr * nrhs;
+        const int ip = ip0 + it;  // row index i' of column j's stack
+        const int i = ip < jcol ? ip : ip + 1;
+        const int jp = jcol < i ? jcol : jcol - 1;
+        p.rz[(int64_t(i) * p.P + p.b + int64_t(jp) * r + pr) * nrhs + cc] = zacc[q];
+      }
+    }
+    __threadfence();
+    named_barrier_sync(1, kFWarps * 32);
+    if (threadIdx.x == 0) mbar_arrive(xfree);  // xs and the scratch may be refilled
+    if (threadIdx.x < items) {
+      const int ip = ip0 + threadIdx.x;
+      const int i = ip < jcol ? ip : ip + 1;
+      atomicAdd(&p.ready[i], 1u);
+    }
+  }
+}
+
+}  // namespace
+
+bool encode_operand(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld,
+                    int64_t stride, int64_t zdim, int box_in, int box_out);
+
+// One fused matvec launch, or false (nothing launched) when the shape is
+// outside what the fused kernel serves: nrhs <= 16, block a multiple of 64,
+// rank dividing 64 (each 64-row W block holds whole items) and a multiple of
+// 4, TMA-addressable operands.
+bool launch_blr_fused(lrb_ctx* ctx, const double* rhs, int64_t nrhs, double* y, int64_t T,
+                      int64_t b, int64_t r, int64_t P, const double* vtcol, const double* x,
+                      const double* dcat, double* rz, unsigned* ready,
+                      unsigned long long* next, cudaStream_t s, lrb_status* st) {
+  const int64_t K = (T - 1) * r;
+  // nrhs <= 8 keeps the three-launch form: its m8 row tiles do not pad the
+  // right-hand sides to 16 (the paper's rank-8 / 8-RHS shape: 0.0758 vs
+  // 0.0799 ms fused)
+  if (T < 2 || nrhs <= 8 || nrhs > FCfg::MB || b % FCfg::KB != 0 || 64 % r != 0 || r % 4 != 0 ||
+      r > kMaxRank)
+    return false;
+  BlrFusedProblem p;
+  std::memset(&p, 0, sizeof(p));
+  const bool ok =
+      encode_operand(&p.tmRhs, rhs, nrhs, b, nrhs, b * nrhs, T, FCfg::MB + kPad, FCfg::KB) &&
+      encode_operand(&p.tmVt, vtcol, b, K, b, K * b, T, FCfg::KB + kPad, FCfg::NB) &&
+      encode_operand(&p.tmZ, rz + b * nrhs, nrhs, K, nrhs, P * nrhs, T, FCfg::MB + kPad,
+                     FCfg::KB) &&
+      encode_operand(&p.tmDcat, dcat, P, b, P, b * P, T, FCfg::KB + kPad, FCfg::NB);
+  if (!ok) return false;
+  p.x = x;
+  p.rz = rz;
+  p.y = y;
+  p.T = int(T), p.b = int(b), p.r = int(r), p.nrhs = int(nrhs), p.K = int(K), p.P = int(P);
+  p.tw = int((K + FCfg::NB - 1) / FCfg::NB);
+  p.tr = int((b + FCfg::NB - 1) / FCfg::NB);
+  p.nw = int64_t(T) * p.tw;
+  p.total = p.nw + int64_t(T) * p.tr;
+  p.ready = ready;
+  p.next = next;
+  p.flags = debug_flags();
+  static int occ_cache[64] = {0};
+  const int dev = ctx->device;
+  int occ = (dev >= 0 && dev < 64) ? occ_cache[dev] : 0;
+  cudaError_t e = cudaSuccess;
+  if (occ == 0) {
+    e = cudaFuncSetAttribute(blr_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(kFSmem));
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, blr_fused_kernel, kFThreads, kFSmem);
+    if (e == cudaSuccess && occ < 1) e = cudaErrorInvalidConfiguration;
+    if (e == cudaSuccess && dev >= 0 && dev < 64) occ_cache[dev] = occ;
+  }
+  if (e == cudaSuccess) {
+    const int64_t grid = std::min<int64_t>(int64_t(ctx->sm_count) * occ, p.total);
+    e = launch_pdl(blr_fused_kernel, dim3(unsigned(grid)), dim3(kFThreads), kFSmem, s, p);
+  }
+  if (e != cudaSuccess) {
+    *st = cuda_fail(ctx, e, "blr_fused_kernel launch");
+    return true;
+  }
+  ctx->launches.fetch_add(1, std::memory_order_relaxed);
+  *st = LRB_OK;
+  return true;
+}
+
+}  // namespace lrb

@@ -122,7 +122,7 @@ def test_device_matvec_in_a_graph_replayed(ctx, tiles, rank, nrhs, block):
     with ctx.capture(s) as cap:
         check(lib.lrb_blr_matvec_device(ctx._h, h, d_rhs.ptr, nrhs, y_graph.ptr, s.handle),
               ctx._h)
-    assert cap.graph.launches == 3
+    assert cap.graph.launches in (1, 3)  # the fused single launch, or the three-launch form
     want = y_eager.download(rhs.data.size)
     _check(m, rhs, DenseBlock(rhs.rows, rhs.cols, want))
     for _ in range(5):
@@ -164,3 +164,44 @@ def test_graph_survives_workspace_growth_and_other_streams(ctx):
     assert np.array_equal(y_graph.download(small.data.size), want)
     _check(m, big, DenseBlock(big.rows, big.cols, y_big1.download(big.data.size)))
     assert np.array_equal(y_big1.download(big.data.size), y_big2.download(big.data.size))
+
+
+FUSED_SHAPES = [(2, 8, 10, 64), (4, 16, 16, 64), (5, 4, 12, 128), (8, 16, 12, 64), (3, 8, 16, 128),
+                (17, 8, 14, 64), (6, 16, 10, 256), (9, 4, 10, 192), (33, 16, 16, 64)]
+
+
+@pytest.mark.parametrize("tiles,rank,nrhs,block", FUSED_SHAPES)
+def test_fused_matvec_equals_three_launch_form(ctx, monkeypatch, tiles, rank, nrhs, block):
+    # the single persistent launch (W tiles with the coupling folded in, row
+    # tiles waiting on per-row ready counts) against the three-launch form and
+    # the FMA-chain oracle, bitwise; replayed from a graph (the tickets and
+    # ready counts reset themselves)
+    from paper_2311_07602_b200.lrbatch import _check as check, lib
+
+    m = B.BlrMatrix.random(tiles * block, block, rank, 300 + tiles + rank)
+    rhs = _rhs(tiles * block, nrhs, 41 + nrhs)
+    h = m.device_handle(ctx)
+    s = ctx.stream()
+    d_rhs = ctx.to_device(rhs.data)
+    y_f, y_3 = ctx.empty(rhs.data.size), ctx.empty(rhs.data.size)
+    n0 = ctx.launch_count
+    check(lib.lrb_blr_matvec_device(ctx._h, h, d_rhs.ptr, nrhs, y_f.ptr, s.handle), ctx._h)
+    s.synchronize()
+    assert ctx.launch_count - n0 == 1
+    monkeypatch.setenv("LRB_BLR_FUSED", "0")
+    check(lib.lrb_blr_matvec_device(ctx._h, h, d_rhs.ptr, nrhs, y_3.ptr, s.handle), ctx._h)
+    s.synchronize()
+    monkeypatch.delenv("LRB_BLR_FUSED")
+    got = y_f.download(rhs.data.size)
+    assert np.array_equal(got, y_3.download(rhs.data.size))
+    _check(m, rhs, DenseBlock(rhs.rows, rhs.cols, got))
+    with ctx.capture(s) as cap:
+        check(lib.lrb_blr_matvec_device(ctx._h, h, d_rhs.ptr, nrhs, y_f.ptr, s.handle), ctx._h)
+    assert cap.graph.launches == 1
+    for _ in range(3):
+        y_f.fill_bytes(0)
+        ctx.synchronize()
+        cap.graph.launch(s)
+        cap.graph.launch(s)
+        s.synchronize()
+        assert np.array_equal(y_f.download(rhs.data.size), got)
