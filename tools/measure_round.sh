@@ -1,10 +1,10 @@
 #!/usr/bin/env bash
 # One GPU-box pass that regenerates the round's measurement artefacts into
 # gpurun_out/ (copied to profiles/ by hand after review):
-#   gpurun -- 'bash tools/measure_round.sh r01'
+#   gpurun -- 'bash tools/measure_round.sh r02'
 # Every ncu command runs only after the same command exited 0 without ncu.
 set -u
-R=${1:-r01}
+R=${1:-r02}
 O=gpurun_out
 mkdir -p $O
 log() { echo "[measure] $*"; }
@@ -13,11 +13,24 @@ log "gpu tests"
 timeout 1500 python -m pytest tests -m gpu -x -q > $O/tests_gpu_$R.log 2>&1
 log "tests rc=$? $(tail -1 $O/tests_gpu_$R.log)"
 
+log "bench lines (default cfg4, then every BASELINE config)"
+timeout 900 python bench.py > $O/bench_$R.json 2> $O/bench_$R.err
+log "bench rc=$? $(head -c 300 $O/bench_$R.json)"
+timeout 900 python bench.py --impl reference > $O/bench_reference_$R.json 2>> $O/bench_$R.err
+log "reference arm rc=$?"
+for c in cfg1 cfg2 cfg5; do
+  timeout 900 python bench.py --config $c > $O/bench_${c}_$R.json 2>> $O/bench_$R.err
+  log "bench $c rc=$?"
+done
+
+log "probes"
+timeout 600 python tools/probe_varn.py > $O/probe_varn_$R.jsonl 2>> $O/probe_$R.err
+timeout 600 python tools/probe_cold.py > $O/probe_cold_$R.jsonl 2>> $O/probe_$R.err
+timeout 300 ./tools/microbench/fp64_mix > $O/fp64_mix_$R.jsonl 2>> $O/probe_$R.err
+
 log "sweeps"
 timeout 900 python tools/sweep.py > $O/sweep_$R.jsonl 2> $O/sweep_$R.err
 log "sweep rc=$?"
-timeout 600 python tools/sweep.py --configs cfg3r_b128_r8,cfg3r_b256_r16,cfg3r_b512_r32,cfg3r_b1024_r64,cfg3r_b2048_r16 > $O/sweep_${R}_rowmajor.jsonl 2>> $O/sweep_$R.err
-log "sweep rowmajor rc=$?"
 timeout 900 python tools/sweep_lowrank.py > $O/sweep_lowrank_$R.jsonl 2>> $O/sweep_$R.err
 log "sweep lowrank rc=$?"
 
@@ -32,22 +45,23 @@ else
   log "profile_all failed: $(tail -3 $O/profile_order_plain.log)"
 fi
 
-log "bench"
-if timeout 900 python bench.py > $O/bench_$R.json 2> $O/bench_$R.err; then
-  cat $O/bench_$R.json
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-    --log-file $O/launches_$R.csv python bench.py --steps 2 --warmup 3 --no-cpu --e2e-steps 0 \
-    > $O/launches_$R.log 2>&1
-  log "launch list rc=$?"
-fi
-timeout 900 python bench.py --impl reference > $O/bench_reference_$R.json 2>> $O/bench_$R.err
-log "reference arm rc=$?"
+log "launch list of the default bench command"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+  --log-file $O/launches_$R.csv python bench.py --steps 2 --warmup 3 --no-cpu --e2e-steps 0 \
+  > $O/launches_$R.log 2>&1
+log "launch list rc=$?"
 
-log "full capture of the cfg2 kernel"
+log "full captures: cfg4 (single-launch kernel) and cfg2 (panel kernel)"
+if timeout 300 python tools/profile_one.py --config cfg4 --launches 2 > /dev/null 2>&1; then
+  timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"lrb_varn" \
+    -c 1 -f -o $O/ncu_cfg4_$R python tools/profile_one.py --config cfg4 --launches 2 \
+    > $O/ncu_cfg4_$R.log 2>&1
+  log "ncu cfg4 rc=$?"
+fi
 if timeout 300 python tools/profile_one.py --config cfg2 --launches 2 > /dev/null 2>&1; then
   timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"lrb_(gemm|panel)_kernel" \
     -c 1 -f -o $O/ncu_cfg2_$R python tools/profile_one.py --config cfg2 --launches 2 \
     > $O/ncu_cfg2_$R.log 2>&1
-  log "ncu full rc=$?"
+  log "ncu cfg2 rc=$?"
 fi
 log "done"

@@ -65,11 +65,14 @@ def traffic(csv_path, order_path, out_path):
         per[key][r["Metric Name"]] = val * scale
     launches = [per[k] for k in sorted(per)]
     order = []
+    items = {}
     for line in open(order_path):
         if "launches=" in line:
             name = line.split()[0]
             n = int(line.split("launches=")[1].split()[0])
             order += [name] * n
+            if "items=" in line:
+                items[name] = int(line.split("items=")[1].split()[0])
     res = {}
     for name, d in zip(order, launches):
         e = res.setdefault(name, {"launches": 0, "dram_bytes_per_launch": 0.0, "kernel_s": 0.0,
@@ -79,8 +82,10 @@ def traffic(csv_path, order_path, out_path):
             "dram__bytes_write.sum", 0)
         e["kernel_s"] += d.get("gpu__time_duration.sum", 0)
         e["kernels"].append(d["kernel"])
-    for e in res.values():  # a cfg4 "launch" is the plan's whole group set
+    for name, e in res.items():  # a cfg4 "launch" is the plan's whole group set
         e["note"] = "ncu serialised, cold-cache replay; bytes summed over the config's launches"
+        if name in items:
+            e["items"] = items[name]  # items per launch of the capture (bench scales by it)
     json.dump(res, open(out_path, "w"), indent=1)
     print(f"wrote {out_path}: {len(res)} configs from {len(launches)} launches")
 

@@ -101,7 +101,7 @@ def main():
             plan = ctx.ptr_plan("C", "N", "N", w.bs, w.rs, w.bs, pa, w.bs, pb, w.bs, pc, w.bs, 0.0)
             plan.execute()
             ctx.synchronize()
-            print(f"{name} launches={plan.launches}", flush=True)
+            print(f"{name} launches={plan.launches} items={w.batch}", flush=True)
             del plan, arena
             continue
         count = w.batch
