@@ -47,7 +47,7 @@ def _roof(fl, by, ms, hbm, fp64, fsrc, hsrc, name=None):
 
 
 def _timed(ctx, stream, step, steps, warmup, pg, B, local):
-    """bench.timed_steps: one CUDA graph per step, events between replays;
+    """bench.timed_steps: the K steps as one CUDA graph, event nodes between steps;
     returns (median step ms of this rank, launches, clocks, job step stats)"""
     total, per, launches, clocks = B.timed_steps(ctx, stream, step, steps, warmup, pg, local)
     med, stats = B.job_step_stats(pg, per, total)
@@ -115,7 +115,7 @@ def run_lowrank_gpu(args, w, world, rank, local, pg, B):
     if rank == 0:
         cfg = dict(w.describe())
         cfg.update({"parallelism": f"shard{world} (independent items, no collective)",
-                    "timed_launch": "one CUDA graph per step",
+                    "timed_launch": "one CUDA graph of the K steps (event nodes between steps)",
                     "l2": "inputs larger than L2 (no flush)" if w.bytes() > 3 * 132644864
                           else "inputs within 3x L2"})
         print(json.dumps({
@@ -262,7 +262,7 @@ def run_blr_gpu(args, w, world, rank, local, pg, B):
     if rank == 0:
         cfg = dict(w.describe())
         cfg.update({"parallelism": f"replicas{world} (one matvec per GPU, no collective)",
-                    "timed_launch": "one CUDA graph per step"})
+                    "timed_launch": "one CUDA graph of the K steps (event nodes between steps)"})
         print(json.dumps({
             "metric": "batched FP64 GFLOP/s", "value": round(fl_all / (ms_step * 1e-3) / 1e9, 2),
             "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -482,7 +482,7 @@ def run_expand_gpu(args, w, world, rank, local, pg, B):
     if rank == 0:
         cfg = dict(w.describe())
         cfg.update({"parallelism": (f"replicas{world}" if dense else f"shard{world}")
-                    + " (no collective)", "timed_launch": "one CUDA graph per step",
+                    + " (no collective)", "timed_launch": "one CUDA graph of the K steps (event nodes between steps)",
                     "l2": "output larger than L2 (no flush)"})
         print(json.dumps({
             "metric": "batched FP64 GFLOP/s", "value": round(fl_all / (ms_step * 1e-3) / 1e9, 2),

@@ -785,7 +785,17 @@ extern "C" lrb_status lrb_event_destroy(lrb_ctx* ctx, void* ev) {
 extern "C" lrb_status lrb_event_record(lrb_ctx* ctx, void* ev, void* stream) {
   lrb_status st = bind(ctx);
   if (st) return st;
-  LRB_CUDA_TRY(ctx, cudaEventRecord(static_cast<cudaEvent_t>(ev), static_cast<cudaStream_t>(stream)));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (s) LRB_CUDA_TRY(ctx, cudaStreamIsCapturing(s, &cap));
+  // under capture: an external event-record node, so each replay records the
+  // event where the host can synchronise on and time it (per-step timing
+  // inside one graph of K steps)
+  if (cap == cudaStreamCaptureStatusActive)
+    LRB_CUDA_TRY(ctx, cudaEventRecordWithFlags(static_cast<cudaEvent_t>(ev), s,
+                                               cudaEventRecordExternal));
+  else
+    LRB_CUDA_TRY(ctx, cudaEventRecord(static_cast<cudaEvent_t>(ev), s));
   return LRB_OK;
 }
 extern "C" lrb_status lrb_event_elapsed_ms(lrb_ctx* ctx, void* e0, void* e1, float* ms) {

@@ -20,9 +20,9 @@ from paper_2311_07602_b200 import Context, workloads as W  # noqa: E402
 
 SETTINGS = [
     ("varn interleaved", {}),
-    ("varn claim-late", {"LRB_DEBUG_FLAGS": "8"}),
+    ("varn claim-ahead", {"LRB_DEBUG_FLAGS": "8"}),
     ("varn interleaved again", {}),
-    ("varn claim-late again", {"LRB_DEBUG_FLAGS": "8"}),
+    ("varn claim-ahead again", {"LRB_DEBUG_FLAGS": "8"}),
     ("varn longest-first", {"LRB_VARN_ORDER": "1"}),
     ("varn item order", {"LRB_VARN_ORDER": "2"}),
     ("varn padded (no scalar columns)", {"LRB_DEBUG_FLAGS": "4"}),
