@@ -65,6 +65,9 @@ bool launch_blr_fused(lrb_ctx* ctx, const double* rhs, int64_t nrhs, double* y, 
                       int64_t b, int64_t r, int64_t P, const double* vtcol, const double* x,
                       const double* dcat, double* rz, unsigned* ready,
                       unsigned long long* next, cudaStream_t s, lrb_status* st);
+bool launch_blr_recon(lrb_ctx* ctx, const double* vtcol, const double* dcat, const double* x,
+                      double* out, int64_t T, int64_t b, int64_t r, int64_t P, cudaStream_t s,
+                      lrb_status* st);
 lrb_status run_strided_rowmajor_beta(lrb_ctx* ctx, int64_t m, int64_t n, int64_t k,
                                      const double* A, int64_t lda, int64_t sA, const double* B,
                                      int64_t ldb, int64_t sB, double* C, int64_t ldc, int64_t sC,
@@ -688,6 +691,14 @@ extern "C" lrb_status lrb_blr_reconstruct_dense(lrb_ctx* ctx, lrb_blr* m, double
     ctx->launches.fetch_add(1, std::memory_order_relaxed);
   }
   if (T == 1) return LRB_OK;
+  // the off-diagonal tiles as one write-streaming launch (lrb_blr_recon.cu)
+  // where the shape allows it; LRB_BLR_RECON=0 keeps the UX + tile-kernel form
+  {
+    const char* re = std::getenv("LRB_BLR_RECON");
+    if (!(re && re[0] == '0') &&
+        lrb::launch_blr_recon(ctx, m->d_vtcol, m->d_dcat, m->d_x, out, T, b, r, m->pitch, s, &st))
+      return st;
+  }
   const int64_t items = T * (T - 1);
   if (!m->d_ux) {
     size_t ux_cap = 0;

@@ -108,3 +108,24 @@ def test_expand_in_a_graph(ctx):
     cap.graph.launch(s)
     s.synchronize()
     assert np.array_equal(out.download(), out2.download())
+
+
+@pytest.mark.parametrize("n,block,rank", [(512, 256, 8), (768, 256, 16), (2048, 512, 16),
+                                          (1024, 512, 8)])
+def test_reconstruct_dense_streaming_kernel(ctx, monkeypatch, n, block, rank):
+    # shapes the write-streaming off-diagonal kernel serves (b a multiple of
+    # 256, r in {8, 16}): bitwise the FMA-chain oracle and the UX + tile form
+    m = B.BlrMatrix.random(n, block, rank, 3 * n + rank)
+    out, alt = ctx.empty(n * n), ctx.empty(n * n)
+    out.fill_bytes(0xFF)
+    n0 = ctx.launch_count
+    m.reconstruct_dense_device(ctx, out)
+    ctx.synchronize()
+    assert ctx.launch_count - n0 == 2  # the diagonal copy + one streaming launch
+    monkeypatch.setenv("LRB_BLR_RECON", "0")
+    m.reconstruct_dense_device(ctx, alt)
+    ctx.synchronize()
+    got = out.download(n * n)
+    assert np.array_equal(got, alt.download(n * n))
+    diag, u, x, vt = m.packed_arrays()
+    assert np.array_equal(got, O.blr_reconstruct(n, block, rank, diag, u, x, vt))
