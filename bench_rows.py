@@ -192,7 +192,7 @@ def run_lowrank_reference(args, w, world, rank, B):
         return
     threads = os.cpu_count() or 1
     driver = lowrank_cpu(w, threads, min(1.0, args.ref_seconds))["driver"]  # picks the driver
-    for _ in range(max(0, args.warmup_ref - 1)):
+    for _ in range(max(0, args.warmup - 1)):  # the driver pick above is the first
         lowrank_cpu(w, threads, min(1.0, args.ref_seconds), driver)
     vals = [lowrank_cpu(w, threads, args.ref_seconds, driver) for _ in range(args.steps)]
     v = statistics.median(x["value"] for x in vals)
@@ -204,8 +204,9 @@ def run_lowrank_reference(args, w, world, rank, B):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (counter RNG, uniform[-1,1))", "config": w.describe(),
-        "cpu_baseline": cb, "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
-                                    "d2h_bytes_per_step": 0}, "gpu_launches": 0}), flush=True)
+        "cpu_baseline": dict(cb, **B.cpu_identity()),
+        "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0, "native_libs": B.mapped_repo_libs()}), flush=True)
 
 
 # ------------------------------------------------------------------ BLR matvec
@@ -313,7 +314,7 @@ def run_blr_reference(args, w, world, rank, B):
         return
     m, rhs = blr_host(w)
     driver = blr_cpu(w, m, rhs)["driver"]  # picks the driver
-    for _ in range(max(0, args.warmup_ref - 1)):
+    for _ in range(max(0, args.warmup - 1)):  # the driver pick above is the first
         blr_cpu(w, m, rhs, driver)
     vals = [blr_cpu(w, m, rhs, driver) for _ in range(args.steps)]
     v = statistics.median(x["value"] for x in vals)
@@ -323,9 +324,9 @@ def run_blr_reference(args, w, world, rank, B):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (counter RNG, uniform[-1,1))", "config": w.describe(),
-        "cpu_baseline": dict(vals[0], value=v),
+        "cpu_baseline": dict(vals[0], value=v, **B.cpu_identity()),
         "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "gpu_launches": 0}), flush=True)
+        "gpu_launches": 0, "native_libs": B.mapped_repo_libs()}), flush=True)
 
 
 # ------------------------------------------- low-rank expansion / BLR dense
@@ -501,7 +502,7 @@ def run_expand_reference(args, w, world, rank, B):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    for _ in range(max(0, args.warmup_ref)):
+    for _ in range(max(0, args.warmup)):
         expand_cpu(w, threads, min(1.0, args.ref_seconds))
     vals = [expand_cpu(w, threads, args.ref_seconds) for _ in range(args.steps)]
     v = statistics.median(x["value"] for x in vals)
@@ -511,6 +512,6 @@ def run_expand_reference(args, w, world, rank, B):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (counter RNG, uniform[-1,1))", "config": w.describe(),
-        "cpu_baseline": dict(vals[0], value=v),
+        "cpu_baseline": dict(vals[0], value=v, **B.cpu_identity()),
         "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "gpu_launches": 0}), flush=True)
+        "gpu_launches": 0, "native_libs": B.mapped_repo_libs()}), flush=True)

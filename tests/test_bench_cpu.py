@@ -86,3 +86,15 @@ def test_reference_arm_rank1_is_silent():
               "--warmup", "0"], env=env)
     assert r.returncode == 0
     assert not [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+
+
+def test_row_reference_arm_isolated():
+    """the widened rows' reference arms (here the BLR matvec) print a line
+    with the warm-up they ran and map no product library"""
+    r = _run(["bench.py", "--impl", "reference", "--config", "blr_n16384_b256_r16_k16",
+              "--steps", "1", "--warmup", "1", "--ref-seconds", "0.2"])
+    assert r.returncode == 0, r.stderr
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert d["impl"] == "reference" and d["warmup"] == 1 and d["value"] > 0
+    assert not any("liblrb.so" in p for p in d["native_libs"])
+    assert "cpu_model" in d["cpu_baseline"]

@@ -1,7 +1,7 @@
 #!/usr/bin/env bash
 # Both arms of every widened-row bench config (low-rank product, BLR matvec)
 # into gpurun_out/bench_rows_$1.jsonl (GPU arm then reference arm per config).
-R=${1:-r01}
+R=${1:-r02}
 O=gpurun_out
 mkdir -p $O
 : > $O/bench_rows_$R.jsonl
