@@ -1056,9 +1056,30 @@ void varn_order(const std::vector<ItemDesc>& items, const std::vector<int64_t>& 
       }
   }
   auto by_time = [](const T& x, const T& y) { return x.t > y.t; };
-  // probe orders (LRB_VARN_ORDER): 1 = one list, longest first; 2 = item order
+  // probe orders (LRB_VARN_ORDER): 1 = one list, longest first; 2 = item order;
+  // 3 = the device-descriptor path's order (items by power-of-two classes of
+  // tiles * k * min(n, 64), costliest class first, item order within a class)
   const char* env = std::getenv("LRB_VARN_ORDER");
   const int mode = env ? std::atoi(env) : 0;
+  if (mode == 3) {
+    std::vector<std::pair<int, int64_t>> cls;
+    for (int64_t id : ids) {
+      const ItemDesc& d = items[size_t(id)];
+      const double tiles = double((d.m + kVarnMB - 1) / kVarnMB) * double((d.n + kVarnNB - 1) / kVarnNB);
+      int e = 0;
+      std::frexp(tiles * double(d.k) * double(std::min(d.n, kVarnNB)), &e);
+      cls.push_back({e, id});
+    }
+    std::stable_sort(cls.begin(), cls.end(), [](auto& x, auto& y) { return x.first > y.first; });
+    for (auto& c : cls) {
+      const ItemDesc& d = items[size_t(c.second)];
+      const int64_t ti = (d.m + kVarnMB - 1) / kVarnMB, tj = (d.n + kVarnNB - 1) / kVarnNB;
+      for (int64_t b = 0; b < tj; ++b)
+        for (int64_t a = 0; a < ti; ++a)
+          out->push_back((uint64_t(c.second) << 32) | (uint64_t(a) << 16) | uint64_t(b));
+    }
+    return;
+  }
   if (mode == 1 || mode == 2) {
     fp.insert(fp.end(), mem.begin(), mem.end());
     if (mode == 1) std::stable_sort(fp.begin(), fp.end(), by_time);

@@ -13,7 +13,9 @@
 //   2. scatter: items into claim order, costliest class first (the
 //      single-launch kernel's tail then holds the short tiles); the rest
 //      (misaligned operands, k = 0) into the generic list;
-//   3. a three-pass exclusive scan of tiles per ordered item (both lists);
+//   3. a three-pass exclusive scan of tiles per ordered item (both lists),
+//      then the single-launch list's tiles expanded in claim order (when they
+//      fit 8 per item on average; otherwise the kernel searches the prefix);
 //   4. lrb_varn_kernel in device mode (tickets -> tiles through the prefix),
 //      and lrb_ptr_generic_kernel for the generic list.
 // Invalid descriptors (negative extents, leading dimensions too small) are
@@ -58,6 +60,8 @@ struct DevWs {
   int64_t* totals;          // [2]
   unsigned long long* tickets;  // [4]: single-launch pair, generic pair
   long long* info;          // [2] invalid count, first invalid (-1)
+  uint64_t* tiles;          // [tile_cap] the single-launch list's tiles, expanded
+  long long tile_cap;
 };
 
 __device__ __forceinline__ void tmr_address(CUtensorMap* m, const void* p) {
@@ -271,6 +275,24 @@ __global__ void ptrdev_scan3(const DevWs w) {
   if (p < cnt) (list ? w.prefix_g : w.prefix)[p] += w.bsum[int64_t(list) * gridDim.x + blockIdx.x];
 }
 
+// pass 4: the single-launch list's tiles written out in claim order (when they
+// fit the expansion buffer), so the kernel's producer decodes a ticket with
+// one load instead of a search through the prefix
+__global__ void ptrdev_expand(const DevWs w) {
+  pdl_entry();
+  const unsigned cnt = list_count(w, 0);
+  if (w.totals[0] > w.tile_cap) return;
+  const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= cnt) return;
+  const uint32_t it = w.order[p];
+  const ItemDesc d = w.items[it];
+  const int64_t ti = (d.m + kVarnMB - 1) / kVarnMB, tj = (d.n + kVarnNB - 1) / kVarnNB;
+  uint64_t* dst = w.tiles + w.prefix[p];
+  for (int64_t b = 0; b < tj; ++b)
+    for (int64_t a = 0; a < ti; ++a)
+      dst[b * ti + a] = (uint64_t(it) << 32) | (uint64_t(a) << 16) | uint64_t(b);
+}
+
 // The generic path: items whose operands TMA cannot address (odd leading
 // dimensions, unaligned bases) or with k = 0. A persistent grid claims 64 x 64
 // C tiles by ticket; 256 threads stage 16-deep k slices of A and B in shared
@@ -450,6 +472,10 @@ extern "C" lrb_status lrb_dgemm_ptr_batched_device(lrb_ctx* ctx, char order, cha
   const size_t o_tot = take(8 * 2, 16);
   const size_t o_tick = take(8 * 4, 16);
   const size_t o_info = take(8 * 2, 16);
+  // room for the expanded tile list: 8 tiles per item on average (cfg4 has
+  // ~4.7); larger lists fall back to the prefix search
+  const long long tile_cap = (long long)(8 * nb + 4096);
+  const size_t o_tiles = take(8 * size_t(tile_cap), 128);
   void* base = nullptr;
   LRB_CUDA_TRY(ctx, pool_alloc(ctx, &base, off, s));
   char* b = static_cast<char*>(base);
@@ -466,6 +492,8 @@ extern "C" lrb_status lrb_dgemm_ptr_batched_device(lrb_ctx* ctx, char order, cha
   w.totals = reinterpret_cast<int64_t*>(b + o_tot);
   w.tickets = reinterpret_cast<unsigned long long*>(b + o_tick);
   w.info = reinterpret_cast<long long*>(b + o_info);
+  w.tiles = reinterpret_cast<uint64_t*>(b + o_tiles);
+  w.tile_cap = tile_cap;
 
   // tensor-map templates: the single-launch kernel's boxes, any valid 16-byte
   // aligned placeholder geometry (address, extents, strides and the B box
@@ -493,18 +521,19 @@ extern "C" lrb_status lrb_dgemm_ptr_batched_device(lrb_ctx* ctx, char order, cha
   if (e == cudaSuccess) e = launch_pdl(ptrdev_scan2, dim3(2), dim3(1024), 0, s, w, int(nblocks));
   if (e == cudaSuccess)
     e = launch_pdl(ptrdev_scan3, dim3(unsigned(nblocks), 2), dim3(1024), 0, s, w);
+  if (e == cudaSuccess) e = launch_pdl(ptrdev_expand, dim3(g1), dim3(256), 0, s, w);
   if (e != cudaSuccess) {
     cudaFreeAsync(base, s);
     return cuda_fail(ctx, e, "lrb_dgemm_ptr_batched_device: plan kernels");
   }
-  ctx->launches.fetch_add(6, std::memory_order_relaxed);
+  ctx->launches.fetch_add(7, std::memory_order_relaxed);
   // the single-launch list's item count (the histogram sum) is published by
   // ptrdev_scan2 at counters[2 kClasses]
   VarnProblem vp{w.items, nullptr, w.maps, 0, w.tickets, w.prefix, w.order,
-                 w.counters + 2 * kClasses, w.totals};
+                 w.counters + 2 * kClasses, w.totals, w.tiles, w.tile_cap};
   int64_t grid = 0;
-  e = launch_varn(a_t, b_t, vp, (beta == 1.0 ? 1 : 0) | (debug_flags() & 30), ctx->device,
-                  ctx->sm_count, s, &grid);
+  e = launch_varn(a_t, b_t, vp, (beta == 1.0 ? 1 : 0) | varn_rem_flags() | (debug_flags() & 30),
+                  ctx->device, ctx->sm_count, s, &grid);
   if (e == cudaSuccess && grid > 0) ctx->launches.fetch_add(1, std::memory_order_relaxed);
   if (e == cudaSuccess) {
     e = launch_pdl(lrb_ptr_generic_kernel, dim3(unsigned(2 * ctx->sm_count)), dim3(256), 0, s, w,

@@ -299,8 +299,12 @@ __global__ void __launch_bounds__(VarnLayout<AT, BT>::THREADS, 2)
       int64_t q = 0;
       // host-built tile list, or (device-built plans) the tile prefix over
       // the ordered items, searched forward from this CTA's last position
-      const bool dev = prob.tiles == nullptr;
-      const long long limit = dev ? static_cast<long long>(*prob.total) : prob.num_tiles;
+      const long long limit = prob.tiles ? prob.num_tiles : static_cast<long long>(*prob.total);
+      // device-built plans: the planning kernels expanded the tile list when
+      // it fit (dev_tiles, dev_cap); otherwise the prefix is searched
+      const uint64_t* tiles = prob.tiles ? prob.tiles
+                                         : (limit <= prob.dev_cap ? prob.dev_tiles : nullptr);
+      const bool dev = tiles == nullptr;
       const int64_t count = dev ? int64_t(*prob.count) : 0;
       int64_t cursor = 0;
       // claim a ticket and decode it into (entry, m, n, k); entry -1 = done
@@ -313,7 +317,7 @@ __global__ void __launch_bounds__(VarnLayout<AT, BT>::THREADS, 2)
         if (t >= limit) return Claim{-1, 0, 0, 0};
         uint64_t e;
         if (!dev) {
-          e = prob.tiles[t];
+          e = tiles[t];
           const ItemDesc* d = prob.items + uint32_t(e >> 32);
           return Claim{static_cast<long long>(e), d->m, d->n, d->k};
         }
@@ -341,7 +345,7 @@ __global__ void __launch_bounds__(VarnLayout<AT, BT>::THREADS, 2)
         const int j0 = int(e & 0xFFFF) * L::NBMAX;
         const void* mA = &prob.maps[2 * size_t(item)];
         const void* mB = &prob.maps[2 * size_t(item) + 1];
-        if (dev && !(flags & 16)) {  // (bit 4: probe without the fences)
+        if (!prob.tiles && !(flags & 16)) {  // (bit 4: probe without the fences)
           // maps written by the planning kernels (tensormap.replace): order
           // those generic-proxy writes before the TMA reads them
           fence_tensormap_acquire(mA);

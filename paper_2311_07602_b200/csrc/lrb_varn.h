@@ -40,6 +40,8 @@ struct VarnProblem {
   const uint32_t* order;       // [count] item ids, claim order
   const unsigned int* count;   // number of ordered items
   const int64_t* total;        // prefix[count]
+  const uint64_t* dev_tiles;   // the expanded tile list, valid when *total <= dev_cap
+  long long dev_cap;
 };
 
 // Position p of ticket t in an exclusive prefix (prefix[p] <= t <
@@ -72,6 +74,10 @@ __device__ __forceinline__ int64_t prefix_search(const int64_t* prefix, int64_t 
 __device__ __forceinline__ void fence_tensormap_acquire(const void* map) {
   asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;\n" ::"l"(map) : "memory");
 }
+
+// the kernel's remainder-column setting (flags bits 8..11), from
+// kVarnRemMax or LRB_VARN_REM_MAX (lrb_api.cu)
+int varn_rem_flags();
 
 // a_t / b_t: op flags of the column-major view; flags bit 0: beta = 1
 cudaError_t launch_varn(int a_t, int b_t, const VarnProblem& p, int flags, int device,

@@ -25,6 +25,7 @@ SETTINGS = [
     ("varn claim-ahead again", {"LRB_DEBUG_FLAGS": "8"}),
     ("varn longest-first", {"LRB_VARN_ORDER": "1"}),
     ("varn item order", {"LRB_VARN_ORDER": "2"}),
+    ("varn device-path order", {"LRB_VARN_ORDER": "3"}),
     ("varn padded (no scalar columns)", {"LRB_DEBUG_FLAGS": "4"}),
     ("varn scalar rem<=1", {"LRB_VARN_REM_MAX": "1"}),
     ("varn scalar rem<=2", {"LRB_VARN_REM_MAX": "2"}),
