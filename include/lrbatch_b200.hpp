@@ -94,6 +94,27 @@ class Context {
                                          lda, strideA, B, ldb, strideB, C, ldc, strideC, batch),
           h_);
   }
+  // variable-size batch over HOST blocks (the reference's own mode;
+  // synchronous, copies pipelined with the kernels)
+  void gemm_ptr_batched_host(char order, char opA, char opB, int64_t batch, const int64_t* m,
+                             const int64_t* n, const int64_t* k, const double* const* A,
+                             const int64_t* lda, const double* const* B, const int64_t* ldb,
+                             double* const* C, const int64_t* ldc, bool accumulate) {
+    check(lrb_dgemm_ptr_batched_host(h_, order, opA, opB, batch, m, n, k, A, lda, B, ldb, C, ldc,
+                                     accumulate ? 1.0 : 0.0),
+          h_);
+  }
+  // variable-size batch whose descriptor arrays live in DEVICE memory
+  // (asynchronous; info: optional device int64_t[2])
+  void gemm_ptr_batched_device(char order, char opA, char opB, int64_t batch, const int64_t* m,
+                               const int64_t* n, const int64_t* k, const double* const* A,
+                               const int64_t* lda, const double* const* B, const int64_t* ldb,
+                               double* const* C, const int64_t* ldc, bool accumulate,
+                               int64_t* info = nullptr, void* stream = nullptr) {
+    check(lrb_dgemm_ptr_batched_device(h_, order, opA, opB, batch, m, n, k, A, lda, B, ldb, C,
+                                       ldc, accumulate ? 1.0 : 0.0, info, stream),
+          h_);
+  }
   void synchronize() { check(lrb_device_sync(h_), h_); }
 
  private:

@@ -85,6 +85,37 @@ int main() {
   }
   CHECK(threw, "lda < m raises ShapeError");
 
+  // variable-size pointer-array batch over host blocks (cfg4's shape family)
+  {
+    const int64_t nb = 4;
+    const int64_t bm[nb] = {256, 512, 256, 130}, rn[nb] = {8, 37, 64, 13};
+    std::vector<std::vector<double>> a(nb), b(nb), c(nb), w(nb);
+    std::vector<const double*> pa(nb), pb(nb);
+    std::vector<double*> pc(nb);
+    for (int64_t i = 0; i < nb; ++i) {
+      a[i].resize(bm[i] * bm[i]);
+      b[i].resize(bm[i] * rn[i]);
+      c[i].assign(bm[i] * rn[i], NAN);
+      w[i].resize(bm[i] * rn[i]);
+      for (auto& v : a[i]) v = U(gen);
+      for (auto& v : b[i]) v = U(gen);
+      pa[i] = a[i].data();
+      pb[i] = b[i].data();
+      pc[i] = c[i].data();
+      for (int64_t j = 0; j < rn[i]; ++j)
+        for (int64_t r = 0; r < bm[i]; ++r) {
+          double s = 0.0;
+          for (int64_t p = 0; p < bm[i]; ++p) s = std::fma(a[i][r + p * bm[i]], b[i][p + j * bm[i]], s);
+          w[i][r + j * bm[i]] = s;
+        }
+    }
+    ctx.gemm_ptr_batched_host('C', 'N', 'N', nb, bm, rn, bm, pa.data(), bm, pb.data(), bm,
+                              pc.data(), bm, false);
+    bool same = true;
+    for (int64_t i = 0; i < nb; ++i) same = same && c[i] == w[i];
+    CHECK(same, "pointer-array host batch == FMA chain (bitwise)");
+  }
+
   // ------------------------------------------------- the low-rank product
   // all-ones factors (test_core.cpp:59-67): block 1 -> 1, block 4 -> 4
   {
