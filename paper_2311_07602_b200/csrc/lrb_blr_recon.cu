@@ -7,16 +7,17 @@
 //   * unit = (tile q, 64-row block, 256-column half): a producer warp lands
 //     the half's Vt_ij (two 3-D boxes of 128 + 4 columns x r rows), the
 //     block's U_ij rows (one box of r + 4 columns x 64 rows from the [D_i |
-//     U_i*] row panel) and X_ij (one bulk copy) into a 2-slot ring;
+//     U_i*] row panel) and X_ij (one bulk copy per row, padded) into a
+//     2-slot ring;
 //   * eight computing warps (a 16 x 32 quarter-strip each) form UX = U X on
-//     DMMA (rounded, the reference's first product) into shared memory, then
+//     DMMA (rounded, the reference's first product) in registers, then
 //     each 64 x 64 block of (UX) Vt on DMMA, k ascending — both chains as the
 //     reference orders them, so results are bitwise the FMA-chain oracle;
-//   * each warp stages its 16 x 32 part of every 64 x 64 output block in the
-//     128-byte swizzle and hands it to the TMA engine itself (two 16 x 16
-//     boxes); three staging buffers per warp rotate, so the warps never meet
-//     at a barrier and two sub-blocks per warp are in flight while the next
-//     one is computed.
+//   * each warp stages its 16 x 32 part of two 64 x 64 output blocks in the
+//     128-byte swizzle and hands them to the TMA engine itself (four 16 x 16
+//     boxes, one proxy fence); two staging pairs per warp alternate, so the
+//     warps never meet at a barrier and one pair per warp is in flight while
+//     the next is computed.
 // The diagonal tiles are copied by blr_diag_kernel (lrb_blr.cu) before it.
 #include <cudaTypedefs.h>
 
@@ -42,37 +43,42 @@ constexpr int kRHalf = 256;                 // output columns per unit
 constexpr int kRBox = 128;                  // Vt box columns (+ kRPad)
 constexpr int kVtElems = (kRHalf / kRBox) * (kRBox + kRPad) * kRMaxRank;  // per slot
 constexpr int kUElems = 64 * (kRMaxRank + kRPad);
-constexpr int kXElems = kRMaxRank * kRMaxRank;
+constexpr int kXPad = 4;                    // X rows land at stride r + 4 (one bulk copy per row)
+constexpr int kXElems = kRMaxRank * (kRMaxRank + kXPad);
 constexpr int kSlotElems = kVtElems + kUElems + kXElems;
-constexpr int kStageBufs = 3;                  // per warp
+constexpr int kStageBufs = 4;                  // per warp: two block pairs
 constexpr int kWarpStage = 16 * 32;            // one warp's 16 x 32 output sub-block
-constexpr int kUxElems = 16 * (kRMaxRank + kRPad);  // one warp's UX rows
 constexpr size_t kRSmem = size_t(kRWarps) * kStageBufs * kWarpStage * 8 +
-                          size_t(2) * kSlotElems * 8 + size_t(kRWarps) * kUxElems * 8 + 64;
+                          size_t(2) * kSlotElems * 8 + 64;
 
 struct ReconProblem {
   CUtensorMap tmVt;   // stacked Vt: (b, r, Q) row-major per item     box (132, r)
   CUtensorMap tmU;    // [D_i | U_i*] rows: (P, n)                  box (r + 4, 64)
   CUtensorMap tmOut;  // out: (n, n) row-major                       box (16, 16), 128B swizzle
   const double* x;    // X_q, (j, i) order
-  int T, b, r, n, P;
+  int T, b, n, P;
   int rb_per_tile, halves;
-  long long units;
+  int units;
 };
 
+// Shared-memory banking (8-byte slots, 16 per 128 B): the Vt and U fragment
+// loads (row strides 132 and R + 4) put exactly two lanes on each slot, the
+// minimum for 32 doubles; X rows land at stride R + 4 for the same reason; the staging stores pair each even row's lanes with the odd
+// row's OTHER half of the fragment columns, so the eight lanes of a
+// quarter-warp cover the eight 16-byte chunks of the swizzled line.
+template <int R>
 __global__ void __launch_bounds__(kRThreads, 1)
     blr_recon_kernel(const __grid_constant__ ReconProblem p) {
+  constexpr int RP = R + kRPad, XP = R + kXPad;
   pdl_entry();
   extern __shared__ __align__(1024) double smem[];
   // per-warp staging first (every 2 KB box 1024-B aligned for the swizzle),
-  // then the operand ring (Vt | U | X per slot), then per-warp UX rows
+  // then the operand ring (Vt | U | X per slot)
   double* stage = smem;
   double* ring = stage + size_t(kRWarps) * kStageBufs * kWarpStage;
-  double* uxs_all = ring + 2 * size_t(kSlotElems);
-  uint64_t* full = reinterpret_cast<uint64_t*>(uxs_all + size_t(kRWarps) * kUxElems);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + 2 * size_t(kSlotElems));
   uint64_t* empty = full + 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = p.r, rp = r + kRPad;
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
       mbar_init(&full[s], 1);
@@ -81,11 +87,10 @@ __global__ void __launch_bounds__(kRThreads, 1)
     fence_mbar_init();
   }
   __syncthreads();
-  const int Tm1 = p.T - 1;
-  auto decode = [&](long long u, int* q, int* i, int* jp, int* rb, int* half) {
-    const int per_tile = p.rb_per_tile * p.halves;
-    *q = int(u / per_tile);
-    const int w = int(u - (long long)(*q) * per_tile);
+  const int Tm1 = p.T - 1, per_tile = p.rb_per_tile * p.halves;
+  auto decode = [&](int u, int* q, int* i, int* jp, int* rb, int* half) {
+    *q = u / per_tile;
+    const int w = u - *q * per_tile;
     *rb = w / p.halves;
     *half = w - *rb * p.halves;
     const int j = *q / Tm1, ip = *q - j * Tm1;
@@ -96,13 +101,12 @@ __global__ void __launch_bounds__(kRThreads, 1)
   if (warp == kRWarps) {  // the producer
     if (lane == 0) {
       const uint32_t bytes =
-          uint32_t((kRHalf / kRBox) * (kRBox + kRPad) * r + 64 * rp + r * r) * 8u;
+          uint32_t((kRHalf / kRBox) * (kRBox + kRPad) * R + 64 * RP + R * R) * 8u;
       const uint64_t pol = policy_evict_normal(), pol_keep = policy_evict_last();
-      int slot = 0;
+      int slot = 0, nq = 0;
       uint32_t phase = 0;
-      long long nq = 0;
 #pragma unroll 1
-      for (long long u = blockIdx.x; u < p.units; u += gridDim.x, ++nq) {
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++nq) {
         int q, i, jp, rb, half;
         decode(u, &q, &i, &jp, &rb, &half);
         if (nq >= 2) mbar_wait(&empty[slot], phase ^ 1);
@@ -111,10 +115,13 @@ __global__ void __launch_bounds__(kRThreads, 1)
         double* xq = us + kUElems;
         mbar_arrive_expect_tx(&full[slot], bytes);
         for (int c = 0; c < kRHalf / kRBox; ++c)
-          tma_load_3d(vt + c * (kRBox + kRPad) * r, &p.tmVt, half * kRHalf + c * kRBox, 0, q,
+          tma_load_3d(vt + c * (kRBox + kRPad) * R, &p.tmVt, half * kRHalf + c * kRBox, 0, q,
                       &full[slot], pol_keep);
-        tma_load_3d(us, &p.tmU, p.b + jp * r, i * p.b + rb * 64, 0, &full[slot], pol);
-        bulk_g2s(xq, p.x + int64_t(q) * r * r, uint32_t(r * r * 8), &full[slot], pol);
+        tma_load_3d(us, &p.tmU, p.b + jp * R, i * p.b + rb * 64, 0, &full[slot], pol);
+        const double* xg = p.x + int64_t(q) * R * R;
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+          bulk_g2s(xq + k * XP, xg + k * R, uint32_t(R * 8), &full[slot], pol);
         if (++slot == 2) {
           slot = 0;
           phase ^= 1;
@@ -124,38 +131,59 @@ __global__ void __launch_bounds__(kRThreads, 1)
     return;
   }
 
-  const int g = lane >> 2, tq = lane & 3;
+  const int g = lane >> 2, tq = lane & 3, odd = g & 1;
   const int row0 = (warp & 3) * 16;  // this warp's 16 rows of the 64-row block
   const int colw = (warp >> 2) * 32;  // and its 32 columns of each 64-column block
-  double* uxs = uxs_all + size_t(warp) * kUxElems;  // 16 x (r + 4), this warp's rows
   double* wstage = stage + size_t(warp) * kStageBufs * kWarpStage;
-  int slot = 0;
+  int slot = 0, sb = 0;  // ring slot; this warp's staging pair (0 or 1)
   uint32_t phase = 0;
-  long long nblk = 0;  // sub-blocks this warp staged (its buffer rotation)
 #pragma unroll 1
-  for (long long u = blockIdx.x; u < p.units; u += gridDim.x) {
+  for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
     int q, i, jp, rb, half;
     decode(u, &q, &i, &jp, &rb, &half);
     mbar_wait(&full[slot], phase);
     const double* vt = ring + size_t(slot) * kSlotElems;
     const double* us = vt + kVtElems;
     const double* xq = us + kUElems;
-    // this warp's UX rows = U (16 x r) X (r x r), p ascending (both warps of
-    // a row band form the same rows: no cross-warp dependency)
-    for (int f = 0; f < 2; ++f)
-      for (int c0 = 0; c0 < r; c0 += 8) {
-        double d0 = 0.0, d1 = 0.0;
-        for (int k0 = 0; k0 < r; k0 += 4)
-          dmma_8x8x4(d0, d1, us[(row0 + 8 * f + g) * rp + k0 + tq], xq[(k0 + tq) * r + c0 + g]);
-        double* dst = uxs + (8 * f + g) * rp + c0 + 2 * tq;
-        dst[0] = d0;
-        dst[1] = d1;
+    // this warp's UX rows = U (16 x R) X (R x R), p ascending; the 2 * R / 8
+    // chains run interleaved (both warps of a row band form the same rows: no
+    // cross-warp dependency). The result stays in registers: quad shuffles
+    // turn the accumulator fragments into the A fragments of the next product
+    double ua[2][R / 4];
+    {
+      double ux[2][R / 8][2];
+#pragma unroll
+      for (int f = 0; f < 2; ++f)
+#pragma unroll
+        for (int c = 0; c < R / 8; ++c) ux[f][c][0] = ux[f][c][1] = 0.0;
+#pragma unroll
+      for (int k0 = 0; k0 < R; k0 += 4) {
+        double a[2], bx[R / 8];
+#pragma unroll
+        for (int f = 0; f < 2; ++f) a[f] = us[(row0 + 8 * f + g) * RP + k0 + tq];
+#pragma unroll
+        for (int c = 0; c < R / 8; ++c) bx[c] = xq[(k0 + tq) * XP + 8 * c + g];
+#pragma unroll
+        for (int f = 0; f < 2; ++f)
+#pragma unroll
+          for (int c = 0; c < R / 8; ++c) dmma_8x8x4(ux[f][c][0], ux[f][c][1], a[f], bx[c]);
       }
-    __syncwarp();
+      // A fragment (row g, column k0 + tq) = accumulator element tq % 2 of
+      // lane (g, (k0 % 8) / 2 + tq / 2) in chain k0 / 8
+#pragma unroll
+      for (int f = 0; f < 2; ++f)
+#pragma unroll
+        for (int kb = 0; kb < R / 4; ++kb) {
+          const int src = g * 4 + ((kb & 1) << 1) + (tq >> 1);
+          const double x0 = __shfl_sync(0xffffffffu, ux[f][kb >> 1][0], src);
+          const double x1 = __shfl_sync(0xffffffffu, ux[f][kb >> 1][1], src);
+          ua[f][kb] = (tq & 1) ? x1 : x0;
+        }
+    }
     // four 64 x 64 output blocks of (UX) Vt, k ascending; this warp's 16 x 32
-    // part of each leaves through its own two TMA stores (16 x 16 boxes).
+    // part of each leaves through its own TMA stores (16 x 16 boxes).
     // Two blocks at a time: 16 independent DMMA chains per warp keep the
-    // tensor pipe busy through the DMMA latency (k = r is only 4 steps deep)
+    // tensor pipe busy through the DMMA latency (k = R is only R / 4 deep)
 #pragma unroll 1
     for (int cp = 0; cp < kRHalf / 64; cp += 2) {
       double acc[2][2][4][2];
@@ -165,15 +193,13 @@ __global__ void __launch_bounds__(kRThreads, 1)
         for (int f = 0; f < 2; ++f)
 #pragma unroll
           for (int h = 0; h < 4; ++h) acc[e][f][h][0] = acc[e][f][h][1] = 0.0;
-#pragma unroll 1
-      for (int k0 = 0; k0 < r; k0 += 4) {
-        double a[2];
 #pragma unroll
-        for (int f = 0; f < 2; ++f) a[f] = uxs[(8 * f + g) * rp + k0 + tq];
+      for (int k0 = 0; k0 < R; k0 += 4) {
+        const double a[2] = {ua[0][k0 / 4], ua[1][k0 / 4]};
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int cb = cp + e;
-          const double* vb = vt + (cb / 2) * (kRBox + kRPad) * r + (cb % 2) * 64 + colw;
+          const double* vb = vt + (cb / 2) * (kRBox + kRPad) * R + (cb % 2) * 64 + colw;
           double bv[4];
 #pragma unroll
           for (int h = 0; h < 4; ++h) bv[h] = vb[(k0 + tq) * (kRBox + kRPad) + 8 * h + g];
@@ -188,34 +214,39 @@ __global__ void __launch_bounds__(kRThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
       }
+      // stage the pair (two sub-blocks) in this warp's free buffer pair: the
+      // stores of the pair before the previous one have read it
+      double* st = wstage + size_t(sb) * 2 * kWarpStage;
+      if (lane == 0) bulk_wait_group_read<1>();
+      __syncwarp();
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int cb = cp + e;
-        // this warp's staging buffer: free once its stores of kStageBufs
-        // sub-blocks ago have read it
-        double* st = wstage + size_t(nblk % kStageBufs) * kWarpStage;
-        if (lane == 0) bulk_wait_group_read<kStageBufs - 1>();
-        __syncwarp();
+      for (int e = 0; e < 2; ++e)
 #pragma unroll
         for (int f = 0; f < 2; ++f)
 #pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            const int row = 8 * f + g;  // row within the warp's 16; row % 8 == g
-            const int box = h >> 1, chunk = ((h & 1) << 2) | tq;
-            sts128(st + box * 256 + row * 16 + ((chunk ^ g) << 1), acc[e][f][h][0],
-                   acc[e][f][h][1]);
-          }
-        fence_proxy_async_shared_cta();
-        __syncwarp();
-        if (lane == 0) {
-          const int x0 = (q / Tm1) * p.b + half * kRHalf + cb * 64 + colw;
-          const int y0 = i * p.b + rb * 64 + row0;
-          tma_store_2d(&p.tmOut, st, x0, y0);
-          tma_store_2d(&p.tmOut, st + 256, x0 + 16, y0);
-          bulk_commit_group();
+          for (int box = 0; box < 2; ++box)
+#pragma unroll
+            for (int hs = 0; hs < 2; ++hs) {
+              const int row = 8 * f + g;  // row within the warp's 16; row % 8 == g
+              const int hh = hs ^ odd;    // odd rows store the other column half first
+              const double v0 = odd ? acc[e][f][2 * box + (hs ^ 1)][0] : acc[e][f][2 * box + hs][0];
+              const double v1 = odd ? acc[e][f][2 * box + (hs ^ 1)][1] : acc[e][f][2 * box + hs][1];
+              const int chunk = (hh << 2) | tq;
+              sts128(st + e * kWarpStage + box * 256 + row * 16 + ((chunk ^ g) << 1), v0, v1);
+            }
+      fence_proxy_async_shared_cta();
+      __syncwarp();
+      if (lane == 0) {
+        const int y0 = i * p.b + rb * 64 + row0;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int x0 = (q / Tm1) * p.b + half * kRHalf + (cp + e) * 64 + colw;
+          tma_store_2d(&p.tmOut, st + e * kWarpStage, x0, y0);
+          tma_store_2d(&p.tmOut, st + e * kWarpStage + 256, x0 + 16, y0);
         }
-        ++nblk;
+        bulk_commit_group();
       }
+      sb ^= 1;
     }
     if (++slot == 2) {
       slot = 0;
@@ -265,15 +296,18 @@ bool launch_blr_recon(lrb_ctx* ctx, const double* vtcol, const double* dcat, con
                   encode_operand(&p.tmU, dcat, P, n, P, 0, 1, int(r) + kRPad, 64);
   if (!ok) return false;
   p.x = x;
-  p.T = int(T), p.b = int(b), p.r = int(r), p.n = int(n), p.P = int(P);
+  p.T = int(T), p.b = int(b), p.n = int(n), p.P = int(P);
   p.rb_per_tile = int(b / 64);
   p.halves = int(b / kRHalf);
-  p.units = (long long)Q * p.rb_per_tile * p.halves;
-  cudaError_t e = cudaFuncSetAttribute(blr_recon_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(kRSmem));
+  const int64_t units = Q * p.rb_per_tile * p.halves;
+  if (units > INT32_MAX) return false;
+  p.units = int(units);
+  auto kern = r == 8 ? blr_recon_kernel<8> : blr_recon_kernel<16>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(kRSmem));
   if (e == cudaSuccess) {
     const int64_t grid = std::min<int64_t>(ctx->sm_count, p.units);
-    e = launch_pdl(blr_recon_kernel, dim3(unsigned(grid)), dim3(kRThreads), kRSmem, s, p);
+    e = launch_pdl(kern, dim3(unsigned(grid)), dim3(kRThreads), kRSmem, s, p);
   }
   if (e != cudaSuccess) {
     *st = cuda_fail(ctx, e, "blr_recon_kernel launch");

@@ -3,6 +3,7 @@
 order, for an ncu metrics pass (dram bytes per launch -> profiles/traffic.json).
 
     python tools/profile_all.py            # prints the config order
+    python tools/profile_all.py --only blrd_n16384_b512_r16   # one row (full ncu capture)
 """
 import os
 import sys
@@ -86,8 +87,14 @@ def blr_one(ctx, name):
 
 
 def main():
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", nargs="*", default=None, help="config / row names (default: all)")
+    args = ap.parse_args()
+    keep = (lambda n: True) if not args.only else (lambda n: n in args.only)
     ctx = Context(0)
-    for name in CONFIGS:
+    for name in filter(keep, CONFIGS):
         w = W.get(name)
         if isinstance(w, W.Variable):
             items = list(range(w.batch))
@@ -115,11 +122,11 @@ def main():
         ctx.synchronize()
         print(f"{name} launches=1 items={count}", flush=True)
         del A, B, Cd
-    for name in LOWRANK:
+    for name in filter(keep, LOWRANK):
         lowrank_one(ctx, name)
-    for name in BLR:
+    for name in filter(keep, BLR):
         blr_one(ctx, name)
-    for name in EXPAND:
+    for name in filter(keep, EXPAND):
         expand_one(ctx, name)
 
 
