@@ -47,8 +47,12 @@ struct BlrFusedProblem {
 
 namespace {
 
-using FCfg = GemmCfg<1, 4, 16, 16, 64, 2, 2, false, false, true>;  // the m16k64 tile
-constexpr int kFStages = 2;
+// the m16 tile, 32-deep chunks in a 4-stage ring (two CTAs per SM). Measured
+// on the 16-RHS bench shape: k64 x 2 stages 0.0676 ms, k32 x 4 0.0656, k16 x
+// 7 0.0697, k32 x 5 or k64 x 3 (one CTA per SM) 0.076-0.082, 32-column tiles
+// 0.072-0.076
+using FCfg = GemmCfg<1, 4, 16, 16, 32, 4, 2, false, false, true>;
+constexpr int kFStages = FCfg::STAGES;
 constexpr int kFWarps = 4;
 constexpr int kFThreads = kFWarps * 32 + 32;  // + the producer warp
 constexpr int kScratch = FCfg::MB * FCfg::NB;  // the W^T tile (nrhs x 64)
@@ -303,12 +307,15 @@ __global__ void __launch_bounds__(kFThreads, 2)
         p.rz[(int64_t(i) * p.P + p.b + int64_t(jp) * r + pr) * nrhs + cc] = zacc[q];
       }
     }
-    __threadfence();
+    // release: the barrier orders every warp's Z stores before the counting
+    // threads' fence (cumulativity), so only those few threads fence (a
+    // fence in every thread cost ~3 % of the launch)
     named_barrier_sync(1, kFWarps * 32);
     if (threadIdx.x == 0) mbar_arrive(xfree);  // xs and the scratch may be refilled
     if (threadIdx.x < items) {
       const int ip = ip0 + threadIdx.x;
       const int i = ip < jcol ? ip : ip + 1;
+      __threadfence();
       atomicAdd(&p.ready[i], 1u);
     }
   }
@@ -320,7 +327,7 @@ bool encode_operand(CUtensorMap* map, const double* base, int64_t rows, int64_t 
                     int64_t stride, int64_t zdim, int box_in, int box_out);
 
 // One fused matvec launch, or false (nothing launched) when the shape is
-// outside what the fused kernel serves: nrhs <= 16, block a multiple of 64,
+// outside what the fused kernel serves: nrhs <= 16, block a multiple of 32,
 // rank dividing 64 (each 64-row W block holds whole items) and a multiple of
 // 4, TMA-addressable operands.
 bool launch_blr_fused(lrb_ctx* ctx, const double* rhs, int64_t nrhs, double* y, int64_t T,
@@ -331,7 +338,7 @@ bool launch_blr_fused(lrb_ctx* ctx, const double* rhs, int64_t nrhs, double* y, 
   // nrhs <= 8 keeps the three-launch form: its m8 row tiles do not pad the
   // right-hand sides to 16 (the paper's rank-8 / 8-RHS shape: 0.0758 vs
   // 0.0799 ms fused)
-  if (T < 2 || nrhs <= 8 || nrhs > FCfg::MB || b % FCfg::KB != 0 || 64 % r != 0 || r % 4 != 0 ||
+  if (T < 2 || nrhs <= 8 || nrhs > FCfg::MB || b % FCfg::KB != 0 || FCfg::NB % r != 0 || r % 4 != 0 ||
       r > kMaxRank)
     return false;
   BlrFusedProblem p;
