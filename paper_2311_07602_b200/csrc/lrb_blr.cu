@@ -395,17 +395,30 @@ __global__ void __launch_bounds__(256) blr_ux_mma_kernel(const double* __restric
 }
 
 // reconstruct_dense: the diagonal tiles into the n x n row-major output, one
-// block per tile row
+// warp per tile row, 16-byte accesses when the rows allow them. One CTA per SM
+// leaves room for the streaming off-diagonal kernel, which starts beside it
+// (it waits for this grid only before it exits: disjoint outputs), so the
+// copy's bandwidth overlaps that kernel's DMMA work. The copy waits for its
+// own predecessor before it lets the streaming kernel launch (write-after-
+// read on `out`).
 __global__ void __launch_bounds__(256) blr_diag_kernel(const double* __restrict__ dcat,
                                                        double* __restrict__ out, int tiles,
-                                                       int block, int64_t pitch) {
-  lrb::pdl_entry();
+                                                       int block, int64_t pitch, int vec) {
+  lrb::pdl_entry_ordered();
   const int64_t n = int64_t(tiles) * block;
-  for (int g = blockIdx.x; g < tiles * block; g += gridDim.x) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  for (int g = blockIdx.x * wpb + warp; g < tiles * block; g += gridDim.x * wpb) {
     const int t = g / block, row = g - t * block;
     const double* src = dcat + int64_t(g) * pitch;
     double* dst = out + (int64_t(t) * block + row) * n + int64_t(t) * block;
-    for (int c = threadIdx.x; c < block; c += blockDim.x) dst[c] = __ldg(src + c);
+    if (vec) {
+#pragma unroll 4
+      for (int c = 2 * lane; c < block; c += 64)
+        *reinterpret_cast<double2*>(dst + c) = __ldg(reinterpret_cast<const double2*>(src + c));
+    } else {
+      for (int c = lane; c < block; c += 32) dst[c] = __ldg(src + c);
+    }
   }
 }
 
@@ -685,9 +698,17 @@ extern "C" lrb_status lrb_blr_reconstruct_dense(lrb_ctx* ctx, lrb_blr* m, double
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   {
-    const int64_t blocks = std::min<int64_t>(T * b, int64_t(ctx->sm_count) * 32);
+    const int64_t blocks = std::min<int64_t>((T * b + 7) / 8, int64_t(ctx->sm_count));
+    const int vec = (b % 2 == 0 && m->pitch % 2 == 0 &&
+                     (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(m->d_dcat) & 15) == 0);
+    // the full shared-memory carve-out, so an SM running a copy CTA can take
+    // a streaming-kernel CTA (224 KB) beside it
+    static const cudaError_t carve = cudaFuncSetAttribute(
+        blr_diag_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    (void)carve;
     LRB_CUDA_TRY(ctx, lrb::launch_pdl(blr_diag_kernel, dim3(unsigned(blocks)), dim3(256), 0, s,
-                                      m->d_dcat, out, int(T), int(b), m->pitch));
+                                      m->d_dcat, out, int(T), int(b), m->pitch, vec));
     ctx->launches.fetch_add(1, std::memory_order_relaxed);
   }
   if (T == 1) return LRB_OK;

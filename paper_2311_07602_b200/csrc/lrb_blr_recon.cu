@@ -1,14 +1,17 @@
-// lrb_blr_recon.cu — the off-diagonal tiles of BlrMatrix::reconstruct_dense
-// (reference blr.hpp:62-86: out tile (i, j) = dense_gemm_naive(dense_gemm_naive(
-// U_ij, X_ij), Vt_ij)) as ONE write-streaming kernel.
+// lrb_blr_recon.cu — (U X) Vt expansions as ONE write-streaming kernel, in
+// two addressing modes:
+//   * the off-diagonal tiles of BlrMatrix::reconstruct_dense (reference
+//     blr.hpp:62-86: out tile (i, j) = dense_gemm_naive(dense_gemm_naive(U_ij,
+//     X_ij), Vt_ij)), U rows read from the [D_i | U_i*] row panel;
+//   * the batched low-rank expansion out_q = (U_q X_q) Vt_q
+//     (lrb_lowrank_expand, the same per-tile product over LowRankOperands).
 //
-// The output (n x n, 2 GiB on the bench shape) is ~90 % of the bytes, so the
-// kernel is built around keeping the TMA store stream full:
-//   * unit = (tile q, 64-row block, 256-column half): a producer warp lands
-//     the half's Vt_ij (two 3-D boxes of 128 + 4 columns x r rows), the
-//     block's U_ij rows (one box of r + 4 columns x 64 rows from the [D_i |
-//     U_i*] row panel) and X_ij (one bulk copy per row, padded) into a
-//     2-slot ring;
+// The output is ~90 % of the bytes, so the kernel is built around keeping the
+// TMA store stream full:
+//   * unit = (item q, 64-row block, 256-column half): a producer warp lands
+//     the half's Vt_q (two 3-D boxes of 128 + 4 columns x r rows), the
+//     block's U_q rows (one box of r + 4 columns x 64 rows) and X_q (one bulk
+//     copy per row, padded) into a 2-slot ring;
 //   * eight computing warps (a 16 x 32 quarter-strip each) form UX = U X on
 //     DMMA (rounded, the reference's first product) in registers, then
 //     each 64 x 64 block of (UX) Vt on DMMA, k ascending — both chains as the
@@ -18,7 +21,8 @@
 //     boxes, one proxy fence); two staging pairs per warp alternate, so the
 //     warps never meet at a barrier and one pair per warp is in flight while
 //     the next is computed.
-// The diagonal tiles are copied by blr_diag_kernel (lrb_blr.cu) before it.
+// The BLR diagonal tiles are copied by blr_diag_kernel (lrb_blr.cu), which
+// runs beside this kernel (one CTA per SM each; disjoint outputs).
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -32,6 +36,8 @@ namespace lrb {
 
 bool encode_operand(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld,
                     int64_t stride, int64_t zdim, int box_in, int box_out);
+bool encode_c_map(CUtensorMap* map, double* C, int64_t m, int64_t n, int64_t ldc, int64_t sC,
+                  int64_t batch, int nb);
 
 namespace {
 
@@ -52,12 +58,14 @@ constexpr size_t kRSmem = size_t(kRWarps) * kStageBufs * kWarpStage * 8 +
                           size_t(2) * kSlotElems * 8 + 64;
 
 struct ReconProblem {
-  CUtensorMap tmVt;   // stacked Vt: (b, r, Q) row-major per item     box (132, r)
-  CUtensorMap tmU;    // [D_i | U_i*] rows: (P, n)                  box (r + 4, 64)
-  CUtensorMap tmOut;  // out: (n, n) row-major                       box (16, 16), 128B swizzle
-  const double* x;    // X_q, (j, i) order
-  int T, b, n, P;
-  int rb_per_tile, halves;
+  CUtensorMap tmVt;   // Vt items: (cols, r, items) row-major            box (132, r)
+  CUtensorMap tmU;    // U rows: BLR (P, n, 1) [D_i | U_i*] panel;
+                      //         batched (r, rows, items)              box (r + 4, 64)
+  CUtensorMap tmOut;  // out: (cols, rows, items) row-major            box (16, 16), 128B swizzle
+  const double* x;    // X_q at x + q sx, r x r row-major
+  long long sx;
+  int T, b;           // BLR: tiles, block (item q = off-diagonal tile in (j, i) order)
+  int rblocks, halves;  // per item: 64-row blocks, 256-column halves
   int units;
 };
 
@@ -66,11 +74,17 @@ struct ReconProblem {
 // minimum for 32 doubles; X rows land at stride R + 4 for the same reason; the staging stores pair each even row's lanes with the odd
 // row's OTHER half of the fragment columns, so the eight lanes of a
 // quarter-warp cover the eight 16-byte chunks of the swizzled line.
-template <int R>
+template <int R, bool BATCHED>
 __global__ void __launch_bounds__(kRThreads, 1)
     blr_recon_kernel(const __grid_constant__ ReconProblem p) {
   constexpr int RP = R + kRPad, XP = R + kXPad;
-  pdl_entry();
+  // batched: the operands may come from the previous kernel, wait for it. BLR:
+  // the operands were uploaded at create and the predecessor is the diagonal
+  // copy (disjoint output), so start beside it and wait only before exiting
+  if (BATCHED)
+    pdl_entry();
+  else
+    pdl_trigger();
   extern __shared__ __align__(1024) double smem[];
   // per-warp staging first (every 2 KB box 1024-B aligned for the swizzle),
   // then the operand ring (Vt | U | X per slot)
@@ -87,15 +101,21 @@ __global__ void __launch_bounds__(kRThreads, 1)
     fence_mbar_init();
   }
   __syncthreads();
-  const int Tm1 = p.T - 1, per_tile = p.rb_per_tile * p.halves;
+  const int Tm1 = p.T - 1, per_item = p.rblocks * p.halves;
+  // unit -> item q, row block rb, column half; for the BLR mode also the
+  // tile's block row i and its index jp among row i's off-diagonal tiles
   auto decode = [&](int u, int* q, int* i, int* jp, int* rb, int* half) {
-    *q = u / per_tile;
-    const int w = u - *q * per_tile;
+    *q = u / per_item;
+    const int w = u - *q * per_item;
     *rb = w / p.halves;
     *half = w - *rb * p.halves;
-    const int j = *q / Tm1, ip = *q - j * Tm1;
-    *i = ip < j ? ip : ip + 1;
-    *jp = j < *i ? j : j - 1;
+    if (BATCHED) {
+      *i = *jp = 0;
+    } else {
+      const int j = *q / Tm1, ip = *q - j * Tm1;
+      *i = ip < j ? ip : ip + 1;
+      *jp = j < *i ? j : j - 1;
+    }
   };
 
   if (warp == kRWarps) {  // the producer
@@ -117,8 +137,11 @@ __global__ void __launch_bounds__(kRThreads, 1)
         for (int c = 0; c < kRHalf / kRBox; ++c)
           tma_load_3d(vt + c * (kRBox + kRPad) * R, &p.tmVt, half * kRHalf + c * kRBox, 0, q,
                       &full[slot], pol_keep);
-        tma_load_3d(us, &p.tmU, p.b + jp * R, i * p.b + rb * 64, 0, &full[slot], pol);
-        const double* xg = p.x + int64_t(q) * R * R;
+        if (BATCHED)
+          tma_load_3d(us, &p.tmU, 0, rb * 64, q, &full[slot], pol);
+        else
+          tma_load_3d(us, &p.tmU, p.b + jp * R, i * p.b + rb * 64, 0, &full[slot], pol);
+        const double* xg = p.x + q * p.sx;
 #pragma unroll
         for (int k = 0; k < R; ++k)
           bulk_g2s(xq + k * XP, xg + k * R, uint32_t(R * 8), &full[slot], pol);
@@ -128,6 +151,7 @@ __global__ void __launch_bounds__(kRThreads, 1)
         }
       }
     }
+    if (!BATCHED) pdl_wait();
     return;
   }
 
@@ -237,12 +261,13 @@ __global__ void __launch_bounds__(kRThreads, 1)
       fence_proxy_async_shared_cta();
       __syncwarp();
       if (lane == 0) {
-        const int y0 = i * p.b + rb * 64 + row0;
+        const int y0 = (BATCHED ? 0 : i * p.b) + rb * 64 + row0;
+        const int z = BATCHED ? q : 0;
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int x0 = (q / Tm1) * p.b + half * kRHalf + (cp + e) * 64 + colw;
-          tma_store_2d(&p.tmOut, st + e * kWarpStage, x0, y0);
-          tma_store_2d(&p.tmOut, st + e * kWarpStage + 256, x0 + 16, y0);
+          const int x0 = (BATCHED ? 0 : (q / Tm1) * p.b) + half * kRHalf + (cp + e) * 64 + colw;
+          tma_store_3d(&p.tmOut, st + e * kWarpStage, x0, y0, z);
+          tma_store_3d(&p.tmOut, st + e * kWarpStage + 256, x0 + 16, y0, z);
         }
         bulk_commit_group();
       }
@@ -254,55 +279,16 @@ __global__ void __launch_bounds__(kRThreads, 1)
     }
   }
   if (lane == 0) bulk_wait_group0();  // the stores land before the grid completes
+  if (!BATCHED) pdl_wait();  // and so does the diagonal copy before this grid
 }
 }  // namespace
 
-// The whole off-diagonal part of the reconstruction in one launch, or false
-// (nothing launched) when the shape is outside what the kernel serves:
-// r a multiple of 8 up to 16, b a multiple of 256, TMA-addressable buffers.
-bool launch_blr_recon(lrb_ctx* ctx, const double* vtcol, const double* dcat, const double* x,
-                      double* out, int64_t T, int64_t b, int64_t r, int64_t P, cudaStream_t s,
-                      lrb_status* st) {
-  const int64_t n = T * b, Q = T * (T - 1);
-  if (T < 2 || r % 8 != 0 || r > kRMaxRank || b % kRHalf != 0 || Q > INT32_MAX) return false;
-  if ((reinterpret_cast<uintptr_t>(out) & 15) != 0 || (reinterpret_cast<uintptr_t>(x) & 15) != 0)
-    return false;
-  ReconProblem p;
-  std::memset(&p, 0, sizeof(p));
-  // out: 2-D (n columns, n rows), box 16 x 64, 128-byte swizzle
-  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
-  if (!enc) {
-    void* fp = nullptr;
-    cudaDriverEntryPointQueryResult qr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &qr) !=
-            cudaSuccess ||
-        qr != cudaDriverEntryPointSuccess) {
-      cudaGetLastError();
-      return false;
-    }
-    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fp);
-  }
-  {
-    cuuint64_t dims[2] = {cuuint64_t(n), cuuint64_t(n)};
-    cuuint64_t strides[1] = {cuuint64_t(n * 8)};
-    cuuint32_t box[2] = {16, 16};
-    cuuint32_t estr[2] = {1, 1};
-    if (enc(&p.tmOut, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, out, dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return false;
-  }
-  const bool ok = encode_operand(&p.tmVt, vtcol, b, r, b, r * b, Q, kRBox + kRPad, int(r)) &&
-                  encode_operand(&p.tmU, dcat, P, n, P, 0, 1, int(r) + kRPad, 64);
-  if (!ok) return false;
-  p.x = x;
-  p.T = int(T), p.b = int(b), p.n = int(n), p.P = int(P);
-  p.rb_per_tile = int(b / 64);
-  p.halves = int(b / kRHalf);
-  const int64_t units = Q * p.rb_per_tile * p.halves;
-  if (units > INT32_MAX) return false;
+template <bool BATCHED>
+static bool launch_recon(lrb_ctx* ctx, ReconProblem& p, int64_t units, int r, cudaStream_t s,
+                         lrb_status* st) {
+  if (units < 1 || units > INT32_MAX) return false;
   p.units = int(units);
-  auto kern = r == 8 ? blr_recon_kernel<8> : blr_recon_kernel<16>;
+  auto kern = r == 8 ? blr_recon_kernel<8, BATCHED> : blr_recon_kernel<16, BATCHED>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(kRSmem));
   if (e == cudaSuccess) {
@@ -316,6 +302,55 @@ bool launch_blr_recon(lrb_ctx* ctx, const double* vtcol, const double* dcat, con
   ctx->launches.fetch_add(1, std::memory_order_relaxed);
   *st = LRB_OK;
   return true;
+}
+
+// The whole off-diagonal part of the reconstruction in one launch, or false
+// (nothing launched) when the shape is outside what the kernel serves:
+// r 8 or 16, b a multiple of 256, TMA-addressable buffers.
+bool launch_blr_recon(lrb_ctx* ctx, const double* vtcol, const double* dcat, const double* x,
+                      double* out, int64_t T, int64_t b, int64_t r, int64_t P, cudaStream_t s,
+                      lrb_status* st) {
+  const int64_t n = T * b, Q = T * (T - 1);
+  if (T < 2 || (r != 8 && r != 16) || b % kRHalf != 0 || Q > INT32_MAX) return false;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) != 0) return false;
+  ReconProblem p;
+  std::memset(&p, 0, sizeof(p));
+  const bool ok = encode_c_map(&p.tmOut, out, n, n, n, 0, 1, 16) &&
+                  encode_operand(&p.tmVt, vtcol, b, r, b, r * b, Q, kRBox + kRPad, int(r)) &&
+                  encode_operand(&p.tmU, dcat, P, n, P, 0, 1, int(r) + kRPad, 64);
+  if (!ok) return false;
+  p.x = x;
+  p.sx = r * r;
+  p.T = int(T), p.b = int(b);
+  p.rblocks = int(b / 64);
+  p.halves = int(b / kRHalf);
+  return launch_recon<false>(ctx, p, Q * p.rblocks * p.halves, int(r), s, st);
+}
+
+// The batched expansion out_q = (U_q X_q) Vt_q (row-major items at base +
+// q stride) in one launch, or false (nothing launched) outside what the kernel
+// serves: r 8 or 16, m a multiple of 64, n a multiple of 256, 16-byte
+// aligned bases, leading dimensions and strides.
+bool launch_expand_stream(lrb_ctx* ctx, int64_t batch, int64_t m, int64_t n, int64_t r,
+                          const double* u, int64_t su, const double* x, int64_t sx,
+                          const double* vt, int64_t svt, double* out, int64_t ldo, int64_t so,
+                          cudaStream_t s, lrb_status* st) {
+  if ((r != 8 && r != 16) || m % 64 != 0 || n % kRHalf != 0 || batch < 1) return false;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) != 0 || (batch > 1 && (sx & 1) != 0)) return false;
+  const int64_t units = batch * (m / 64) * (n / kRHalf);
+  if (units > INT32_MAX) return false;
+  ReconProblem p;
+  std::memset(&p, 0, sizeof(p));
+  const bool ok = encode_c_map(&p.tmOut, out, n, m, ldo, so, batch, 16) &&
+                  encode_operand(&p.tmVt, vt, n, r, n, svt, batch, kRBox + kRPad, int(r)) &&
+                  encode_operand(&p.tmU, u, r, m, r, su, batch, int(r) + kRPad, 64);
+  if (!ok) return false;
+  p.x = x;
+  p.sx = sx;
+  p.T = 1, p.b = 0;
+  p.rblocks = int(m / 64);
+  p.halves = int(n / kRHalf);
+  return launch_recon<true>(ctx, p, units, int(r), s, st);
 }
 
 }  // namespace lrb

@@ -579,6 +579,10 @@ lrb_status run_strided_rowmajor_beta(lrb_ctx* ctx, int64_t m, int64_t n, int64_t
                                      const double* A, int64_t lda, int64_t sA, const double* B,
                                      int64_t ldb, int64_t sB, double* C, int64_t ldc, int64_t sC,
                                      int64_t batch, int beta_one, cudaStream_t stream);
+bool launch_expand_stream(lrb_ctx* ctx, int64_t batch, int64_t m, int64_t n, int64_t r,
+                          const double* u, int64_t su, const double* x, int64_t sx,
+                          const double* vt, int64_t svt, double* out, int64_t ldo, int64_t so,
+                          cudaStream_t s, lrb_status* st);
 }
 
 // out_i = (U_i X_i) Vt_i, the reference's per-tile expansion (blr.hpp:75-78):
@@ -611,6 +615,12 @@ extern "C" lrb_status lrb_lowrank_expand(lrb_ctx* ctx, int64_t batch, int64_t m,
   lrb_status st = bind(ctx);
   if (st) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // rank 8 / 16 with 64-row, 256-column items: one write-streaming launch, UX
+  // kept on chip (lrb_blr_recon.cu); LRB_EXPAND_STREAM=0 keeps the two GEMMs
+  const char* es = std::getenv("LRB_EXPAND_STREAM");
+  if (!(es && es[0] == '0') &&
+      lrb::launch_expand_stream(ctx, batch, m, n, rank, u, su, x, sx, vt, svt, out, ldo, so, s, &st))
+    return st;
   double* ux = nullptr;
   bool temp = false;
   const size_t bytes = size_t(batch) * size_t(m * rank) * sizeof(double);

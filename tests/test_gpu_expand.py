@@ -129,3 +129,49 @@ def test_reconstruct_dense_streaming_kernel(ctx, monkeypatch, n, block, rank):
     assert np.array_equal(got, alt.download(n * n))
     diag, u, x, vt = m.packed_arrays()
     assert np.array_equal(got, O.blr_reconstruct(n, block, rank, diag, u, x, vt))
+
+
+@pytest.mark.parametrize("batch,m,n,r,pad", [(3, 64, 256, 8, 0), (2, 128, 512, 16, 0),
+                                             (5, 192, 256, 16, 6), (1, 512, 768, 8, 2)])
+def test_expand_streaming_kernel(ctx, monkeypatch, batch, m, n, r, pad):
+    # rank 8 / 16 with 64-row, 256-column items: one write-streaming launch
+    # (UX on chip), bitwise the FMA-chain oracle and the two-GEMM form, padded
+    # leading dimensions and item strides left untouched
+    u, x, vt = _operands(batch, m, n, r, 7 * m + r)
+    du, dx, dvt = ctx.to_device(u), ctx.to_device(x), ctx.to_device(vt)
+    ldo = n + pad
+    so = m * ldo + 2 * pad
+    size = (batch - 1) * so + (m - 1) * ldo + n
+    poison = np.full(size, -7.5)
+    dout, dalt = ctx.to_device(poison), ctx.to_device(poison)
+    n0 = ctx.launch_count
+    B.lowrank_expand_device(ctx, batch, m, n, r, du, dx, dvt, dout, ldo=ldo, so=so)
+    ctx.synchronize()
+    assert ctx.launch_count - n0 == 1
+    monkeypatch.setenv("LRB_EXPAND_STREAM", "0")
+    n0 = ctx.launch_count
+    B.lowrank_expand_device(ctx, batch, m, n, r, du, dx, dvt, dalt, ldo=ldo, so=so)
+    ctx.synchronize()
+    assert ctx.launch_count - n0 == 2
+    got = dout.download()
+    assert np.array_equal(got, dalt.download())
+    want = O.lowrank_expand(batch, m, n, r, u, x, vt, ldo=ldo, so=so, out=poison.copy())
+    assert np.array_equal(got, want)
+
+
+def test_expand_streaming_kernel_in_a_graph(ctx):
+    batch, m, n, r = 3, 128, 256, 16
+    u, x, vt = _operands(batch, m, n, r, 5)
+    du, dx, dvt = ctx.to_device(u), ctx.to_device(x), ctx.to_device(vt)
+    out, out2 = ctx.empty(batch * m * n), ctx.empty(batch * m * n)
+    s = ctx.stream()
+    B.lowrank_expand_device(ctx, batch, m, n, r, du, dx, dvt, out, stream=s)
+    s.synchronize()
+    with ctx.capture(s) as cap:
+        B.lowrank_expand_device(ctx, batch, m, n, r, du, dx, dvt, out2, stream=s)
+    assert cap.graph.launches == 1
+    for _ in range(2):
+        cap.graph.launch(s)
+    s.synchronize()
+    assert np.array_equal(out.download(), out2.download())
+    assert np.array_equal(out.download(), O.lowrank_expand(batch, m, n, r, u, x, vt))
