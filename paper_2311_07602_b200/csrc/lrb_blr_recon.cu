@@ -44,18 +44,27 @@ namespace {
 constexpr int kRPad = 4;
 constexpr int kRWarps = 8;
 constexpr int kRThreads = kRWarps * 32 + 32;  // + the producer warp
-constexpr int kRMaxRank = 16;
 constexpr int kRHalf = 256;                 // output columns per unit
 constexpr int kRBox = 128;                  // Vt box columns (+ kRPad)
-constexpr int kVtElems = (kRHalf / kRBox) * (kRBox + kRPad) * kRMaxRank;  // per slot
-constexpr int kUElems = 64 * (kRMaxRank + kRPad);
 constexpr int kXPad = 4;                    // X rows land at stride r + 4 (one bulk copy per row)
-constexpr int kXElems = kRMaxRank * (kRMaxRank + kXPad);
-constexpr int kSlotElems = kVtElems + kUElems + kXElems;
 constexpr int kStageBufs = 4;                  // per warp: two block pairs
 constexpr int kWarpStage = 16 * 32;            // one warp's 16 x 32 output sub-block
+// the operand ring per rank: Vt | U | X per slot; rank 8 units are half the
+// size and half the DMMA work, so the same space holds four slots instead of
+// two (the producer runs further ahead of the shorter units)
+template <int R>
+struct Ring {
+  static constexpr int VT = (kRHalf / kRBox) * (kRBox + kRPad) * R;
+  static constexpr int U = 64 * (R + kRPad);
+  static constexpr int X = R * (R + kXPad);
+  static constexpr int SLOT = VT + U + X;
+  static constexpr int SLOTS = R == 8 ? 4 : 2;
+  static constexpr int ELEMS = SLOT * SLOTS;
+};
+constexpr int kMaxSlots = 4;
+constexpr int kRingElems = Ring<8>::ELEMS > Ring<16>::ELEMS ? Ring<8>::ELEMS : Ring<16>::ELEMS;
 constexpr size_t kRSmem = size_t(kRWarps) * kStageBufs * kWarpStage * 8 +
-                          size_t(2) * kSlotElems * 8 + 64;
+                          size_t(kRingElems) * 8 + size_t(2 * kMaxSlots) * 8;
 
 struct ReconProblem {
   CUtensorMap tmVt;   // Vt items: (cols, r, items) row-major            box (132, r)
@@ -67,6 +76,7 @@ struct ReconProblem {
   int T, b;           // BLR: tiles, block (item q = off-diagonal tile in (j, i) order)
   int rblocks, halves;  // per item: 64-row blocks, 256-column halves
   int units;
+  int flags;          // LRB_DEBUG_FLAGS probe bits: 64 = skip the (UX) Vt DMMAs (wrong results)
 };
 
 // Shared-memory banking (8-byte slots, 16 per 128 B): the Vt and U fragment
@@ -90,11 +100,12 @@ __global__ void __launch_bounds__(kRThreads, 1)
   // then the operand ring (Vt | U | X per slot)
   double* stage = smem;
   double* ring = stage + size_t(kRWarps) * kStageBufs * kWarpStage;
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + 2 * size_t(kSlotElems));
-  uint64_t* empty = full + 2;
+  using L = Ring<R>;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + size_t(kRingElems));
+  uint64_t* empty = full + kMaxSlots;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < L::SLOTS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kRWarps);
     }
@@ -129,10 +140,10 @@ __global__ void __launch_bounds__(kRThreads, 1)
       for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++nq) {
         int q, i, jp, rb, half;
         decode(u, &q, &i, &jp, &rb, &half);
-        if (nq >= 2) mbar_wait(&empty[slot], phase ^ 1);
-        double* vt = ring + size_t(slot) * kSlotElems;
-        double* us = vt + kVtElems;
-        double* xq = us + kUElems;
+        if (nq >= L::SLOTS) mbar_wait(&empty[slot], phase ^ 1);
+        double* vt = ring + size_t(slot) * L::SLOT;
+        double* us = vt + L::VT;
+        double* xq = us + L::U;
         mbar_arrive_expect_tx(&full[slot], bytes);
         for (int c = 0; c < kRHalf / kRBox; ++c)
           tma_load_3d(vt + c * (kRBox + kRPad) * R, &p.tmVt, half * kRHalf + c * kRBox, 0, q,
@@ -145,7 +156,7 @@ __global__ void __launch_bounds__(kRThreads, 1)
 #pragma unroll
         for (int k = 0; k < R; ++k)
           bulk_g2s(xq + k * XP, xg + k * R, uint32_t(R * 8), &full[slot], pol);
-        if (++slot == 2) {
+        if (++slot == L::SLOTS) {
           slot = 0;
           phase ^= 1;
         }
@@ -166,9 +177,9 @@ __global__ void __launch_bounds__(kRThreads, 1)
     int q, i, jp, rb, half;
     decode(u, &q, &i, &jp, &rb, &half);
     mbar_wait(&full[slot], phase);
-    const double* vt = ring + size_t(slot) * kSlotElems;
-    const double* us = vt + kVtElems;
-    const double* xq = us + kUElems;
+    const double* vt = ring + size_t(slot) * L::SLOT;
+    const double* us = vt + L::VT;
+    const double* xq = us + L::U;
     // this warp's UX rows = U (16 x R) X (R x R), p ascending; the 2 * R / 8
     // chains run interleaved (both warps of a row band form the same rows: no
     // cross-warp dependency). The result stays in registers: quad shuffles
@@ -218,7 +229,7 @@ __global__ void __launch_bounds__(kRThreads, 1)
 #pragma unroll
           for (int h = 0; h < 4; ++h) acc[e][f][h][0] = acc[e][f][h][1] = 0.0;
 #pragma unroll
-      for (int k0 = 0; k0 < R; k0 += 4) {
+      for (int k0 = 0; k0 < ((p.flags & 64) ? 0 : R); k0 += 4) {
         const double a[2] = {ua[0][k0 / 4], ua[1][k0 / 4]};
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
@@ -273,7 +284,7 @@ __global__ void __launch_bounds__(kRThreads, 1)
       }
       sb ^= 1;
     }
-    if (++slot == 2) {
+    if (++slot == L::SLOTS) {
       slot = 0;
       phase ^= 1;
     }
@@ -288,6 +299,7 @@ static bool launch_recon(lrb_ctx* ctx, ReconProblem& p, int64_t units, int r, cu
                          lrb_status* st) {
   if (units < 1 || units > INT32_MAX) return false;
   p.units = int(units);
+  p.flags = debug_flags();
   auto kern = r == 8 ? blr_recon_kernel<8, BATCHED> : blr_recon_kernel<16, BATCHED>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(kRSmem));
