@@ -121,11 +121,11 @@ class RaggedDevice:
     """ragged shapes with padded / odd leading dimensions and unaligned
     bases, descriptor arrays uploaded to the device"""
 
-    def __init__(self, ctx, order, opA, opB, beta, seed, odd=True):
+    def __init__(self, ctx, order, opA, opB, beta, seed, odd=True, dims=None):
         rng = np.random.default_rng(seed)
         self.ctx, self.order, self.opA, self.opB, self.beta = ctx, order, opA, opB, beta
-        dims = [(70, 9, 50), (130, 40, 17), (33, 64, 96), (256, 16, 256), (1, 1, 1), (12, 7, 0),
-                (65, 57, 129), (128, 64, 64), (200, 100, 33), (6, 3, 2)]
+        dims = dims or [(70, 9, 50), (130, 40, 17), (33, 64, 96), (256, 16, 256), (1, 1, 1),
+                        (12, 7, 0), (65, 57, 129), (128, 64, 64), (200, 100, 33), (6, 3, 2)]
         self.dims = dims
         self.h = []
         ptrs = {"A": [], "B": [], "C": []}
@@ -227,3 +227,45 @@ def test_empty_batch(ctx):
                                  info.data_ptr())
     ctx.synchronize()
     assert info.cpu().tolist() == [0, -1]
+
+
+class SpanDevice(RaggedDevice):
+    """aligned operands whose byte spans sit on either side of 128 KiB: the
+    encoded tensor map carries a large-tensor flag tensormap.replace does not
+    recompute (csrc/lrb_ptr_device.cu, MapTemplates)"""
+
+    def __init__(self, ctx, opA, opB):
+        self.DIMS = [(128, 8, 128), (126, 8, 128), (128, 8, 126), (130, 16, 126), (256, 63, 256),
+                     (256, 64, 256), (254, 64, 258), (64, 16, 256), (64, 16, 254), (2, 8, 8192),
+                     (2, 8, 8194), (1024, 8, 16), (1024, 9, 18), (16384, 8, 2), (6, 3, 2),
+                     (70, 9, 50), (512, 24, 512)]
+        super().__init__(ctx, "C", opA, opB, 0.0, seed=13, odd=False, dims=self.DIMS)
+
+
+@pytest.mark.parametrize("ops", [("N", "N"), ("N", "T"), ("T", "N"), ("T", "T")])
+def test_device_built_maps_equal_the_host_encoding(ctx, ops, monkeypatch, capfd):
+    """LRB_PTRDEV_VERIFY=1 copies the device-built plan back and compares every
+    single-launch item's tensor maps with cuTensorMapEncodeTiled's own encoding
+    (all 128 bytes), and the tile list with the host's"""
+    monkeypatch.setenv("LRB_PTRDEV_VERIFY", "1")
+    c = SpanDevice(ctx, ops[0], ops[1])
+    c.run()
+    err = capfd.readouterr().err
+    lines = [ln for ln in err.splitlines() if "[ptrdev verify]" in ln]
+    assert lines and lines[-1].endswith(" 0 differences"), "\n".join(lines[-12:])
+    assert "single-launch items" in lines[0] and not lines[0].split(": ")[1].startswith("0 ")
+    c.check()
+
+
+def test_device_built_maps_cfg4_classes_verified(ctx, monkeypatch, capfd):
+    monkeypatch.setenv("LRB_PTRDEV_VERIFY", "1")
+    w = W.get("cfg4")
+    items = _class_sample(w, per_class=1)
+    desc, arena, pc_h = _device_descriptors(ctx, w, items)
+    _sync()
+    _call(ctx, desc, len(items))
+    ctx.synchronize()
+    err = capfd.readouterr().err
+    lines = [ln for ln in err.splitlines() if "[ptrdev verify]" in ln]
+    assert lines and lines[-1].endswith(" 0 differences"), "\n".join(lines[-12:])
+    _check_cfg4(ctx, w, items, pc_h)
