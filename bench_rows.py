@@ -84,7 +84,10 @@ def run_lowrank_gpu(args, w, world, rank, local, pg, B):
                                                       B, local)
     fl_all, by_all = B.all_sum(pg, w.flops()), B.all_sum(pg, w.bytes())
     roof = _roof(w.flops(), w.bytes(), ms_med, hbm, fp64, fsrc, hsrc, w.name)
-    roof["kernel"] = "lrb_lowrank_kernel<R>" if r <= 32 else "lrb_gemm_kernel x3"
+    per_step = launches // max(1, args.steps)
+    roof["kernel"] = ("lrb_lowrank_kernel<R> (fused, one warp per item)" if r <= 32 else
+                      "lrb_lowrank_r128_kernel (one launch, T and E on chip)" if per_step == 1 else
+                      "lrb_gemm_kernel x3 (T and E in the workspace)")
     roof["kernel_ms"] = round(ms_med * args.steps / max(1, launches), 4)
     e2e = None
     if args.e2e_steps > 0:
@@ -237,7 +240,9 @@ def run_blr_gpu(args, w, world, rank, local, pg, B):
                                                       B, local)
     fl_all, by_all = B.all_sum(pg, w.flops()), B.all_sum(pg, w.bytes())
     roof = _roof(w.flops(), w.bytes(), ms_med, hbm, fp64, fsrc, hsrc, w.name)
-    roof["kernel"] = "lrb_gemm_kernel x2 + blr_couple_kernel per matvec"
+    per_step = launches // max(1, args.steps)
+    roof["kernel"] = ("blr_fused_kernel (one persistent launch per matvec)" if per_step == 1 else
+                      "lrb_gemm_kernel x2 + blr_couple_warp_kernel per matvec")
     roof["kernel_ms"] = round(ms_med * args.steps / max(1, launches), 4)
     e2e = None
     if args.e2e_steps > 0:
@@ -408,7 +413,7 @@ def run_expand_gpu(args, w, world, rank, local, pg, B):
         out = ctx.empty(w.n * w.n)
         step = lambda: mat.reconstruct_dense_device(ctx, out, stream=s)  # noqa: E731
         fl, by = w.flops(), w.bytes()
-        kernel = "blr_diag_kernel + blr_ux_mma_kernel + lrb_gemm_kernel<q64, BlrTileProblem> (TMA-store epilogue)"
+        kernel = "dense"
     else:
         m, r, n = w.m, w.rank, w.batch
         bufs = [ctx.empty(n * m * r), ctx.empty(n * r * r), ctx.empty(n * r * m)]
@@ -425,7 +430,14 @@ def run_expand_gpu(args, w, world, rank, local, pg, B):
                                                       B, local)
     fl_all, by_all = B.all_sum(pg, fl), B.all_sum(pg, by)
     roof = _roof(fl, by, ms_med, hbm, fp64, fsrc, hsrc, w.name)
-    if kernel is None:
+    per_step = launches // max(1, args.steps)
+    if kernel == "dense":
+        kernel = ("blr_diag_kernel beside blr_recon_kernel (streaming (U X) Vt, TMA stores)"
+                  if per_step == 2 else
+                  "blr_diag_kernel + blr_ux_mma_kernel + lrb_gemm_kernel<q64, BlrTileProblem>")
+    elif per_step == 1:
+        kernel = "blr_recon_kernel (streaming (U X) Vt, UX on chip, TMA stores)"
+    else:
         v = ctx.last_variant
         kernel = ("lrb_gemm_kernel<q64> (UX), then " +
                   ("lrb_panel_kernel<p256>" if v == "p256" else f"lrb_gemm_kernel<{v}>") +
