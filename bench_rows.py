@@ -86,7 +86,7 @@ def run_lowrank_gpu(args, w, world, rank, local, pg, B):
     roof = _roof(w.flops(), w.bytes(), ms_med, hbm, fp64, fsrc, hsrc, w.name)
     per_step = launches // max(1, args.steps)
     roof["kernel"] = ("lrb_lowrank_kernel<R> (fused, one warp per item)" if r <= 32 else
-                      "lrb_lowrank_r128_kernel (one launch, T and E on chip)" if per_step == 1 else
+                      f"lrb_lowrank_big_kernel<{r}> (one launch, T and E on chip)" if per_step == 1 else
                       "lrb_gemm_kernel x3 (T and E in the workspace)")
     roof["kernel_ms"] = round(ms_med * args.steps / max(1, launches), 4)
     e2e = None

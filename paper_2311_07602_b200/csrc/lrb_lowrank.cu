@@ -38,12 +38,12 @@ lrb_status run_strided_rowmajor(lrb_ctx* ctx, int64_t m, int64_t n, int64_t k, c
                                 int64_t sA, const double* B, int64_t sB, double* C, int64_t sC,
                                 int64_t batch, cudaStream_t stream);
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn();
-// lrb_lowrank_big.cu: rank 128 in one launch, T and E on chip
+// lrb_lowrank_big.cu: ranks 64 / 96 / 128 in one launch, T and E on chip
 bool lowrank_big_eligible(int64_t batch, int64_t block, int64_t rank, const void* a_vt,
                           const void* b_u, const void* a_x, const void* b_x);
-lrb_status run_lowrank_big(lrb_ctx* ctx, int64_t batch, int64_t block, const double* a_vt,
-                           const double* b_u, const double* a_x, const double* b_x, double* g,
-                           cudaStream_t s);
+lrb_status run_lowrank_big(lrb_ctx* ctx, int64_t batch, int64_t block, int64_t rank,
+                           const double* a_vt, const double* b_u, const double* a_x,
+                           const double* b_x, double* g, cudaStream_t s);
 
 template <int R>
 struct LrCfg {
@@ -449,7 +449,7 @@ lrb_status run_lowrank(lrb_ctx* ctx, int64_t batch, int64_t block, int64_t rank,
     }
   }
   if (path == 1 && lowrank_big_eligible(batch, block, rank, a_vt, b_u, a_x, b_x))
-    return run_lowrank_big(ctx, batch, block, a_vt, b_u, a_x, b_x, g, s);
+    return run_lowrank_big(ctx, batch, block, rank, a_vt, b_u, a_x, b_x, g, s);
   if (path == 1) {
     // C = A_Vt B_U, E = A_X C, G = E B_X as three row-major batched GEMMs
     // (the context workspace, not a stream-ordered allocation: inside a CUDA

@@ -88,7 +88,7 @@ def test_three_gemm_path_in_a_graph(eager_first):
 
     c = Context(0)
     try:
-        n, blk, r = 5, 256, 64
+        n, blk, r = 5, 256, 48  # (ranks 64 / 96 / 128 run fused: test_gpu_lowrank_big.py)
         b = L.LowRankBatch.random(n, blk, r, 4242)
         d = [c.to_device(x) for x in (b.a_vt_batch, b.b_u_batch, b.a_x_batch, b.b_x_batch)]
         g_eager, g_graph = c.empty(n * r * r), c.empty(n * r * r)
@@ -158,7 +158,7 @@ def test_graph_survives_context_workspace_growth():
 
     c = Context(0)
     try:
-        blk, r = 256, 64
+        blk, r = 256, 48
         small = L.LowRankBatch.random(3, blk, r, 5151)
         big = L.LowRankBatch.random(40, blk, r, 5152)
         ds = [c.to_device(x) for x in (small.a_vt_batch, small.b_u_batch, small.a_x_batch,

@@ -43,8 +43,10 @@ def main():
             ctx.fill_uniform(bufs[2], r, r, r, r * r, n, w.seed, 2)
             ctx.fill_uniform(bufs[3], r, r, r, r * r, n, w.seed, 3)
             go = lambda: L.lowrank_multiply_device(ctx, n, b, r, *bufs, stream=s)  # noqa: E731
+            n0 = ctx.launch_count
             for _ in range(3):
                 go()
+            per_call = (ctx.launch_count - n0) // 3
             ts = []
             for _ in range(args.reps):
                 e0.record(s)
@@ -59,7 +61,9 @@ def main():
                               "gflops": round(fl / ms / 1e6, 1), "gbs": round(by / ms / 1e6, 1),
                               "intensity": round(fl / by, 2),
                               "roofline_frac": round(fl / (ms * 1e-3) / roof, 4),
-                              "path": "fused TMA+DMMA" if r <= 32 else "3 batched GEMMs"}),
+                              "path": ("fused TMA+DMMA (one warp per item)" if r <= 32 else
+                                       "one launch, T and E on chip" if per_call == 1 else
+                                       "3 batched GEMMs")}),
                   flush=True)
             del bufs
 
