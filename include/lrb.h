@@ -222,6 +222,8 @@ lrb_status lrb_dgemm_ptr_batched_host(lrb_ctx* ctx, char order, char opA, char o
  * (kernels.hpp:133-135, 246-248). G is overwritten (stored once per item).
  * Each product is an in-order FMA chain, i.e. the reference oracle
  * low_rank_multiply_reference_raw (low_rank.hpp:73-87) with fused rounding.
+ * One launch for rank <= 32 (a warp per item) and for ranks 64, 96 and 128
+ * (a CTA per item, the intermediates on chip); three batched GEMMs otherwise.
  * Replaces: fused_multiply (kernels.hpp:131-161), packed_multiply
  * (kernels.hpp:243-349), naive_multiply_batch (bench.hpp:55-77).
  */
@@ -276,9 +278,11 @@ lrb_status lrb_batch_file_save(lrb_ctx* ctx, const char* path, int64_t batch, in
  * row-major (u block x rank, x rank x rank, vt rank x block).
  * lrb_blr_matvec: y = M rhs (blr_matvec, blr.hpp:141-175) for row-major
  * n x nrhs HOST buffers; the _device form takes device buffers and is
- * asynchronous. Two batched GEMM launches around one coupling kernel, on the
- * caller's stream, every chain in the reference's order (y_i = D_i rhs_i,
- * then += U_ij X_ij Vt_ij rhs_j for j ascending). The matrix owns a
+ * asynchronous. One persistent launch for 9..16 right-hand sides (block a
+ * multiple of 64, rank dividing 64, TMA-addressable operands), otherwise two
+ * batched GEMM launches around one coupling kernel; on the caller's stream,
+ * every chain in the reference's order (y_i = D_i rhs_i, then
+ * += U_ij X_ij Vt_ij rhs_j for j ascending). The matrix owns a
  * grow-only matvec workspace: eager calls on different streams are ordered
  * through an event, and buffers a captured graph references stay alive
  * until lrb_blr_destroy.

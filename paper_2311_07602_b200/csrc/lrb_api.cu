@@ -980,7 +980,6 @@ struct lrb_ptr_plan {
   uint64_t* d_tiles = nullptr;
   CUtensorMap* d_maps = nullptr;  // 2 per item on the TMA path
   unsigned long long* d_ticket = nullptr;  // the single-launch kernel's tile tickets
-  int varn_flags = 0;                      // its kernel flags (scalar-column threshold)
   struct Group {
     int variant;  // a tile variant, or kVarnGroup: the single-launch kernel
     int64_t offset, count;
@@ -1000,16 +999,6 @@ bool varn_enabled(const lrb_ctx* ctx) {
   const char* s = std::getenv("LRB_PTR_BUCKETS");
   return !(s && s[0] == '1');
 }
-
-// Columns past the last full 8-column fragment: up to `rem_max` of them run
-// as scalar DFMA chains, more as one zero-padded fragment. LRB_VARN_REM_MAX
-// (0..7) overrides the default.
-int varn_rem_max() {
-  const char* s = std::getenv("LRB_VARN_REM_MAX");
-  if (s && *s) return std::max(0, std::min(7, std::atoi(s)));
-  return kVarnRemMax;
-}
-int varn_rem_flags() { return (varn_rem_max() + 1) << 8; }
 
 // per-item tensor maps for the single-launch kernel's boxes
 bool encode_varn_pair(int a_t, int b_t, const ItemDesc& d, CUtensorMap* mA, CUtensorMap* mB) {
@@ -1187,7 +1176,6 @@ extern "C" lrb_status lrb_ptr_plan_create(lrb_ctx* ctx, char order, char opA, ch
       ids.swap(keep);
     }
     if (!varn_ids.empty()) {
-      plan->varn_flags = varn_rem_flags();
       std::sort(varn_ids.begin(), varn_ids.end());
       varn_order(items, varn_ids, &tiles);
       plan->groups.push_back({kVarnGroup, 0, int64_t(tiles.size()), 1});
@@ -1291,7 +1279,7 @@ extern "C" lrb_status lrb_ptr_plan_execute(lrb_ctx* ctx, const lrb_ptr_plan* pla
                      plan->d_ticket};
       int64_t grid = 0;
       cudaError_t e = launch_varn(plan->a_t, plan->b_t, vp,
-                                  plan->beta_one | plan->varn_flags | (debug_flags() & 14),
+                                  plan->beta_one | (debug_flags() & 14),
                                   ctx->device, ctx->sm_count, s, &grid);
       if (e != cudaSuccess) return cuda_fail(ctx, e, "lrb_varn_kernel launch");
       if (grid > 0) ctx->launches.fetch_add(1, std::memory_order_relaxed);

@@ -22,6 +22,7 @@
 // themselves at the end of the launch (last CTA out), so graph replays need
 // no memset.
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "lrb_gemm.cuh"
@@ -51,15 +52,22 @@ namespace {
 // on the 16-RHS bench shape: k64 x 2 stages 0.0676 ms, k32 x 4 0.0656, k16 x
 // 7 0.0697, k32 x 5 or k64 x 3 (one CTA per SM) 0.076-0.082, 32-column tiles
 // 0.072-0.076
-using FCfg = GemmCfg<1, 4, 16, 16, 32, 4, 2, false, false, true>;
-constexpr int kFStages = FCfg::STAGES;
+// (MBT = 16 serves 9..16 right-hand sides; MBT = 8 serves up to 8 without
+// padding them to 16 rows: half the DMMA work and half the rhs / Z traffic)
+template <int MBT>
+using FCfgT = GemmCfg<1, 4, MBT, 16, 32, 4, 2, false, false, true>;
+constexpr int kFStages = 4;
 constexpr int kFWarps = 4;
 constexpr int kFThreads = kFWarps * 32 + 32;  // + the producer warp
-constexpr int kScratch = FCfg::MB * FCfg::NB;  // the W^T tile (nrhs x 64)
+constexpr int kFNB = 64, kFKB = 32;
 constexpr int kMaxRank = 16;                   // X tiles of one W tile: 64 / r items of r x r
-constexpr int kXs = FCfg::NB * kMaxRank;
-constexpr size_t kFSmem = size_t(kFStages) * FCfg::STAGE_ELEMS * 8 + size_t(kScratch) * 8 +
-                          size_t(kXs) * 8 + size_t(kFStages) * 8 * 3 + 16;
+constexpr int kXs = kFNB * kMaxRank;
+template <int MBT>
+constexpr size_t fused_smem() {
+  // ring, the W^T tile (nrhs x 64), X staging, barriers + slot table
+  return size_t(kFStages) * FCfgT<MBT>::STAGE_ELEMS * 8 + size_t(MBT * kFNB) * 8 +
+         size_t(kXs) * 8 + size_t(kFStages) * 8 * 3 + 16;
+}
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
@@ -70,8 +78,12 @@ __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;\n" ::: "memory");
 }
 
+template <int MBT>
 __global__ void __launch_bounds__(kFThreads, 2)
     blr_fused_kernel(const __grid_constant__ BlrFusedProblem p) {
+  using FCfg = FCfgT<MBT>;
+  static_assert(FCfg::STAGES == kFStages && FCfg::NB == kFNB && FCfg::KB == kFKB, "ring geometry");
+  constexpr int kScratch = FCfg::MB * FCfg::NB;
   pdl_entry();
   constexpr int KB = FCfg::KB, NB = FCfg::NB, MB = FCfg::MB;
   extern __shared__ __align__(1024) double smem[];
@@ -119,8 +131,14 @@ __global__ void __launch_bounds__(kFThreads, 2)
         }
         const bool wtile = t < p.nw;
         const long long u = wtile ? t : t - p.nw;
-        const int z = int(wtile ? u / p.tw : u / p.tr);  // column j / row i
-        const int n0 = int(wtile ? u % p.tw : u % p.tr) * NB;
+        // W tickets run column-major (all of column j's blocks, then column
+        // j + 1). Bit 6 probes the row-block-major order (every column's block
+        // 0 first, so the early rows' Z are complete long before the first row
+        // tickets): no change on the 16-RHS shape, 2.5 % slower on the paper's
+        // 8-RHS shape (a column's tiles share rhs_j in L2).
+        const bool colmajor = (p.flags & 64) == 0;
+        const int z = int(wtile ? (colmajor ? u / p.tw : u % p.T) : u / p.tr);  // column j / row i
+        const int n0 = int(wtile ? (colmajor ? u % p.tw : u / p.T) : u % p.tr) * NB;
         const int kend = wtile ? p.b : p.P;
         bool waited = false;
         long long t_next = -1;
@@ -195,8 +213,9 @@ __global__ void __launch_bounds__(kFThreads, 2)
     if (t < 0) break;
     const bool wtile = t < p.nw;
     const long long u = wtile ? t : t - p.nw;
-    const int z = int(wtile ? u / p.tw : u / p.tr);
-    const int n0 = int(wtile ? u % p.tw : u % p.tr) * NB;
+    const bool colmajor = (p.flags & 64) == 0;
+    const int z = int(wtile ? (colmajor ? u / p.tw : u % p.T) : u / p.tr);
+    const int n0 = int(wtile ? (colmajor ? u % p.tw : u / p.T) : u % p.tr) * NB;
     const int chunks = ((wtile ? p.b : p.P) + KB - 1) / KB;
     double acc[FCfg::FJ][FCfg::FI][2];
 #pragma unroll
@@ -226,11 +245,16 @@ __global__ void __launch_bounds__(kFThreads, 2)
         const int j = n0 + FCfg::load_col(wj, fj, g);
         if (j >= p.b) continue;
         double* yr = p.y + (int64_t(i) * p.b + j) * p.nrhs;
-        const int c0 = FCfg::acc_row(wi, 0, 0, tq);  // rows c0 .. c0 + 3
-        const double v[4] = {acc[fj][0][0], acc[fj][1][0], acc[fj][0][1], acc[fj][1][1]};
+        const int c0 = FCfg::acc_row(wi, 0, 0, tq);
+        if constexpr (FCfg::FI == 2) {  // paired fragments: rows c0 .. c0 + 3
+          const double v[4] = {acc[fj][0][0], acc[fj][1][0], acc[fj][0][1], acc[fj][1][1]};
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (c0 + e < p.nrhs) yr[c0 + e] = v[e];
+          for (int e = 0; e < 4; ++e)
+            if (c0 + e < p.nrhs) yr[c0 + e] = v[e];
+        } else {  // rows c0, c0 + 1
+          if (c0 < p.nrhs) yr[c0] = acc[fj][0][0];
+          if (c0 + 1 < p.nrhs) yr[c0 + 1] = acc[fj][0][1];
+        }
       }
       continue;
     }
@@ -241,10 +265,15 @@ __global__ void __launch_bounds__(kFThreads, 2)
     for (int fj = 0; fj < FCfg::FJ; ++fj) {
       const int j = FCfg::load_col(wj, fj, g);
       const int c0 = FCfg::acc_row(wi, 0, 0, tq);
-      scratch[j * MB + c0 + 0] = acc[fj][0][0];
-      scratch[j * MB + c0 + 1] = acc[fj][1][0];
-      scratch[j * MB + c0 + 2] = acc[fj][0][1];
-      scratch[j * MB + c0 + 3] = acc[fj][1][1];
+      if constexpr (FCfg::FI == 2) {
+        scratch[j * MB + c0 + 0] = acc[fj][0][0];
+        scratch[j * MB + c0 + 1] = acc[fj][1][0];
+        scratch[j * MB + c0 + 2] = acc[fj][0][1];
+        scratch[j * MB + c0 + 3] = acc[fj][1][1];
+      } else {
+        scratch[j * MB + c0 + 0] = acc[fj][0][0];
+        scratch[j * MB + c0 + 1] = acc[fj][0][1];
+      }
     }
     named_barrier_sync(1, kFWarps * 32);
     const int jcol = z, r = p.r, nrhs = p.nrhs;
@@ -330,17 +359,14 @@ bool encode_operand(CUtensorMap* map, const double* base, int64_t rows, int64_t 
 // outside what the fused kernel serves: nrhs <= 16, block a multiple of 32,
 // rank dividing 64 (each 64-row W block holds whole items) and a multiple of
 // 4, TMA-addressable operands.
-bool launch_blr_fused(lrb_ctx* ctx, const double* rhs, int64_t nrhs, double* y, int64_t T,
-                      int64_t b, int64_t r, int64_t P, const double* vtcol, const double* x,
-                      const double* dcat, double* rz, unsigned* ready,
-                      unsigned long long* next, cudaStream_t s, lrb_status* st) {
+template <int MBT>
+bool launch_blr_fused_t(lrb_ctx* ctx, const double* rhs, int64_t nrhs, double* y, int64_t T,
+                        int64_t b, int64_t r, int64_t P, const double* vtcol, const double* x,
+                        const double* dcat, double* rz, unsigned* ready,
+                        unsigned long long* next, cudaStream_t s, lrb_status* st) {
+  using FCfg = FCfgT<MBT>;
+  constexpr size_t kFSmem = fused_smem<MBT>();
   const int64_t K = (T - 1) * r;
-  // nrhs <= 8 keeps the three-launch form: its m8 row tiles do not pad the
-  // right-hand sides to 16 (the paper's rank-8 / 8-RHS shape: 0.0758 vs
-  // 0.0799 ms fused)
-  if (T < 2 || nrhs <= 8 || nrhs > FCfg::MB || b % FCfg::KB != 0 || FCfg::NB % r != 0 || r % 4 != 0 ||
-      r > kMaxRank)
-    return false;
   BlrFusedProblem p;
   std::memset(&p, 0, sizeof(p));
   const bool ok =
@@ -366,16 +392,17 @@ bool launch_blr_fused(lrb_ctx* ctx, const double* rhs, int64_t nrhs, double* y, 
   int occ = (dev >= 0 && dev < 64) ? occ_cache[dev] : 0;
   cudaError_t e = cudaSuccess;
   if (occ == 0) {
-    e = cudaFuncSetAttribute(blr_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(blr_fused_kernel<MBT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(kFSmem));
     if (e == cudaSuccess)
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, blr_fused_kernel, kFThreads, kFSmem);
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, blr_fused_kernel<MBT>, kFThreads,
+                                                        kFSmem);
     if (e == cudaSuccess && occ < 1) e = cudaErrorInvalidConfiguration;
     if (e == cudaSuccess && dev >= 0 && dev < 64) occ_cache[dev] = occ;
   }
   if (e == cudaSuccess) {
     const int64_t grid = std::min<int64_t>(int64_t(ctx->sm_count) * occ, p.total);
-    e = launch_pdl(blr_fused_kernel, dim3(unsigned(grid)), dim3(kFThreads), kFSmem, s, p);
+    e = launch_pdl(blr_fused_kernel<MBT>, dim3(unsigned(grid)), dim3(kFThreads), kFSmem, s, p);
   }
   if (e != cudaSuccess) {
     *st = cuda_fail(ctx, e, "blr_fused_kernel launch");
@@ -384,6 +411,25 @@ bool launch_blr_fused(lrb_ctx* ctx, const double* rhs, int64_t nrhs, double* y, 
   ctx->launches.fetch_add(1, std::memory_order_relaxed);
   *st = LRB_OK;
   return true;
+}
+
+bool launch_blr_fused(lrb_ctx* ctx, const double* rhs, int64_t nrhs, double* y, int64_t T,
+                      int64_t b, int64_t r, int64_t P, const double* vtcol, const double* x,
+                      const double* dcat, double* rz, unsigned* ready,
+                      unsigned long long* next, cudaStream_t s, lrb_status* st) {
+  if (T < 2 || nrhs < 1 || nrhs > 16 || b % kFKB != 0 || kFNB % r != 0 || r % 4 != 0 ||
+      r > kMaxRank)
+    return false;
+  if (nrhs <= 8) {
+    // the m8 tile; LRB_BLR_FUSED_M8=0 keeps the three-launch form for <= 8
+    // right-hand sides
+    const char* e8 = std::getenv("LRB_BLR_FUSED_M8");
+    if (e8 && e8[0] == '0') return false;
+    return launch_blr_fused_t<8>(ctx, rhs, nrhs, y, T, b, r, P, vtcol, x, dcat, rz, ready, next, s,
+                                 st);
+  }
+  return launch_blr_fused_t<16>(ctx, rhs, nrhs, y, T, b, r, P, vtcol, x, dcat, rz, ready, next, s,
+                                st);
 }
 
 }  // namespace lrb

@@ -665,7 +665,7 @@ extern "C" lrb_status lrb_dgemm_ptr_batched_device(lrb_ctx* ctx, char order, cha
                  w.counters + 2 * kClasses, w.totals, w.tiles, w.tile_cap};
   int64_t grid = 0;
   const char* stage = "single-launch kernel";
-  e = launch_varn(a_t, b_t, vp, (beta == 1.0 ? 1 : 0) | varn_rem_flags() | (debug_flags() & 30),
+  e = launch_varn(a_t, b_t, vp, (beta == 1.0 ? 1 : 0) | (debug_flags() & 30),
                   ctx->device, ctx->sm_count, s, &grid);
   if (e == cudaSuccess && grid > 0) ctx->launches.fetch_add(1, std::memory_order_relaxed);
   if (e == cudaSuccess) {

@@ -43,6 +43,9 @@
 //         epilogue's synchronous slot hand-back for the write-bound k <= 16.
 //   q64q : q64p with a 3-stage ring at two CTAs per SM, for k >= 256 (the
 //         low-rank r = 64 product's 64 x 64 x b GEMM: +5-6%).
+// (Measured and dropped: n32 with 16-deep chunks in a 3-stage ring at three
+// CTAs per SM, 0.80-0.87 of the r = 32 class's roofline against n32's
+// 0.88-0.95 on the same box.)
 // The 4-warp variants run a producer warp on their TMA path (VariantProd):
 // the computing warps then only wait on full / arrive on empty per chunk.
 #pragma once

@@ -13,11 +13,12 @@
 //     of 32-deep k chunks (per-item 2-D tensor maps; the B box is only as wide
 //     as the item's columns, rounded to 8).
 //   * The column count is a run-time property of the tile: the warps run
-//     F = cols / 8 DMMA fragment columns (a compile-time specialisation per F,
-//     dispatched per tile) and the last cols % 8 columns as scalar DFMA chains
-//     (each thread owns one row of them), so no padded column reaches the
-//     tensor pipe. Both paths consume k in ascending order — each C entry is
-//     one in-order FMA chain, bitwise the reference's FMA-contracted loop.
+//     F = ceil(cols / 8) DMMA fragment columns (a compile-time specialisation
+//     per F, dispatched per tile; the last fragment zero-padded), k in
+//     ascending order — each C entry is one in-order FMA chain, bitwise the
+//     reference's FMA-contracted loop. (Two scalar-DFMA forms of the last
+//     cols % 8 columns were measured and dropped; carrying
+//     them as a run-time option also cost the hot loop register spills.)
 //   * Tiles are claimed dynamically (one atomic ticket per tile, taken by the
 //     producer and passed to the computing warps through the ring slot), in a
 //     host-chosen order that interleaves FP64-bound and HBM-bound tiles so the
@@ -89,59 +90,20 @@ struct VarnLayout {
 // 64-byte descriptor load
 __device__ __forceinline__ ItemDesc load_desc(const ItemDesc* p) { return *p; }
 
-// Four k steps (k .. k+3) of the scalar columns 8F .. 8F+rem-1 for this
-// thread's row: each column's chain advances in ascending k. Issued between
-// the DMMA k steps so the DFMA latency hides behind the tensor pipe.
-template <class Cfg, int F>
-__device__ __forceinline__ void rem_step4(double (&racc)[7], const double* As, const double* Bs,
-                                          int row, int k, int rem) {
-  double a[4];
-  if constexpr (Cfg::A_T) {
-    const double2 a01 = *reinterpret_cast<const double2*>(&As[Cfg::a_off(row, k)]);
-    const double2 a23 = *reinterpret_cast<const double2*>(&As[Cfg::a_off(row, k + 2)]);
-    a[0] = a01.x, a[1] = a01.y, a[2] = a23.x, a[3] = a23.y;
-  } else {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) a[u] = As[Cfg::a_off(row, k + u)];
-  }
-#pragma unroll
-  for (int q = 0; q < 7; ++q) {
-    if (q < rem) {
-      double b[4];
-      if constexpr (!Cfg::B_T) {  // K-contiguous: the four k values are adjacent
-        const double2 b01 = *reinterpret_cast<const double2*>(&Bs[Cfg::b_off(k, 8 * F + q)]);
-        const double2 b23 = *reinterpret_cast<const double2*>(&Bs[Cfg::b_off(k + 2, 8 * F + q)]);
-        b[0] = b01.x, b[1] = b01.y, b[2] = b23.x, b[3] = b23.y;
-      } else {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) b[u] = Bs[Cfg::b_off(k + u, 8 * F + q)];
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) racc[q] = fma(a[u], b[u], racc[q]);
-    }
-  }
-}
-
 template <bool AT, bool BT, int F>
-__device__ __forceinline__ void varn_tile(const ItemDesc& d, int i0, int j0, int cols,
+__device__ __forceinline__ void varn_tile(const ItemDesc& d, int i0, int j0,
                                           const double* smem, uint64_t* full, uint64_t* empty,
                                           int& stage, uint32_t& phase, int beta_one, int flags) {
   using Cfg = VarnCfg<AT, BT, F>;
   using L = VarnLayout<AT, BT>;
   constexpr int FI = Cfg::FI, FJ = Cfg::FJ, KB = L::KB;
-  constexpr bool HAS_REM = F < 8;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wi = warp, wj = 0, g = lane >> 2, tq = lane & 3;
-  const int rem = HAS_REM ? cols - 8 * F : 0;  // scalar columns after the fragments
-  const int my_row = wi * 32 + lane;           // this thread's row of the scalar columns
   double acc[FJ][FI][2];
-  double racc[HAS_REM ? 7 : 1];
 #pragma unroll
   for (int fj = 0; fj < FJ; ++fj)
 #pragma unroll
     for (int fi = 0; fi < FI; ++fi) acc[fj][fi][0] = acc[fj][fi][1] = 0.0;
-#pragma unroll
-  for (int q = 0; q < (HAS_REM ? 7 : 1); ++q) racc[q] = 0.0;
   if (beta_one) {
 #pragma unroll
     for (int fj = 0; fj < FJ; ++fj) {
@@ -157,12 +119,6 @@ __device__ __forceinline__ void varn_tile(const ItemDesc& d, int i0, int j0, int
           }
       }
     }
-    if constexpr (HAS_REM) {
-      const int i = i0 + my_row;
-#pragma unroll
-      for (int q = 0; q < 7; ++q)
-        if (q < rem && i < d.m) racc[q] = d.C[int64_t(j0 + 8 * F + q) * d.ldc + i];
-    }
   }
   bool first = true;
 #pragma unroll 1
@@ -173,16 +129,8 @@ __device__ __forceinline__ void varn_tile(const ItemDesc& d, int i0, int j0, int
     const double* As = smem + size_t(stage) * L::STAGE_ELEMS;
     const double* Bs = As + L::A_ELEMS;
     if (kvalid == KB) {
-      if (HAS_REM && rem > 0) {
 #pragma unroll
-        for (int kq = 0; kq < KB / 4; ++kq) {
-          mma_kstep<Cfg>(acc, As, Bs, wi, wj, g, kq * 4 + tq);
-          if constexpr (HAS_REM) rem_step4<Cfg, F>(racc, As, Bs, my_row, kq * 4, rem);
-        }
-      } else {
-#pragma unroll
-        for (int kq = 0; kq < KB / 4; ++kq) mma_kstep<Cfg>(acc, As, Bs, wi, wj, g, kq * 4 + tq);
-      }
+      for (int kq = 0; kq < KB / 4; ++kq) mma_kstep<Cfg>(acc, As, Bs, wi, wj, g, kq * 4 + tq);
     } else {
       const int nq = kvalid >> 2;
 #pragma unroll 1
@@ -198,18 +146,6 @@ __device__ __forceinline__ void varn_tile(const ItemDesc& d, int i0, int j0, int
             for (int c = 0; c < 2; ++c)
               acc[fj][fi][c] = fma(As[Cfg::a_off(Cfg::acc_row(wi, fi, c, tq), kk)], bv,
                                    acc[fj][fi][c]);
-        }
-      }
-    }
-    if constexpr (HAS_REM) {
-      if (rem > 0 && kvalid < KB) {
-        // the scalar columns of a partial chunk: one row per thread, k ascending
-#pragma unroll 1
-        for (int kk = 0; kk < kvalid; ++kk) {
-          const double a = As[Cfg::a_off(my_row, kk)];
-#pragma unroll
-          for (int q = 0; q < 7; ++q)
-            if (q < rem) racc[q] = fma(a, Bs[Cfg::b_off(kk, 8 * F + q)], racc[q]);
         }
       }
     }
@@ -256,14 +192,6 @@ __device__ __forceinline__ void varn_tile(const ItemDesc& d, int i0, int j0, int
           }
         }
       }
-    }
-  }
-  if constexpr (HAS_REM) {
-    const int i = i0 + my_row;
-    if (i < d.m) {
-#pragma unroll
-      for (int q = 0; q < 7; ++q)
-        if (q < rem) st_global_cs(d.C + int64_t(j0 + 8 * F + q) * d.ldc + i, racc[q]);
     }
   }
 }
@@ -415,23 +343,17 @@ __global__ void __launch_bounds__(VarnLayout<AT, BT>::THREADS, 2)
     const ItemDesc d = load_desc(prob.items + uint32_t(e >> 32));
     const int i0 = int((e >> 16) & 0xFFFF) * L::MB;
     const int j0 = int(e & 0xFFFF) * L::NBMAX;
-    int cols = min(L::NBMAX, d.n - j0);
-    // columns past the last full fragment run as scalar chains up to rem_max
-    // of them, else as one more zero-padded fragment (flags bits 8..11 hold
-    // rem_max + 1; bit 2 pads every tile, a probe)
-    const int rem_max = (flags & 4) ? 0 : (((flags >> 8) & 15) ? ((flags >> 8) & 15) - 1 : 7);
-    if ((cols & 7) > rem_max) cols = (cols + 7) & ~7;
-    const int F = cols >> 3;
+    // columns of this tile, rounded up to whole 8-column fragments
+    const int F = (min(L::NBMAX, d.n - j0) + 7) >> 3;
     switch (F) {
-      case 0:  // fewer than 8 columns: one zero-padded fragment column
-      case 1: varn_tile<AT, BT, 1>(d, i0, j0, cols < 8 ? 8 : cols, smem, full, empty, stage, phase, beta_one, flags); break;
-      case 2: varn_tile<AT, BT, 2>(d, i0, j0, cols, smem, full, empty, stage, phase, beta_one, flags); break;
-      case 3: varn_tile<AT, BT, 3>(d, i0, j0, cols, smem, full, empty, stage, phase, beta_one, flags); break;
-      case 4: varn_tile<AT, BT, 4>(d, i0, j0, cols, smem, full, empty, stage, phase, beta_one, flags); break;
-      case 5: varn_tile<AT, BT, 5>(d, i0, j0, cols, smem, full, empty, stage, phase, beta_one, flags); break;
-      case 6: varn_tile<AT, BT, 6>(d, i0, j0, cols, smem, full, empty, stage, phase, beta_one, flags); break;
-      case 7: varn_tile<AT, BT, 7>(d, i0, j0, cols, smem, full, empty, stage, phase, beta_one, flags); break;
-      default: varn_tile<AT, BT, 8>(d, i0, j0, cols, smem, full, empty, stage, phase, beta_one, flags); break;
+      case 1: varn_tile<AT, BT, 1>(d, i0, j0, smem, full, empty, stage, phase, beta_one, flags); break;
+      case 2: varn_tile<AT, BT, 2>(d, i0, j0, smem, full, empty, stage, phase, beta_one, flags); break;
+      case 3: varn_tile<AT, BT, 3>(d, i0, j0, smem, full, empty, stage, phase, beta_one, flags); break;
+      case 4: varn_tile<AT, BT, 4>(d, i0, j0, smem, full, empty, stage, phase, beta_one, flags); break;
+      case 5: varn_tile<AT, BT, 5>(d, i0, j0, smem, full, empty, stage, phase, beta_one, flags); break;
+      case 6: varn_tile<AT, BT, 6>(d, i0, j0, smem, full, empty, stage, phase, beta_one, flags); break;
+      case 7: varn_tile<AT, BT, 7>(d, i0, j0, smem, full, empty, stage, phase, beta_one, flags); break;
+      default: varn_tile<AT, BT, 8>(d, i0, j0, smem, full, empty, stage, phase, beta_one, flags); break;
     }
   }
 }

@@ -13,14 +13,15 @@ struct ItemDesc;  // lrb_gemm.cuh
 
 constexpr int kVarnMB = 128;    // rows of C per tile (4 warps x 32)
 constexpr int kVarnNB = 64;     // max columns of C per tile
-constexpr int kVarnKB = 32;     // k chunk per ring slot
-constexpr int kVarnStages = 2;  // ring depth (two CTAs per SM)
-// Columns past the last full fragment default to one zero-padded fragment:
-// the scalar-chain form measured slower at every threshold on cfg4 (rem <= 1:
-// 8.49 ms, rem <= 7: 9.10 ms vs 8.29 ms padded; tools/probe_varn.py), so it
-// stays an opt-in (LRB_VARN_REM_MAX)
-constexpr int kVarnRemMax = 0;
-
+// (overridable at build time for A/B probes: -DLRB_VARN_KB=16 -DLRB_VARN_STAGES=4)
+#ifndef LRB_VARN_KB
+#define LRB_VARN_KB 32
+#endif
+#ifndef LRB_VARN_STAGES
+#define LRB_VARN_STAGES 2
+#endif
+constexpr int kVarnKB = LRB_VARN_KB;          // k chunk per ring slot
+constexpr int kVarnStages = LRB_VARN_STAGES;  // ring depth (two CTAs per SM)
 // TMA box width (columns) of an op(B) = N operand for an item with n
 // columns: the tile's columns rounded up to the DMMA fragment width
 __host__ __device__ __forceinline__ int varn_box_cols(int n) {
@@ -74,10 +75,6 @@ __device__ __forceinline__ int64_t prefix_search(const int64_t* prefix, int64_t 
 __device__ __forceinline__ void fence_tensormap_acquire(const void* map) {
   asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;\n" ::"l"(map) : "memory");
 }
-
-// the kernel's remainder-column setting (flags bits 8..11), from
-// kVarnRemMax or LRB_VARN_REM_MAX (lrb_api.cu)
-int varn_rem_flags();
 
 // a_t / b_t: op flags of the column-major view; flags bit 0: beta = 1
 cudaError_t launch_varn(int a_t, int b_t, const VarnProblem& p, int flags, int device,

@@ -167,7 +167,10 @@ def test_graph_survives_workspace_growth_and_other_streams(ctx):
 
 
 FUSED_SHAPES = [(2, 8, 10, 64), (4, 16, 16, 64), (5, 4, 12, 128), (8, 16, 12, 64), (3, 8, 16, 128),
-                (17, 8, 14, 64), (6, 16, 10, 256), (9, 4, 10, 192), (33, 16, 16, 64)]
+                (17, 8, 14, 64), (6, 16, 10, 256), (9, 4, 10, 192), (33, 16, 16, 64),
+                # up to 8 right-hand sides: the m8 tile
+                (4, 8, 8, 64), (5, 16, 8, 128), (3, 4, 6, 64), (9, 8, 2, 128), (17, 16, 4, 64),
+                (8, 8, 8, 512)]
 
 
 @pytest.mark.parametrize("tiles,rank,nrhs,block", FUSED_SHAPES)

@@ -1,7 +1,7 @@
 """GPU: the single-launch variable-size pointer-array kernel (lrb_varn.cu)
-against the oracle's FMA chain, bitwise: ragged rows and columns (fragment
-columns plus 1..7 scalar columns, several 64-column tiles, fewer than 8
-columns), k tails, every op combination, beta = 1, padded leading dimensions,
+against the oracle's FMA chain, bitwise: ragged rows and columns (every
+column count 1..71: whole fragments plus a zero-padded last one, several
+64-column tiles, fewer than 8 columns), k tails, every op combination, beta = 1, padded leading dimensions,
 repeated and graph-replayed executions (the self-resetting tile tickets), and
 equality with the per-variant bucket path it replaced."""
 import numpy as np
@@ -114,14 +114,13 @@ def test_odd_shapes_mix_single_launch_and_buckets(ctx, ops):
     c.check()
 
 
-@pytest.mark.parametrize("rem_max", ["0", "1", "7"])
+@pytest.mark.parametrize("beta", [0.0, 1.0])
 @pytest.mark.parametrize("ops", OPS)
-def test_remainder_columns_every_width(ctx, monkeypatch, rem_max, ops):
+def test_remainder_columns_every_width(ctx, beta, ops):
     # n = 8F + rem for every F in 0..8 and rem in 0..7, two row tiles, a k
-    # tail; remainder columns padded (default) or as scalar DFMA chains
-    monkeypatch.setenv("LRB_VARN_REM_MAX", rem_max)
+    # tail: the last fragment column is zero-padded
     dims = [(150, n, 38) for n in range(1, 72)]
-    c = PtrCase(ctx, dims, ops[0], ops[1], 1.0 if rem_max == "1" else 0.0, seed=9)
+    c = PtrCase(ctx, dims, ops[0], ops[1], beta, seed=9)
     p = c.plan()
     assert p.launches == 1
     p.execute()

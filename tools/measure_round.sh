@@ -27,6 +27,11 @@ log "probes"
 timeout 600 python tools/probe_varn.py > $O/probe_varn_$R.jsonl 2>> $O/probe_$R.err
 timeout 600 python tools/probe_cold.py > $O/probe_cold_$R.jsonl 2>> $O/probe_$R.err
 timeout 300 ./tools/microbench/fp64_mix > $O/fp64_mix_$R.jsonl 2>> $O/probe_$R.err
+timeout 300 ./tools/microbench/write_bw > $O/write_bw_$R.jsonl 2>> $O/probe_$R.err
+timeout 120 ./tools/microbench/tmap_probe > $O/tmap_probe_$R.txt 2>> $O/probe_$R.err
+
+log "widened rows, both arms"
+bash tools/bench_rows_all.sh $R
 
 log "sweeps"
 timeout 900 python tools/sweep.py > $O/sweep_$R.jsonl 2> $O/sweep_$R.err
@@ -64,4 +69,16 @@ if timeout 300 python tools/profile_one.py --config cfg2 --launches 2 > /dev/nul
     > $O/ncu_cfg2_$R.log 2>&1
   log "ncu cfg2 rc=$?"
 fi
+if timeout 300 python tools/profile_all.py --only lr_r64_b2048 > /dev/null 2>&1; then
+  timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"lrb_lowrank_big" \
+    -c 1 -f -o $O/ncu_lr_r64_$R python tools/profile_all.py --only lr_r64_b2048 \
+    > $O/ncu_lr_r64_$R.log 2>&1
+  log "ncu lr_r64 rc=$?"
+fi
+for f in ncu_cfg4_$R ncu_cfg2_$R ncu_lr_r64_$R; do
+  [ -f $O/$f.ncu-rep ] && python tools/ncu_summary.py rep $O/$f.ncu-rep > $O/$f.json 2>> $O/probe_$R.err
+done
+log "smoke"
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke_$R.txt 2>&1
+log "smoke rc=$? $(tail -1 $O/smoke_$R.txt | cut -c1-200)"
 log "done"

@@ -1,7 +1,6 @@
 #!/usr/bin/env python3
 """A/B probe of the cfg4 pointer-array paths on one box: the single-launch
-kernel under its tile orders and with the scalar remainder columns padded
-away, against the per-variant buckets.
+kernel under its tile orders, against the per-variant buckets.
 
     python tools/probe_varn.py [--reps 10] [--items N]
 prints one JSON line per setting (median ms per execute, fraction of FP64 peak)
@@ -26,12 +25,6 @@ SETTINGS = [
     ("varn longest-first", {"LRB_VARN_ORDER": "1"}),
     ("varn item order", {"LRB_VARN_ORDER": "2"}),
     ("varn device-path order", {"LRB_VARN_ORDER": "3"}),
-    ("varn padded (no scalar columns)", {"LRB_DEBUG_FLAGS": "4"}),
-    ("varn scalar rem<=1", {"LRB_VARN_REM_MAX": "1"}),
-    ("varn scalar rem<=2", {"LRB_VARN_REM_MAX": "2"}),
-    ("varn scalar rem<=3", {"LRB_VARN_REM_MAX": "3"}),
-    ("varn scalar rem<=4", {"LRB_VARN_REM_MAX": "4"}),
-    ("varn scalar rem<=5", {"LRB_VARN_REM_MAX": "5"}),
     ("varn no stores", {"LRB_DEBUG_FLAGS": "2"}),
     ("buckets", {"LRB_PTR_BUCKETS": "1"}),
 ]
@@ -84,7 +77,7 @@ def main():
     for name, env in SETTINGS:
         if args.only and args.only not in name:
             continue
-        for k in ("LRB_VARN_ORDER", "LRB_DEBUG_FLAGS", "LRB_PTR_BUCKETS", "LRB_VARN_REM_MAX"):
+        for k in ("LRB_VARN_ORDER", "LRB_DEBUG_FLAGS", "LRB_PTR_BUCKETS"):
             os.environ.pop(k, None)
         os.environ.update(env)
         plan = ctx.ptr_plan("C", "N", "N", vs.bs, vs.rs, vs.bs, vs.pa, vs.bs, vs.pb, vs.bs,
