@@ -182,6 +182,55 @@ def test_cfg4_pointer_array_sampled(ctx):
         assert bad == 0
 
 
+def test_cfg4_full_batch_three_paths_agree_bitwise(ctx, monkeypatch):
+    """BASELINE cfg4 at full size (8192 items, 31 GB): every entry of every
+    item from the single-launch kernel equals (a) the per-variant bucket
+    launches of the tile kernel, an independent kernel family, and (b) the
+    device-descriptor call, whose plan and tensor maps are built on the GPU.
+    Together with the sampled oracle check above this pins all 8192 results."""
+    w = W.get("cfg4")
+    items = list(range(w.batch))
+    offs, (na, nb, nc) = W.variable_layout(w, items)
+    arena_a, arena_b = ctx.malloc(na), ctx.malloc(nb)
+    outs = [ctx.malloc(nc) for _ in range(3)]
+    pa = [arena_a.ptr + o[0] for o in offs]
+    pb = [arena_b.ptr + o[1] for o in offs]
+    pcs = [[out.ptr + o[2] for o in offs] for out in outs]
+    ctx.fill_uniform_ptr(pa, w.bs, w.bs, w.bs, w.seed, W.ROLE_A)
+    ctx.fill_uniform_ptr(pb, w.bs, w.rs, w.bs, w.seed, W.ROLE_B)
+    for out in outs:
+        out.fill_bytes(0xFF)  # NaN: beta = 0 must overwrite every entry
+    # 1. the single launch
+    plan = ctx.ptr_plan("C", "N", "N", w.bs, w.rs, w.bs, pa, w.bs, pb, w.bs, pcs[0], w.bs, 0.0)
+    assert plan.launches == 1
+    plan.execute()
+    # 2. the bucket launches of the tile kernel
+    monkeypatch.setenv("LRB_PTR_BUCKETS", "1")
+    plan_b = ctx.ptr_plan("C", "N", "N", w.bs, w.rs, w.bs, pa, w.bs, pb, w.bs, pcs[1], w.bs, 0.0)
+    monkeypatch.delenv("LRB_PTR_BUCKETS")
+    assert plan_b.launches > 1
+    plan_b.execute()
+    # 3. device descriptors
+    d = {k: ctx.to_device(np.asarray(v, dtype=np.int64)) for k, v in
+         dict(m=w.bs, n=w.rs, A=pa, B=pb, C=pcs[2]).items()}
+    ctx.dgemm_ptr_batched_device("C", "N", "N", w.batch, d["m"], d["n"], d["m"], d["A"], d["m"],
+                                 d["B"], d["m"], d["C"], d["m"], 0.0, None, None)
+    ctx.synchronize()
+    # compare in 64 MiB pieces (the gaps between items are padding: NaN in all three)
+    step = 8 << 20
+    total = nc // 8
+    for lo in range(0, total, step):
+        n = min(step, total - lo)
+        ref = outs[0].download(n, offset_bytes=8 * lo)
+        for which, out in (("bucket kernels", outs[1]), ("device descriptors", outs[2])):
+            got = out.download(n, offset_bytes=8 * lo)
+            assert np.array_equal(ref, got, equal_nan=True), f"{which}: doubles {lo}..{lo + n}"
+    # and no result entry is left NaN
+    for i in (0, 1, w.batch // 2, w.batch - 1):
+        got = outs[0].download(w.bs[i] * w.rs[i], offset_bytes=offs[i][2])
+        assert np.isfinite(got).all()
+
+
 def test_pointer_array_mixed_ragged_full(ctx):
     # every item checked: mixed variants, odd shapes, transposes, beta = 1
     rng = np.random.default_rng(21)
