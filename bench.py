@@ -225,6 +225,14 @@ def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("LRB_BENCH_SHARE_GPU") == "1":
+        # functional test of the multi-rank path on fewer GPUs than ranks: the
+        # ranks share devices (they never wait on one another's kernels: the
+        # only collectives are host-side). The numbers are NOT a measurement;
+        # the line is tagged.
+        local = local % max(1, visible_gpus())
+        print("bench.py: LRB_BENCH_SHARE_GPU=1, ranks share GPUs: a functional test, not a "
+              "measurement", file=sys.stderr)
     pg = None
     if world > 1:
         import torch.distributed as dist
@@ -714,6 +722,8 @@ def run_gpu_arm_variable(args, w, world, rank, local, pg, spans, scaling):
             "step_ms": stats, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clocks, "gpu_launches": int(launches),
         }
+        if os.environ.get("LRB_BENCH_SHARE_GPU") == "1":
+            line["shared_gpu_test"] = True
         print(json.dumps(line), flush=True)
     ctx.close()
 
@@ -843,6 +853,8 @@ def run_gpu_arm(args, w, world, rank, local, pg):
             "roofline": roof,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches),
         }
+        if os.environ.get("LRB_BENCH_SHARE_GPU") == "1":
+            line["shared_gpu_test"] = True
         print(json.dumps(line), flush=True)
     ctx.close()
 
