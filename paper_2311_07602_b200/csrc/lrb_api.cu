@@ -275,7 +275,7 @@ int auto_variant(int64_t m, int64_t n, int64_t k_hint, int64_t batch, int sm_cou
 // step through the strided path instead of the two-source BlrRowProblem
 int debug_flags() {
   const char* s = std::getenv("LRB_DEBUG_FLAGS");
-  return s ? (std::atoi(s) & 1022) : 0;
+  return s ? (std::atoi(s) & 4094) : 0;
 }
 
 int env_variant() {

@@ -58,15 +58,19 @@ template <int MBT>
 using FCfgT = GemmCfg<1, 4, MBT, 16, 32, 4, 2, false, false, true>;
 constexpr int kFStages = 4;
 constexpr int kFWarps = 4;
-constexpr int kFThreads = kFWarps * 32 + 32;  // + the producer warp
+constexpr int kFThreads = kFWarps * 32 + 64;  // + the producer warp + the coupling warp
 constexpr int kFNB = 64, kFKB = 32;
 constexpr int kMaxRank = 16;                   // X tiles of one W tile: 64 / r items of r x r
 constexpr int kXs = kFNB * kMaxRank;
+// the W tile in shared memory: 64 rows of W, pitch MB + 4 doubles (the coupling
+// warp's B fragments, lanes (g, tq) at tq * pitch + g, are conflict-free)
+template <int MBT>
+constexpr int w_pitch() { return MBT + kPad; }
 template <int MBT>
 constexpr size_t fused_smem() {
-  // ring, the W^T tile (nrhs x 64), X staging, barriers + slot table
-  return size_t(kFStages) * FCfgT<MBT>::STAGE_ELEMS * 8 + size_t(MBT * kFNB) * 8 +
-         size_t(kXs) * 8 + size_t(kFStages) * 8 * 3 + 16;
+  // ring, the W tile (64 x nrhs), X staging, barriers + slot table + tile id
+  return size_t(kFStages) * FCfgT<MBT>::STAGE_ELEMS * 8 + size_t(w_pitch<MBT>() * kFNB) * 8 +
+         size_t(kXs) * 8 + size_t(kFStages) * 8 * 3 + 48;
 }
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
@@ -83,7 +87,8 @@ __global__ void __launch_bounds__(kFThreads, 2)
     blr_fused_kernel(const __grid_constant__ BlrFusedProblem p) {
   using FCfg = FCfgT<MBT>;
   static_assert(FCfg::STAGES == kFStages && FCfg::NB == kFNB && FCfg::KB == kFKB, "ring geometry");
-  constexpr int kScratch = FCfg::MB * FCfg::NB;
+  constexpr int WP = w_pitch<MBT>();
+  constexpr int kScratch = WP * FCfg::NB;
   pdl_entry();
   constexpr int KB = FCfg::KB, NB = FCfg::NB, MB = FCfg::MB;
   extern __shared__ __align__(1024) double smem[];
@@ -92,10 +97,13 @@ __global__ void __launch_bounds__(kFThreads, 2)
   uint64_t* full = reinterpret_cast<uint64_t*>(xs + kXs);
   uint64_t* empty = full + kFStages;
   volatile long long* slot = reinterpret_cast<volatile long long*>(empty + kFStages);
-  // X staging: xfull (producer's bulk copy landed), xfree (the computing
-  // warps are done with the previous W tile's X)
+  // W tile hand-over to the coupling warp: xfull (the producer's bulk copy
+  // of the tile's X_ij landed), wfull (the computing warps have written the
+  // W tile and its ticket), cfree (the coupling warp is done with both)
   uint64_t* xfull = reinterpret_cast<uint64_t*>(const_cast<long long*>(slot + kFStages));
-  uint64_t* xfree = xfull + 1;
+  uint64_t* wfull = xfull + 1;
+  uint64_t* cfree = xfull + 2;
+  volatile long long* ctile = reinterpret_cast<volatile long long*>(xfull + 3);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kFStages; ++s) {
@@ -103,7 +111,8 @@ __global__ void __launch_bounds__(kFThreads, 2)
       mbar_init(&empty[s], kFWarps);
     }
     mbar_init(xfull, 1);
-    mbar_init(xfree, 1);
+    mbar_init(wfull, kFWarps * 32);
+    mbar_init(cfree, 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -114,9 +123,16 @@ __global__ void __launch_bounds__(kFThreads, 2)
       uint32_t phase = 0;
       long long q = 0;
       long long nwt = 0;  // W tiles issued (X staging parity)
-      const uint32_t bytes = uint32_t(FCfg::A_BOX + FCfg::B_BOX) * 8u;
+      // (bits 8 / 9: streaming probes, wrong results — no rhs / Z operand
+      // loads; big-operand boxes without the 4-element pad)
+      const bool no_a = (p.flags & 256) != 0;
+      const uint32_t b_box = (p.flags & 512) ? uint32_t(KB * NB) : uint32_t(FCfg::B_BOX);
+      const uint32_t bytes = (uint32_t(no_a ? 0 : FCfg::A_BOX) + b_box) * 8u;
       const uint64_t pol_stream = policy_evict_normal(), pol_keep = policy_evict_last();
-      long long t = static_cast<long long>(atomicAdd(p.next, 1ull));
+      // (bits 10 / 11: phase probes, wrong results — W tiles only / row tiles only)
+      const long long t_off = (p.flags & 2048) ? p.nw : 0;
+      const long long t_end = (p.flags & 1024) ? p.nw : p.total;
+      long long t = static_cast<long long>(atomicAdd(p.next, 1ull)) + t_off;
       // (bit 3: probe, claim the next tile while this one's first chunk is in
       // flight; measured slower: a CTA busy on a long row tile then holds a
       // ticket other CTAs could start)
@@ -124,7 +140,7 @@ __global__ void __launch_bounds__(kFThreads, 2)
 #pragma unroll 1
       while (true) {
         if (q >= kFStages) mbar_wait(&empty[stage], phase ^ 1);
-        if (t >= p.total) {
+        if (t >= t_end) {
           slot[stage] = -1;
           mbar_arrive(&full[stage]);
           break;
@@ -162,7 +178,7 @@ __global__ void __launch_bounds__(kFThreads, 2)
           double* As = smem + size_t(stage) * FCfg::STAGE_ELEMS;
           double* Bs = As + FCfg::A_ELEMS;
           mbar_arrive_expect_tx(&full[stage], bytes);
-          tma_load_3d(As, mapA, 0, ka, z, &full[stage], pol_keep);
+          if (!no_a) tma_load_3d(As, mapA, 0, ka, z, &full[stage], pol_keep);
           if (wtile)
             tma_load_3d(Bs, &p.tmVt, k0, n0, z, &full[stage], pol_stream);
           else
@@ -172,14 +188,14 @@ __global__ void __launch_bounds__(kFThreads, 2)
             stage = 0;
             phase ^= 1;
           }
-          if (k0 == 0 && ahead) t_next = static_cast<long long>(atomicAdd(p.next, 1ull));
+          if (k0 == 0 && ahead) t_next = static_cast<long long>(atomicAdd(p.next, 1ull)) + t_off;
         }
         if (wtile) {
           // the tile's X_ij (items ip0 .. of column j are consecutive in
           // (j, i) order: one contiguous bulk copy), issued after the tile's
-          // chunks: by now the computing warps have finished the previous W
-          // tile's coupling and released xs
-          if (nwt > 0) mbar_wait(xfree, uint32_t((nwt - 1) & 1));
+          // chunks: by now the coupling warp has finished the previous W
+          // tile and released xs
+          if (nwt > 0) mbar_wait(cfree, uint32_t((nwt - 1) & 1));
           const int items = min(NB, p.K - n0) / p.r;
           const uint32_t xb = uint32_t(items) * p.r * p.r * 8u;
           mbar_arrive_expect_tx(xfull, xb);
@@ -187,7 +203,7 @@ __global__ void __launch_bounds__(kFThreads, 2)
                    pol_stream);
           ++nwt;
         }
-        t = ahead ? t_next : static_cast<long long>(atomicAdd(p.next, 1ull));
+        t = ahead ? t_next : static_cast<long long>(atomicAdd(p.next, 1ull)) + t_off;
       }
       // the last CTA out resets the tickets and ready counts
       __threadfence();
@@ -202,15 +218,117 @@ __global__ void __launch_bounds__(kFThreads, 2)
     return;
   }
 
-  const int wi = 0, wj = warp, g = lane >> 2, tq = lane & 3;
+  const int g = lane >> 2, tq = lane & 3;
+  if (warp == kFWarps + 1) {
+    // The coupling warp: Z_ij = X_ij W_ij for the items of each W tile this
+    // CTA computes, off the computing warps' path (they go straight on to the
+    // next tile's chunks). Z goes into row i's operand block, then row i's
+    // ready count is bumped (release).
+    long long nwc = 0;  // W tiles handled (barrier parity)
+#pragma unroll 1
+    while (true) {
+      mbar_wait(wfull, uint32_t(nwc & 1));
+      const long long t = *ctile;
+      if (t < 0) break;
+      const bool colmajor = (p.flags & 64) == 0;
+      const int jcol = int(colmajor ? t / p.tw : t % p.T);
+      const int n0 = int(colmajor ? t % p.tw : t / p.T) * NB;
+      const int r = p.r, nrhs = p.nrhs;
+      const int items = min(NB, p.K - n0) / r;
+      const int ip0 = n0 / r;
+      mbar_wait(xfull, uint32_t(nwc & 1));  // this tile's X_ij landed
+      ++nwc;
+      if (p.flags & 16) {
+        // (bit 4: probe, no coupling)
+      } else if (r % 8 == 0) {
+        // DMMA: 8x8 output blocks, k ascending in steps of 4 (each entry one
+        // in-order FMA chain). W columns nrhs..MB-1 are zero (TMA fills the
+        // rhs box past its extent) and are not stored.
+        for (int it = 0; it < items; ++it) {
+          const int ip = ip0 + it;
+          const int i = ip < jcol ? ip : ip + 1;
+          const int jp = jcol < i ? jcol : jcol - 1;
+          double* zrow = p.rz + (int64_t(i) * p.P + p.b + int64_t(jp) * r) * nrhs;
+          constexpr int CN = MB / 8;
+          double d[2][CN][2];
+#pragma unroll
+          for (int pi = 0; pi < 2; ++pi)
+#pragma unroll
+            for (int ci = 0; ci < CN; ++ci) d[pi][ci][0] = d[pi][ci][1] = 0.0;
+          const double* xi = xs + it * r * r;
+          const double* wt = scratch + it * r * WP;
+          const bool two = r > 8;  // r in {8, 16}
+#pragma unroll 1
+          for (int k0 = 0; k0 < r; k0 += 4) {
+            double a[2], bv[CN];
+            a[0] = xi[g * r + k0 + tq];
+            a[1] = two ? xi[(8 + g) * r + k0 + tq] : 0.0;
+#pragma unroll
+            for (int ci = 0; ci < CN; ++ci) bv[ci] = wt[(k0 + tq) * WP + ci * 8 + g];
+#pragma unroll
+            for (int ci = 0; ci < CN; ++ci) {
+              dmma_8x8x4(d[0][ci][0], d[0][ci][1], a[0], bv[ci]);
+              if (two) dmma_8x8x4(d[1][ci][0], d[1][ci][1], a[1], bv[ci]);
+            }
+          }
+#pragma unroll
+          for (int pi = 0; pi < 2; ++pi) {
+            if (pi == 1 && !two) break;
+#pragma unroll
+            for (int ci = 0; ci < CN; ++ci) {
+              const int c = ci * 8 + 2 * tq;
+              double* zp = zrow + int64_t(pi * 8 + g) * nrhs + c;
+              if (c + 1 < nrhs)
+                *reinterpret_cast<double2*>(zp) = make_double2(d[pi][ci][0], d[pi][ci][1]);
+              else if (c < nrhs)
+                *zp = d[pi][ci][0];
+            }
+          }
+        }
+      } else {
+        // scalar chains (r = 4): one Z entry per lane and round, k ascending
+        const int per = r * nrhs, total = items * per;
+        for (int e = lane; e < total; e += 32) {
+          const int it = e / per, rem = e - it * per;
+          const int pr = rem / nrhs, cc = rem - pr * nrhs;
+          const double* xr = xs + (it * r + pr) * r;
+          const double* wc = scratch + it * r * WP + cc;
+          double zacc = 0.0;
+          for (int k = 0; k < r; ++k) zacc = fma(xr[k], wc[k * WP], zacc);
+          const int ip = ip0 + it;  // row index i' of column j's stack
+          const int i = ip < jcol ? ip : ip + 1;
+          const int jp = jcol < i ? jcol : jcol - 1;
+          p.rz[(int64_t(i) * p.P + p.b + int64_t(jp) * r + pr) * nrhs + cc] = zacc;
+        }
+      }
+      // release: the warp barrier orders every lane's Z stores before the
+      // counting lanes' fences (cumulativity), so only those lanes fence
+      __syncwarp();
+      if (lane == 0) mbar_arrive(cfree);  // xs and the W tile may be refilled
+      if (lane < items) {
+        const int ip = ip0 + lane;
+        const int i = ip < jcol ? ip : ip + 1;
+        __threadfence();
+        atomicAdd(&p.ready[i], 1u);
+      }
+    }
+    return;
+  }
+
+  const int wi = 0, wj = warp;
   int stage = 0;
   uint32_t phase = 0;
-  long long nwc = 0;  // W tiles consumed (X staging parity)
+  long long nwm = 0;  // W tiles handed to the coupling warp (barrier parity)
 #pragma unroll 1
   while (true) {
     mbar_wait(&full[stage], phase);
     const long long t = slot[stage];
-    if (t < 0) break;
+    if (t < 0) {  // tell the coupling warp too
+      if (nwm > 0) mbar_wait(cfree, uint32_t((nwm - 1) & 1));
+      if (threadIdx.x == 0) *ctile = -1;
+      mbar_arrive(wfull);
+      break;
+    }
     const bool wtile = t < p.nw;
     const long long u = wtile ? t : t - p.nw;
     const bool colmajor = (p.flags & 64) == 0;
@@ -228,8 +346,10 @@ __global__ void __launch_bounds__(kFThreads, 2)
       const double* As = smem + size_t(stage) * FCfg::STAGE_ELEMS;
       const double* Bs = As + FCfg::A_ELEMS;
       // a partial last chunk is zero-filled by TMA: +0 terms leave the chains exact
+      if (!(p.flags & 128)) {  // (bit 7: probe, no products)
 #pragma unroll
-      for (int kq = 0; kq < KB / 4; ++kq) mma_kstep<FCfg>(acc, As, Bs, wi, wj, g, kq * 4 + tq);
+        for (int kq = 0; kq < KB / 4; ++kq) mma_kstep<FCfg>(acc, As, Bs, wi, wj, g, kq * 4 + tq);
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
       if (++stage == kFStages) {
@@ -258,95 +378,26 @@ __global__ void __launch_bounds__(kFThreads, 2)
       }
       continue;
     }
-    // W tile: W^T (nrhs x 64) into the scratch as W rows (col-major C^T:
-    // scratch[j * MB + c] = W(n0 + j, c)), then the coupling of its items
-    named_barrier_sync(1, kFWarps * 32);  // the previous tile's coupling is done
+    // W tile: W rows into shared memory (scratch[j * WP + c] = W(n0 + j, c))
+    // with the ticket, handed to the coupling warp; the computing warps go on
+    if (nwm > 0) mbar_wait(cfree, uint32_t((nwm - 1) & 1));  // the previous W tile is consumed
+    ++nwm;
 #pragma unroll
     for (int fj = 0; fj < FCfg::FJ; ++fj) {
       const int j = FCfg::load_col(wj, fj, g);
       const int c0 = FCfg::acc_row(wi, 0, 0, tq);
       if constexpr (FCfg::FI == 2) {
-        scratch[j * MB + c0 + 0] = acc[fj][0][0];
-        scratch[j * MB + c0 + 1] = acc[fj][1][0];
-        scratch[j * MB + c0 + 2] = acc[fj][0][1];
-        scratch[j * MB + c0 + 3] = acc[fj][1][1];
+        scratch[j * WP + c0 + 0] = acc[fj][0][0];
+        scratch[j * WP + c0 + 1] = acc[fj][1][0];
+        scratch[j * WP + c0 + 2] = acc[fj][0][1];
+        scratch[j * WP + c0 + 3] = acc[fj][1][1];
       } else {
-        scratch[j * MB + c0 + 0] = acc[fj][0][0];
-        scratch[j * MB + c0 + 1] = acc[fj][0][1];
+        scratch[j * WP + c0 + 0] = acc[fj][0][0];
+        scratch[j * WP + c0 + 1] = acc[fj][0][1];
       }
     }
-    named_barrier_sync(1, kFWarps * 32);
-    const int jcol = z, r = p.r, nrhs = p.nrhs;
-    const int items = min(NB, p.K - n0) / r;
-    const int ip0 = n0 / r;
-    const int per = r * nrhs, total = items * per;
-    mbar_wait(xfull, uint32_t(nwc & 1));  // this tile's X_ij landed
-    ++nwc;
-    if (!(p.flags & 16) && r % 8 == 0 && nrhs % 8 == 0) {
-      // Z_ij = X_ij W_ij on DMMA: item it on warp it % 4, 8x8 output blocks,
-      // k ascending in steps of 4 (each entry one in-order FMA chain)
-      for (int it = warp; it < items; it += kFWarps) {
-        const int ip = ip0 + it;
-        const int i = ip < jcol ? ip : ip + 1;
-        const int jp = jcol < i ? jcol : jcol - 1;
-        double* zrow = p.rz + (int64_t(i) * p.P + p.b + int64_t(jp) * r) * nrhs;
-        for (int p0 = 0; p0 < r; p0 += 8)
-          for (int c0 = 0; c0 < nrhs; c0 += 8) {
-            double d0 = 0.0, d1 = 0.0;
-            for (int k0 = 0; k0 < r; k0 += 4) {
-              const double a = xs[(it * r + p0 + g) * r + k0 + tq];
-              const double bv = scratch[(it * r + k0 + tq) * MB + c0 + g];
-              dmma_8x8x4(d0, d1, a, bv);
-            }
-            *reinterpret_cast<double2*>(zrow + int64_t(p0 + g) * nrhs + c0 + 2 * tq) =
-                make_double2(d0, d1);
-          }
-      }
-    } else {
-      // scalar: every thread keeps up to 8 independent Z chains (k
-      // ascending), X from xs and W from the scratch, both in shared memory
-      constexpr int U = (FCfg::NB * FCfg::MB) / (kFWarps * 32);
-      int xo[U], wo[U];
-      double zacc[U];
-#pragma unroll
-      for (int q = 0; q < U; ++q) {
-        const int e = threadIdx.x + q * kFWarps * 32;
-        const int it = e / per, rem = e - it * per;
-        const int pr = rem / nrhs, cc = rem - pr * nrhs;
-        xo[q] = (it * r + pr) * r;
-        wo[q] = (it * r) * MB + cc;
-        zacc[q] = 0.0;
-      }
-#pragma unroll 1
-      for (int k = 0; k < ((p.flags & 16) ? 0 : r); ++k) {  // (bit 4: probe, no coupling)
-#pragma unroll
-        for (int q = 0; q < U; ++q)
-          if (threadIdx.x + q * kFWarps * 32 < total)
-            zacc[q] = fma(xs[xo[q] + k], scratch[wo[q] + k * MB], zacc[q]);
-      }
-#pragma unroll
-      for (int q = 0; q < U; ++q) {
-        const int e = threadIdx.x + q * kFWarps * 32;
-        if (e >= total) continue;
-        const int it = e / per, rem = e - it * per;
-        const int pr = rem / nrhs, cc = rem - pr * nrhs;
-        const int ip = ip0 + it;  // row index i' of column j's stack
-        const int i = ip < jcol ? ip : ip + 1;
-        const int jp = jcol < i ? jcol : jcol - 1;
-        p.rz[(int64_t(i) * p.P + p.b + int64_t(jp) * r + pr) * nrhs + cc] = zacc[q];
-      }
-    }
-    // release: the barrier orders every warp's Z stores before the counting
-    // threads' fence (cumulativity), so only those few threads fence (a
-    // fence in every thread cost ~3 % of the launch)
-    named_barrier_sync(1, kFWarps * 32);
-    if (threadIdx.x == 0) mbar_arrive(xfree);  // xs and the scratch may be refilled
-    if (threadIdx.x < items) {
-      const int ip = ip0 + threadIdx.x;
-      const int i = ip < jcol ? ip : ip + 1;
-      __threadfence();
-      atomicAdd(&p.ready[i], 1u);
-    }
+    if (threadIdx.x == 0) *ctile = u;
+    mbar_arrive(wfull);
   }
 }
 
@@ -369,12 +420,13 @@ bool launch_blr_fused_t(lrb_ctx* ctx, const double* rhs, int64_t nrhs, double* y
   const int64_t K = (T - 1) * r;
   BlrFusedProblem p;
   std::memset(&p, 0, sizeof(p));
+  const int bpad = (debug_flags() & 512) ? 0 : kPad;
   const bool ok =
       encode_operand(&p.tmRhs, rhs, nrhs, b, nrhs, b * nrhs, T, FCfg::MB + kPad, FCfg::KB) &&
-      encode_operand(&p.tmVt, vtcol, b, K, b, K * b, T, FCfg::KB + kPad, FCfg::NB) &&
+      encode_operand(&p.tmVt, vtcol, b, K, b, K * b, T, FCfg::KB + bpad, FCfg::NB) &&
       encode_operand(&p.tmZ, rz + b * nrhs, nrhs, K, nrhs, P * nrhs, T, FCfg::MB + kPad,
                      FCfg::KB) &&
-      encode_operand(&p.tmDcat, dcat, P, b, P, b * P, T, FCfg::KB + kPad, FCfg::NB);
+      encode_operand(&p.tmDcat, dcat, P, b, P, b * P, T, FCfg::KB + bpad, FCfg::NB);
   if (!ok) return false;
   p.x = x;
   p.rz = rz;
