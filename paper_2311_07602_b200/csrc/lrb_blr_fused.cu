@@ -188,7 +188,8 @@ __global__ void __launch_bounds__(kFThreads, 2)
             stage = 0;
             phase ^= 1;
           }
-          if (k0 == 0 && ahead) t_next = static_cast<long long>(atomicAdd(p.next, 1ull)) + t_off;
+          if (k0 == 0 && ahead && wtile)
+            t_next = static_cast<long long>(atomicAdd(p.next, 1ull)) + t_off;
         }
         if (wtile) {
           // the tile's X_ij (items ip0 .. of column j are consecutive in
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(kFThreads, 2)
                    pol_stream);
           ++nwt;
         }
-        t = ahead ? t_next : static_cast<long long>(atomicAdd(p.next, 1ull)) + t_off;
+        t = (ahead && wtile) ? t_next : static_cast<long long>(atomicAdd(p.next, 1ull)) + t_off;
       }
       // the last CTA out resets the tickets and ready counts
       __threadfence();
@@ -258,17 +259,24 @@ __global__ void __launch_bounds__(kFThreads, 2)
           const double* xi = xs + it * r * r;
           const double* wt = scratch + it * r * WP;
           const bool two = r > 8;  // r in {8, 16}
-#pragma unroll 1
-          for (int k0 = 0; k0 < r; k0 += 4) {
-            double a[2], bv[CN];
-            a[0] = xi[g * r + k0 + tq];
-            a[1] = two ? xi[(8 + g) * r + k0 + tq] : 0.0;
+          // all fragment loads of the item first, then the chains
+          double a[2][4], bv[CN][4];
 #pragma unroll
-            for (int ci = 0; ci < CN; ++ci) bv[ci] = wt[(k0 + tq) * WP + ci * 8 + g];
+          for (int kq = 0; kq < 4; ++kq) {
+            const int k = min(kq * 4 + tq, r - 1);  // (r = 8: steps 2, 3 are not used)
+            a[0][kq] = xi[g * r + k];
+            a[1][kq] = two ? xi[(8 + g) * r + k] : 0.0;
 #pragma unroll
-            for (int ci = 0; ci < CN; ++ci) {
-              dmma_8x8x4(d[0][ci][0], d[0][ci][1], a[0], bv[ci]);
-              if (two) dmma_8x8x4(d[1][ci][0], d[1][ci][1], a[1], bv[ci]);
+            for (int ci = 0; ci < CN; ++ci) bv[ci][kq] = wt[k * WP + ci * 8 + g];
+          }
+#pragma unroll
+          for (int kq = 0; kq < 4; ++kq) {
+            if (kq * 4 < r) {
+#pragma unroll
+              for (int ci = 0; ci < CN; ++ci) {
+                dmma_8x8x4(d[0][ci][0], d[0][ci][1], a[0][kq], bv[ci][kq]);
+                if (two) dmma_8x8x4(d[1][ci][0], d[1][ci][1], a[1][kq], bv[ci][kq]);
+              }
             }
           }
 #pragma unroll
