@@ -48,8 +48,10 @@ struct lrb_blr {
   double* d_rz = nullptr;     // per row i: pitch x nrhs, [rhs_i; Z_i0; Z_i1; ...]
   cudaEvent_t ws_ev = nullptr;
   bool ws_pending = false;
-  // the fused matvec's self-resetting sync words: [T] ready counts, then two
-  // 64-bit ticket words (allocated and zeroed at create)
+  // the fused matvec's sync words: [T][4] ready counts (row i, quarter of its
+  // Z columns; they only ever grow, a launch waits for epoch + 1 times the
+  // quarter's size), then three 64-bit words: tickets, finished CTAs (both
+  // reset by the last CTA out) and the epoch (allocated and zeroed at create)
   unsigned* d_sync = nullptr;
   std::vector<void*> retired;
   std::vector<lrb_ptr_plan*> retired_plans;
@@ -477,7 +479,7 @@ extern "C" lrb_status lrb_blr_create(lrb_ctx* ctx, int64_t n, int64_t block, int
     }
   cudaError_t e = upload(&m->d_dcat, dcat);
   if (e == cudaSuccess && T > 1) {
-    const size_t sync_bytes = (size_t(T) * 4 + 15) / 16 * 16 + 16;
+    const size_t sync_bytes = size_t(T) * 16 + 32;
     e = cudaMalloc(&m->d_sync, sync_bytes);
     if (e == cudaSuccess) e = cudaMemset(m->d_sync, 0, sync_bytes);
   }
@@ -550,7 +552,7 @@ lrb_status matvec_steps(lrb_ctx* ctx, lrb_blr* m, const double* rhs, int64_t nrh
   if (!(fe && fe[0] == '0') && !(lrb::debug_flags() & 512) && m->d_sync) {
     unsigned* ready = m->d_sync;
     auto* next = reinterpret_cast<unsigned long long*>(
-        reinterpret_cast<char*>(m->d_sync) + (size_t(T) * 4 + 15) / 16 * 16);
+        reinterpret_cast<char*>(m->d_sync) + size_t(T) * 16);
     if (lrb::launch_blr_fused(ctx, rhs, nrhs, y, T, b, r, P, m->d_vtcol, m->d_x, m->d_dcat,
                               m->d_rz, ready, next, s, &st))
       return st;

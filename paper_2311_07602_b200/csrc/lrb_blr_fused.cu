@@ -18,9 +18,10 @@
 // tiles already claimed by running CTAs: progress is guaranteed. Every entry
 // keeps the reference's chain order (W and Z chains over their k ascending;
 // y_i's chain over D's columns, then j-major, p), so results are bitwise the
-// three-launch path and the FMA-chain oracle. Tickets and ready counts reset
-// themselves at the end of the launch (last CTA out), so graph replays need
-// no memset.
+// three-launch path and the FMA-chain oracle. The last CTA out resets the
+// tickets and bumps an epoch word; the ready counts only ever grow (a launch
+// waits for epoch + 1 times the expected count), so graph replays need no
+// memset and a launch ends without a tail of reset stores.
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -41,8 +42,9 @@ struct BlrFusedProblem {
   int T, b, r, nrhs, K, P;
   int tw, tr;          // 64-row blocks per W column, 64-column blocks per row
   long long nw, total;  // W tiles, all tiles
-  unsigned* ready;     // [T] Z items landed per row
-  unsigned long long* next;  // [0] tickets, [1] finished CTAs
+  unsigned* ready;     // [T][4] Z items landed per row and quarter of its T - 1 columns
+  int gs;              // columns per quarter: ceil((T - 1) / 4)
+  unsigned long long* next;  // [0] tickets, [1] finished CTAs, [2] epoch (completed launches)
   int flags;           // debug probe bits (LRB_DEBUG_FLAGS)
 };
 
@@ -123,11 +125,9 @@ __global__ void __launch_bounds__(kFThreads, 2)
       uint32_t phase = 0;
       long long q = 0;
       long long nwt = 0;  // W tiles issued (X staging parity)
-      // (bits 8 / 9: streaming probes, wrong results — no rhs / Z operand
-      // loads; big-operand boxes without the 4-element pad)
+      // (bit 8: streaming probe, wrong results — no rhs / Z operand loads)
       const bool no_a = (p.flags & 256) != 0;
-      const uint32_t b_box = (p.flags & 512) ? uint32_t(KB * NB) : uint32_t(FCfg::B_BOX);
-      const uint32_t bytes = (uint32_t(no_a ? 0 : FCfg::A_BOX) + b_box) * 8u;
+      const uint32_t bytes = (uint32_t(no_a ? 0 : FCfg::A_BOX) + uint32_t(FCfg::B_BOX)) * 8u;
       const uint64_t pol_stream = policy_evict_normal(), pol_keep = policy_evict_last();
       // (bits 10 / 11: phase probes, wrong results — W tiles only / row tiles only)
       const long long t_off = (p.flags & 2048) ? p.nw : 0;
@@ -137,6 +137,9 @@ __global__ void __launch_bounds__(kFThreads, 2)
       // flight; measured slower: a CTA busy on a long row tile then holds a
       // ticket other CTAs could start)
       const bool ahead = (p.flags & 8) != 0;
+      const unsigned long long epoch = p.next[2];  // launches completed on these sync words
+      // (bit 1: probe, wait for every quarter of Z_i* before the first Z chunk)
+      const bool all_first = (p.flags & 2) != 0;
 #pragma unroll 1
       while (true) {
         if (q >= kFStages) mbar_wait(&empty[stage], phase ^ 1);
@@ -156,7 +159,8 @@ __global__ void __launch_bounds__(kFThreads, 2)
         const int z = int(wtile ? (colmajor ? u / p.tw : u % p.T) : u / p.tr);  // column j / row i
         const int n0 = int(wtile ? (colmajor ? u % p.tw : u / p.T) : u % p.tr) * NB;
         const int kend = wtile ? p.b : p.P;
-        bool waited = false;
+        int grp = 0;  // quarters of row z's Z columns known to have landed
+        int zk = p.b;  // first k of quarter grp's Z rows
         long long t_next = -1;
 #pragma unroll 1
         for (int k0 = 0; k0 < kend; k0 += KB) {
@@ -164,11 +168,22 @@ __global__ void __launch_bounds__(kFThreads, 2)
           const void* mapA = &p.tmRhs;
           int ka = k0;
           if (!wtile && k0 >= p.b) {
-            if (!waited) {  // Z_i* lands from the W tiles' coupling
-              while (!(p.flags & 32) && ld_acquire_u32(&p.ready[z]) < unsigned(p.T - 1))
-                __nanosleep(64);  // (bit 5: probe, no wait: wrong results)
+            // Z_i* lands from the W tiles' coupling, column j ascending like
+            // the tickets: wait (acquire) only for the quarters of columns
+            // this chunk reaches, so a row tile starts its Z part while the
+            // last columns' W tiles are still running
+            if (grp < 4 && (all_first || k0 + KB > zk)) {
+              do {
+                const unsigned want =
+                    (unsigned(epoch) + 1u) * unsigned(min(p.gs, p.T - 1 - grp * p.gs));
+                while (!(p.flags & 32) &&
+                       int(ld_acquire_u32(&p.ready[z * 4 + grp]) - want) < 0)
+                  __nanosleep(64);  // (bit 5: probe, no wait: wrong results)
+                ++grp;
+                zk += p.gs * p.r;  // first k of the next quarter's Z rows
+              } while (grp < 4 && (all_first || k0 + KB > zk) && zk < kend);
+              if (zk >= kend) grp = 4;
               fence_proxy_async_global();
-              waited = true;
             }
             mapA = &p.tmZ;
             ka = k0 - p.b;
@@ -206,13 +221,14 @@ __global__ void __launch_bounds__(kFThreads, 2)
         }
         t = (ahead && wtile) ? t_next : static_cast<long long>(atomicAdd(p.next, 1ull)) + t_off;
       }
-      // the last CTA out resets the tickets and ready counts
+      // the last CTA out resets the tickets and opens the next epoch (the
+      // ready counts are never reset: no tail of stores at the end of a launch)
       __threadfence();
       const unsigned long long done = atomicAdd(p.next + 1, 1ull);
       if (done == gridDim.x - 1) {
-        for (int i = 0; i < p.T; ++i) p.ready[i] = 0;
         p.next[0] = 0;
         p.next[1] = 0;
+        p.next[2] = epoch + 1;
         __threadfence();
       }
     }
@@ -316,8 +332,9 @@ __global__ void __launch_bounds__(kFThreads, 2)
       if (lane < items) {
         const int ip = ip0 + lane;
         const int i = ip < jcol ? ip : ip + 1;
+        const int jp = jcol < i ? jcol : jcol - 1;
         __threadfence();
-        atomicAdd(&p.ready[i], 1u);
+        atomicAdd(&p.ready[i * 4 + jp / p.gs], 1u);
       }
     }
     return;
@@ -428,13 +445,12 @@ bool launch_blr_fused_t(lrb_ctx* ctx, const double* rhs, int64_t nrhs, double* y
   const int64_t K = (T - 1) * r;
   BlrFusedProblem p;
   std::memset(&p, 0, sizeof(p));
-  const int bpad = (debug_flags() & 512) ? 0 : kPad;
   const bool ok =
       encode_operand(&p.tmRhs, rhs, nrhs, b, nrhs, b * nrhs, T, FCfg::MB + kPad, FCfg::KB) &&
-      encode_operand(&p.tmVt, vtcol, b, K, b, K * b, T, FCfg::KB + bpad, FCfg::NB) &&
+      encode_operand(&p.tmVt, vtcol, b, K, b, K * b, T, FCfg::KB + kPad, FCfg::NB) &&
       encode_operand(&p.tmZ, rz + b * nrhs, nrhs, K, nrhs, P * nrhs, T, FCfg::MB + kPad,
                      FCfg::KB) &&
-      encode_operand(&p.tmDcat, dcat, P, b, P, b * P, T, FCfg::KB + bpad, FCfg::NB);
+      encode_operand(&p.tmDcat, dcat, P, b, P, b * P, T, FCfg::KB + kPad, FCfg::NB);
   if (!ok) return false;
   p.x = x;
   p.rz = rz;
@@ -445,6 +461,7 @@ bool launch_blr_fused_t(lrb_ctx* ctx, const double* rhs, int64_t nrhs, double* y
   p.nw = int64_t(T) * p.tw;
   p.total = p.nw + int64_t(T) * p.tr;
   p.ready = ready;
+  p.gs = int((T - 1 + 3) / 4);
   p.next = next;
   p.flags = debug_flags();
   static int occ_cache[64] = {0};
