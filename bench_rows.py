@@ -268,7 +268,9 @@ def run_blr_gpu(args, w, world, rank, local, pg, B):
     if rank == 0:
         cfg = dict(w.describe())
         cfg.update({"parallelism": f"replicas{world} (one matvec per GPU, no collective)",
-                    "timed_launch": "one CUDA graph of the K steps (event nodes between steps)"})
+                    "timed_launch": "one CUDA graph of the K steps (event nodes between steps)",
+                    "l2": (f"matrix streamed once per step, {w.bytes() / 132644864:.1f}x the L2 "
+                           "(no flush)")})
         print(json.dumps({
             "metric": "batched FP64 GFLOP/s", "value": round(fl_all / (ms_step * 1e-3) / 1e9, 2),
             "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,

@@ -132,7 +132,11 @@ __global__ void __launch_bounds__(kFThreads, 2)
       // (bits 10 / 11: phase probes, wrong results — W tiles only / row tiles only)
       const long long t_off = (p.flags & 2048) ? p.nw : 0;
       const long long t_end = (p.flags & 1024) ? p.nw : p.total;
-      long long t = static_cast<long long>(atomicAdd(p.next, 1ull)) + t_off;
+      // the first ticket is the CTA's own index: 296 CTAs claiming from one
+      // word at launch would queue behind each other at the L2 (same-address
+      // atomics serialise); the ticket word then counts from gridDim.x
+      const long long t_dyn = t_off + gridDim.x;
+      long long t = t_off + blockIdx.x;
       // (bit 3: probe, claim the next tile while this one's first chunk is in
       // flight; measured slower: a CTA busy on a long row tile then holds a
       // ticket other CTAs could start)
@@ -204,7 +208,7 @@ __global__ void __launch_bounds__(kFThreads, 2)
             phase ^= 1;
           }
           if (k0 == 0 && ahead && wtile)
-            t_next = static_cast<long long>(atomicAdd(p.next, 1ull)) + t_off;
+            t_next = static_cast<long long>(atomicAdd(p.next, 1ull)) + t_dyn;
         }
         if (wtile) {
           // the tile's X_ij (items ip0 .. of column j are consecutive in
@@ -219,7 +223,7 @@ __global__ void __launch_bounds__(kFThreads, 2)
                    pol_stream);
           ++nwt;
         }
-        t = (ahead && wtile) ? t_next : static_cast<long long>(atomicAdd(p.next, 1ull)) + t_off;
+        t = (ahead && wtile) ? t_next : static_cast<long long>(atomicAdd(p.next, 1ull)) + t_dyn;
       }
       // the last CTA out resets the tickets and opens the next epoch (the
       // ready counts are never reset: no tail of stores at the end of a launch)

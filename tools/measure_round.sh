@@ -23,12 +23,12 @@ for c in cfg1 cfg2 cfg5; do
   log "bench $c rc=$?"
 done
 
-log "probes"
+log "probes (microbenchmarks only where their binaries were built: nvcc -arch=sm_100a -O3 -lcuda)"
 timeout 600 python tools/probe_varn.py > $O/probe_varn_$R.jsonl 2>> $O/probe_$R.err
 timeout 600 python tools/probe_cold.py > $O/probe_cold_$R.jsonl 2>> $O/probe_$R.err
-timeout 300 ./tools/microbench/fp64_mix > $O/fp64_mix_$R.jsonl 2>> $O/probe_$R.err
-timeout 300 ./tools/microbench/write_bw > $O/write_bw_$R.jsonl 2>> $O/probe_$R.err
-timeout 120 ./tools/microbench/tmap_probe > $O/tmap_probe_$R.txt 2>> $O/probe_$R.err
+[ -x tools/microbench/fp64_mix ] && timeout 300 ./tools/microbench/fp64_mix > $O/fp64_mix_$R.jsonl 2>> $O/probe_$R.err
+[ -x tools/microbench/write_bw ] && timeout 300 ./tools/microbench/write_bw > $O/write_bw_$R.jsonl 2>> $O/probe_$R.err
+[ -x tools/microbench/tmap_probe ] && timeout 120 ./tools/microbench/tmap_probe > $O/tmap_probe_$R.txt 2>> $O/probe_$R.err
 
 log "widened rows, both arms"
 bash tools/bench_rows_all.sh $R
@@ -41,7 +41,7 @@ log "sweep lowrank rc=$?"
 
 log "traffic pass"
 if timeout 900 python tools/profile_all.py > $O/profile_order_plain.log 2>&1; then
-  timeout 1800 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
+  timeout 1800 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,dram__throughput.avg.pct_of_peak_sustained_elapsed,sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active \
     --clock-control none --csv --log-file $O/traffic_$R.csv python tools/profile_all.py \
     > $O/profile_order.log 2>&1
   log "ncu traffic rc=$?"
@@ -75,7 +75,19 @@ if timeout 300 python tools/profile_all.py --only lr_r64_b2048 > /dev/null 2>&1;
     > $O/ncu_lr_r64_$R.log 2>&1
   log "ncu lr_r64 rc=$?"
 fi
-for f in ncu_cfg4_$R ncu_cfg2_$R ncu_lr_r64_$R; do
+if timeout 300 python tools/profile_all.py --only blr_n16384_b256_r16_k16 > /dev/null 2>&1; then
+  timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"blr_fused" \
+    -c 1 -f -o $O/ncu_blr_k16_$R python tools/profile_all.py --only blr_n16384_b256_r16_k16 \
+    > $O/ncu_blr_k16_$R.log 2>&1
+  log "ncu blr k16 rc=$?"
+  # steady-state DRAM bytes of repeated launches (no cache flush between them)
+  timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
+    --clock-control none --cache-control none -k regex:"blr_fused" --csv \
+    --log-file $O/blr_k16_warm_traffic_$R.csv python tools/profile_all.py \
+    --only blr_n16384_b256_r16_k16 --repeat 6 > /dev/null 2>&1
+  log "ncu blr warm traffic rc=$?"
+fi
+for f in ncu_cfg4_$R ncu_cfg2_$R ncu_lr_r64_$R ncu_blr_k16_$R; do
   [ -f $O/$f.ncu-rep ] && python tools/ncu_summary.py rep $O/$f.ncu-rep > $O/$f.json 2>> $O/probe_$R.err
 done
 log "smoke"

@@ -80,9 +80,19 @@ def traffic(csv_path, order_path, out_path):
         e["launches"] += 1
         e["dram_bytes_per_launch"] += d.get("dram__bytes_read.sum", 0) + d.get(
             "dram__bytes_write.sum", 0)
-        e["kernel_s"] += d.get("gpu__time_duration.sum", 0)
+        t = d.get("gpu__time_duration.sum", 0)
+        e["kernel_s"] += t
         e["kernels"].append(d["kernel"])
+        # duration-weighted pipe evidence (present when the pass asked for it)
+        for key, out in (("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram_pct"),
+                         ("sm__pipe_tensor_subpipe_dmma_cycles_active.avg."
+                          "pct_of_peak_sustained_active", "dmma_pct")):
+            if key in d:
+                e[out + "_x_s"] = e.get(out + "_x_s", 0.0) + d[key] * t
     for name, e in res.items():  # a cfg4 "launch" is the plan's whole group set
+        for out in ("dram_pct", "dmma_pct"):
+            if out + "_x_s" in e:
+                e[out] = round(e.pop(out + "_x_s") / e["kernel_s"], 2) if e["kernel_s"] else None
         e["note"] = "ncu serialised, cold-cache replay; bytes summed over the config's launches"
         if name in items:
             e["items"] = items[name]  # items per launch of the capture (bench scales by it)

@@ -65,7 +65,7 @@ def lowrank_one(ctx, name):
     print(f"{name} launches={ctx.launch_count - n0}", flush=True)
 
 
-def blr_one(ctx, name):
+def blr_one(ctx, name, repeat=1):
     import bench_rows as R
     from paper_2311_07602_b200.lrbatch import _check, lib
 
@@ -80,7 +80,8 @@ def blr_one(ctx, name):
     ctx.synchronize()
     print(f"{name}_warm launches={ctx.launch_count - n0}", flush=True)
     n0 = ctx.launch_count
-    run()
+    for _ in range(repeat):  # > 1: back-to-back launches (warm-cache traffic with --cache-control none)
+        run()
     ctx.synchronize()
     print(f"{name} launches={ctx.launch_count - n0}", flush=True)
     m.invalidate()
@@ -91,6 +92,7 @@ def main():
 
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", nargs="*", default=None, help="config / row names (default: all)")
+    ap.add_argument("--repeat", type=int, default=1, help="BLR matvec: launches after the warm-up")
     args = ap.parse_args()
     keep = (lambda n: True) if not args.only else (lambda n: n in args.only)
     ctx = Context(0)
@@ -125,7 +127,7 @@ def main():
     for name in filter(keep, LOWRANK):
         lowrank_one(ctx, name)
     for name in filter(keep, BLR):
-        blr_one(ctx, name)
+        blr_one(ctx, name, args.repeat)
     for name in filter(keep, EXPAND):
         expand_one(ctx, name)
 
