@@ -46,7 +46,8 @@ constexpr int kRWarps = 8;
 constexpr int kRThreads = kRWarps * 32 + 32;  // + the producer warp
 constexpr int kRHalf = 256;                 // output columns per unit
 constexpr int kRBox = 128;                  // Vt box columns (+ kRPad)
-constexpr int kXPad = 4;                    // X rows land at stride r + 4 (one bulk copy per row)
+constexpr int kXPad = 0;                    // X lands unpadded by ONE bulk copy (a copy per padded row
+                                            // was 8-16 tiny TMA ops per unit beside the store stream)
 constexpr int kStageBufs = 4;                  // per warp: two block pairs
 constexpr int kWarpStage = 16 * 32;            // one warp's 16 x 32 output sub-block
 // the operand ring per rank: Vt | U | X per slot; rank 8 units are half the
@@ -76,7 +77,8 @@ struct ReconProblem {
   int T, b;           // BLR: tiles, block (item q = off-diagonal tile in (j, i) order)
   int rblocks, halves;  // per item: 64-row blocks, 256-column halves
   int units;
-  int flags;          // LRB_DEBUG_FLAGS probe bits: 64 = skip the (UX) Vt DMMAs (wrong results)
+  int flags;          // LRB_DEBUG_FLAGS probe bits (wrong results): 64 = skip the (UX) Vt DMMAs,
+                      // 128 = no stores, 256 = no operand loads
 };
 
 // Shared-memory banking (8-byte slots, 16 per 128 B): the Vt and U fragment
@@ -144,6 +146,14 @@ __global__ void __launch_bounds__(kRThreads, 1)
         double* vt = ring + size_t(slot) * L::SLOT;
         double* us = vt + L::VT;
         double* xq = us + L::U;
+        if (p.flags & 256) {  // (bit 8: probe, no operand loads)
+          mbar_arrive(&full[slot]);
+          if (++slot == L::SLOTS) {
+            slot = 0;
+            phase ^= 1;
+          }
+          continue;
+        }
         mbar_arrive_expect_tx(&full[slot], bytes);
         for (int c = 0; c < kRHalf / kRBox; ++c)
           tma_load_3d(vt + c * (kRBox + kRPad) * R, &p.tmVt, half * kRHalf + c * kRBox, 0, q,
@@ -153,9 +163,8 @@ __global__ void __launch_bounds__(kRThreads, 1)
         else
           tma_load_3d(us, &p.tmU, p.b + jp * R, i * p.b + rb * 64, 0, &full[slot], pol);
         const double* xg = p.x + q * p.sx;
-#pragma unroll
-        for (int k = 0; k < R; ++k)
-          bulk_g2s(xq + k * XP, xg + k * R, uint32_t(R * 8), &full[slot], pol);
+        static_assert(kXPad == 0, "one contiguous copy");
+        bulk_g2s(xq, xg, uint32_t(R * R * 8), &full[slot], pol);
         if (++slot == L::SLOTS) {
           slot = 0;
           phase ^= 1;
@@ -271,7 +280,7 @@ __global__ void __launch_bounds__(kRThreads, 1)
             }
       fence_proxy_async_shared_cta();
       __syncwarp();
-      if (lane == 0) {
+      if (lane == 0 && !(p.flags & 128)) {  // (bit 7: probe, no stores)
         const int y0 = (BATCHED ? 0 : i * p.b) + rb * 64 + row0;
         const int z = BATCHED ? q : 0;
 #pragma unroll
