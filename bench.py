@@ -450,9 +450,11 @@ def pick_sample(w, threads, target_s):
 
 def cpu_baseline(w, threads, target_s, what=None):
     items = pick_sample(w, threads, target_s)
+    cpu_sample_run(w, items, threads)  # one untimed pass: threads, pages and clocks warm
     dt, fl, _, kind = cpu_sample_run(w, items, threads)
     d = {"value": round(fl / dt / 1e9, 3), "unit": "GFLOP/s", "cores": threads, "kind": kind,
-         "sample": f"{len(items)} of {w.batch} items of {w.name} ({dt:.1f} s), per-item rate; "
+         "sample": f"{len(items)} of {w.batch} items of {w.name} ({dt:.1f} s, after one untimed "
+                   f"pass), per-item rate; "
                    f"std::thread contiguous split like naive_multiply_batch"}
     d.update(cpu_identity())
     return d
