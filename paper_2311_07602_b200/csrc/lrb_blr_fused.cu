@@ -6,14 +6,19 @@
 // is a single partial wave (T x b/64 tiles on 2 x 148 slots). Here every tile
 // of both GEMMs comes from one ticket sequence on one persistent grid:
 //   * W tiles (column j, 64 rows of the stacked [Vt_ij]_i): W^T = rhs_j^T Vt_j^T
-//     on DMMA, then — with the tile still in shared memory — the coupling
-//     Z_ij = X_ij W_ij of its 64 / r items as r-long FMA chains, Z written
-//     into row i's operand block and row i's ready count bumped (release).
-//     W itself is never stored.
+//     on DMMA by the four computing warps, which leave the tile in shared
+//     memory with its ticket and go straight on to the next tile's chunks. A
+//     sixth warp, the coupling warp, picks it up there: Z_ij = X_ij W_ij of
+//     its 64 / r items (DMMA, k ascending; scalar chains at r = 4), Z written
+//     into row i's operand block, then the ready count of (row i, quarter of
+//     its Z columns) bumped (release). W itself is never stored.
 //   * row tiles (row i, 64 columns of y_i): y_i^T = [rhs_i; Z_i*]^T [D_i|U_i*]^T
 //     over K' = b + (T-1) r in ascending k; the producer streams the D_i part
-//     straight from rhs and, before the first Z chunk, waits until all T-1
-//     items of row i have landed (acquire), then fences the async proxy.
+//     straight from rhs and, before the first Z chunk of each quarter of row
+//     i's T-1 columns, waits until that quarter's items have landed (acquire),
+//     then fences the async proxy. Z columns land in ticket order (j
+//     ascending), so a row tile runs most of its Z part while the last
+//     columns' W tiles are still in flight.
 // W tickets precede row tickets, so a waiting row tile only ever waits on
 // tiles already claimed by running CTAs: progress is guaranteed. Every entry
 // keeps the reference's chain order (W and Z chains over their k ascending;
