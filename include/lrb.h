@@ -279,7 +279,7 @@ lrb_status lrb_batch_file_save(lrb_ctx* ctx, const char* path, int64_t batch, in
  * lrb_blr_matvec: y = M rhs (blr_matvec, blr.hpp:141-175) for row-major
  * n x nrhs HOST buffers; the _device form takes device buffers and is
  * asynchronous. One persistent launch for up to 16 right-hand sides (an even
- * count, block a multiple of 32, rank dividing 64, 16-byte aligned
+ * count, block a multiple of 32, rank 4, 8, 16 or 32, 16-byte aligned
  * operands), otherwise two
  * batched GEMM launches around one coupling kernel; on the caller's stream,
  * every chain in the reference's order (y_i = D_i rhs_i, then

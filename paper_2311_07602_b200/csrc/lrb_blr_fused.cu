@@ -67,8 +67,9 @@ constexpr int kFStages = 4;
 constexpr int kFWarps = 4;
 constexpr int kFThreads = kFWarps * 32 + 64;  // + the producer warp + the coupling warp
 constexpr int kFNB = 64, kFKB = 32;
-constexpr int kMaxRank = 16;                   // X tiles of one W tile: 64 / r items of r x r
-constexpr int kXs = kFNB * kMaxRank;
+constexpr int kMaxRank = 32;                   // ranks served (r | 64)
+constexpr int kStagedRank = 16;                // up to here X_ij is staged in shared memory
+constexpr int kXs = kFNB * kStagedRank;       // X tiles of one W tile: 64 / r items of r x r
 // the W tile in shared memory: 64 rows of W, pitch MB + 4 doubles (the coupling
 // warp's B fragments, lanes (g, tq) at tq * pitch + g, are conflict-free)
 template <int MBT>
@@ -215,7 +216,7 @@ __global__ void __launch_bounds__(kFThreads, 2)
           if (k0 == 0 && ahead && wtile)
             t_next = static_cast<long long>(atomicAdd(p.next, 1ull)) + t_dyn;
         }
-        if (wtile) {
+        if (wtile && p.r <= kStagedRank) {
           // the tile's X_ij (items ip0 .. of column j are consecutive in
           // (j, i) order: one contiguous bulk copy), issued after the tile's
           // chunks: by now the coupling warp has finished the previous W
@@ -262,10 +263,56 @@ __global__ void __launch_bounds__(kFThreads, 2)
       const int r = p.r, nrhs = p.nrhs;
       const int items = min(NB, p.K - n0) / r;
       const int ip0 = n0 / r;
-      mbar_wait(xfull, uint32_t(nwc & 1));  // this tile's X_ij landed
+      if (r <= kStagedRank) mbar_wait(xfull, uint32_t(nwc & 1));  // this tile's X_ij landed
       ++nwc;
       if (p.flags & 16) {
         // (bit 4: probe, no coupling)
+      } else if (r == 32) {
+        // rank 32: the tile's two X_ij do not fit beside the ring, so the
+        // fragments come straight from global memory (read once; all of an
+        // item's loads are in flight before its chains start). Same 8x8
+        // blocks, k ascending in steps of 4.
+        for (int it = 0; it < items; ++it) {
+          const int ip = ip0 + it;
+          const int i = ip < jcol ? ip : ip + 1;
+          const int jp = jcol < i ? jcol : jcol - 1;
+          double* zrow = p.rz + (int64_t(i) * p.P + p.b + int64_t(jp) * 32) * nrhs;
+          const double* xg = p.x + (int64_t(jcol) * (p.T - 1) + ip) * 1024;
+          const double* wt = scratch + it * 32 * WP;
+          constexpr int CN = MB / 8;
+          double a[4][8];
+#pragma unroll
+          for (int pi = 0; pi < 4; ++pi)
+#pragma unroll
+            for (int kq = 0; kq < 8; ++kq) a[pi][kq] = __ldg(xg + (pi * 8 + g) * 32 + kq * 4 + tq);
+          double d[4][CN][2];
+#pragma unroll
+          for (int pi = 0; pi < 4; ++pi)
+#pragma unroll
+            for (int ci = 0; ci < CN; ++ci) d[pi][ci][0] = d[pi][ci][1] = 0.0;
+#pragma unroll
+          for (int kq = 0; kq < 8; ++kq) {
+            double bv[CN];
+#pragma unroll
+            for (int ci = 0; ci < CN; ++ci) bv[ci] = wt[(kq * 4 + tq) * WP + ci * 8 + g];
+#pragma unroll
+            for (int pi = 0; pi < 4; ++pi)
+#pragma unroll
+              for (int ci = 0; ci < CN; ++ci)
+                dmma_8x8x4(d[pi][ci][0], d[pi][ci][1], a[pi][kq], bv[ci]);
+          }
+#pragma unroll
+          for (int pi = 0; pi < 4; ++pi)
+#pragma unroll
+            for (int ci = 0; ci < CN; ++ci) {
+              const int c = ci * 8 + 2 * tq;
+              double* zp = zrow + int64_t(pi * 8 + g) * nrhs + c;
+              if (c + 1 < nrhs)
+                *reinterpret_cast<double2*>(zp) = make_double2(d[pi][ci][0], d[pi][ci][1]);
+              else if (c < nrhs)
+                *zp = d[pi][ci][0];
+            }
+        }
       } else if (r % 8 == 0) {
         // DMMA: 8x8 output blocks, k ascending in steps of 4 (each entry one
         // in-order FMA chain). W columns nrhs..MB-1 are zero (TMA fills the

@@ -170,7 +170,9 @@ FUSED_SHAPES = [(2, 8, 10, 64), (4, 16, 16, 64), (5, 4, 12, 128), (8, 16, 12, 64
                 (17, 8, 14, 64), (6, 16, 10, 256), (9, 4, 10, 192), (33, 16, 16, 64),
                 # up to 8 right-hand sides: the m8 tile
                 (4, 8, 8, 64), (5, 16, 8, 128), (3, 4, 6, 64), (9, 8, 2, 128), (17, 16, 4, 64),
-                (8, 8, 8, 512)]
+                (8, 8, 8, 512),
+                # rank 32: X_ij read straight from global memory by the coupling warp
+                (3, 32, 16, 64), (5, 32, 8, 128), (9, 32, 10, 256), (17, 32, 2, 64)]
 
 
 @pytest.mark.parametrize("tiles,rank,nrhs,block", FUSED_SHAPES)
