@@ -17,7 +17,7 @@ CONFIGS = ["cfg1", "cfg2"] + [f"cfg3_b{b}_r{r}" for b in W.CFG3_B for r in W.CFG
     "cfg4", "cfg5"]
 # the widened rows (bench.py --config): low-rank product and BLR matvec
 LOWRANK = ["lr_r8_b1024", "lr_r16_b1024", "lr_r32_b2048", "lr_r64_b2048", "lr_r96_b1024", "lr_r128_b1024"]
-BLR = ["blr_n32768_b512_r8_k8", "blr_n16384_b256_r16_k16"]
+BLR = ["blr_n32768_b512_r8_k8", "blr_n16384_b256_r16_k16", "blr_n16384_b512_r32_k16"]
 EXPAND = ["lrx_m512_r8", "lrx_m512_r32", "blrd_n16384_b512_r16"]
 
 
