@@ -175,6 +175,32 @@ FUSED_SHAPES = [(2, 8, 10, 64), (4, 16, 16, 64), (5, 4, 12, 128), (8, 16, 12, 64
                 (3, 32, 16, 64), (5, 32, 8, 128), (9, 32, 10, 256), (17, 32, 2, 64)]
 
 
+@pytest.mark.parametrize("tiles,rank,block", [(9, 16, 128), (6, 32, 64), (17, 8, 64)])
+def test_fused_matvec_changing_rhs_counts_on_one_matrix(ctx, monkeypatch, tiles, rank, block):
+    # one matrix, a sequence of calls with different right-hand-side counts
+    # (the m16 and the m8 tile share the matrix's sync words: ready counts that
+    # only grow, one epoch word), with three-launch calls in between (they
+    # leave the words alone): every fused result bitwise the three-launch one
+    from paper_2311_07602_b200.lrbatch import _check as check, lib
+
+    m = B.BlrMatrix.random(tiles * block, block, rank, 900 + tiles)
+    h = m.device_handle(ctx)
+    s = ctx.stream()
+    for rep, nrhs in enumerate([16, 8, 16, 2, 10, 10, 4, 16]):
+        rhs = _rhs(tiles * block, nrhs, 70 + rep)
+        d_rhs = ctx.to_device(rhs.data)
+        y_f, y_3 = ctx.empty(rhs.data.size), ctx.empty(rhs.data.size)
+        n0 = ctx.launch_count
+        check(lib.lrb_blr_matvec_device(ctx._h, h, d_rhs.ptr, nrhs, y_f.ptr, s.handle), ctx._h)
+        s.synchronize()
+        assert ctx.launch_count - n0 == 1
+        monkeypatch.setenv("LRB_BLR_FUSED", "0")
+        check(lib.lrb_blr_matvec_device(ctx._h, h, d_rhs.ptr, nrhs, y_3.ptr, s.handle), ctx._h)
+        s.synchronize()
+        monkeypatch.delenv("LRB_BLR_FUSED")
+        assert np.array_equal(y_f.download(rhs.data.size), y_3.download(rhs.data.size)), (rep, nrhs)
+
+
 @pytest.mark.parametrize("tiles,rank,nrhs,block", FUSED_SHAPES)
 def test_fused_matvec_equals_three_launch_form(ctx, monkeypatch, tiles, rank, nrhs, block):
     # the single persistent launch (W tiles with the coupling folded in, row
