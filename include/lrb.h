@@ -278,9 +278,10 @@ lrb_status lrb_batch_file_save(lrb_ctx* ctx, const char* path, int64_t batch, in
  * row-major (u block x rank, x rank x rank, vt rank x block).
  * lrb_blr_matvec: y = M rhs (blr_matvec, blr.hpp:141-175) for row-major
  * n x nrhs HOST buffers; the _device form takes device buffers and is
- * asynchronous. One persistent launch for up to 16 right-hand sides (an even
- * count, block a multiple of 32, rank 4, 8, 16 or 32, 16-byte aligned
- * operands), otherwise two
+ * asynchronous. One persistent launch for up to 16 right-hand sides (block a
+ * multiple of 32, rank 4, 8, 16 or 32, 16-byte aligned operands; an odd
+ * count, e.g. the plain matvec, runs it on copies padded with one zero
+ * column: two small copy kernels around it), otherwise two
  * batched GEMM launches around one coupling kernel; on the caller's stream,
  * every chain in the reference's order (y_i = D_i rhs_i, then
  * += U_ij X_ij Vt_ij rhs_j for j ascending). The matrix owns a

@@ -44,6 +44,11 @@ struct lrb_blr {
   // lrb_blr_destroy. ws_ev orders the matrix's eager matvecs on different
   // streams (they share d_w / d_rz).
   size_t w_cap = 0, rz_cap = 0;  // doubles
+  // odd right-hand-side counts: rhs / y copies with one more (zero) column,
+  // so the fused matvec's 16-byte operand rule holds
+  double* d_rpad = nullptr;
+  double* d_ypad = nullptr;
+  size_t rpad_cap = 0, ypad_cap = 0;
   double* d_w = nullptr;
   double* d_rz = nullptr;     // per row i: pitch x nrhs, [rhs_i; Z_i0; Z_i1; ...]
   cudaEvent_t ws_ev = nullptr;
@@ -67,6 +72,7 @@ bool launch_blr_fused(lrb_ctx* ctx, const double* rhs, int64_t nrhs, double* y, 
                       int64_t b, int64_t r, int64_t P, const double* vtcol, const double* x,
                       const double* dcat, double* rz, unsigned* ready,
                       unsigned long long* next, cudaStream_t s, lrb_status* st);
+bool blr_fused_shape_ok(int64_t T, int64_t b, int64_t r, int64_t nrhs);
 bool launch_blr_recon(lrb_ctx* ctx, const double* vtcol, const double* dcat, const double* x,
                       double* out, int64_t T, int64_t b, int64_t r, int64_t P, cudaStream_t s,
                       lrb_status* st);
@@ -89,13 +95,15 @@ void free_all(lrb_ctx* ctx, lrb_blr* m) {
   if (m->d_ux) cudaFree(m->d_ux);
   if (m->d_w) cudaFree(m->d_w);
   if (m->d_rz) cudaFree(m->d_rz);
+  if (m->d_rpad) cudaFree(m->d_rpad);
+  if (m->d_ypad) cudaFree(m->d_ypad);
   if (m->ws_ev) cudaEventDestroy(m->ws_ev);
   if (m->d_sync) cudaFree(m->d_sync);
   m->d_sync = nullptr;
   m->retired.clear();
   m->retired_plans.clear();
   m->recon_plan = nullptr;
-  m->d_ux = m->d_w = m->d_rz = nullptr;
+  m->d_ux = m->d_w = m->d_rz = m->d_rpad = m->d_ypad = nullptr;
   m->ws_ev = nullptr;
 }
 
@@ -542,6 +550,21 @@ extern "C" lrb_status lrb_blr_matvec_device(lrb_ctx* ctx, lrb_blr* m, const doub
 }
 
 namespace {
+// dst (rows x kd, row-major) = the first min(ks, kd) columns of src (rows x
+// ks), further columns zero: the odd-count matvec's padded copies
+__global__ void __launch_bounds__(256) blr_repitch_kernel(const double* __restrict__ src, int ks,
+                                                          double* __restrict__ dst, int kd,
+                                                          int64_t rows) {
+  lrb::pdl_entry();
+  const int64_t total = rows * kd;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t row = e / kd;
+    const int c = int(e - row * kd);
+    dst[e] = c < ks ? src[row * ks + c] : 0.0;
+  }
+}
+
 lrb_status matvec_steps(lrb_ctx* ctx, lrb_blr* m, const double* rhs, int64_t nrhs, double* y,
                         cudaStream_t s) {
   lrb_status st = LRB_OK;
@@ -556,6 +579,31 @@ lrb_status matvec_steps(lrb_ctx* ctx, lrb_blr* m, const double* rhs, int64_t nrh
     if (lrb::launch_blr_fused(ctx, rhs, nrhs, y, T, b, r, P, m->d_vtcol, m->d_x, m->d_dcat,
                               m->d_rz, ready, next, s, &st))
       return st;
+    // An odd count (the plain matvec, nrhs = 1, first of all) leaves rhs and y
+    // rows that are not 16-byte multiples, which TMA cannot address: run the
+    // same launch on copies with one more, zero, column. Every column's
+    // chains are its own, so the results are the unpadded ones bit for bit,
+    // and the two copies move n x nrhs doubles against the whole matrix.
+    if ((nrhs & 1) && lrb::blr_fused_shape_ok(T, b, r, nrhs + 1)) {
+      const int64_t n = T * b, k2 = nrhs + 1;
+      st = ensure_ws(ctx, m, k2);
+      if (!st) st = grow(ctx, m, &m->d_rpad, &m->rpad_cap, size_t(n * k2));
+      if (!st) st = grow(ctx, m, &m->d_ypad, &m->ypad_cap, size_t(n * k2));
+      if (st) return st;
+      const unsigned blocks = unsigned(std::min<int64_t>((n * k2 + 255) / 256, 148 * 8));
+      LRB_CUDA_TRY(ctx, lrb::launch_pdl(blr_repitch_kernel, dim3(blocks), dim3(256), 0, s, rhs,
+                                        int(nrhs), m->d_rpad, int(k2), n));
+      ctx->launches.fetch_add(1, std::memory_order_relaxed);
+      if (lrb::launch_blr_fused(ctx, m->d_rpad, k2, m->d_ypad, T, b, r, P, m->d_vtcol, m->d_x,
+                                m->d_dcat, m->d_rz, ready, next, s, &st)) {
+        if (st) return st;
+        LRB_CUDA_TRY(ctx, lrb::launch_pdl(blr_repitch_kernel, dim3(blocks), dim3(256), 0, s,
+                                          static_cast<const double*>(m->d_ypad), int(k2), y,
+                                          int(nrhs), n));
+        ctx->launches.fetch_add(1, std::memory_order_relaxed);
+        return LRB_OK;
+      }
+    }
   }
   // 1. W_.j = [Vt_ij]_i rhs_j
   st = lrb::run_strided_rowmajor_beta(ctx, K, nrhs, b, m->d_vtcol, b, K * b, rhs, nrhs, b * nrhs,

@@ -546,13 +546,17 @@ bool launch_blr_fused_t(lrb_ctx* ctx, const double* rhs, int64_t nrhs, double* y
   return true;
 }
 
+// the shapes the fused kernel serves (its operands must be TMA-addressable too)
+bool blr_fused_shape_ok(int64_t T, int64_t b, int64_t r, int64_t nrhs) {
+  return T >= 2 && nrhs >= 1 && nrhs <= 16 && r >= 4 && b % kFKB == 0 && kFNB % r == 0 &&
+         r % 4 == 0 && r <= kMaxRank;
+}
+
 bool launch_blr_fused(lrb_ctx* ctx, const double* rhs, int64_t nrhs, double* y, int64_t T,
                       int64_t b, int64_t r, int64_t P, const double* vtcol, const double* x,
                       const double* dcat, double* rz, unsigned* ready,
                       unsigned long long* next, cudaStream_t s, lrb_status* st) {
-  if (T < 2 || nrhs < 1 || nrhs > 16 || b % kFKB != 0 || kFNB % r != 0 || r % 4 != 0 ||
-      r > kMaxRank)
-    return false;
+  if (!blr_fused_shape_ok(T, b, r, nrhs)) return false;
   if (nrhs <= 8) {
     // the m8 tile; LRB_BLR_FUSED_M8=0 keeps the three-launch form for <= 8
     // right-hand sides

@@ -175,6 +175,43 @@ FUSED_SHAPES = [(2, 8, 10, 64), (4, 16, 16, 64), (5, 4, 12, 128), (8, 16, 12, 64
                 (3, 32, 16, 64), (5, 32, 8, 128), (9, 32, 10, 256), (17, 32, 2, 64)]
 
 
+@pytest.mark.parametrize("tiles,rank,nrhs,block", [(4, 8, 1, 64), (9, 16, 1, 128), (5, 8, 3, 128),
+                                                   (6, 32, 7, 64), (17, 16, 15, 64),
+                                                   (3, 4, 5, 96)])
+def test_fused_matvec_odd_rhs_counts(ctx, monkeypatch, tiles, rank, nrhs, block):
+    # an odd count (the plain matvec first of all) runs the fused launch on
+    # copies padded with one zero column: three launches (pad, fused, unpad),
+    # results bitwise the three-launch form's and the oracle's; replayed from
+    # a graph
+    from paper_2311_07602_b200.lrbatch import _check as check, lib
+
+    m = B.BlrMatrix.random(tiles * block, block, rank, 500 + tiles + rank)
+    rhs = _rhs(tiles * block, nrhs, 91 + nrhs)
+    h = m.device_handle(ctx)
+    s = ctx.stream()
+    d_rhs = ctx.to_device(rhs.data)
+    y_f, y_3 = ctx.empty(rhs.data.size), ctx.empty(rhs.data.size)
+    n0 = ctx.launch_count
+    check(lib.lrb_blr_matvec_device(ctx._h, h, d_rhs.ptr, nrhs, y_f.ptr, s.handle), ctx._h)
+    s.synchronize()
+    assert ctx.launch_count - n0 == 3
+    monkeypatch.setenv("LRB_BLR_FUSED", "0")
+    check(lib.lrb_blr_matvec_device(ctx._h, h, d_rhs.ptr, nrhs, y_3.ptr, s.handle), ctx._h)
+    s.synchronize()
+    monkeypatch.delenv("LRB_BLR_FUSED")
+    got = y_f.download(rhs.data.size)
+    assert np.array_equal(got, y_3.download(rhs.data.size))
+    _check(m, rhs, DenseBlock(rhs.rows, rhs.cols, got))
+    with ctx.capture(s) as cap:
+        check(lib.lrb_blr_matvec_device(ctx._h, h, d_rhs.ptr, nrhs, y_f.ptr, s.handle), ctx._h)
+    for _ in range(2):
+        y_f.fill_bytes(0)
+        ctx.synchronize()
+        cap.graph.launch(s)
+        s.synchronize()
+        assert np.array_equal(y_f.download(rhs.data.size), got)
+
+
 @pytest.mark.parametrize("tiles,rank,block", [(9, 16, 128), (6, 32, 64), (17, 8, 64)])
 def test_fused_matvec_changing_rhs_counts_on_one_matrix(ctx, monkeypatch, tiles, rank, block):
     # one matrix, a sequence of calls with different right-hand-side counts
@@ -186,14 +223,14 @@ def test_fused_matvec_changing_rhs_counts_on_one_matrix(ctx, monkeypatch, tiles,
     m = B.BlrMatrix.random(tiles * block, block, rank, 900 + tiles)
     h = m.device_handle(ctx)
     s = ctx.stream()
-    for rep, nrhs in enumerate([16, 8, 16, 2, 10, 10, 4, 16]):
+    for rep, nrhs in enumerate([16, 8, 16, 2, 1, 10, 10, 3, 4, 16]):
         rhs = _rhs(tiles * block, nrhs, 70 + rep)
         d_rhs = ctx.to_device(rhs.data)
         y_f, y_3 = ctx.empty(rhs.data.size), ctx.empty(rhs.data.size)
         n0 = ctx.launch_count
         check(lib.lrb_blr_matvec_device(ctx._h, h, d_rhs.ptr, nrhs, y_f.ptr, s.handle), ctx._h)
         s.synchronize()
-        assert ctx.launch_count - n0 == 1
+        assert ctx.launch_count - n0 == (3 if nrhs % 2 else 1)
         monkeypatch.setenv("LRB_BLR_FUSED", "0")
         check(lib.lrb_blr_matvec_device(ctx._h, h, d_rhs.ptr, nrhs, y_3.ptr, s.handle), ctx._h)
         s.synchronize()
