@@ -10,8 +10,10 @@
 // over its inner index, so G is bitwise the reference oracle's three naive
 // products computed with fused multiply-adds.
 //
-// Fast path (r <= 32, even r and block, 16-B aligned roles): one warp per
-// item, four items per CTA, persistent CTAs.
+// Fast path (r <= 32, even block, 16-B aligned roles): one warp per item,
+// four items per CTA, persistent CTAs. Odd ranks included: B_U's rows are
+// then r doubles, not a 16-byte multiple, and the tensor map views each item
+// as b/2 rows of 2r instead (LrCfg::P2; the columns past r are masked).
 //   * C^T = B_U^T A_Vt^T on FP64 DMMA with k ascending; the A_Vt and B_U
 //     chunks of the CTA's four items arrive with ONE 3-D TMA box each
 //     (z = item), padded so fragment loads are bank-conflict free.
@@ -26,6 +28,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "lrb_dispatch.cuh"
@@ -61,6 +64,14 @@ struct LrCfg {
   static constexpr int PR = R + 4;   // B_U tile  [kk][n]
   static constexpr int AV = PK * R;  // per item: box (KB+4, R, G)
   static constexpr int BU = PR * KB; // per item: box (R+4, KB, G)
+  // odd ranks (PAIR): B_U's rows are r doubles, not a 16-byte multiple, so
+  // the map views each item as b/2 rows of 2r (rows kk, kk+1 side by side):
+  // box (2R+4, KB/2, G). Element (kk, n) sits at (kk/2) P2 + (kk%2) r + n;
+  // past 2r the box is zero-filled, so n >= r reads zeros on odd kk and the
+  // neighbouring row (masked to zero) on even kk. It fits B_U's buffer.
+  static constexpr int P2 = 2 * R + 4;
+  static constexpr int BUP = P2 * (KB / 2);
+  static_assert(BUP <= BU, "the paired box fits the B_U buffer");
   static constexpr int AV_ELEMS = round_up_c(AV * G, 16);
   static constexpr int BU_ELEMS = round_up_c(BU * G, 16);
   static constexpr int STAGE = AV_ELEMS + BU_ELEMS;
@@ -82,7 +93,7 @@ struct LrProblem {
   int64_t groups;  // ceil(batch / G)
 };
 
-template <class Cf>
+template <class Cf, bool PAIR>
 __device__ __forceinline__ void lr_issue(const LrProblem& p, double* smem, uint64_t* full,
                                          IssueState* st, int stage, int lane) {
   long long t_ll = 0;
@@ -104,10 +115,10 @@ __device__ __forceinline__ void lr_issue(const LrProblem& p, double* smem, uint6
     // box and the ring is 4 deep, stays evict-first)
     const uint64_t pol_av = (Cf::F >= 2) ? policy_evict_normal() : policy_evict_first();
     const uint64_t pol_bu = policy_evict_first();
-    mbar_arrive_expect_tx(&full[stage], uint32_t(Cf::AV + Cf::BU) * Cf::G * 8u);
+    mbar_arrive_expect_tx(&full[stage], uint32_t(Cf::AV + (PAIR ? Cf::BUP : Cf::BU)) * Cf::G * 8u);
     const int z = static_cast<int>(t * Cf::G);
     tma_load_3d(av, &p.tmAV, k0, 0, z, &full[stage], pol_av);
-    tma_load_3d(bu, &p.tmBU, 0, k0, z, &full[stage], pol_bu);
+    tma_load_3d(bu, &p.tmBU, 0, PAIR ? k0 / 2 : k0, z, &full[stage], pol_bu);
     int nk0 = k0 + Cf::KB;
     int64_t nt = t;
     if (nk0 >= p.block) {
@@ -120,7 +131,7 @@ __device__ __forceinline__ void lr_issue(const LrProblem& p, double* smem, uint6
   __syncwarp();
 }
 
-template <int R>
+template <int R, bool PAIR>
 __global__ void __launch_bounds__(LrCfg<R>::THREADS, 2)
     lrb_lowrank_kernel(const __grid_constant__ LrProblem p) {
   using Cf = LrCfg<R>;
@@ -162,13 +173,13 @@ __global__ void __launch_bounds__(LrCfg<R>::THREADS, 2)
         long long t_ll = 0;
         if (lane == 0) t_ll = st->t;
         if (__shfl_sync(0xffffffffu, t_ll, 0) >= p.groups) break;
-        lr_issue<Cf>(p, smem, full, st, s, lane);
+        lr_issue<Cf, PAIR>(p, smem, full, st, s, lane);
       }
       return;
     }
   } else {
     if (warp == 0)
-      for (int s = 0; s < STAGES; ++s) lr_issue<Cf>(p, smem, full, st, s, lane);
+      for (int s = 0; s < STAGES; ++s) lr_issue<Cf, PAIR>(p, smem, full, st, s, lane);
   }
 
   int stage = 0;
@@ -199,14 +210,24 @@ __global__ void __launch_bounds__(LrCfg<R>::THREADS, 2)
       const int kvalid = min(KB, p.block - k0);
       mbar_wait(&full[stage], phase);
       const double* As = smem + size_t(stage) * Cf::STAGE + warp * Cf::AV;       // [m][kk]
-      const double* Bs = smem + size_t(stage) * Cf::STAGE + Cf::AV_ELEMS + warp * Cf::BU;  // [kk][n]
+      const double* Bs = smem + size_t(stage) * Cf::STAGE + Cf::AV_ELEMS +
+                         warp * (PAIR ? Cf::BUP : Cf::BU);  // [kk][n]
+      // B_U[kk][n] (PAIR: the row-pair layout, columns past r masked)
+      auto bu_at = [&](int kk, int n) -> double {
+        if constexpr (PAIR) {
+          const double v = Bs[(kk >> 1) * Cf::P2 + (kk & 1) * r + n];
+          return ((kk & 1) || n < r) ? v : 0.0;
+        } else {
+          return Bs[kk * Cf::PR + n];
+        }
+      };
       const int nq = kvalid >> 2;
 #pragma unroll 4
       for (int kq = 0; kq < nq; ++kq) {
         const int kk = kq * 4 + tq;
         double af[F], bf[F];
 #pragma unroll
-        for (int fn = 0; fn < F; ++fn) af[fn] = Bs[kk * Cf::PR + fn * 8 + g];  // B_U[kk][n]
+        for (int fn = 0; fn < F; ++fn) af[fn] = bu_at(kk, fn * 8 + g);  // B_U[kk][n]
 #pragma unroll
         for (int fm = 0; fm < F; ++fm) bf[fm] = As[(fm * 8 + g) * Cf::PK + kk];  // A_Vt[m][kk]
 #pragma unroll
@@ -218,7 +239,7 @@ __global__ void __launch_bounds__(LrCfg<R>::THREADS, 2)
       for (int kk = nq * 4; kk < kvalid; ++kk) {
 #pragma unroll
         for (int fn = 0; fn < F; ++fn) {
-          const double bv = Bs[kk * Cf::PR + fn * 8 + g];
+          const double bv = bu_at(kk, fn * 8 + g);
 #pragma unroll
           for (int fm = 0; fm < F; ++fm)
 #pragma unroll
@@ -236,7 +257,7 @@ __global__ void __launch_bounds__(LrCfg<R>::THREADS, 2)
           if (last) released[stage] = 0;
         }
         last = __shfl_sync(0xffffffffu, last, 0);
-        if (last) lr_issue<Cf>(p, smem, full, st, stage, lane);
+        if (last) lr_issue<Cf, PAIR>(p, smem, full, st, stage, lane);
       }
       if (++stage == STAGES) {
         stage = 0;
@@ -385,11 +406,11 @@ bool encode3(CUtensorMap* map, const double* base, int64_t d0, int64_t d1, int64
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int R>
+template <int R, bool PAIR>
 cudaError_t launch_fast(const LrProblem& p, int device, int sm_count, cudaStream_t s,
                         int64_t* grid_out) {
   using Cf = LrCfg<R>;
-  auto kern = lrb_lowrank_kernel<R>;
+  auto kern = lrb_lowrank_kernel<R, PAIR>;
   static int occ_cache[64] = {0};
   int occ = (device >= 0 && device < 64) ? occ_cache[device] : 0;
   if (occ == 0) {
@@ -413,7 +434,8 @@ cudaError_t launch_fast(const LrProblem& p, int device, int sm_count, cudaStream
 int lowrank_path(int64_t block, int64_t rank, const void* a_vt, const void* b_u) {
   if (rank > 32) return 1;
   const bool aligned = ((reinterpret_cast<uintptr_t>(a_vt) | reinterpret_cast<uintptr_t>(b_u)) & 15) == 0;
-  if ((rank & 1) == 0 && (block & 1) == 0 && aligned && encode_fn()) return 0;
+  // (odd ranks too: B_U is then mapped as row pairs, LrCfg::P2)
+  if ((block & 1) == 0 && aligned && encode_fn()) return 0;
   return 2;
 }
 
@@ -436,13 +458,21 @@ lrb_status run_lowrank(lrb_ctx* ctx, int64_t batch, int64_t block, int64_t rank,
     const int R = rank <= 8 ? 8 : rank <= 16 ? 16 : 32;
     const int G = 4, KB = R >= 32 ? 16 : 32;
     p.groups = (batch + G - 1) / G;
+    const bool pair = (rank & 1) != 0;
     bool ok = encode3(&p.tmAV, a_vt, block, rank, batch, block, rank * block, KB + kPad, R, G) &&
-              encode3(&p.tmBU, b_u, rank, block, batch, rank, block * rank, R + kPad, KB, G);
+              (pair ? encode3(&p.tmBU, b_u, 2 * rank, block / 2, batch, 2 * rank, block * rank,
+                              2 * R + 4, KB / 2, G)
+                    : encode3(&p.tmBU, b_u, rank, block, batch, rank, block * rank, R + kPad, KB, G));
     if (ok) {
       int64_t grid = 0;
-      cudaError_t e = R == 8    ? launch_fast<8>(p, ctx->device, ctx->sm_count, s, &grid)
-                      : R == 16 ? launch_fast<16>(p, ctx->device, ctx->sm_count, s, &grid)
-                                : launch_fast<32>(p, ctx->device, ctx->sm_count, s, &grid);
+      const int dev = ctx->device, sms = ctx->sm_count;
+      cudaError_t e =
+          pair ? (R == 8    ? launch_fast<8, true>(p, dev, sms, s, &grid)
+                  : R == 16 ? launch_fast<16, true>(p, dev, sms, s, &grid)
+                            : launch_fast<32, true>(p, dev, sms, s, &grid))
+               : (R == 8    ? launch_fast<8, false>(p, dev, sms, s, &grid)
+                  : R == 16 ? launch_fast<16, false>(p, dev, sms, s, &grid)
+                            : launch_fast<32, false>(p, dev, sms, s, &grid));
       if (e != cudaSuccess) return cuda_fail(ctx, e, "lrb_lowrank_kernel launch");
       if (grid > 0) ctx->launches.fetch_add(1, std::memory_order_relaxed);
       return LRB_OK;

@@ -49,9 +49,25 @@ def test_trivial_all_ones(ctx):
 @pytest.mark.parametrize("rank", [1, 3, 4, 6, 8, 12, 16, 24, 32])
 @pytest.mark.parametrize("block", [1, 17, 64, 256])
 def test_grid_matches_reference(ctx, rank, block):
-    # odd rank / odd block take the per-item kernel, the rest the TMA+DMMA path
+    # odd blocks take the per-item kernel, the rest the TMA+DMMA path (odd ranks
+    # with B_U mapped as row pairs)
     b = L.LowRankBatch.random(7, block, rank, 1000 + rank * 10 + block)
     L.fused_multiply(b, ctx=ctx)
+    _check(b)
+
+
+@pytest.mark.parametrize("rank,block,batch", [(1, 64, 9), (3, 512, 41), (5, 256, 17), (7, 1024, 10),
+                                              (9, 128, 33), (11, 66, 6), (15, 512, 13),
+                                              (17, 256, 5), (23, 130, 7), (31, 1024, 6),
+                                              (31, 34, 3), (13, 2, 4)])
+def test_odd_ranks_on_the_fast_path(ctx, rank, block, batch):
+    # B_U's rows are r doubles (not a 16-byte multiple): the map views each item
+    # as b/2 rows of 2r, the kernel masks the columns past r. One launch,
+    # bitwise the FMA-chain oracle, batches that do not fill the last CTA
+    b = L.LowRankBatch.random(batch, block, rank, 77 * rank + block + batch)
+    n0 = ctx.launch_count
+    L.fused_multiply(b, ctx=ctx)
+    assert ctx.launch_count - n0 == 1
     _check(b)
 
 
