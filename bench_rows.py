@@ -250,6 +250,8 @@ def run_blr_gpu(args, w, world, rank, local, pg, B):
     roof["kernel"] = ("blr_fused_kernel (one persistent launch per matvec)" if per_step == 1 else
                       "blr_repitch_kernel, blr_fused_kernel on rhs / y padded to an even count, "
                       "blr_repitch_kernel" if padded else
+                      "blr_repitch_kernel x2 around lrb_gemm_kernel x2 + blr_couple_warp_kernel "
+                      "(odd count, padded to even)" if per_step == 5 and w.nrhs % 2 == 1 else
                       "lrb_gemm_kernel x2 + blr_couple_warp_kernel per matvec")
     roof["kernel_ms"] = round(ms_med * args.steps / max(1, launches), 4)
     e2e = None

@@ -281,7 +281,8 @@ lrb_status lrb_batch_file_save(lrb_ctx* ctx, const char* path, int64_t batch, in
  * asynchronous. One persistent launch for up to 16 right-hand sides (block a
  * multiple of 32, rank 4, 8, 16 or 32, 16-byte aligned operands; an odd
  * count, e.g. the plain matvec, runs it on copies padded with one zero
- * column: two small copy kernels around it), otherwise two
+ * column: two small copy kernels around it; 17 to 64 right-hand sides at
+ * rank >= 16 run it once per column range of 16), otherwise two
  * batched GEMM launches around one coupling kernel; on the caller's stream,
  * every chain in the reference's order (y_i = D_i rhs_i, then
  * += U_ij X_ij Vt_ij rhs_j for j ascending). The matrix owns a

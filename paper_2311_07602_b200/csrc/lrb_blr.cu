@@ -68,7 +68,8 @@ struct lrb_blr {
 };
 
 namespace lrb {
-bool launch_blr_fused(lrb_ctx* ctx, const double* rhs, int64_t nrhs, double* y, int64_t T,
+bool launch_blr_fused(lrb_ctx* ctx, const double* rhs, int64_t nrhs, int64_t ld, double* y,
+                      int64_t T,
                       int64_t b, int64_t r, int64_t P, const double* vtcol, const double* x,
                       const double* dcat, double* rz, unsigned* ready,
                       unsigned long long* next, cudaStream_t s, lrb_status* st);
@@ -569,6 +570,30 @@ lrb_status matvec_steps(lrb_ctx* ctx, lrb_blr* m, const double* rhs, int64_t nrh
                         cudaStream_t s) {
   lrb_status st = LRB_OK;
   const int64_t T = m->tiles, b = m->block, r = m->rank, K = (T - 1) * r, P = m->pitch;
+  // An odd count (the plain matvec, nrhs = 1, first of all) leaves rhs and y
+  // rows that are not 16-byte multiples, which TMA cannot address: every
+  // launch form would fall to its per-lane loaders (0.3 of HBM). Run the even
+  // count on copies with one more, zero, column instead. Every column's
+  // chains are its own, so the results are the unpadded ones bit for bit,
+  // and the two copies move n x nrhs doubles against the whole matrix.
+  if (nrhs & 1) {
+    const int64_t n = T * b, k2 = nrhs + 1;
+    st = ensure_ws(ctx, m, k2);
+    if (!st) st = grow(ctx, m, &m->d_rpad, &m->rpad_cap, size_t(n * k2));
+    if (!st) st = grow(ctx, m, &m->d_ypad, &m->ypad_cap, size_t(n * k2));
+    if (st) return st;
+    const unsigned blocks = unsigned(std::min<int64_t>((n * k2 + 255) / 256, 148 * 8));
+    LRB_CUDA_TRY(ctx, lrb::launch_pdl(blr_repitch_kernel, dim3(blocks), dim3(256), 0, s, rhs,
+                                      int(nrhs), m->d_rpad, int(k2), n));
+    ctx->launches.fetch_add(1, std::memory_order_relaxed);
+    st = matvec_steps(ctx, m, m->d_rpad, k2, m->d_ypad, s);
+    if (st) return st;
+    LRB_CUDA_TRY(ctx, lrb::launch_pdl(blr_repitch_kernel, dim3(blocks), dim3(256), 0, s,
+                                      static_cast<const double*>(m->d_ypad), int(k2), y,
+                                      int(nrhs), n));
+    ctx->launches.fetch_add(1, std::memory_order_relaxed);
+    return LRB_OK;
+  }
   // one persistent launch when the shape allows it (lrb_blr_fused.cu);
   // LRB_BLR_FUSED=0 or debug bit 9 keeps the three-launch form below
   const char* fe = std::getenv("LRB_BLR_FUSED");
@@ -576,33 +601,27 @@ lrb_status matvec_steps(lrb_ctx* ctx, lrb_blr* m, const double* rhs, int64_t nrh
     unsigned* ready = m->d_sync;
     auto* next = reinterpret_cast<unsigned long long*>(
         reinterpret_cast<char*>(m->d_sync) + size_t(T) * 16);
-    if (lrb::launch_blr_fused(ctx, rhs, nrhs, y, T, b, r, P, m->d_vtcol, m->d_x, m->d_dcat,
+    if (lrb::launch_blr_fused(ctx, rhs, nrhs, nrhs, y, T, b, r, P, m->d_vtcol, m->d_x, m->d_dcat,
                               m->d_rz, ready, next, s, &st))
       return st;
-    // An odd count (the plain matvec, nrhs = 1, first of all) leaves rhs and y
-    // rows that are not 16-byte multiples, which TMA cannot address: run the
-    // same launch on copies with one more, zero, column. Every column's
-    // chains are its own, so the results are the unpadded ones bit for bit,
-    // and the two copies move n x nrhs doubles against the whole matrix.
-    if ((nrhs & 1) && lrb::blr_fused_shape_ok(T, b, r, nrhs + 1)) {
-      const int64_t n = T * b, k2 = nrhs + 1;
-      st = ensure_ws(ctx, m, k2);
-      if (!st) st = grow(ctx, m, &m->d_rpad, &m->rpad_cap, size_t(n * k2));
-      if (!st) st = grow(ctx, m, &m->d_ypad, &m->ypad_cap, size_t(n * k2));
-      if (st) return st;
-      const unsigned blocks = unsigned(std::min<int64_t>((n * k2 + 255) / 256, 148 * 8));
-      LRB_CUDA_TRY(ctx, lrb::launch_pdl(blr_repitch_kernel, dim3(blocks), dim3(256), 0, s, rhs,
-                                        int(nrhs), m->d_rpad, int(k2), n));
-      ctx->launches.fetch_add(1, std::memory_order_relaxed);
-      if (lrb::launch_blr_fused(ctx, m->d_rpad, k2, m->d_ypad, T, b, r, P, m->d_vtcol, m->d_x,
-                                m->d_dcat, m->d_rz, ready, next, s, &st)) {
-        if (st) return st;
-        LRB_CUDA_TRY(ctx, lrb::launch_pdl(blr_repitch_kernel, dim3(blocks), dim3(256), 0, s,
-                                          static_cast<const double*>(m->d_ypad), int(k2), y,
-                                          int(nrhs), n));
-        ctx->launches.fetch_add(1, std::memory_order_relaxed);
-        return LRB_OK;
+    // More than 16 right-hand sides: the same launch over column ranges of 16
+    // (the last one shorter), the matrix streamed once per range. Measured
+    // against the three launches' wide-tile forms at 18..64 columns: 27-30 %
+    // faster at rank 16 and 32 (n16384 b256 r16 k32 0.155 -> 0.112 ms, b512
+    // r16 0.115 -> 0.080, b512 r32 0.167 -> 0.124), 11 % slower at rank 8
+    // (n32768 b512 r8 k32 0.130 vs 0.146), hence the rank gate.
+    if (nrhs > 16 && nrhs <= 64 && r >= 16 && lrb::blr_fused_shape_ok(T, b, r, 16)) {
+      bool all = true;
+      for (int64_t c0 = 0; c0 < nrhs && all; c0 += 16) {
+        const int64_t w = std::min<int64_t>(16, nrhs - c0);
+        all = lrb::launch_blr_fused(ctx, rhs + c0, w, nrhs, y + c0, T, b, r, P, m->d_vtcol, m->d_x,
+                                    m->d_dcat, m->d_rz, ready, next, s, &st);
+        if (all && st) return st;
+        if (!all && c0 > 0)  // (cannot happen: every range has the first one's alignment)
+          return fail(ctx, LRB_ERR_UNSUPPORTED, "lrb_blr_matvec: column range %lld not addressable",
+                      (long long)c0);
       }
+      if (all) return LRB_OK;
     }
   }
   // 1. W_.j = [Vt_ij]_i rhs_j

@@ -45,6 +45,7 @@ struct BlrFusedProblem {
   double* rz;          // per row i: P x nrhs, Z_ij at rows b + jp r
   double* y;           // n x nrhs row-major
   int T, b, r, nrhs, K, P;
+  int ld;              // row pitch of rhs and y (>= nrhs: a column range of a wider right-hand side)
   int tw, tr;          // 64-row blocks per W column, 64-column blocks per row
   long long nw, total;  // W tiles, all tiles
   unsigned* ready;     // [T][4] Z items landed per row and quarter of its T - 1 columns
@@ -445,7 +446,7 @@ __global__ void __launch_bounds__(kFThreads, 2)
       for (int fj = 0; fj < FCfg::FJ; ++fj) {
         const int j = n0 + FCfg::load_col(wj, fj, g);
         if (j >= p.b) continue;
-        double* yr = p.y + (int64_t(i) * p.b + j) * p.nrhs;
+        double* yr = p.y + (int64_t(i) * p.b + j) * p.ld;
         const int c0 = FCfg::acc_row(wi, 0, 0, tq);
         if constexpr (FCfg::FI == 2) {  // paired fragments: rows c0 .. c0 + 3
           const double v[4] = {acc[fj][0][0], acc[fj][1][0], acc[fj][0][1], acc[fj][1][1]};
@@ -492,7 +493,8 @@ bool encode_operand(CUtensorMap* map, const double* base, int64_t rows, int64_t 
 // rank dividing 64 (each 64-row W block holds whole items) and a multiple of
 // 4, TMA-addressable operands.
 template <int MBT>
-bool launch_blr_fused_t(lrb_ctx* ctx, const double* rhs, int64_t nrhs, double* y, int64_t T,
+bool launch_blr_fused_t(lrb_ctx* ctx, const double* rhs, int64_t nrhs, int64_t ld, double* y,
+                        int64_t T,
                         int64_t b, int64_t r, int64_t P, const double* vtcol, const double* x,
                         const double* dcat, double* rz, unsigned* ready,
                         unsigned long long* next, cudaStream_t s, lrb_status* st) {
@@ -502,7 +504,7 @@ bool launch_blr_fused_t(lrb_ctx* ctx, const double* rhs, int64_t nrhs, double* y
   BlrFusedProblem p;
   std::memset(&p, 0, sizeof(p));
   const bool ok =
-      encode_operand(&p.tmRhs, rhs, nrhs, b, nrhs, b * nrhs, T, FCfg::MB + kPad, FCfg::KB) &&
+      encode_operand(&p.tmRhs, rhs, nrhs, b, ld, b * ld, T, FCfg::MB + kPad, FCfg::KB) &&
       encode_operand(&p.tmVt, vtcol, b, K, b, K * b, T, FCfg::KB + kPad, FCfg::NB) &&
       encode_operand(&p.tmZ, rz + b * nrhs, nrhs, K, nrhs, P * nrhs, T, FCfg::MB + kPad,
                      FCfg::KB) &&
@@ -512,6 +514,7 @@ bool launch_blr_fused_t(lrb_ctx* ctx, const double* rhs, int64_t nrhs, double* y
   p.rz = rz;
   p.y = y;
   p.T = int(T), p.b = int(b), p.r = int(r), p.nrhs = int(nrhs), p.K = int(K), p.P = int(P);
+  p.ld = int(ld);
   p.tw = int((K + FCfg::NB - 1) / FCfg::NB);
   p.tr = int((b + FCfg::NB - 1) / FCfg::NB);
   p.nw = int64_t(T) * p.tw;
@@ -552,7 +555,8 @@ bool blr_fused_shape_ok(int64_t T, int64_t b, int64_t r, int64_t nrhs) {
          r % 4 == 0 && r <= kMaxRank;
 }
 
-bool launch_blr_fused(lrb_ctx* ctx, const double* rhs, int64_t nrhs, double* y, int64_t T,
+bool launch_blr_fused(lrb_ctx* ctx, const double* rhs, int64_t nrhs, int64_t ld, double* y,
+                      int64_t T,
                       int64_t b, int64_t r, int64_t P, const double* vtcol, const double* x,
                       const double* dcat, double* rz, unsigned* ready,
                       unsigned long long* next, cudaStream_t s, lrb_status* st) {
@@ -562,10 +566,10 @@ bool launch_blr_fused(lrb_ctx* ctx, const double* rhs, int64_t nrhs, double* y, 
     // right-hand sides
     const char* e8 = std::getenv("LRB_BLR_FUSED_M8");
     if (e8 && e8[0] == '0') return false;
-    return launch_blr_fused_t<8>(ctx, rhs, nrhs, y, T, b, r, P, vtcol, x, dcat, rz, ready, next, s,
+    return launch_blr_fused_t<8>(ctx, rhs, nrhs, ld, y, T, b, r, P, vtcol, x, dcat, rz, ready, next, s,
                                  st);
   }
-  return launch_blr_fused_t<16>(ctx, rhs, nrhs, y, T, b, r, P, vtcol, x, dcat, rz, ready, next, s,
+  return launch_blr_fused_t<16>(ctx, rhs, nrhs, ld, y, T, b, r, P, vtcol, x, dcat, rz, ready, next, s,
                                 st);
 }
 

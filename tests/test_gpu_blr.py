@@ -212,6 +212,37 @@ def test_fused_matvec_odd_rhs_counts(ctx, monkeypatch, tiles, rank, nrhs, block)
         assert np.array_equal(y_f.download(rhs.data.size), got)
 
 
+@pytest.mark.parametrize("tiles,rank,nrhs,block", [(5, 8, 18, 64), (9, 16, 32, 128), (4, 32, 24, 64),
+                                                   (6, 16, 33, 96), (3, 16, 64, 64), (7, 4, 47, 32),
+                                                   (5, 32, 47, 64)])
+def test_fused_matvec_column_ranges_beyond_16_rhs(ctx, monkeypatch, tiles, rank, nrhs, block):
+    # 17..64 right-hand sides: the fused launch once per column range of 16
+    # (rhs and y addressed with the full row pitch), odd counts padded first;
+    # bitwise the three-launch form and the oracle
+    from paper_2311_07602_b200.lrbatch import _check as check, lib
+
+    m = B.BlrMatrix.random(tiles * block, block, rank, 700 + tiles + rank)
+    rhs = _rhs(tiles * block, nrhs, 17 + nrhs)
+    h = m.device_handle(ctx)
+    s = ctx.stream()
+    d_rhs = ctx.to_device(rhs.data)
+    y_f, y_3 = ctx.empty(rhs.data.size), ctx.empty(rhs.data.size)
+    n0 = ctx.launch_count
+    check(lib.lrb_blr_matvec_device(ctx._h, h, d_rhs.ptr, nrhs, y_f.ptr, s.handle), ctx._h)
+    s.synchronize()
+    even = nrhs + (nrhs & 1)
+    # (ranks below 16 keep the three launches there: measured faster)
+    core = (even + 15) // 16 if rank >= 16 else 3
+    assert ctx.launch_count - n0 == core + (2 if nrhs & 1 else 0)
+    monkeypatch.setenv("LRB_BLR_FUSED", "0")
+    check(lib.lrb_blr_matvec_device(ctx._h, h, d_rhs.ptr, nrhs, y_3.ptr, s.handle), ctx._h)
+    s.synchronize()
+    monkeypatch.delenv("LRB_BLR_FUSED")
+    got = y_f.download(rhs.data.size)
+    assert np.array_equal(got, y_3.download(rhs.data.size))
+    _check(m, rhs, DenseBlock(rhs.rows, rhs.cols, got))
+
+
 @pytest.mark.parametrize("tiles,rank,block", [(9, 16, 128), (6, 32, 64), (17, 8, 64)])
 def test_fused_matvec_changing_rhs_counts_on_one_matrix(ctx, monkeypatch, tiles, rank, block):
     # one matrix, a sequence of calls with different right-hand-side counts
