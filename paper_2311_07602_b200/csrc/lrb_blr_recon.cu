@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <type_traits>
 
 #include "lrb_device.cuh"
 #include "lrb_internal.h"
@@ -76,6 +77,7 @@ struct ReconProblem {
   const double* x;    // X_q at x + q sx, r x r row-major
   long long sx;
   int T, b;           // BLR: tiles, block (item q = off-diagonal tile in (j, i) order)
+  int rank;           // the items' rank r <= R (even): rows / columns past r are zero-filled or masked
   int rblocks, halves;  // per item: 64-row blocks, 256-column halves
   int units;
   int flags;          // LRB_DEBUG_FLAGS probe bits (wrong results): 64 = skip the (UX) Vt DMMAs,
@@ -90,7 +92,7 @@ struct ReconProblem {
 template <int R, bool BATCHED>
 __global__ void __launch_bounds__(kRThreads, 1)
     blr_recon_kernel(const __grid_constant__ ReconProblem p) {
-  constexpr int RP = R + kRPad, XP = R + kXPad;
+  constexpr int RP = R + kRPad;
   // batched: the operands may come from the previous kernel, wait for it. BLR:
   // the operands were uploaded at create and the predecessor is the diagonal
   // copy (disjoint output), so start beside it and wait only before exiting
@@ -134,8 +136,9 @@ __global__ void __launch_bounds__(kRThreads, 1)
 
   if (warp == kRWarps) {  // the producer
     if (lane == 0) {
+      const int r = p.rank;
       const uint32_t bytes =
-          uint32_t((kRHalf / kRBox) * (kRBox + kRPad) * R + 64 * RP + R * R) * 8u;
+          uint32_t((kRHalf / kRBox) * (kRBox + kRPad) * R + 64 * RP + r * r) * 8u;
       const uint64_t pol = policy_evict_normal(), pol_keep = policy_evict_last();
       int slot = 0, nq = 0;
       uint32_t phase = 0;
@@ -162,10 +165,10 @@ __global__ void __launch_bounds__(kRThreads, 1)
         if (BATCHED)
           tma_load_3d(us, &p.tmU, 0, rb * 64, q, &full[slot], pol);
         else
-          tma_load_3d(us, &p.tmU, p.b + jp * R, i * p.b + rb * 64, 0, &full[slot], pol);
+          tma_load_3d(us, &p.tmU, p.b + jp * r, i * p.b + rb * 64, 0, &full[slot], pol);
         const double* xg = p.x + q * p.sx;
         static_assert(kXPad == 0, "one contiguous copy");
-        bulk_g2s(xq, xg, uint32_t(R * R * 8), &full[slot], pol);
+        bulk_g2s(xq, xg, uint32_t(r * r * 8), &full[slot], pol);
         if (++slot == L::SLOTS) {
           slot = 0;
           phase ^= 1;
@@ -177,6 +180,7 @@ __global__ void __launch_bounds__(kRThreads, 1)
   }
 
   const int g = lane >> 2, tq = lane & 3, odd = g & 1;
+  const int rk = p.rank;
   const int row0 = (warp & 3) * 16;  // this warp's 16 rows of the 64-row block
   const int colw = (warp >> 2) * 32;  // and its 32 columns of each 64-column block
   double* wstage = stage + size_t(warp) * kStageBufs * kWarpStage;
@@ -201,18 +205,32 @@ __global__ void __launch_bounds__(kRThreads, 1)
       for (int f = 0; f < 2; ++f)
 #pragma unroll
         for (int c = 0; c < R / 8; ++c) ux[f][c][0] = ux[f][c][1] = 0.0;
+      // X lands r x r dense. At the template rank the reads keep their
+      // compile-time pitch (a run-time pitch and mask there cost the rank-16
+      // expansion 7 %); a smaller even rank reads zeros past r
+      auto ux_steps = [&](auto full_rank) {
 #pragma unroll
-      for (int k0 = 0; k0 < R; k0 += 4) {
-        double a[2], bx[R / 8];
+        for (int k0 = 0; k0 < R; k0 += 4) {
+          double a[2], bx[R / 8];
 #pragma unroll
-        for (int f = 0; f < 2; ++f) a[f] = us[(row0 + 8 * f + g) * RP + k0 + tq];
+          for (int f = 0; f < 2; ++f) a[f] = us[(row0 + 8 * f + g) * RP + k0 + tq];
 #pragma unroll
-        for (int c = 0; c < R / 8; ++c) bx[c] = xq[(k0 + tq) * XP + 8 * c + g];
+          for (int c = 0; c < R / 8; ++c) {
+            if constexpr (decltype(full_rank)::value)
+              bx[c] = xq[(k0 + tq) * R + 8 * c + g];
+            else
+              bx[c] = (k0 + tq < rk && 8 * c + g < rk) ? xq[(k0 + tq) * rk + 8 * c + g] : 0.0;
+          }
 #pragma unroll
-        for (int f = 0; f < 2; ++f)
+          for (int f = 0; f < 2; ++f)
 #pragma unroll
-          for (int c = 0; c < R / 8; ++c) dmma_8x8x4(ux[f][c][0], ux[f][c][1], a[f], bx[c]);
-      }
+            for (int c = 0; c < R / 8; ++c) dmma_8x8x4(ux[f][c][0], ux[f][c][1], a[f], bx[c]);
+        }
+      };
+      if (rk == R)
+        ux_steps(std::true_type{});
+      else
+        ux_steps(std::false_type{});
       // A fragment (row g, column k0 + tq) = accumulator element tq % 2 of
       // lane (g, (k0 % 8) / 2 + tq / 2) in chain k0 / 8
 #pragma unroll
@@ -328,51 +346,57 @@ static bool launch_recon(lrb_ctx* ctx, ReconProblem& p, int64_t units, int r, cu
 
 // The whole off-diagonal part of the reconstruction in one launch, or false
 // (nothing launched) when the shape is outside what the kernel serves:
-// r 8 or 16, b a multiple of 256, TMA-addressable buffers.
+// even r <= 16, b a multiple of 256, TMA-addressable buffers.
 bool launch_blr_recon(lrb_ctx* ctx, const double* vtcol, const double* dcat, const double* x,
                       double* out, int64_t T, int64_t b, int64_t r, int64_t P, cudaStream_t s,
                       lrb_status* st) {
   const int64_t n = T * b, Q = T * (T - 1);
-  if (T < 2 || (r != 8 && r != 16) || b % kRHalf != 0 || Q > INT32_MAX) return false;
+  // even ranks up to 16: the template rank R is 8 or 16, a smaller r rides on
+  // the boxes' zero fill (Vt rows) and the masked X reads
+  if (T < 2 || r < 2 || r > 16 || (r & 1) || b % kRHalf != 0 || Q > INT32_MAX) return false;
+  const int R = r <= 8 ? 8 : 16;
   if ((reinterpret_cast<uintptr_t>(x) & 15) != 0) return false;
   ReconProblem p;
   std::memset(&p, 0, sizeof(p));
   const bool ok = encode_c_map(&p.tmOut, out, n, n, n, 0, 1, 16) &&
-                  encode_operand(&p.tmVt, vtcol, b, r, b, r * b, Q, kRBox + kRPad, int(r)) &&
-                  encode_operand(&p.tmU, dcat, P, n, P, 0, 1, int(r) + kRPad, 64);
+                  encode_operand(&p.tmVt, vtcol, b, r, b, r * b, Q, kRBox + kRPad, R) &&
+                  encode_operand(&p.tmU, dcat, P, n, P, 0, 1, R + kRPad, 64);
   if (!ok) return false;
   p.x = x;
   p.sx = r * r;
   p.T = int(T), p.b = int(b);
   p.rblocks = int(b / 64);
   p.halves = int(b / kRHalf);
-  return launch_recon<false>(ctx, p, Q * p.rblocks * p.halves, int(r), s, st);
+  p.rank = int(r);
+  return launch_recon<false>(ctx, p, Q * p.rblocks * p.halves, R, s, st);
 }
 
 // The batched expansion out_q = (U_q X_q) Vt_q (row-major items at base +
 // q stride) in one launch, or false (nothing launched) outside what the kernel
-// serves: r 8 or 16, m a multiple of 64, n a multiple of 256, 16-byte
+// serves: even r <= 16, m a multiple of 64, n a multiple of 256, 16-byte
 // aligned bases, leading dimensions and strides.
 bool launch_expand_stream(lrb_ctx* ctx, int64_t batch, int64_t m, int64_t n, int64_t r,
                           const double* u, int64_t su, const double* x, int64_t sx,
                           const double* vt, int64_t svt, double* out, int64_t ldo, int64_t so,
                           cudaStream_t s, lrb_status* st) {
-  if ((r != 8 && r != 16) || m % 64 != 0 || n % kRHalf != 0 || batch < 1) return false;
+  if (r < 2 || r > 16 || (r & 1) || m % 64 != 0 || n % kRHalf != 0 || batch < 1) return false;
+  const int R = r <= 8 ? 8 : 16;
   if ((reinterpret_cast<uintptr_t>(x) & 15) != 0 || (batch > 1 && (sx & 1) != 0)) return false;
   const int64_t units = batch * (m / 64) * (n / kRHalf);
   if (units > INT32_MAX) return false;
   ReconProblem p;
   std::memset(&p, 0, sizeof(p));
   const bool ok = encode_c_map(&p.tmOut, out, n, m, ldo, so, batch, 16) &&
-                  encode_operand(&p.tmVt, vt, n, r, n, svt, batch, kRBox + kRPad, int(r)) &&
-                  encode_operand(&p.tmU, u, r, m, r, su, batch, int(r) + kRPad, 64);
+                  encode_operand(&p.tmVt, vt, n, r, n, svt, batch, kRBox + kRPad, R) &&
+                  encode_operand(&p.tmU, u, r, m, r, su, batch, R + kRPad, 64);
   if (!ok) return false;
   p.x = x;
   p.sx = sx;
   p.T = 1, p.b = 0;
   p.rblocks = int(m / 64);
   p.halves = int(n / kRHalf);
-  return launch_recon<true>(ctx, p, units, int(r), s, st);
+  p.rank = int(r);
+  return launch_recon<true>(ctx, p, units, R, s, st);
 }
 
 }  // namespace lrb

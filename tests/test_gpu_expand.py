@@ -111,10 +111,14 @@ def test_expand_in_a_graph(ctx):
 
 
 @pytest.mark.parametrize("n,block,rank", [(512, 256, 8), (768, 256, 16), (2048, 512, 16),
-                                          (1024, 512, 8)])
+                                          (1024, 512, 8),
+                                          # even ranks below the template rank (8 or 16)
+                                          (768, 256, 12), (512, 256, 6), (1024, 256, 2),
+                                          (1536, 512, 14), (768, 256, 10), (512, 256, 4)])
 def test_reconstruct_dense_streaming_kernel(ctx, monkeypatch, n, block, rank):
     # shapes the write-streaming off-diagonal kernel serves (b a multiple of
-    # 256, r in {8, 16}): bitwise the FMA-chain oracle and the UX + tile form
+    # 256, even r <= 16: a rank below 8 / 16 rides on the boxes' zero fill and
+    # masked X reads): bitwise the FMA-chain oracle and the UX + tile form
     m = B.BlrMatrix.random(n, block, rank, 3 * n + rank)
     out, alt = ctx.empty(n * n), ctx.empty(n * n)
     out.fill_bytes(0xFF)
@@ -132,9 +136,12 @@ def test_reconstruct_dense_streaming_kernel(ctx, monkeypatch, n, block, rank):
 
 
 @pytest.mark.parametrize("batch,m,n,r,pad", [(3, 64, 256, 8, 0), (2, 128, 512, 16, 0),
-                                             (5, 192, 256, 16, 6), (1, 512, 768, 8, 2)])
+                                             (5, 192, 256, 16, 6), (1, 512, 768, 8, 2),
+                                             (4, 128, 256, 12, 0), (3, 64, 512, 6, 4),
+                                             (2, 256, 256, 2, 0), (3, 128, 512, 14, 2),
+                                             (5, 64, 256, 10, 0), (2, 192, 256, 4, 6)])
 def test_expand_streaming_kernel(ctx, monkeypatch, batch, m, n, r, pad):
-    # rank 8 / 16 with 64-row, 256-column items: one write-streaming launch
+    # even ranks up to 16 with 64-row, 256-column items: one write-streaming launch
     # (UX on chip), bitwise the FMA-chain oracle and the two-GEMM form, padded
     # leading dimensions and item strides left untouched
     u, x, vt = _operands(batch, m, n, r, 7 * m + r)
